@@ -1,0 +1,167 @@
+/*
+ * fdp.h -- C ABI of the B200-native FlashDP per-layer DP weight-gradient backward.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   dpflows.workflows.run_backward / backward_flashdp
+ *   (/root/reference/pkg/src/dpflows/workflows.py:340-440)
+ * The reference binds nothing native (it is numpy); the Python mirror in
+ * paper_2507_01154_b200/_lib.py binds these symbols with ctypes, exactly as a
+ * maintainer would bind them from dpflows.
+ *
+ * Conventions (all entry points):
+ *   - Layer convention Y = X W^T: X is (B,T,P), dY is (B,T,D), row-major,
+ *     grad_w is (D,P) fp32 row-major (= nn.Linear.weight layout),
+ *     norms_sq is (B,) fp32 (workflows.py:1-5, 40-44).
+ *   - All pointers are DEVICE pointers owned by the caller. Nothing is
+ *     allocated and nothing synchronises the host on the hot path.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - Work is stream-ordered. Two calls that may overlap (different streams)
+ *     need distinct workspaces: the workspace holds the in-kernel norm
+ *     all-reduce counters (the analogue of memmodel.py:261-285).
+ *   - A workspace must be zero-filled once before first use
+ *     (fdp_workspace_init); every call leaves it zeroed again.
+ *   - Return codes mirror the reference exception types (errors.py):
+ *     FDP_ERR_SHAPE    -> ShapeError   (workflows.py:47-52)
+ *     FDP_ERR_USAGE    -> UsageError   (dpcore.py:32-38, workflows.py:330-337)
+ *     FDP_ERR_CAPACITY -> CapacityError (workspace too small; errors.py:12-22)
+ *     FDP_ERR_CUDA     -> RuntimeError (launch/device failure)
+ *   fdp_last_error() returns the message of the last failing call on the
+ *   calling host thread.
+ */
+#ifndef FDP_H_
+#define FDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FDP_API __attribute__((visibility("default")))
+#else
+#define FDP_API
+#endif
+
+enum fdp_status {
+  FDP_OK = 0,
+  FDP_ERR_SHAPE = 1,
+  FDP_ERR_USAGE = 2,
+  FDP_ERR_CAPACITY = 3,
+  FDP_ERR_CUDA = 4
+};
+
+/* Input element type of X and dY. Accumulation is always fp32. */
+enum fdp_dtype { FDP_DTYPE_BF16 = 0, FDP_DTYPE_F32 = 1 };
+
+/* dpcore.REDUCTIONS (dpcore.py:20) */
+enum fdp_reduction { FDP_REDUCE_SUM = 0, FDP_REDUCE_MEAN = 1 };
+
+/* Noise generator.
+ * KEYED_F32: the reference's keyed construction (rng.py:35-85: splitmix64
+ *            absorb of (seed, layer_id, step, flat_index), two salted words,
+ *            Box-Muller cosine branch) with the final transform in fp32.
+ * KEYED_F64: same keys, transform in fp64 (matches the reference draw to
+ *            ~1e-15; parity/debug mode).
+ * PHILOX:    Philox4x32-10 keyed by absorb(seed, layer_id, step), counter =
+ *            flat_index; Box-Muller. Statistically checked only. */
+enum fdp_noise_impl { FDP_NOISE_KEYED_F32 = 0, FDP_NOISE_KEYED_F64 = 1, FDP_NOISE_PHILOX = 2 };
+
+/* Workflow kinds (workflows.py:33-37, WorkflowKind). */
+enum fdp_kind {
+  FDP_KIND_NON_DP = 0,
+  FDP_KIND_EXPLICIT_DP = 1,
+  FDP_KIND_IMPLICIT_DP = 2,
+  FDP_KIND_FLASHDP = 3
+};
+
+/* Execution path for FDP_KIND_FLASHDP.
+ * FUSED:     one persistent tcgen05 launch: per-sample G tiles in TMEM, norm
+ *            all-reduce across CTAs + grid barrier, in-register clip, batch sum,
+ *            noise epilogue (Algorithm 1).
+ * TWO_PHASE: norms from a first phase (ghost Gram norms or a norm-only tcgen05
+ *            pass), then one reweighted tcgen05 pass (for layers whose
+ *            per-sample gradient tiles exceed on-chip capacity).
+ * SIMT:      generic CUDA-core path (any shape, fp32 inputs).
+ * AUTO:      FUSED when it fits, else TWO_PHASE, SIMT for unaligned/fp32. */
+enum fdp_path { FDP_PATH_AUTO = 0, FDP_PATH_FUSED = 1, FDP_PATH_TWO_PHASE = 2, FDP_PATH_SIMT = 3 };
+
+/* Debug flags. SKIP_BARRIER removes the in-kernel norm barrier wait (the
+ * analogue of backward_flashdp(skip_barrier=True), workflows.py:341,394) and
+ * delays one CTA so the premature clip is observable. */
+enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2 };
+
+/* Norm phase of the TWO_PHASE path. */
+enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2 };
+
+typedef struct fdp_desc {
+  int64_t B, T, P, D;       /* X (B,T,P), dY (B,T,D)                          */
+  int32_t in_dtype;         /* fdp_dtype                                      */
+  int32_t reduction;        /* fdp_reduction (DPConfig.reduction)             */
+  double clip_c;            /* DPConfig.clip_c  (> 0)                         */
+  double sigma;             /* DPConfig.sigma   (>= 0)                        */
+  int64_t seed;             /* DPConfig.seed    (any sign; masked to 64 bits) */
+  int64_t layer_id;         /* DPConfig.layer_id                              */
+  int64_t step;             /* DPConfig.step                                  */
+  int32_t rank, world;      /* noise partition: rank adds noise only on its
+                               contiguous slice of [0, D*P) (world >= 1)     */
+  int64_t mean_batch;       /* divisor for reduction=mean; 0 -> B (global B
+                               under data parallelism)                       */
+  int32_t accumulate;       /* 1: grad_w += result (micro-batch accumulation) */
+  int32_t add_noise;        /* 0: skip noise (micro-steps; sigma still valid) */
+  int32_t noise_impl;       /* fdp_noise_impl                                 */
+  int32_t path;             /* fdp_path                                       */
+  int32_t flags;            /* fdp_flags                                      */
+  int32_t norm_phase;       /* fdp_norm_phase                                 */
+} fdp_desc;
+
+/* Plan actually taken for a descriptor (analogue of tiling.BlockPlan,
+ * tiling.py:31-44). Filled by fdp_plan(). */
+typedef struct fdp_plan_info {
+  int32_t path;             /* resolved fdp_path                              */
+  int32_t norm_phase;       /* resolved fdp_norm_phase (TWO_PHASE only)       */
+  int32_t tile_d, tile_p;   /* output tile extents (d, p)                     */
+  int32_t tile_t;           /* t extent of one pipeline stage                 */
+  int32_t n_d, n_p;         /* tile counts                                    */
+  int32_t groups;           /* sample groups (CTAs sharing one output tile)   */
+  int32_t grid;             /* CTAs of the main launch                        */
+  int32_t launches;         /* kernel launches per call                       */
+  int32_t sms;              /* SMs of the device                              */
+  int64_t workspace_bytes;  /* bytes fdp_backward needs for this kind         */
+} fdp_plan_info;
+
+FDP_API int fdp_abi_version(void);
+FDP_API const char* fdp_last_error(void);
+
+/* Device properties relevant to planning (SM count, smem per block). */
+FDP_API int fdp_device_info(int32_t* sms, int32_t* cc_major, int32_t* cc_minor);
+
+FDP_API int fdp_plan(const fdp_desc* d, int32_t kind, fdp_plan_info* out);
+FDP_API int fdp_workspace_bytes(const fdp_desc* d, int32_t kind, size_t* bytes);
+FDP_API int fdp_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* run_backward(kind, x, dy, cfg, ...) (workflows.py:427-440).
+ * norms_sq may be NULL for FDP_KIND_NON_DP (which ignores clip/noise). */
+FDP_API int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const void* dy,
+                 float* grad_w, float* norms_sq, void* ws, size_t ws_bytes, void* stream);
+
+/* backward_flashdp(x, dy, cfg, plan, spec) (workflows.py:340-421). */
+FDP_API int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
+           void* ws, size_t ws_bytes, void* stream);
+
+/* dpcore.noise_for_indices for flat indices [lo, hi) scaled by `scale`
+ * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
+FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);
+
+/* Noise slice [lo, hi) of [0, n) owned by `rank` of `world` (data-parallel
+ * noise-once partition). Pure host arithmetic. */
+FDP_API int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FDP_H_ */

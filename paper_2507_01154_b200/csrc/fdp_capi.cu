@@ -1,0 +1,567 @@
+// fdp_capi.cu -- the C ABI (include/fdp.h): validation, planning, workspace
+// layout, TMA descriptors and dispatch of the four workflow kinds
+// (workflows.py:427-440).
+#include "../../include/fdp.h"
+#include "fdp_internal.h"
+#include "fdp_rng.cuh"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(FDP_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ---- reference key construction (rng.py:35-47), host side
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+uint64_t absorb3(int64_t seed, int64_t layer, int64_t step) {
+  uint64_t h = fdp::mix64(static_cast<uint64_t>(seed));
+  h = fdp::mix64((h + kGamma) ^ static_cast<uint64_t>(layer));
+  h = fdp::mix64((h + kGamma) ^ static_cast<uint64_t>(step));
+  return h;
+}
+
+struct DevInfo {
+  int dev = -1;
+  int sms = 0;
+  int major = 0, minor = 0;
+};
+
+int get_dev(DevInfo& di) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  static std::mutex mu;
+  static DevInfo cache[64];
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && cache[dev].dev == dev) {
+    di = cache[dev];
+    return FDP_OK;
+  }
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  di.dev = dev;
+  di.sms = prop.multiProcessorCount;
+  di.major = prop.major;
+  di.minor = prop.minor;
+  if (dev >= 0 && dev < 64) cache[dev] = di;
+  return FDP_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// bf16 (inner, T, B) tensor, box (64, kBK, 1), 128B swizzle.
+int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t T, int64_t B) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(FDP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(B)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * 2), static_cast<cuuint64_t>(inner * T * 2)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(fdp::kBK), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FDP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return FDP_OK;
+}
+
+int validate(const fdp_desc* d, int32_t kind) {
+  if (!d) return fail(FDP_ERR_USAGE, "null descriptor");
+  if (kind < FDP_KIND_NON_DP || kind > FDP_KIND_FLASHDP) return fail(FDP_ERR_USAGE, "unknown workflow kind %d", kind);
+  if (d->B < 1 || d->T < 1 || d->P < 1 || d->D < 1)
+    return fail(FDP_ERR_SHAPE, "all extents must be >= 1, got B=%lld T=%lld P=%lld D=%lld", (long long)d->B,
+                (long long)d->T, (long long)d->P, (long long)d->D);
+  if (d->B > (1ll << 30) || d->T > (1ll << 30) || d->P > (1ll << 30) || d->D > (1ll << 30))
+    return fail(FDP_ERR_SHAPE, "extent too large");
+  if (d->in_dtype != FDP_DTYPE_BF16 && d->in_dtype != FDP_DTYPE_F32)
+    return fail(FDP_ERR_USAGE, "in_dtype must be bf16 (0) or f32 (1), got %d", d->in_dtype);
+  if (kind != FDP_KIND_NON_DP) {
+    if (!(d->clip_c > 0.0) || !std::isfinite(d->clip_c))
+      return fail(FDP_ERR_USAGE, "clip_c must be positive, got %g", d->clip_c);
+    if (!(d->sigma >= 0.0) || !std::isfinite(d->sigma))
+      return fail(FDP_ERR_USAGE, "sigma must be >= 0, got %g", d->sigma);
+    if (d->reduction != FDP_REDUCE_SUM && d->reduction != FDP_REDUCE_MEAN)
+      return fail(FDP_ERR_USAGE, "reduction must be sum (0) or mean (1), got %d", d->reduction);
+  }
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
+    return fail(FDP_ERR_USAGE, "rank %d out of range for world %d", d->rank, d->world);
+  if (d->mean_batch < 0) return fail(FDP_ERR_USAGE, "mean_batch must be >= 0");
+  if (d->noise_impl < FDP_NOISE_KEYED_F32 || d->noise_impl > FDP_NOISE_PHILOX)
+    return fail(FDP_ERR_USAGE, "unknown noise_impl %d", d->noise_impl);
+  if (d->path < FDP_PATH_AUTO || d->path > FDP_PATH_SIMT) return fail(FDP_ERR_USAGE, "unknown path %d", d->path);
+  return FDP_OK;
+}
+
+struct Plan {
+  int path = FDP_PATH_SIMT;
+  int norm_phase = FDP_NORMS_RECOMPUTE;
+  int bn = 128;
+  int n_dt = 0, n_pt = 0, n_tiles = 0;
+  int groups = 1;
+  int grid = 0;
+  int launches = 0;
+  bool tc = false;
+  // workspace layout (byte offsets)
+  size_t off_ctrl = 0, off_cnt = 0, off_tile_cnt = 0, off_part = 0, off_factor = 0, off_acc = 0, off_g = 0,
+         off_gp = 0, total = 0;
+  int part_tiles = 0;  // partial norms per sample
+  int expl_chunks = 0;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool tc_shape_ok(const fdp_desc* d) {
+  return d->in_dtype == FDP_DTYPE_BF16 && d->P % 8 == 0 && d->D % 8 == 0 && d->T <= (1ll << 30);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
+  const bool tc_dev = di.major == 10;  // sm_100 family
+  const bool tc_ok = tc_dev && tc_shape_ok(d);
+  const int want = d->path;
+  pl = Plan();
+  const int forced_bn = env_int("FDP_FORCE_BN", 0);
+
+  auto tiles_for = [&](int bn, int& ndt, int& npt) {
+    ndt = static_cast<int>((d->D + fdp::kBM - 1) / fdp::kBM);
+    npt = static_cast<int>((d->P + bn - 1) / bn);
+    return static_cast<long long>(ndt) * npt;
+  };
+
+  if (kind == FDP_KIND_FLASHDP) {
+    if ((want == FDP_PATH_FUSED || want == FDP_PATH_TWO_PHASE) && !tc_ok)
+      return fail(FDP_ERR_USAGE,
+                  "path %d needs bf16 inputs, P %% 8 == 0, D %% 8 == 0 and an sm_100 device (got dtype=%d P=%lld "
+                  "D=%lld cc=%d.%d)",
+                  want, d->in_dtype, (long long)d->P, (long long)d->D, di.major, di.minor);
+    if (want == FDP_PATH_SIMT || !tc_ok) {
+      pl.path = FDP_PATH_SIMT;
+    } else {
+      // choose the tile width that best fills the SMs with co-resident CTAs
+      double best = -1.0;
+      int best_bn = 0, best_groups = 1;
+      for (int bn : {256, 128}) {
+        if (forced_bn && bn != forced_bn) continue;
+        int ndt, npt;
+        const long long nt = tiles_for(bn, ndt, npt);
+        const int cores = fdp::tc_max_coresident(bn);
+        const long long cap = static_cast<long long>(di.sms) * (cores > 0 ? 1 : 0);
+        if (nt > cap || cap == 0) continue;
+        long long g = cap / nt;
+        if (g > d->B) g = d->B;
+        if (g > 8) g = 8;
+        const double util = static_cast<double>(nt * g) / di.sms;
+        if (util > best + 1e-9) {
+          best = util;
+          best_bn = bn;
+          best_groups = static_cast<int>(g);
+        }
+      }
+      if (best_bn && want != FDP_PATH_TWO_PHASE) {
+        pl.path = FDP_PATH_FUSED;
+        pl.bn = best_bn;
+        pl.groups = best_groups;
+      } else {
+        pl.path = FDP_PATH_TWO_PHASE;
+        pl.bn = forced_bn ? forced_bn : 256;
+        pl.norm_phase = FDP_NORMS_RECOMPUTE;
+      }
+    }
+  } else if (kind == FDP_KIND_IMPLICIT_DP) {
+    pl.path = (tc_ok && want != FDP_PATH_SIMT) ? FDP_PATH_TWO_PHASE : FDP_PATH_SIMT;
+    pl.bn = forced_bn ? forced_bn : 256;
+    pl.norm_phase = FDP_NORMS_RECOMPUTE;
+  } else {  // NON_DP / EXPLICIT_DP: tensor-core GEMM stage when possible
+    pl.path = (tc_ok && want != FDP_PATH_SIMT) ? FDP_PATH_FUSED : FDP_PATH_SIMT;
+    pl.bn = forced_bn ? forced_bn : 256;
+  }
+  pl.tc = pl.path != FDP_PATH_SIMT;
+
+  if (pl.tc) {
+    tiles_for(pl.bn, pl.n_dt, pl.n_pt);
+    pl.n_tiles = pl.n_dt * pl.n_pt;
+  } else {
+    pl.n_dt = static_cast<int>((d->D + 31) / 32);
+    pl.n_pt = static_cast<int>((d->P + 31) / 32);
+    pl.n_tiles = pl.n_dt * pl.n_pt;
+  }
+
+  // grid + launch count
+  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED) {
+    pl.grid = pl.n_tiles * pl.groups;
+    pl.launches = 1;
+  } else if (pl.tc) {
+    pl.grid = pl.n_tiles < di.sms ? pl.n_tiles : di.sms;
+    if (kind == FDP_KIND_NON_DP) pl.launches = 1;
+    else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;  // G, norms, reduce, clip, sum
+    else pl.launches = 3;                                     // norms, reduce, reweight
+  } else {
+    pl.grid = pl.n_tiles;
+    if (kind == FDP_KIND_NON_DP) pl.launches = 1;
+    else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;
+    else pl.launches = 3;
+  }
+
+  // workspace layout
+  const long long B = d->B;
+  pl.part_tiles = pl.n_tiles;
+  if (kind == FDP_KIND_EXPLICIT_DP) {
+    pl.expl_chunks = 64;
+    pl.part_tiles = pl.expl_chunks;
+  }
+  size_t off = 0;
+  pl.off_ctrl = off;
+  off += 256;
+  pl.off_cnt = off;
+  off = align_up(off + 4 * B, 256);
+  pl.off_tile_cnt = off;
+  off = align_up(off + 4ull * pl.n_tiles, 256);
+  pl.off_part = off;
+  off = align_up(off + 4ull * B * pl.part_tiles, 256);
+  pl.off_factor = off;
+  off = align_up(off + 4 * B, 256);
+  pl.off_acc = off;
+  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED && pl.groups > 1)
+    off = align_up(off + 4ull * (pl.groups - 1) * pl.n_tiles * fdp::kBM * pl.bn, 256);
+  pl.off_g = off;
+  pl.off_gp = off;
+  if (kind == FDP_KIND_EXPLICIT_DP) {
+    const size_t gbytes = 4ull * B * d->D * d->P;
+    pl.off_gp = align_up(off + gbytes, 256);
+    off = align_up(pl.off_gp + gbytes, 256);
+  }
+  pl.total = off;
+  return FDP_OK;
+}
+
+struct Common {
+  uint64_t key_base, key_base_g;
+  long long noise_lo, noise_hi;
+  float noise_scale;
+  float inv_batch;
+  int add_noise;
+};
+
+Common common_of(const fdp_desc* d) {
+  Common c;
+  c.key_base = absorb3(d->seed, d->layer_id, d->step);
+  c.key_base_g = c.key_base + kGamma;
+  const long long n = d->D * d->P;
+  c.noise_lo = n * d->rank / d->world;
+  c.noise_hi = n * (d->rank + 1) / d->world;
+  c.noise_scale = static_cast<float>(d->sigma * d->clip_c);
+  c.add_noise = (d->add_noise && d->sigma > 0.0) ? 1 : 0;
+  const long long mb = d->mean_batch > 0 ? d->mean_batch : d->B;
+  c.inv_batch = d->reduction == FDP_REDUCE_MEAN ? static_cast<float>(1.0 / static_cast<double>(mb)) : 1.0f;
+  return c;
+}
+
+template <typename T>
+T* ws_at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+fdp::SimtParams simt_params(const fdp_desc* d, const Plan& pl, const Common& c, const void* x, const void* dy,
+                            float* grad_w, float* norms, void* ws) {
+  fdp::SimtParams s{};
+  s.B = static_cast<int>(d->B);
+  s.T = static_cast<int>(d->T);
+  s.P = static_cast<int>(d->P);
+  s.D = static_cast<int>(d->D);
+  s.in_f32 = d->in_dtype == FDP_DTYPE_F32;
+  s.x = x;
+  s.dy = dy;
+  s.n_dt = static_cast<int>((d->D + 31) / 32);
+  s.n_pt = static_cast<int>((d->P + 31) / 32);
+  s.n_tiles = s.n_dt * s.n_pt;
+  s.clip_c = d->clip_c;
+  s.clip_c2 = d->clip_c * d->clip_c;
+  s.inv_batch = c.inv_batch;
+  s.accumulate = d->accumulate;
+  s.add_noise = c.add_noise;
+  s.noise_impl = d->noise_impl;
+  s.noise_scale = c.noise_scale;
+  s.key_base = c.key_base;
+  s.key_base_g = c.key_base_g;
+  s.noise_lo = c.noise_lo;
+  s.noise_hi = c.noise_hi;
+  s.grad_w = grad_w;
+  s.norms_out = norms;
+  s.ws_part = ws_at<float>(ws, pl.off_part);
+  s.ws_factor = ws_at<float>(ws, pl.off_factor);
+  s.with_clip = 1;
+  return s;
+}
+
+fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, float* grad_w, float* norms, void* ws,
+                        int mode) {
+  fdp::TcParams p{};
+  p.B = static_cast<int>(d->B);
+  p.T = static_cast<int>(d->T);
+  p.P = static_cast<int>(d->P);
+  p.D = static_cast<int>(d->D);
+  p.n_dt = pl.n_dt;
+  p.n_pt = pl.n_pt;
+  p.n_tiles = pl.n_tiles;
+  p.groups = mode == fdp::MODE_FUSED ? pl.groups : 1;
+  p.mode = mode;
+  p.n_kb = static_cast<int>((d->T + fdp::kBK - 1) / fdp::kBK);
+  p.clip_c = d->clip_c;
+  p.clip_c2 = d->clip_c * d->clip_c;
+  p.inv_batch = c.inv_batch;
+  p.accumulate = d->accumulate;
+  p.add_noise = c.add_noise;
+  p.noise_impl = d->noise_impl;
+  p.noise_scale = c.noise_scale;
+  p.key_base = c.key_base;
+  p.key_base_g = c.key_base_g;
+  p.noise_lo = c.noise_lo;
+  p.noise_hi = c.noise_hi;
+  p.grad_w = grad_w;
+  p.norms_out = norms;
+  p.g_out = nullptr;
+  p.factors_in = ws_at<float>(ws, pl.off_factor);
+  p.ws_part = ws_at<float>(ws, pl.off_part);
+  p.ws_cnt = ws_at<unsigned>(ws, pl.off_cnt);
+  p.ws_tile_cnt = ws_at<unsigned>(ws, pl.off_tile_cnt);
+  p.ws_ctrl = ws_at<unsigned>(ws, pl.off_ctrl);
+  p.ws_acc = ws_at<float>(ws, pl.off_acc);
+  p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
+  p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+  return p;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms, void* ws,
+        size_t ws_bytes, cudaStream_t s) {
+  int rc = validate(d, kind);
+  if (rc) return rc;
+  if (!x || !dy || !grad_w) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if (kind != FDP_KIND_NON_DP && !norms) return fail(FDP_ERR_USAGE, "norms_sq must not be null for DP workflows");
+  DevInfo di;
+  if ((rc = get_dev(di))) return rc;
+  Plan pl;
+  if ((rc = make_plan(d, kind, di, pl))) return rc;
+  if (!ws || ws_bytes < pl.total)
+    return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
+                pl.total);
+  if (pl.tc && !(aligned16(x) && aligned16(dy)))
+    return fail(FDP_ERR_USAGE, "x and dy must be 16-byte aligned for the tensor-core path");
+  const Common c = common_of(d);
+  cudaError_t e;
+
+  if (!pl.tc) {
+    fdp::SimtParams sp = simt_params(d, pl, c, x, dy, grad_w, norms, ws);
+    if (kind == FDP_KIND_NON_DP) {
+      sp.with_clip = 0;
+      if ((e = fdp::simt_weighted_sum(sp, s)) != cudaSuccess) return cuda_fail(e, "simt nondp");
+      return FDP_OK;
+    }
+    if (kind == FDP_KIND_EXPLICIT_DP) {
+      const long long DP = d->D * d->P;
+      float* g = ws_at<float>(ws, pl.off_g);
+      float* gp = ws_at<float>(ws, pl.off_gp);
+      float* part = ws_at<float>(ws, pl.off_part);
+      float* fac = ws_at<float>(ws, pl.off_factor);
+      if ((e = fdp::explicit_store_g_simt(sp, g, s)) != cudaSuccess) return cuda_fail(e, "explicit G");
+      if ((e = fdp::explicit_norms(g, sp.B, DP, part, pl.expl_chunks, s)) != cudaSuccess)
+        return cuda_fail(e, "explicit norms");
+      if ((e = fdp::reduce_norms_to_factors(part, sp.B, pl.expl_chunks, d->clip_c, sp.clip_c2, 1.0f, norms, fac, s)) !=
+          cudaSuccess)
+        return cuda_fail(e, "explicit reduce");
+      if ((e = fdp::explicit_clip(g, gp, fac, sp.B, DP, s)) != cudaSuccess) return cuda_fail(e, "explicit clip");
+      if ((e = fdp::explicit_sum_finalize(gp, sp.B, DP, sp.P, sp, s)) != cudaSuccess)
+        return cuda_fail(e, "explicit sum");
+      return FDP_OK;
+    }
+    // FLASHDP (generic) and IMPLICIT: norm pass, factor reduce, weighted pass
+    if ((e = fdp::simt_partial_norms(sp, s)) != cudaSuccess) return cuda_fail(e, "simt norms");
+    if ((e = fdp::reduce_norms_to_factors(sp.ws_part, sp.B, sp.n_tiles, d->clip_c, sp.clip_c2, c.inv_batch, norms,
+                                          sp.ws_factor, s)) != cudaSuccess)
+      return cuda_fail(e, "simt reduce");
+    if ((e = fdp::simt_weighted_sum(sp, s)) != cudaSuccess) return cuda_fail(e, "simt weighted sum");
+    return FDP_OK;
+  }
+
+  // ---- tensor-core paths
+  CUtensorMap tm_dy, tm_x;
+  if ((rc = make_tmap(&tm_dy, dy, d->D, d->T, d->B))) return rc;
+  if ((rc = make_tmap(&tm_x, x, d->P, d->T, d->B))) return rc;
+
+  if (kind == FDP_KIND_NON_DP) {
+    fdp::TcParams p = tc_params(d, pl, c, grad_w, nullptr, ws, fdp::MODE_NONDP);
+    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+      return cuda_fail(e, "tc nondp launch");
+    return FDP_OK;
+  }
+  if (kind == FDP_KIND_EXPLICIT_DP) {
+    const long long DP = d->D * d->P;
+    float* g = ws_at<float>(ws, pl.off_g);
+    float* gp = ws_at<float>(ws, pl.off_gp);
+    float* part = ws_at<float>(ws, pl.off_part);
+    float* fac = ws_at<float>(ws, pl.off_factor);
+    fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_STORE_G);
+    p.g_out = g;
+    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+      return cuda_fail(e, "tc explicit G launch");
+    fdp::SimtParams sp = simt_params(d, pl, c, x, dy, grad_w, norms, ws);
+    if ((e = fdp::explicit_norms(g, sp.B, DP, part, pl.expl_chunks, s)) != cudaSuccess)
+      return cuda_fail(e, "explicit norms");
+    if ((e = fdp::reduce_norms_to_factors(part, sp.B, pl.expl_chunks, d->clip_c, sp.clip_c2, 1.0f, norms, fac, s)) !=
+        cudaSuccess)
+      return cuda_fail(e, "explicit reduce");
+    if ((e = fdp::explicit_clip(g, gp, fac, sp.B, DP, s)) != cudaSuccess) return cuda_fail(e, "explicit clip");
+    if ((e = fdp::explicit_sum_finalize(gp, sp.B, DP, sp.P, sp, s)) != cudaSuccess)
+      return cuda_fail(e, "explicit sum");
+    return FDP_OK;
+  }
+  if (pl.path == FDP_PATH_FUSED) {
+    fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_FUSED);
+    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, true, s)) != cudaSuccess)
+      return cuda_fail(e, "tc fused launch");
+    return FDP_OK;
+  }
+  // TWO_PHASE: norm phase (recompute), factors, one reweighted pass
+  {
+    fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_NORMS);
+    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+      return cuda_fail(e, "tc norm-phase launch");
+    if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pl.n_tiles, d->clip_c, p.clip_c2, c.inv_batch, norms,
+                                          ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+      return cuda_fail(e, "factor reduce");
+    fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
+    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, q, pl.grid, false, s)) != cudaSuccess)
+      return cuda_fail(e, "tc reweight launch");
+  }
+  return FDP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fdp_abi_version(void) { return FDP_ABI_VERSION; }
+
+const char* fdp_last_error(void) { return g_last_error.c_str(); }
+
+int fdp_device_info(int32_t* sms, int32_t* cc_major, int32_t* cc_minor) {
+  DevInfo di;
+  int rc = get_dev(di);
+  if (rc) return rc;
+  if (sms) *sms = di.sms;
+  if (cc_major) *cc_major = di.major;
+  if (cc_minor) *cc_minor = di.minor;
+  return FDP_OK;
+}
+
+int fdp_plan(const fdp_desc* d, int32_t kind, fdp_plan_info* out) {
+  int rc = validate(d, kind);
+  if (rc) return rc;
+  if (!out) return fail(FDP_ERR_USAGE, "null plan output");
+  DevInfo di;
+  if ((rc = get_dev(di))) return rc;
+  Plan pl;
+  if ((rc = make_plan(d, kind, di, pl))) return rc;
+  out->path = pl.path;
+  out->norm_phase = pl.path == FDP_PATH_TWO_PHASE ? pl.norm_phase : 0;
+  out->tile_d = pl.tc ? fdp::kBM : 32;
+  out->tile_p = pl.tc ? pl.bn : 32;
+  out->tile_t = pl.tc ? fdp::kBK : 32;
+  out->n_d = pl.n_dt;
+  out->n_p = pl.n_pt;
+  out->groups = pl.groups;
+  out->grid = pl.grid;
+  out->launches = pl.launches;
+  out->sms = di.sms;
+  out->workspace_bytes = static_cast<int64_t>(pl.total);
+  return FDP_OK;
+}
+
+int fdp_workspace_bytes(const fdp_desc* d, int32_t kind, size_t* bytes) {
+  fdp_plan_info info;
+  int rc = fdp_plan(d, kind, &info);
+  if (rc) return rc;
+  if (!bytes) return fail(FDP_ERR_USAGE, "null output");
+  *bytes = static_cast<size_t>(info.workspace_bytes);
+  return FDP_OK;
+}
+
+int fdp_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+  if (!ws && ws_bytes) return fail(FDP_ERR_USAGE, "null workspace");
+  if (!ws_bytes) return FDP_OK;
+  cudaError_t e = cudaMemsetAsync(ws, 0, ws_bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  return FDP_OK;
+}
+
+int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
+                 void* ws, size_t ws_bytes, void* stream) {
+  return run(kind, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq, void* ws,
+           size_t ws_bytes, void* stream) {
+  return run(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream) {
+  if (!d) return fail(FDP_ERR_USAGE, "null descriptor");
+  if (lo < 0 || hi < lo) return fail(FDP_ERR_USAGE, "bad index range [%lld, %lld)", (long long)lo, (long long)hi);
+  if (hi > lo && !out) return fail(FDP_ERR_USAGE, "null output");
+  if (d->noise_impl < FDP_NOISE_KEYED_F32 || d->noise_impl > FDP_NOISE_PHILOX)
+    return fail(FDP_ERR_USAGE, "unknown noise_impl %d", d->noise_impl);
+  const uint64_t base = absorb3(d->seed, d->layer_id, d->step);
+  cudaError_t e = fdp::noise_fill(out, lo, hi, scale, d->noise_impl, base, base + kGamma,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "noise_fill");
+  return FDP_OK;
+}
+
+int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world) return fail(FDP_ERR_USAGE, "bad partition arguments");
+  if (lo) *lo = n * rank / world;
+  if (hi) *hi = n * (rank + 1) / world;
+  return FDP_OK;
+}
+
+}  // extern "C"

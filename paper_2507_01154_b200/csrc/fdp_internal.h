@@ -1,0 +1,95 @@
+// fdp_internal.h -- shared declarations between the C-ABI layer and the kernels.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace fdp {
+
+constexpr int kBM = 128;  // d rows per output tile (UMMA M, one TMEM lane per row)
+constexpr int kBK = 64;   // t extent of one pipeline stage (4 x UMMA K=16)
+constexpr int kEpiWarps = 8;
+constexpr int kTcThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warps 2..9 epilogue
+
+enum TcMode : int {
+  MODE_FUSED = 0,     // per-sample G tile -> norm all-reduce + grid barrier -> clip -> sum -> noise
+  MODE_NORMS = 1,     // per-sample G tile -> partial norm^2 only (recompute norm phase)
+  MODE_REWEIGHT = 2,  // per-sample G tile scaled by a precomputed factor -> sum -> noise
+  MODE_STORE_G = 3,   // per-sample G tile stored to HBM (explicit / Opacus-style stage 1)
+  MODE_NONDP = 4      // plain sum_b dY_b^T X_b (non-DP baseline)
+};
+
+struct TcParams {
+  int B, T, P, D;
+  int n_dt, n_pt, n_tiles;
+  int groups;  // sample groups per output tile (FUSED)
+  int mode;
+  int n_kb;
+  double clip_c;
+  double clip_c2;
+  float inv_batch;
+  int accumulate;
+  int add_noise;
+  int noise_impl;
+  float noise_scale;
+  uint64_t key_base;    // absorb(seed, layer_id, step)
+  uint64_t key_base_g;  // key_base + GAMMA
+  long long noise_lo, noise_hi;
+  float* grad_w;
+  float* norms_out;
+  float* g_out;
+  const float* factors_in;
+  float* ws_part;          // [B][n_tiles]
+  unsigned* ws_cnt;        // [B]
+  unsigned* ws_tile_cnt;   // [n_tiles]
+  unsigned* ws_ctrl;       // [0] exit counter, [1] error word
+  float* ws_acc;           // [(groups-1)][n_tiles][kBM*BN]
+  int skip_barrier;
+  unsigned long long budget_ns;
+};
+
+// Launch the tcgen05 kernel (BN = 128 or 256). cooperative=true for MODE_FUSED.
+cudaError_t launch_tc(int bn, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
+                      bool cooperative, cudaStream_t stream);
+int tc_max_coresident(int bn);  // CTAs per SM that can be co-resident (0 if the kernel cannot run)
+size_t tc_smem_bytes(int bn);
+
+// ---- SIMT (CUDA-core) kernels: generic shapes, fp32 inputs, explicit baseline
+struct SimtParams {
+  int B, T, P, D;
+  int in_f32;  // 1: fp32 inputs, 0: bf16
+  const void* x;
+  const void* dy;
+  int n_dt, n_pt, n_tiles;  // 32x32 tiles
+  double clip_c;
+  double clip_c2;
+  float inv_batch;
+  int accumulate;
+  int add_noise;
+  int noise_impl;
+  float noise_scale;
+  uint64_t key_base, key_base_g;
+  long long noise_lo, noise_hi;
+  float* grad_w;
+  float* norms_out;
+  float* ws_part;     // [B][n_tiles]
+  float* ws_factor;   // [B]
+  int with_clip;      // 0: non-DP sum
+};
+cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s);
+cudaError_t reduce_norms_to_factors(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
+                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s);
+cudaError_t simt_weighted_sum(const SimtParams& p, cudaStream_t s);
+
+// explicit (Opacus-style) stages over a materialised G (B,D,P)
+cudaError_t explicit_store_g_simt(const SimtParams& p, float* g, cudaStream_t s);
+cudaError_t explicit_norms(const float* g, int B, long long DP, float* part, int nchunks, cudaStream_t s);
+cudaError_t explicit_clip(const float* g, float* gp, const float* factors, int B, long long DP, cudaStream_t s);
+cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int P, const SimtParams& p,
+                                  cudaStream_t s);
+
+cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int impl, uint64_t base,
+                       uint64_t base_g, cudaStream_t s);
+
+}  // namespace fdp

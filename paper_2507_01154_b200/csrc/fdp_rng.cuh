@@ -1,0 +1,81 @@
+// fdp_rng.cuh -- counter-based Gaussian noise for the DP epilogue.
+//
+// KEYED: the reference's construction (/root/reference/pkg/src/dpflows/rng.py:24-85):
+//   base  = absorb(seed, layer_id, step)                        rng.py:42-47 (host side)
+//   h     = mix64((base + GAMMA) ^ flat_index)                   rng.py:77 (vector tail)
+//   w1,w2 = mix64(h ^ SALT_A), mix64(h ^ SALT_B)                 rng.py:51-52
+//   u1    = ((w1 >> 11) + 1) * 2^-53  in (0, 1]                  rng.py:53
+//   u2    = (w2 >> 11) * 2^-53        in [0, 1)                  rng.py:54
+//   n     = sqrt(-2 ln u1) * cos(2 pi u2)                        rng.py:55
+// The host passes base_g = base + GAMMA (mod 2^64).
+// PHILOX: Philox4x32-10 keyed by base, counter = flat_index (statistical mode).
+#pragma once
+#include <cstdint>
+
+namespace fdp {
+
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMix2 = 0x94D049BB133111EBull;
+constexpr uint64_t kSaltA = 0xD1B54A32D192ED03ull;
+constexpr uint64_t kSaltB = 0x8BB84B93962EACC9ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMix1;
+  z = (z ^ (z >> 27)) * kMix2;
+  return z ^ (z >> 31);
+}
+
+// Reference-keyed draw, final transform in fp32 (|err| vs the fp64 draw ~1e-6).
+__device__ __forceinline__ float keyed_normal_f32(uint64_t base_g, uint64_t idx) {
+  const uint64_t h = mix64(base_g ^ idx);
+  const uint64_t w1 = mix64(h ^ kSaltA) >> 11;
+  const uint64_t w2 = mix64(h ^ kSaltB) >> 11;
+  // One rounding of the exact 53-bit integer, then an exact power-of-two scale.
+  const float u1 = __ull2float_rn(w1 + 1) * 0x1p-53f;
+  const float u2 = __ull2float_rn(w2) * 0x1p-53f;
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+// Reference-keyed draw in fp64 (libdevice log/cos are within ~1 ulp of libm).
+__device__ __forceinline__ double keyed_normal_f64(uint64_t base_g, uint64_t idx) {
+  const uint64_t h = mix64(base_g ^ idx);
+  const uint64_t w1 = mix64(h ^ kSaltA) >> 11;
+  const uint64_t w2 = mix64(h ^ kSaltB) >> 11;
+  const double u1 = static_cast<double>(w1 + 1) * 0x1p-53;
+  const double u2 = static_cast<double>(w2) * 0x1p-53;
+  const double two_pi = 6.283185307179586;  // 2.0 * math.pi as a double (rng.py:33)
+  return sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+}
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ float philox_normal(uint64_t base, uint64_t idx) {
+  uint32_t c[4] = {static_cast<uint32_t>(idx), static_cast<uint32_t>(idx >> 32), 0x44504E5Au, 0u};
+  philox4x32_10(c, static_cast<uint32_t>(base), static_cast<uint32_t>(base >> 32));
+  const float u1 = (static_cast<float>(c[0] >> 8) + 1.0f) * 0x1p-24f;  // (0, 1]
+  const float u2 = static_cast<float>(c[1] >> 8) * 0x1p-24f;           // [0, 1)
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+// impl: 0 keyed f32, 1 keyed f64, 2 philox. `base_g` = absorb(...) + GAMMA,
+// `base` = absorb(...) (philox key).
+__device__ __forceinline__ float noise_draw(int impl, uint64_t base_g, uint64_t base, uint64_t idx) {
+  if (impl == 2) return philox_normal(base, idx);
+  if (impl == 1) return static_cast<float>(keyed_normal_f64(base_g, idx));
+  return keyed_normal_f32(base_g, idx);
+}
+
+}  // namespace fdp

@@ -1,0 +1,252 @@
+// fdp_simt.cu -- CUDA-core kernels: the generic path for any shape / fp32 inputs,
+// the explicit (Opacus-style) baseline stages, the norm->clip-factor reduction and
+// standalone keyed noise.
+//
+// The generic DP path is the two-pass structure of backward_implicit
+// (workflows.py:246-324): pass 1 reduces per-sample norm^2 partials per 32x32
+// tile without storing G, pass 2 recomputes the tiles and sums c_b * G_b. It is
+// exact fp32 FMA arithmetic, so fp32 inputs meet the 1e-5 bar.
+#include "fdp_internal.h"
+#include "fdp_rng.cuh"
+#include <cuda_bf16.h>
+
+namespace fdp {
+
+namespace {
+
+constexpr int kTS = 32;  // tile extent (d, p, and t chunk)
+
+__device__ __forceinline__ float load_in(const void* base, long long idx, int in_f32) {
+  if (in_f32) return static_cast<const float*>(base)[idx];
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
+// Accumulate the 2x2 micro-tile of G_b[d0 + 2ty + {0,1}, p0 + 2tx + {0,1}] over all t.
+__device__ __forceinline__ void sample_tile(const SimtParams& p, int b, int d0, int p0, float (&g)[2][2],
+                                            float (*sy)[kTS + 1], float (*sx)[kTS + 1]) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  g[0][0] = g[0][1] = g[1][0] = g[1][1] = 0.0f;
+  const long long ybase = static_cast<long long>(b) * p.T * p.D;
+  const long long xbase = static_cast<long long>(b) * p.T * p.P;
+  for (int t0 = 0; t0 < p.T; t0 += kTS) {
+    for (int e = threadIdx.x; e < kTS * kTS; e += blockDim.x) {
+      const int tt = e / kTS, cc = e % kTS;
+      const int t = t0 + tt;
+      const int dd = d0 + cc, pp = p0 + cc;
+      sy[tt][cc] = (t < p.T && dd < p.D) ? load_in(p.dy, ybase + static_cast<long long>(t) * p.D + dd, p.in_f32) : 0.0f;
+      sx[tt][cc] = (t < p.T && pp < p.P) ? load_in(p.x, xbase + static_cast<long long>(t) * p.P + pp, p.in_f32) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int tt = 0; tt < kTS; ++tt) {
+      const float y0 = sy[tt][2 * ty], y1 = sy[tt][2 * ty + 1];
+      const float x0 = sx[tt][2 * tx], x1 = sx[tt][2 * tx + 1];
+      g[0][0] = fmaf(y0, x0, g[0][0]);
+      g[0][1] = fmaf(y0, x1, g[0][1]);
+      g[1][0] = fmaf(y1, x0, g[1][0]);
+      g[1][1] = fmaf(y1, x1, g[1][1]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_partial_norms(const SimtParams p) {
+  __shared__ float sy[kTS][kTS + 1];
+  __shared__ float sx[kTS][kTS + 1];
+  __shared__ float red[8];
+  const int pt = blockIdx.x, dt = blockIdx.y, b = blockIdx.z;
+  float g[2][2];
+  sample_tile(p, b, dt * kTS, pt * kTS, g, sy, sx);
+  float s = g[0][0] * g[0][0] + g[0][1] * g[0][1] + g[1][0] * g[1][0] + g[1][1] * g[1][1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    p.ws_part[static_cast<long long>(b) * p.n_tiles + dt * p.n_pt + pt] = t;
+  }
+}
+
+// One warp per sample: fixed-order double sum of the partials -> norm^2, clip factor.
+__global__ void k_reduce_norms(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
+                               float inv_batch, float* norms_out, float* factors) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int i = lane; i < n_tiles; i += 32) s += static_cast<double>(part[static_cast<long long>(b) * n_tiles + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const double cf = (s <= clip_c2) ? 1.0 : clip_c / sqrt(s);  // dpcore.py:41-47
+    if (norms_out) norms_out[b] = static_cast<float>(s);
+    if (factors) factors[b] = static_cast<float>(cf) * inv_batch;
+  }
+}
+
+__device__ __forceinline__ float draw(const SimtParams& p, long long flat) {
+  return noise_draw(p.noise_impl, p.key_base_g, p.key_base, static_cast<uint64_t>(flat));
+}
+
+__global__ void __launch_bounds__(256) k_weighted_sum(const SimtParams p) {
+  __shared__ float sy[kTS][kTS + 1];
+  __shared__ float sx[kTS][kTS + 1];
+  const int pt = blockIdx.x, dt = blockIdx.y;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  for (int b = 0; b < p.B; ++b) {
+    float g[2][2];
+    sample_tile(p, b, dt * kTS, pt * kTS, g, sy, sx);
+    const float f = p.with_clip ? p.ws_factor[b] : 1.0f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j] = fmaf(f, g[i][j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int d = dt * kTS + 2 * ty + i;
+    if (d >= p.D) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int pp = pt * kTS + 2 * tx + j;
+      if (pp >= p.P) continue;
+      const long long flat = static_cast<long long>(d) * p.P + pp;
+      float v = acc[i][j];
+      if (p.with_clip && p.add_noise && flat >= p.noise_lo && flat < p.noise_hi) v += p.noise_scale * draw(p, flat);
+      if (p.accumulate) v += p.grad_w[flat];
+      p.grad_w[flat] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_store_g(const SimtParams p, float* gout) {
+  __shared__ float sy[kTS][kTS + 1];
+  __shared__ float sx[kTS][kTS + 1];
+  const int pt = blockIdx.x, dt = blockIdx.y, b = blockIdx.z;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float g[2][2];
+  sample_tile(p, b, dt * kTS, pt * kTS, g, sy, sx);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int d = dt * kTS + 2 * ty + i;
+    if (d >= p.D) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int pp = pt * kTS + 2 * tx + j;
+      if (pp < p.P) gout[(static_cast<long long>(b) * p.D + d) * p.P + pp] = g[i][j];
+    }
+  }
+}
+
+// Explicit stage 2 (workflows.py:197-210): per-sample squared norm partials.
+__global__ void __launch_bounds__(256) k_explicit_norms(const float* g, long long DP, int nchunks, float* part) {
+  __shared__ float red[8];
+  const int chunk = blockIdx.x, b = blockIdx.y;
+  const long long per = (DP + nchunks - 1) / nchunks;
+  const long long lo = chunk * per, hi = (lo + per < DP) ? lo + per : DP;
+  const float* gb = g + static_cast<long long>(b) * DP;
+  float s = 0.0f;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) s = fmaf(gb[i], gb[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[static_cast<long long>(b) * nchunks + chunk] = t;
+  }
+}
+
+// Explicit stage 3 (workflows.py:212-225): G' = c_b * G, written to a second buffer.
+__global__ void k_explicit_clip(const float* __restrict__ g, float* __restrict__ gp, const float* factors, int B,
+                                long long DP) {
+  const long long n = static_cast<long long>(B) * DP;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    gp[i] = factors[i / DP] * g[i];
+}
+
+// Explicit stage 4 (workflows.py:227-237): sum over samples, finalize with noise.
+__global__ void k_explicit_sum(const float* __restrict__ gp, int B, long long DP, const SimtParams p) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < DP;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += gp[static_cast<long long>(b) * DP + i];
+    float v = s * p.inv_batch;
+    if (p.add_noise && i >= p.noise_lo && i < p.noise_hi) v += p.noise_scale * draw(p, i);
+    if (p.accumulate) v += p.grad_w[i];
+    p.grad_w[i] = v;
+  }
+}
+
+__global__ void k_noise_fill(float* out, long long lo, long long hi, float scale, int impl, uint64_t base,
+                             uint64_t base_g) {
+  for (long long i = lo + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < hi;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (impl == 1)
+      out[i - lo] = static_cast<float>(static_cast<double>(scale) * keyed_normal_f64(base_g, static_cast<uint64_t>(i)));
+    else
+      out[i - lo] = scale * noise_draw(impl, base_g, base, static_cast<uint64_t>(i));
+  }
+}
+
+int grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s) {
+  k_partial_norms<<<dim3(p.n_pt, p.n_dt, p.B), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_norms_to_factors(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
+                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s) {
+  const int warps_per_block = 4;
+  k_reduce_norms<<<(B + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, s>>>(
+      part, B, n_tiles, clip_c, clip_c2, inv_batch, norms_out, factors);
+  return cudaGetLastError();
+}
+
+cudaError_t simt_weighted_sum(const SimtParams& p, cudaStream_t s) {
+  k_weighted_sum<<<dim3(p.n_pt, p.n_dt), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t explicit_store_g_simt(const SimtParams& p, float* g, cudaStream_t s) {
+  k_store_g<<<dim3(p.n_pt, p.n_dt, p.B), 256, 0, s>>>(p, g);
+  return cudaGetLastError();
+}
+
+cudaError_t explicit_norms(const float* g, int B, long long DP, float* part, int nchunks, cudaStream_t s) {
+  k_explicit_norms<<<dim3(nchunks, B), 256, 0, s>>>(g, DP, nchunks, part);
+  return cudaGetLastError();
+}
+
+cudaError_t explicit_clip(const float* g, float* gp, const float* factors, int B, long long DP, cudaStream_t s) {
+  k_explicit_clip<<<grid_for(static_cast<long long>(B) * DP, 256), 256, 0, s>>>(g, gp, factors, B, DP);
+  return cudaGetLastError();
+}
+
+cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int /*P*/, const SimtParams& p,
+                                  cudaStream_t s) {
+  k_explicit_sum<<<grid_for(DP, 256), 256, 0, s>>>(gp, B, DP, p);
+  return cudaGetLastError();
+}
+
+cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int impl, uint64_t base,
+                       uint64_t base_g, cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  k_noise_fill<<<grid_for(hi - lo, 256), 256, 0, s>>>(out, lo, hi, static_cast<float>(scale), impl, base, base_g);
+  return cudaGetLastError();
+}
+
+}  // namespace fdp

@@ -1,0 +1,115 @@
+"""Memory-spec and traffic-ledger types of the reference API.
+
+``MemSpec``/``TrafficReport``/``merge_reports`` keep the reference's fields
+and serialisation order (memmodel.py:30-79). On B200 nothing is simulated: the
+kernels run on the device, and the report attached to a result is the
+reference's exact ledger for the workflow evaluated in closed form
+(``ledger``), in elements x ``dtype_width_bytes``. The closed forms are pinned
+against the reference simulator by tests/test_ledger.py; measured DRAM bytes
+(ncu) are reported next to them by bench.py.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable
+
+from .errors import UsageError
+
+_ALLOWED_WIDTHS = (2, 4, 8)
+
+
+@dataclass(frozen=True)
+class MemSpec:
+    scratchpad_capacity_bytes: int
+    dtype_width_bytes: int = 8
+
+    def __post_init__(self):
+        if self.dtype_width_bytes not in _ALLOWED_WIDTHS:
+            raise UsageError(f"dtype_width_bytes must be one of {_ALLOWED_WIDTHS}, got {self.dtype_width_bytes}")
+        if self.scratchpad_capacity_bytes < 1:
+            raise UsageError(f"scratchpad_capacity_bytes must be positive, got {self.scratchpad_capacity_bytes}")
+
+
+# Per-SM shared memory of a B200 (227 KB usable per CTA + 1 KB reserved) with
+# bf16 elements: the default spec when a caller passes none.
+B200_SPEC = MemSpec(228 * 1024, 2)
+
+
+@dataclass
+class TrafficReport:
+    bytes_loaded: int = 0
+    bytes_stored: int = 0
+    flops: int = 0
+    redundant_flops: int = 0
+    barriers: int = 0
+    kernel_launches: int = 0
+    peak_scratch_bytes: int = 0
+    per_sample_grad_bytes_stored: int = 0
+
+    def to_dict(self) -> dict:
+        return {
+            "bytes_loaded": self.bytes_loaded,
+            "bytes_stored": self.bytes_stored,
+            "flops": self.flops,
+            "redundant_flops": self.redundant_flops,
+            "barriers": self.barriers,
+            "kernel_launches": self.kernel_launches,
+            "peak_scratch_bytes": self.peak_scratch_bytes,
+            "per_sample_grad_bytes_stored": self.per_sample_grad_bytes_stored,
+        }
+
+
+def merge_reports(reports: Iterable[TrafficReport]) -> TrafficReport:
+    """Sum counters; the peak is a max (memmodel.py:67-79)."""
+    out = TrafficReport()
+    for r in reports:
+        out.bytes_loaded += r.bytes_loaded
+        out.bytes_stored += r.bytes_stored
+        out.flops += r.flops
+        out.redundant_flops += r.redundant_flops
+        out.barriers += r.barriers
+        out.kernel_launches += r.kernel_launches
+        out.peak_scratch_bytes = max(out.peak_scratch_bytes, r.peak_scratch_bytes)
+        out.per_sample_grad_bytes_stored += r.per_sample_grad_bytes_stored
+    return out
+
+
+def ledger(kind: str, B: int, T: int, P: int, D: int, width: int, plan=None, dp: bool = True) -> TrafficReport:
+    """Closed-form traffic ledger of one workflow (elements x width).
+
+    Derived from the dataflow of workflows.py (loads of X/dY once per fused
+    pass, norm/accumulator round trips, per-sample G materialisation); the
+    formulas are cross-checked against the reference simulator in the tests.
+    ``plan`` (a BlockPlan) only matters for flashdp (norm reloads per (p,d)
+    block and one accumulator spill per batch chunk). ``dp`` False drops the
+    finalize flops (non-DP has no emit step).
+    """
+    inputs = B * T * (P + D)
+    g = B * D * P
+    dp_elems = D * P
+    grad_flops = 2 * B * T * D * P
+    if kind == "non_dp":
+        return TrafficReport(bytes_loaded=inputs * width, bytes_stored=dp_elems * width, flops=grad_flops,
+                             kernel_launches=1)
+    emit = dp_elems
+    if kind == "explicit_dp":
+        return TrafficReport(bytes_loaded=(inputs + 3 * g + B) * width,
+                             bytes_stored=(2 * g + B + dp_elems) * width,
+                             flops=grad_flops + 4 * g + emit, kernel_launches=4,
+                             per_sample_grad_bytes_stored=2 * g * width)
+    if kind == "implicit_dp":
+        return TrafficReport(bytes_loaded=(2 * inputs + B) * width, bytes_stored=(B + dp_elems) * width,
+                             flops=2 * grad_flops + 4 * g + emit, redundant_flops=grad_flops,
+                             kernel_launches=2)
+    if kind == "flashdp":
+        if plan is None:
+            raise UsageError("flashdp ledger needs the block plan")
+        blocks = plan.n_p * plan.n_d
+        return TrafficReport(bytes_loaded=(inputs + blocks * B + dp_elems) * width,
+                             bytes_stored=(blocks * B + plan.n_b * dp_elems + dp_elems) * width,
+                             flops=grad_flops + 4 * g + emit, barriers=plan.n_b + 1,
+                             kernel_launches=plan.n_b,
+                             peak_scratch_bytes=(plan.b * plan.t * (plan.p + plan.d) + plan.b * plan.d * plan.p
+                                                 + plan.b) * width)
+    raise UsageError(f"unknown workflow kind {kind!r}")

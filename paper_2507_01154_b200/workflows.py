@@ -1,0 +1,239 @@
+"""Drop-in replacement of the reference workflow API (workflows.py:33-440).
+
+``run_backward(kind, x, dy, cfg, spec, plan=None, *, sim=None)`` and
+``backward_{flashdp,explicit,implicit,nondp}`` keep the reference names,
+argument meaning, result type and exceptions. The body of every workflow is
+one C-ABI call (include/fdp.h) that launches sm_100a kernels:
+
+  flashdp      fused tcgen05 kernel (per-sample tiles in TMEM, in-kernel norm
+               all-reduce + grid barrier, clip, batch sum, noise), or the
+               two-phase tcgen05 path for layers too large for on-chip tiles
+  implicit_dp  norm pass + recompute pass (GhostClip-style, workflows.py:246-324)
+  explicit_dp  G materialised in HBM, then norms / clip / sum+noise stages
+               (Opacus-style, workflows.py:156-240)
+  non_dp       plain sum_b dY_b^T X_b (workflows.py:121-150)
+
+Inputs may be torch tensors on the GPU (the hot path: no copies), or host
+objects (reference ``Tensor``, numpy, CPU torch) which are copied to the GPU
+and whose results come back as reference-style host objects.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from enum import Enum
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dpcore import DPConfig
+from .errors import OrderingFault, ShapeError, UsageError
+from .memmodel import B200_SPEC, MemSpec, TrafficReport, ledger
+from .tensor import Tensor
+from .tiling import BlockPlan, LayerDims, check_plan, plan_blocks
+
+
+class WorkflowKind(Enum):
+    NON_DP = "non_dp"
+    EXPLICIT_DP = "explicit_dp"
+    IMPLICIT_DP = "implicit_dp"
+    FLASHDP = "flashdp"
+
+
+@dataclass
+class BackwardResult:
+    grad_w: object             # torch (D,P) fp32 on the GPU, or Tensor for host callers
+    report: TrafficReport      # closed-form ledger of the workflow (memmodel.ledger)
+    per_sample_norms_sq: object  # torch (B,) fp32, or np.ndarray for host callers
+
+
+# ---------------------------------------------------------------- workspaces
+
+class _WorkspacePool:
+    """One zero-initialised device workspace per (device, stream); grows on demand.
+
+    The kernels leave their counters zeroed, so a workspace is reused without a
+    memset; distinct streams get distinct workspaces (include/fdp.h)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._bufs: dict = {}
+
+    def get(self, nbytes: int, device: torch.device, stream: torch.cuda.Stream) -> torch.Tensor:
+        key = (device.index, stream.cuda_stream)
+        with self._lock:
+            buf = self._bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.zeros(max(nbytes, 4096), dtype=torch.uint8, device=device)
+                self._bufs[key] = buf
+            return buf
+
+
+_POOL = _WorkspacePool()
+
+
+def _dims(x, dy) -> LayerDims:
+    xs, ys = tuple(x.shape), tuple(dy.shape)
+    if len(xs) != 3 or len(ys) != 3:
+        raise ShapeError(f"expected (B,T,P) and (B,T,D), got {xs} and {ys}")
+    if xs[0] != ys[0] or xs[1] != ys[1]:
+        raise ShapeError(f"batch/time extents differ: {xs} vs {ys}")
+    return LayerDims(B=xs[0], T=xs[1], P=xs[2], D=ys[2])
+
+
+def _to_device(t, dtype, device) -> tuple[torch.Tensor, bool]:
+    """-> (contiguous device tensor, came_from_host)."""
+    if isinstance(t, torch.Tensor) and t.is_cuda:
+        if dtype is not None and t.dtype != dtype:
+            t = t.to(dtype)
+        return t.contiguous(), False
+    if isinstance(t, Tensor):
+        arr = t.array
+    elif isinstance(t, torch.Tensor):
+        arr = t.detach().numpy()
+    else:
+        arr = np.asarray(t)
+    host = torch.from_numpy(np.ascontiguousarray(arr))
+    target = dtype if dtype is not None else (torch.bfloat16 if host.dtype == torch.bfloat16 else torch.float32)
+    return host.to(device=device, dtype=target, non_blocking=False).contiguous(), True
+
+
+def _input_dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.DTYPE_BF16
+    if t.dtype == torch.float32:
+        return _lib.DTYPE_F32
+    raise UsageError(f"inputs must be bfloat16 or float32 on the device, got {t.dtype}")
+
+
+def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemSpec], plan: Optional[BlockPlan], *,
+         path: str = "auto", noise_impl: str = "keyed_f32", dtype: Optional[torch.dtype] = None,
+         grad_out: Optional[torch.Tensor] = None, norms_out: Optional[torch.Tensor] = None,
+         accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
+         skip_barrier: bool = False, short_timeout: bool = False) -> BackwardResult:
+    dims = _dims(x, dy)
+    if kind != WorkflowKind.NON_DP and cfg is None:
+        raise UsageError("DP workflows need a DPConfig")
+    device = x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    xd, host_x = _to_device(x, dtype, device)
+    yd, host_y = _to_device(dy, xd.dtype, device)
+    host = host_x or host_y
+    if xd.dtype != yd.dtype:
+        raise UsageError(f"x and dy must share a dtype, got {xd.dtype} and {yd.dtype}")
+    in_dtype = _input_dtype_code(xd)
+
+    c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
+    flags = (_lib.FLAG_SKIP_BARRIER if skip_barrier else 0) | (_lib.FLAG_TIMEOUT_SHORT if short_timeout else 0)
+    desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=in_dtype, reduction=c.reduction,
+                          clip_c=c.clip_c, sigma=c.sigma, seed=c.seed, layer_id=c.layer_id, step=c.step, rank=rank,
+                          world=world, mean_batch=mean_batch, accumulate=accumulate, add_noise=add_noise,
+                          noise_impl=noise_impl, path=path, flags=flags)
+    lib = _lib.load()
+    k = _lib.KIND[kind.value]
+    ws_bytes = ctypes.c_size_t()
+    _lib.check(lib.fdp_workspace_bytes(ctypes.byref(desc), k, ctypes.byref(ws_bytes)))
+
+    if grad_out is None:
+        grad = (torch.zeros if accumulate else torch.empty)((dims.D, dims.P), dtype=torch.float32, device=device)
+    else:
+        if tuple(grad_out.shape) != (dims.D, dims.P) or grad_out.dtype != torch.float32 or not grad_out.is_contiguous():
+            raise ShapeError(f"grad_out must be a contiguous float32 ({dims.D}, {dims.P}) tensor")
+        grad = grad_out
+    if kind == WorkflowKind.NON_DP:
+        norms = None
+    elif norms_out is not None:
+        norms = norms_out
+    else:
+        norms = torch.empty(dims.B, dtype=torch.float32, device=device)
+
+    stream = torch.cuda.current_stream(device)
+    ws = _POOL.get(ws_bytes.value, device, stream)
+    rc = lib.fdp_backward(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                          norms.data_ptr() if norms is not None else None, ws.data_ptr(), ws.numel(),
+                          stream.cuda_stream)
+    _lib.check(rc)
+
+    if skip_barrier:
+        # The kernel records whether a clip read the norm accumulator before every
+        # tile had published (device fault word, workspace word 1).
+        word = ws[4:8].view(torch.int32)
+        fault = int(word.item())
+        word.zero_()
+        if fault & 0x200:
+            raise OrderingFault("clip read the per-sample norm accumulator before the block-wise all-reduce "
+                                "completed (barrier skipped)")
+
+    wplan = plan
+    if kind == WorkflowKind.FLASHDP and wplan is None:
+        wplan = plan_blocks(dims, spec or B200_SPEC)
+    width = (spec or B200_SPEC).dtype_width_bytes
+    report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)
+
+    if host:
+        g_host = Tensor((dims.D, dims.P), grad.double().cpu().numpy())
+        n_host = norms.double().cpu().numpy() if norms is not None else np.zeros(0)
+        return BackwardResult(g_host, report, n_host)
+    return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device))
+
+
+def backward_nondp(x, dy, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:
+    """grad_w = sum_b sum_t dY^T X; no per-sample quantity (workflows.py:121-150)."""
+    return _run(WorkflowKind.NON_DP, x, dy, None, spec, None, **opts)
+
+
+def backward_explicit(x, dy, cfg: DPConfig, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:
+    """Opacus-style: materialise G, norms, clip into G', sum + noise (workflows.py:156-240)."""
+    return _run(WorkflowKind.EXPLICIT_DP, x, dy, cfg, spec, None, **opts)
+
+
+def backward_implicit(x, dy, cfg: DPConfig, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:
+    """Norm pass, then recompute + clip + sum + noise (workflows.py:246-324)."""
+    return _run(WorkflowKind.IMPLICIT_DP, x, dy, cfg, spec, None, **opts)
+
+
+def backward_flashdp(x, dy, cfg: DPConfig, plan: Optional[BlockPlan] = None, spec: Optional[MemSpec] = None, *,
+                     sim=None, skip_barrier: bool = False, **opts) -> BackwardResult:
+    """Fused DP backward (workflows.py:340-421), one sm_100a launch on the fused path.
+
+    ``plan`` is validated against the extents (UsageError, workflows.py:330-337)
+    and recorded in the ledger; the device tiling is fixed by the tcgen05 shape.
+    ``skip_barrier=True`` removes the in-kernel wait of the norm all-reduce and
+    delays one CTA; the kernel detects the premature read and the call raises
+    ``OrderingFault`` like the reference simulator."""
+    dims = _dims(x, dy)
+    if plan is not None:
+        check_plan(plan, dims)
+    if skip_barrier:
+        opts.setdefault("path", "fused")
+    return _run(WorkflowKind.FLASHDP, x, dy, cfg, spec, plan, skip_barrier=skip_barrier, **opts)
+
+
+def run_backward(kind: WorkflowKind, x, dy, cfg: DPConfig, spec: Optional[MemSpec] = None,
+                 plan: Optional[BlockPlan] = None, *, sim=None, **opts) -> BackwardResult:
+    """Run one workflow; flashdp derives a block plan if none is given (workflows.py:427-440)."""
+    if kind == WorkflowKind.NON_DP:
+        return backward_nondp(x, dy, spec, **opts)
+    if kind == WorkflowKind.EXPLICIT_DP:
+        return backward_explicit(x, dy, cfg, spec, **opts)
+    if kind == WorkflowKind.IMPLICIT_DP:
+        return backward_implicit(x, dy, cfg, spec, **opts)
+    if kind == WorkflowKind.FLASHDP:
+        return backward_flashdp(x, dy, cfg, plan, spec, **opts)
+    raise UsageError(f"unknown workflow kind {kind!r}")
+
+
+def execution_plan(x_shape, dy_shape, kind: WorkflowKind = WorkflowKind.FLASHDP, *, dtype=torch.bfloat16,
+                   path: str = "auto") -> dict:
+    """The device plan the native layer will take (path, tiles, groups, grid, workspace)."""
+    B, T, P = x_shape
+    D = dy_shape[2]
+    desc = _lib.make_desc(B=B, T=T, P=P, D=D, in_dtype=_lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F32,
+                          path=path)
+    info = _lib.plan(desc, kind.value)
+    return {"path": _lib.PATH_NAMES[info.path], "tile_d": info.tile_d, "tile_p": info.tile_p, "tile_t": info.tile_t,
+            "n_d": info.n_d, "n_p": info.n_p, "groups": info.groups, "grid": info.grid, "launches": info.launches,
+            "sms": info.sms, "workspace_bytes": info.workspace_bytes}
