@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the FlashDP hot path on B200: the fused per-layer DP-SGD
+weight-gradient backward of every linear layer of GPT-2 small.
+
+A "step" is one pass of the hot path over one batch of synthetic activations:
+for each of the 48 linear layers of GPT-2 small (12 blocks x c_attn 768->2304,
+attn c_proj 768->768, mlp c_fc 768->3072, mlp c_proj 3072->768) the DP weight
+gradient  mean_b clip_C(dY_b^T X_b) + sigma*C*N(seed, layer, step, idx)  with
+per-sample per-layer clipping (reference workflows.py:340-421), at B=8
+sequences x T=1024 tokens, bf16 inputs, fp32 accumulate/output.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 (under torchrun): data parallel over ranks, weak scaling (B=8 per rank);
+each rank adds noise only on its slice of every layer's index space and the
+clipped sums are summed with one NCCL all-reduce per step.
+
+Prints ONE JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GPT2_LAYERS = [("c_attn", 768, 2304), ("attn_proj", 768, 768), ("c_fc", 768, 3072), ("mlp_proj", 3072, 768)]
+N_BLOCKS = 12
+METRIC = "DP-train tokens/sec + % of non-DP at 1/2/4/8 B200; fused DP-linear TFLOP/s vs peak"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--seq", type=int, default=1024)
+    ap.add_argument("--clip", type=float, default=1.0)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--noise", default="keyed_f32", choices=["keyed_f32", "keyed_f64", "philox"])
+    ap.add_argument("--path", default="auto")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-nondp", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
+    return ap.parse_args()
+
+
+def layer_list():
+    out = []
+    for blk in range(N_BLOCKS):
+        for j, (name, P, D) in enumerate(GPT2_LAYERS):
+            out.append((blk * len(GPT2_LAYERS) + j, f"h{blk}.{name}", P, D))
+    return out
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ----------------------------------------------------------------------------- reference (CPU) arm
+
+def time_cpu_layer(j: int, B: int, T: int, sigma: float, clip: float, n_seq: int = 1) -> float:
+    """Seconds the oracle port (numpy float64, BLAS threads) needs for layer type
+    j of one block at the full batch: per-sample work (G_b, norm, clip,
+    accumulate) timed on `n_seq` sequences and scaled to B (it is linear in B),
+    finalize (mean + keyed noise over D*P) timed once, as in the full step."""
+    import numpy as np
+
+    from oracle import dp_oracle as O
+
+    _, P, D = GPT2_LAYERS[j]
+    rng = np.random.default_rng(j)
+    x = rng.standard_normal((n_seq, T, P)).astype(np.float32)
+    dy = (rng.standard_normal((n_seq, T, D)) * 1e-3).astype(np.float32)
+    cfg = O.Cfg(clip, sigma, "mean", 1234, j, 0)
+    t0 = time.perf_counter()
+    acc, _ = O.per_sample_accumulate(x, dy, clip)
+    t1 = time.perf_counter()
+    O.finalize(acc, B, cfg, exact_noise=False)
+    t2 = time.perf_counter()
+    return (t1 - t0) * (B / n_seq) + (t2 - t1)
+
+
+def cpu_sample_desc(B: int, n_seq: int = 1) -> str:
+    return (f"oracle/dp_oracle.py numpy float64 (reference backward_flashdp arithmetic) on the host's BLAS threads: "
+            f"each step times one of the 4 GPT-2 layer types in rotation (per-sample work on {n_seq} of {B} "
+            f"sequences x{B // n_seq}, finalize+noise once), x{4 * N_BLOCKS} to the 48-layer step")
+
+
+def run_reference_arm(a, rank: int, world: int):
+    if rank != 0:
+        return
+    B, T = a.batch, a.seq
+    tokens_per_step = B * T  # one rank's workload (the metric is per-N aggregate; the CPU arm runs once)
+    per = []
+    steps = max(4, (a.steps + 3) // 4 * 4)  # whole rotations over the 4 layer types
+    for i in range(a.warmup + steps):
+        s = time_cpu_layer(i % 4, B, T, a.sigma, a.clip)
+        if i >= a.warmup:
+            per.append(s * 4 * N_BLOCKS)
+    step_s = statistics.mean(per)
+    sample = cpu_sample_desc(B)
+    value = tokens_per_step / step_s
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "gpt2-small 48 DP linear layers, weight-gradient backward", "global_batch": B,
+                       "seq_len": T, "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import torch
+    import torch.distributed as dist
+
+    if a.impl == "reference":
+        if world > 1:
+            dist.init_process_group("gloo")
+        run_reference_arm(a, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2507_01154_b200 as fdp
+
+    B, T = a.batch, a.seq
+    layers = layer_list()
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    xs, dys = {}, {}
+    for _, name, P, D in layers:
+        # activations O(1), upstream gradients small (typical backward magnitudes)
+        xs[name] = torch.randn(B, T, P, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+        dys[name] = (torch.randn(B, T, D, device=dev, generator=g, dtype=torch.float32) * 1e-3).to(torch.bfloat16)
+    n_params = sum(P * D for _, _, P, D in layers)
+    flat = torch.zeros(n_params, dtype=torch.float32, device=dev)
+    device_step = torch.zeros(1, dtype=torch.int64, device=dev)
+    calls, off = [], 0
+    global_B = B * world
+    # one workspace shared by all layers (they run in order on one stream)
+    shared_ws = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    for lid, name, P, D in layers:
+        grad = flat[off:off + P * D].view(D, P)
+        off += P * D
+        cfg = fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234, layer_id=lid, step=0)
+        c = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, xs[name], dys[name], cfg, grad_w=grad, path=a.path,
+                                 noise_impl=a.noise, rank=rank, world=world, mean_batch=global_B,
+                                 device_step=device_step, workspace=shared_ws)
+        calls.append((name, c))
+    plans = {n: c.plan for n, c in calls[:4]}
+
+    stream = torch.cuda.current_stream(dev)
+    dominant = "h0.c_fc"  # largest per-launch work; every block's c_fc is timed
+    dom_events = []
+
+    def step(record=False):
+        for name, c in calls:
+            if record and name.endswith(".c_fc"):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                c(stream)
+                e1.record(stream)
+                dom_events.append((e0, e1))
+            else:
+                c(stream)
+        device_step.add_(1)
+        if world > 1:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+
+    graph = None
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if a.graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0e.record(stream)
+    for _ in range(a.steps):
+        if graph is not None:
+            graph.replay()
+        else:
+            step(record=True)
+    t1e.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t0e.elapsed_time(t1e)
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    ms_per_step = elapsed_ms / a.steps
+    tokens_per_step = global_B * T
+    value = tokens_per_step / (ms_per_step * 1e-3)
+    flops_per_step_rank = sum(2 * B * T * P * D for _, _, P, D in layers)
+
+    # dominant kernel: fused DP-dW launch of the c_fc layers, CUDA events on the launch stream
+    dom_ms = [e0.elapsed_time(e1) for e0, e1 in dom_events] if dom_events else []
+    dom_flops = 2 * B * T * 768 * 3072
+    peaks, peak_kind = load_peaks()
+    dom_avg_s = (statistics.mean(dom_ms) * 1e-3) if dom_ms else None
+    achieved = dom_flops / dom_avg_s / 1e12 if dom_avg_s else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("fused_c_fc_dram_bytes")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": (achieved / peaks["bf16_tflops"]) if achieved else None, "traffic": traffic,
+                "peak_source": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
+                "frac_of_sustained": (achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+                if achieved else None,
+                "kernel": "dpdw_tc_kernel (MODE_FUSED) on c_fc: B=%d T=%d P=768 D=3072" % (B, T),
+                "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_avg_s * 1e3 if dom_avg_s else None,
+                "launches_timed": len(dom_ms)}
+
+    extra = {}
+    # ---- non-DP baseline (same layers, plain bf16 dW GEMM): cuBLAS and our tcgen05 kernel
+    if not a.no_nondp:
+        def nondp_cublas():
+            for _, name, P, D in layers:
+                x2 = xs[name].view(-1, P)
+                y2 = dys[name].view(-1, D)
+                torch.mm(y2.t(), x2, out_dtype=torch.float32)
+
+        nd_calls = [fdp.PreparedBackward(fdp.WorkflowKind.NON_DP, xs[n], dys[n], None, grad_w=c.grad_w)
+                    for n, c in calls]
+
+        def nondp_ours():
+            for c in nd_calls:
+                c(stream)
+
+        def timeit(fn, n):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / n
+
+        try:
+            nd_ms = timeit(nondp_cublas, max(10, a.steps // 4))
+        except Exception as e:  # noqa: BLE001
+            nd_ms = None
+            extra["nondp_cublas_error"] = repr(e)[:200]
+        nd_ours_ms = timeit(nondp_ours, max(10, a.steps // 4))
+        extra["nondp"] = {
+            "cublas_ms_per_step": nd_ms, "tcgen05_nondp_ms_per_step": nd_ours_ms,
+            "dp_over_nondp_pct_vs_cublas": (100.0 * nd_ms / ms_per_step) if nd_ms else None,
+            "dp_over_nondp_pct_vs_own": 100.0 * nd_ours_ms / ms_per_step,
+            "nondp_tflops_cublas": flops_per_step_rank / (nd_ms * 1e-3) / 1e12 if nd_ms else None,
+        }
+        # restore DP grads (non-DP calls overwrote them); not part of any timing
+        for _ in range(1):
+            step()
+        torch.cuda.synchronize()
+
+    # ---- end to end through the public API with host buffers (H2D in, D2H out)
+    e2e = None
+    if not a.no_e2e:
+        host = {}
+        for _, name, P, D in layers[:4]:
+            host[name.split(".")[1]] = (xs[name].cpu().pin_memory(), dys[name].cpu().pin_memory())
+        h2d = sum(B * T * (P + D) * 2 for _, _, P, D in layers)
+        d2h = sum(P * D * 4 + B * 4 for _, _, P, D in layers)
+
+        def e2e_step(step_idx):
+            for lid, name, P, D in layers:
+                xh, yh = host[name.split(".")[1]]
+                cfg = fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234, layer_id=lid,
+                                   step=step_idx)
+                res = fdp.run_backward(fdp.WorkflowKind.FLASHDP, xh, yh, cfg, rank=rank, world=world,
+                                       mean_batch=global_B, noise_impl=a.noise)
+                assert res.grad_w.device.type == "cpu"
+
+        e2e_step(0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(a.e2e_steps):
+            e2e_step(i + 1)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / a.e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": tokens_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_s * 1e3,
+               "api": "paper_2507_01154_b200.run_backward(WorkflowKind.FLASHDP, pinned host bf16 X/dY) per layer"}
+
+    # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
+    cpu = None
+    if not a.no_cpu and world == 1 and rank == 0:
+        s = sum(time_cpu_layer(j, B, T, a.sigma, a.clip) for j in range(4)) * N_BLOCKS
+        cpu = {"value": tokens_per_step / s, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": cpu_sample_desc(B).replace("each step times one of the 4 GPT-2 layer types in rotation",
+                                                    "one pass over the 4 GPT-2 layer types")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "gpt2-small: DP weight-gradient backward of all 48 linear layers "
+                                   "(per-sample per-layer clip, mean, keyed noise)",
+                       "global_batch": global_B, "seq_len": T, "parallelism": f"dp{world}",
+                       "clip_c": a.clip, "sigma": a.sigma, "noise": a.noise,
+                       "l2": "inputs larger than L2 (%.2f GB of X/dY per rank per step)" % (
+                           sum(B * T * (P + D) * 2 for _, _, P, D in layers) / 1e9),
+                       "graph": bool(graph is not None)},
+            "tflops_per_gpu": flops_per_step_rank / (ms_per_step * 1e-3) / 1e12,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": (len(calls) * a.steps),
+            "plans": {k: {"path": fdp._lib.PATH_NAMES[v.path], "tile": [v.tile_d, v.tile_p], "groups": v.groups,
+                          "grid": v.grid} for k, v in plans.items()},
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,7 +92,11 @@ enum fdp_path { FDP_PATH_AUTO = 0, FDP_PATH_FUSED = 1, FDP_PATH_TWO_PHASE = 2, F
 /* Debug flags. SKIP_BARRIER removes the in-kernel norm barrier wait (the
  * analogue of backward_flashdp(skip_barrier=True), workflows.py:341,394) and
  * delays one CTA so the premature clip is observable. */
-enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2 };
+enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2,
+                 /* record per-CTA phase timestamps (%globaltimer, ns) of the fused kernel
+                    in the workspace tail: grid x 128 uint64 after fdp_plan_info.workspace_bytes
+                    minus grid*1024 bytes (see paper_2507_01154_b200/trace.py) */
+                 FDP_FLAG_TRACE = 4 };
 
 /* Norm phase of the TWO_PHASE path. */
 enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2 };
@@ -116,6 +120,9 @@ typedef struct fdp_desc {
   int32_t path;             /* fdp_path                                       */
   int32_t flags;            /* fdp_flags                                      */
   int32_t norm_phase;       /* fdp_norm_phase                                 */
+  const int64_t* device_step; /* optional DEVICE pointer: when non-NULL the noise
+                               key uses *device_step instead of `step`, so a
+                               captured CUDA graph draws fresh noise per replay */
 } fdp_desc;
 
 /* Plan actually taken for a descriptor (analogue of tiling.BlockPlan,

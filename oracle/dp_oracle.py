@@ -184,6 +184,19 @@ def dp_backward_streaming(x: np.ndarray, dy: np.ndarray, cfg: Cfg, exact_noise: 
     return finalize(acc, B, cfg, exact_noise), norms
 
 
+def per_sample_accumulate(x: np.ndarray, dy: np.ndarray, clip_c: float, scale: float = 1.0):
+    """Per-sample G_b, norm, clip, accumulate (workflows.py:381-407 with whole-layer
+    blocks); no finalize. Returns (acc (D,P), norms (B,))."""
+    B = x.shape[0]
+    acc = np.zeros((dy.shape[2], x.shape[2]))
+    norms = np.zeros(B)
+    for b in range(B):
+        gb = np.asarray(dy[b], dtype=np.float64).T @ np.asarray(x[b], dtype=np.float64)
+        norms[b] = float(np.einsum("dp,dp->", gb, gb))
+        acc += (clip_factor(norms[b], clip_c) * scale) * gb
+    return acc, norms
+
+
 def nondp_backward(x: np.ndarray, dy: np.ndarray) -> np.ndarray:
     """workflows.py:121-150."""
     return per_sample_grads(x, dy).sum(axis=0)

@@ -44,6 +44,7 @@ class FdpDesc(ctypes.Structure):
         ("accumulate", ctypes.c_int32), ("add_noise", ctypes.c_int32),
         ("noise_impl", ctypes.c_int32), ("path", ctypes.c_int32),
         ("flags", ctypes.c_int32), ("norm_phase", ctypes.c_int32),
+        ("device_step", ctypes.c_void_p),
     ]
 
 
@@ -114,7 +115,7 @@ def check(rc: int) -> None:
 
 def make_desc(*, B, T, P, D, in_dtype=DTYPE_BF16, reduction="sum", clip_c=1.0, sigma=0.0, seed=0, layer_id=0,
               step=0, rank=0, world=1, mean_batch=0, accumulate=False, add_noise=True, noise_impl="keyed_f32",
-              path="auto", flags=0, norm_phase=0) -> FdpDesc:
+              path="auto", flags=0, norm_phase=0, device_step=None) -> FdpDesc:
     if reduction not in REDUCE:
         raise UsageError(f"reduction must be one of {tuple(REDUCE)}, got {reduction!r}")
     if noise_impl not in NOISE:
@@ -125,7 +126,7 @@ def make_desc(*, B, T, P, D, in_dtype=DTYPE_BF16, reduction="sum", clip_c=1.0, s
                    sigma=float(sigma), seed=_wrap64(seed), layer_id=_wrap64(layer_id), step=_wrap64(step),
                    rank=rank, world=world, mean_batch=mean_batch, accumulate=int(bool(accumulate)),
                    add_noise=int(bool(add_noise)), noise_impl=NOISE[noise_impl], path=PATH[path], flags=flags,
-                   norm_phase=norm_phase)
+                   norm_phase=norm_phase, device_step=device_step)
 
 
 def plan(desc: FdpDesc, kind: str) -> FdpPlanInfo:

@@ -32,12 +32,9 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 // ---- reference key construction (rng.py:35-47), host side
-constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+using fdp::kGamma;
 uint64_t absorb3(int64_t seed, int64_t layer, int64_t step) {
-  uint64_t h = fdp::mix64(static_cast<uint64_t>(seed));
-  h = fdp::mix64((h + kGamma) ^ static_cast<uint64_t>(layer));
-  h = fdp::mix64((h + kGamma) ^ static_cast<uint64_t>(step));
-  return h;
+  return fdp::absorb3(static_cast<uint64_t>(seed), static_cast<uint64_t>(layer), static_cast<uint64_t>(step));
 }
 
 struct DevInfo {
@@ -261,7 +258,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   off = align_up(off + 4 * B, 256);
   pl.off_acc = off;
   if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED && pl.groups > 1)
-    off = align_up(off + 4ull * (pl.groups - 1) * pl.n_tiles * fdp::kBM * pl.bn, 256);
+    off = align_up(off + 4ull * pl.groups * pl.n_tiles * fdp::kBM * pl.bn, 256);
   pl.off_g = off;
   pl.off_gp = off;
   if (kind == FDP_KIND_EXPLICIT_DP) {
@@ -269,6 +266,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     pl.off_gp = align_up(off + gbytes, 256);
     off = align_up(pl.off_gp + gbytes, 256);
   }
+  if (d->flags & FDP_FLAG_TRACE) off = align_up(off, 256) + 1024ull * (pl.grid > 0 ? pl.grid : 1);
   pl.total = off;
   return FDP_OK;
 }
@@ -322,6 +320,9 @@ fdp::SimtParams simt_params(const fdp_desc* d, const Plan& pl, const Common& c, 
   s.noise_scale = c.noise_scale;
   s.key_base = c.key_base;
   s.key_base_g = c.key_base_g;
+  s.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+  s.seed_u = static_cast<uint64_t>(d->seed);
+  s.layer_u = static_cast<uint64_t>(d->layer_id);
   s.noise_lo = c.noise_lo;
   s.noise_hi = c.noise_hi;
   s.grad_w = grad_w;
@@ -354,6 +355,9 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.noise_scale = c.noise_scale;
   p.key_base = c.key_base;
   p.key_base_g = c.key_base_g;
+  p.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+  p.seed_u = static_cast<uint64_t>(d->seed);
+  p.layer_u = static_cast<uint64_t>(d->layer_id);
   p.noise_lo = c.noise_lo;
   p.noise_hi = c.noise_hi;
   p.grad_w = grad_w;
@@ -367,6 +371,7 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.ws_acc = ws_at<float>(ws, pl.off_acc);
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+  p.trace = (d->flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, pl.total - 1024ull * pl.grid) : nullptr;
   return p;
 }
 

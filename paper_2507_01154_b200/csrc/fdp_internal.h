@@ -10,7 +10,8 @@ namespace fdp {
 constexpr int kBM = 128;  // d rows per output tile (UMMA M, one TMEM lane per row)
 constexpr int kBK = 64;   // t extent of one pipeline stage (4 x UMMA K=16)
 constexpr int kEpiWarps = 8;
-constexpr int kTcThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warps 2..9 epilogue
+constexpr int kEpiWarp0 = 4;                        // warpgroup 0: TMA, MMA, 2 spare warps
+constexpr int kTcThreads = 32 * kEpiWarp0 + 32 * kEpiWarps;  // warpgroups 1-2: epilogue
 
 enum TcMode : int {
   MODE_FUSED = 0,     // per-sample G tile -> norm all-reduce + grid barrier -> clip -> sum -> noise
@@ -35,6 +36,8 @@ struct TcParams {
   float noise_scale;
   uint64_t key_base;    // absorb(seed, layer_id, step)
   uint64_t key_base_g;  // key_base + GAMMA
+  const long long* step_ptr;  // device step counter (nullptr: use key_base)
+  uint64_t seed_u, layer_u;
   long long noise_lo, noise_hi;
   float* grad_w;
   float* norms_out;
@@ -47,6 +50,7 @@ struct TcParams {
   float* ws_acc;           // [(groups-1)][n_tiles][kBM*BN]
   int skip_barrier;
   unsigned long long budget_ns;
+  unsigned long long* trace;  // [grid][128] phase timestamps or nullptr
 };
 
 // Launch the tcgen05 kernel (BN = 128 or 256). cooperative=true for MODE_FUSED.
@@ -70,6 +74,8 @@ struct SimtParams {
   int noise_impl;
   float noise_scale;
   uint64_t key_base, key_base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
   long long noise_lo, noise_hi;
   float* grad_w;
   float* norms_out;

@@ -37,7 +37,7 @@ __device__ __forceinline__ float keyed_normal_f32(uint64_t base_g, uint64_t idx)
 }
 
 // Reference-keyed draw in fp64 (libdevice log/cos are within ~1 ulp of libm).
-__device__ __forceinline__ double keyed_normal_f64(uint64_t base_g, uint64_t idx) {
+static __device__ __noinline__ double keyed_normal_f64(uint64_t base_g, uint64_t idx) {
   const uint64_t h = mix64(base_g ^ idx);
   const uint64_t w1 = mix64(h ^ kSaltA) >> 11;
   const uint64_t w2 = mix64(h ^ kSaltB) >> 11;
@@ -62,12 +62,37 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
   }
 }
 
-__device__ __forceinline__ float philox_normal(uint64_t base, uint64_t idx) {
-  uint32_t c[4] = {static_cast<uint32_t>(idx), static_cast<uint32_t>(idx >> 32), 0x44504E5Au, 0u};
+// Philox noise: flat indices are grouped in aligned blocks of 4; block g uses
+// one Philox4x32-10 call (counter = g) whose 4 words feed two Box-Muller pairs
+// (cos and sin branches). u1 = (w + 1) 2^-32 in (0, 1], u2 = w 2^-32.
+__device__ __forceinline__ float4 philox_normal4(uint64_t base, uint64_t block) {
+  uint32_t c[4] = {static_cast<uint32_t>(block), static_cast<uint32_t>(block >> 32), 0x44504E5Au, 0u};
   philox4x32_10(c, static_cast<uint32_t>(base), static_cast<uint32_t>(base >> 32));
-  const float u1 = (static_cast<float>(c[0] >> 8) + 1.0f) * 0x1p-24f;  // (0, 1]
-  const float u2 = static_cast<float>(c[1] >> 8) * 0x1p-24f;           // [0, 1)
-  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  const float r0 = sqrtf(-2.0f * logf((__uint2float_rn(c[0]) + 1.0f) * 0x1p-32f));
+  const float r1 = sqrtf(-2.0f * logf((__uint2float_rn(c[2]) + 1.0f) * 0x1p-32f));
+  float s0, c0, s1, c1;
+  sincospif(__uint2float_rn(c[1]) * 0x1p-31f, &s0, &c0);
+  sincospif(__uint2float_rn(c[3]) * 0x1p-31f, &s1, &c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
+__device__ __forceinline__ float philox_normal(uint64_t base, uint64_t idx) {
+  const float4 v = philox_normal4(base, idx >> 2);
+  switch (idx & 3) {
+    case 0: return v.x;
+    case 1: return v.y;
+    case 2: return v.z;
+    default: return v.w;
+  }
+}
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+// absorb(seed, layer_id, step) of rng.py:42-47 (device side, for device step counters)
+__host__ __device__ __forceinline__ uint64_t absorb3(uint64_t seed, uint64_t layer, uint64_t step) {
+  uint64_t h = mix64(seed);
+  h = mix64((h + kGamma) ^ layer);
+  return mix64((h + kGamma) ^ step);
 }
 
 // impl: 0 keyed f32, 1 keyed f64, 2 philox. `base_g` = absorb(...) + GAMMA,
@@ -76,6 +101,17 @@ __device__ __forceinline__ float noise_draw(int impl, uint64_t base_g, uint64_t 
   if (impl == 2) return philox_normal(base, idx);
   if (impl == 1) return static_cast<float>(keyed_normal_f64(base_g, idx));
   return keyed_normal_f32(base_g, idx);
+}
+
+// Draws for the 4 consecutive flat indices idx4*4 .. idx4*4+3.
+__device__ __forceinline__ float4 noise_draw4(int impl, uint64_t base_g, uint64_t base, uint64_t idx4) {
+  if (impl == 2) return philox_normal4(base, idx4);
+  const uint64_t i0 = idx4 << 2;
+  if (impl == 1)
+    return make_float4(static_cast<float>(keyed_normal_f64(base_g, i0)), static_cast<float>(keyed_normal_f64(base_g, i0 + 1)),
+                       static_cast<float>(keyed_normal_f64(base_g, i0 + 2)), static_cast<float>(keyed_normal_f64(base_g, i0 + 3)));
+  return make_float4(keyed_normal_f32(base_g, i0), keyed_normal_f32(base_g, i0 + 1), keyed_normal_f32(base_g, i0 + 2),
+                     keyed_normal_f32(base_g, i0 + 3));
 }
 
 }  // namespace fdp

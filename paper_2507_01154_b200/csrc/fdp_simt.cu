@@ -87,7 +87,12 @@ __global__ void k_reduce_norms(const float* part, int B, int n_tiles, double cli
 }
 
 __device__ __forceinline__ float draw(const SimtParams& p, long long flat) {
-  return noise_draw(p.noise_impl, p.key_base_g, p.key_base, static_cast<uint64_t>(flat));
+  uint64_t kb = p.key_base, kbg = p.key_base_g;
+  if (p.step_ptr) {
+    kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
+    kbg = kb + kGamma;
+  }
+  return noise_draw(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat));
 }
 
 __global__ void __launch_bounds__(256) k_weighted_sum(const SimtParams p) {

@@ -41,6 +41,11 @@ struct TcCfg {
   static constexpr uint32_t kIdesc = make_idesc_bf16_mn(kBM, BN);
 };
 
+#define FDP_TRACE(slot)                                                           \
+  do {                                                                            \
+    if (p.trace && etid == 0 && (slot) < 128) p.trace[blockIdx.x * 128 + (slot)] = globaltimer_ns(); \
+  } while (0)
+
 template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     dpdw_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
@@ -54,7 +59,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tempty = tfull + C::kNBuf;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps]
-  volatile float* bcast = red + kEpiWarps;                  // [1]
+  float* bcast = red + kEpiWarps;                           // [1] (ordered by named barriers)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -79,6 +84,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+
+  // Register budget: the TMA/MMA warpgroup needs few registers, the epilogue
+  // warpgroups hold BN/2 fp32 accumulators per thread.
+#if FDP_SETMAXNREG
+  if (warp < kEpiWarp0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+  }
+#endif
 
   // ---- work assignment
   const bool fused = p.mode == MODE_FUSED;
@@ -157,15 +172,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp >= kEpiWarp0) {
     // ======================= epilogue (8 warps) =======================
-    const int ew = warp - 2;
+    const int ew = warp - kEpiWarp0;
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int half = ew >> 2;            // column half
     const int etid = ew * 32 + lane;     // 0..255
     const int row = q * 32 + lane;       // tile-local d
     const int col0 = half * C::kCPT;     // tile-local first p
     uint32_t buf = 0, tphase = 0;
+
+    const bool dp_sum = p.mode == MODE_FUSED || p.mode == MODE_REWEIGHT;
+    uint64_t kb = p.key_base, kbg = p.key_base_g;
+    if (p.step_ptr) {
+      kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
+      kbg = kb + kGamma;
+    }
+    const bool reduce_scatter = fused && p.groups > 1;
+    // noise is pre-written into grad_w in chunks while the MMA of the next
+    // sample runs (single-group tiles); with sample groups it is drawn in the
+    // reduce-scatter phase, split across the group's CTAs.
+    const bool pre_noise = dp_sum && p.add_noise;
+    const bool rmw_store = pre_noise || p.accumulate;
+    const int n_units = per_sample ? (p.B - b0 + b_step - 1) / b_step : 1;
+    // rows of the tile this CTA finalizes (its reduce-scatter slice with sample groups)
+    const int own_r0 = reduce_scatter ? group * kBM / p.groups : 0;
+    const int own_r1 = reduce_scatter ? (group + 1) * kBM / p.groups : kBM;
 
     for (int tile = first_tile; tile < p.n_tiles; tile += tile_stride) {
       const int d0 = (tile / p.n_pt) * kBM;
@@ -175,9 +207,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
 
-      for (int ub = b0; ub < p.B; ub += unit_step) {
+      int unit = 0;
+      FDP_TRACE(0);
+      for (int ub = b0; ub < p.B; ub += unit_step, ++unit) {
+        if (pre_noise) {
+          // chunk `unit` of this CTA's noise, drawn while the MMA of sample `ub`
+          // runs: grad_w = (accumulate ? grad_w : 0) + sigma*C*n(flat), 4 at a time
+          // (P % 8 == 0: a float4 never straddles a row or the tile edge).
+          const int q_all = (own_r1 - own_r0) * (BN / 4);
+          const int q_lo = static_cast<int>((static_cast<long long>(unit) * q_all) / n_units);
+          const int q_hi = static_cast<int>((static_cast<long long>(unit + 1) * q_all) / n_units);
+          for (int e4 = q_lo + etid; e4 < q_hi; e4 += 32 * kEpiWarps) {
+            const int dd = d0 + own_r0 + e4 / (BN / 4);
+            const int pp = p0 + (e4 % (BN / 4)) * 4;
+            if (dd < p.D && pp < p.P) {
+              const long long flat = static_cast<long long>(dd) * p.P + pp;
+              float4* dst = reinterpret_cast<float4*>(p.grad_w + flat);
+              float4 v = p.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
+              if (flat + 3 >= p.noise_lo && flat < p.noise_hi) {
+                const float4 n = noise_draw4(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
+                const float s = p.noise_scale;
+                if (flat + 0 >= p.noise_lo && flat + 0 < p.noise_hi) v.x += s * n.x;
+                if (flat + 1 >= p.noise_lo && flat + 1 < p.noise_hi) v.y += s * n.y;
+                if (flat + 2 >= p.noise_lo && flat + 2 < p.noise_hi) v.z += s * n.z;
+                if (flat + 3 >= p.noise_lo && flat + 3 < p.noise_hi) v.w += s * n.w;
+              }
+              __stcg(dst, v);
+            }
+          }
+        }
+        FDP_TRACE(8 + 4 * unit);
         mbar_wait(&tfull[buf], tphase, err, p.budget_ns, 0x104);
         tc_fence_after();
+        FDP_TRACE(9 + 4 * unit);
         const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
 
         if (p.mode == MODE_NONDP || p.mode == MODE_STORE_G) {
@@ -190,11 +252,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
               for (int i = 0; i < 32; ++i) acc[c * 32 + i] = v[i];
             } else if (d < p.D) {
-              float* dst = p.g_out + (static_cast<long long>(ub) * p.D + d) * p.P;
+              float* dst = p.g_out + (static_cast<long long>(ub) * p.D + d) * p.P + p0 + col0 + c * 32;
+              if (p0 + col0 + c * 32 + 32 <= p.P) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const int pp = p0 + col0 + c * 32 + i;
-                if (pp < p.P) dst[pp] = v[i];
+                for (int i = 0; i < 32; i += 4) __stcs(reinterpret_cast<float4*>(dst + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (p0 + col0 + c * 32 + i < p.P) dst[i] = v[i];
               }
             }
           }
@@ -266,6 +331,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             named_bar_sync(1, 32 * kEpiWarps);
             f = *bcast;
+            FDP_TRACE(10 + 4 * unit);
           }
           // ---- pass 2: clip and aggregate on chip
 #pragma unroll
@@ -283,65 +349,103 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
       }
 
+      FDP_TRACE(1);
       if (p.mode == MODE_NORMS || p.mode == MODE_STORE_G) continue;
 
-      // ---- cross-group reduction of the clipped sums (fixed order -> deterministic)
-      if (fused && p.groups > 1) {
-        float* slot0 = p.ws_acc + static_cast<long long>(tile) * (kBM * BN);
-        const long long gstride = static_cast<long long>(p.n_tiles) * (kBM * BN);
-        if (group > 0) {
-          float* slot = slot0 + (group - 1) * gstride;
+      if (reduce_scatter) {
+        // ---- reduce-scatter of the clipped sums across the tile's sample groups:
+        // every group parks its partial tile (row-major) in L2, then group g sums
+        // rows [g*BM/S, (g+1)*BM/S) of all S partials in a fixed order
+        // (deterministic), adds noise and writes them.
+        const long long tile_elems = static_cast<long long>(kBM) * BN;
+        float* slots = p.ws_acc + static_cast<long long>(tile) * p.groups * tile_elems;
+        {
+          float* mine = slots + group * tile_elems + static_cast<long long>(row) * BN + col0;
 #pragma unroll
-          for (int i = 0; i < C::kCPT; ++i) __stcg(slot + i * 256 + etid, acc[i]);
-          __threadfence();
-          named_bar_sync(1, 32 * kEpiWarps);
-          if (etid == 0) red_release_add_u32(&p.ws_tile_cnt[tile], 1u);
-          continue;
+          for (int i = 0; i < C::kCPT; i += 4)
+            __stcg(reinterpret_cast<float4*>(mine + i), make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
         }
+        __threadfence();
+        named_bar_sync(1, 32 * kEpiWarps);
         if (etid == 0) {
+          red_release_add_u32(&p.ws_tile_cnt[tile], 1u);
           const uint64_t t0 = globaltimer_ns();
-          while (ld_acquire_u32(&p.ws_tile_cnt[tile]) < static_cast<unsigned>(p.groups - 1)) {
+          while (ld_acquire_u32(&p.ws_tile_cnt[tile]) < static_cast<unsigned>(p.groups)) {
             if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x106);
             __nanosleep(64);
           }
         }
         named_bar_sync(1, 32 * kEpiWarps);
-        for (int g = 1; g < p.groups; ++g) {
-          const float* slot = slot0 + (g - 1) * gstride;
+        const int n4 = (own_r1 - own_r0) * BN / 4;
+        constexpr int kU = 4;  // float4 groups in flight per thread
+        for (int base4 = etid; base4 < n4; base4 += kU * 32 * kEpiWarps) {
+          float4 s[kU], o[kU];
+          long long off[kU], flat[kU];
+          bool ok[kU];
 #pragma unroll
-          for (int i = 0; i < C::kCPT; ++i) acc[i] += __ldcg(slot + i * 256 + etid);
+          for (int u = 0; u < kU; ++u) {
+            const int e4 = base4 + u * 32 * kEpiWarps;
+            const int r = own_r0 + (e4 * 4) / BN, c = (e4 * 4) % BN;
+            ok[u] = e4 < n4 && d0 + r < p.D && p0 + c < p.P;  // P % 8 == 0: all-in or all-out
+            off[u] = static_cast<long long>(r) * BN + c;
+            flat[u] = static_cast<long long>(d0 + r) * p.P + p0 + c;
+            s[u] = ok[u] ? __ldcg(reinterpret_cast<const float4*>(slots + off[u])) : make_float4(0.f, 0.f, 0.f, 0.f);
+            o[u] = (ok[u] && rmw_store) ? __ldcg(reinterpret_cast<const float4*>(p.grad_w + flat[u]))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int g = 1; g < p.groups; ++g) {
+            float4 t4[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+              t4[u] = ok[u] ? __ldcg(reinterpret_cast<const float4*>(slots + g * tile_elems + off[u]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              s[u].x += t4[u].x; s[u].y += t4[u].y; s[u].z += t4[u].z; s[u].w += t4[u].w;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (!ok[u]) continue;
+            // noise (and the accumulated gradient) already sit in grad_w when rmw_store
+            s[u].x += o[u].x; s[u].y += o[u].y; s[u].z += o[u].z; s[u].w += o[u].w;
+            *reinterpret_cast<float4*>(p.grad_w + flat[u]) = s[u];
+          }
         }
+        FDP_TRACE(2);
+        continue;
       }
 
-      // ---- finalize: mean is folded into the clip factor; store, then add
-      // sigma*C*noise in a coalesced sweep over the (L2-resident) tile.
-      if (d < p.D) {
-        float* dst = p.grad_w + static_cast<long long>(d) * p.P;
-#pragma unroll
-        for (int i = 0; i < C::kCPT; ++i) {
-          const int pp = p0 + col0 + i;
-          if (pp < p.P) {
-            float v = acc[i];
-            if (p.accumulate) v += dst[pp];
-            dst[pp] = v;
-          }
-        }
-      }
-      if (p.mode != MODE_NONDP && p.add_noise) {
+      // ---- finalize: mean is folded into the clip factor; the noise (if any) is
+      // already in grad_w from the pre_noise chunks.
+      if (pre_noise) {
         __threadfence_block();
         named_bar_sync(1, 32 * kEpiWarps);
-        for (int e = etid; e < kBM * BN; e += 32 * kEpiWarps) {
-          const int dd = d0 + e / BN;
-          const int pp = p0 + e % BN;
-          if (dd < p.D && pp < p.P) {
-            const long long flat = static_cast<long long>(dd) * p.P + pp;
-            if (flat >= p.noise_lo && flat < p.noise_hi)
-              __stcg(p.grad_w + flat, __ldcg(p.grad_w + flat) +
-                                          p.noise_scale * noise_draw(p.noise_impl, p.key_base_g, p.key_base,
-                                                                     static_cast<uint64_t>(flat)));
+      }
+      if (d < p.D) {
+        float* dst = p.grad_w + static_cast<long long>(d) * p.P + p0 + col0;
+        if (p0 + col0 + C::kCPT <= p.P) {
+#pragma unroll
+          for (int i = 0; i < C::kCPT; i += 4) {
+            float4 v = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+            if (rmw_store) {
+              const float4 old = __ldcg(reinterpret_cast<const float4*>(dst + i));
+              v.x += old.x; v.y += old.y; v.z += old.z; v.w += old.w;
+            }
+            *reinterpret_cast<float4*>(dst + i) = v;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < C::kCPT; ++i) {
+            if (p0 + col0 + i < p.P) {
+              float v = acc[i];
+              if (rmw_store) v += __ldcg(dst + i);
+              dst[i] = v;
+            }
           }
         }
       }
+      FDP_TRACE(2);
     }
   }
 
@@ -368,12 +472,14 @@ template <int BN>
 static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
                                   bool cooperative, cudaStream_t stream) {
   using C = TcCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(dpdw_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -401,6 +507,13 @@ cudaError_t launch_tc(int bn, const CUtensorMap& tm_dy, const CUtensorMap& tm_x,
 size_t tc_smem_bytes(int bn) { return bn == 256 ? TcCfg<256>::kSmem : TcCfg<128>::kSmem; }
 
 int tc_max_coresident(int bn) {
+  // cached per device and tile width (the occupancy query is not free)
+  static int cache[64][2];
+  static bool have[64][2];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  const int k = bn == 256 ? 1 : 0;
+  if (have[dev][k]) return cache[dev][k];
   int n = 0;
   cudaError_t e;
   if (bn == 256) {
@@ -412,7 +525,10 @@ int tc_max_coresident(int bn) {
                          static_cast<int>(TcCfg<128>::kSmem));
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dpdw_tc_kernel<128>, kTcThreads, TcCfg<128>::kSmem);
   }
-  return e == cudaSuccess ? n : 0;
+  if (e != cudaSuccess) return 0;
+  cache[dev][k] = n;
+  have[dev][k] = true;
+  return n;
 }
 
 }  // namespace fdp

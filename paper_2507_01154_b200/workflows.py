@@ -91,12 +91,11 @@ def _to_device(t, dtype, device) -> tuple[torch.Tensor, bool]:
         if dtype is not None and t.dtype != dtype:
             t = t.to(dtype)
         return t.contiguous(), False
-    if isinstance(t, Tensor):
-        arr = t.array
-    elif isinstance(t, torch.Tensor):
-        arr = t.detach().numpy()
-    else:
-        arr = np.asarray(t)
+    if isinstance(t, torch.Tensor):  # host torch tensor (bf16 allowed): one H2D copy
+        target = dtype if dtype is not None else (t.dtype if t.dtype in (torch.bfloat16, torch.float32)
+                                                  else torch.float32)
+        return t.detach().to(device=device, dtype=target, non_blocking=t.is_pinned()).contiguous(), True
+    arr = t.array if isinstance(t, Tensor) else np.asarray(t)
     host = torch.from_numpy(np.ascontiguousarray(arr))
     target = dtype if dtype is not None else (torch.bfloat16 if host.dtype == torch.bfloat16 else torch.float32)
     return host.to(device=device, dtype=target, non_blocking=False).contiguous(), True
@@ -114,7 +113,8 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
          path: str = "auto", noise_impl: str = "keyed_f32", dtype: Optional[torch.dtype] = None,
          grad_out: Optional[torch.Tensor] = None, norms_out: Optional[torch.Tensor] = None,
          accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
-         skip_barrier: bool = False, short_timeout: bool = False) -> BackwardResult:
+         skip_barrier: bool = False, short_timeout: bool = False, workspace: Optional[torch.Tensor] = None,
+         device_step: Optional[torch.Tensor] = None) -> BackwardResult:
     dims = _dims(x, dy)
     if kind != WorkflowKind.NON_DP and cfg is None:
         raise UsageError("DP workflows need a DPConfig")
@@ -122,6 +122,7 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     xd, host_x = _to_device(x, dtype, device)
     yd, host_y = _to_device(dy, xd.dtype, device)
     host = host_x or host_y
+    host_torch = host and isinstance(x, torch.Tensor)
     if xd.dtype != yd.dtype:
         raise UsageError(f"x and dy must share a dtype, got {xd.dtype} and {yd.dtype}")
     in_dtype = _input_dtype_code(xd)
@@ -131,7 +132,8 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=in_dtype, reduction=c.reduction,
                           clip_c=c.clip_c, sigma=c.sigma, seed=c.seed, layer_id=c.layer_id, step=c.step, rank=rank,
                           world=world, mean_batch=mean_batch, accumulate=accumulate, add_noise=add_noise,
-                          noise_impl=noise_impl, path=path, flags=flags)
+                          noise_impl=noise_impl, path=path, flags=flags,
+                          device_step=_step_ptr(device_step))
     lib = _lib.load()
     k = _lib.KIND[kind.value]
     ws_bytes = ctypes.c_size_t()
@@ -151,7 +153,12 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         norms = torch.empty(dims.B, dtype=torch.float32, device=device)
 
     stream = torch.cuda.current_stream(device)
-    ws = _POOL.get(ws_bytes.value, device, stream)
+    if workspace is not None:
+        if workspace.numel() * workspace.element_size() < ws_bytes.value:
+            raise fdp_capacity(ws_bytes.value, workspace.numel() * workspace.element_size())
+        ws = workspace.view(torch.uint8) if workspace.dtype != torch.uint8 else workspace
+    else:
+        ws = _POOL.get(ws_bytes.value, device, stream)
     rc = lib.fdp_backward(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
                           norms.data_ptr() if norms is not None else None, ws.data_ptr(), ws.numel(),
                           stream.cuda_stream)
@@ -173,11 +180,80 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     width = (spec or B200_SPEC).dtype_width_bytes
     report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)
 
+    if host_torch:
+        return BackwardResult(grad.cpu(), report, norms.cpu() if norms is not None else torch.zeros(0))
     if host:
         g_host = Tensor((dims.D, dims.P), grad.double().cpu().numpy())
         n_host = norms.double().cpu().numpy() if norms is not None else np.zeros(0)
         return BackwardResult(g_host, report, n_host)
     return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device))
+
+
+def _step_ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == torch.int64 and t.numel() >= 1):
+        raise UsageError("device_step must be a CUDA int64 tensor")
+    return t.data_ptr()
+
+
+def fdp_capacity(need: int, have: int):
+    from .errors import CapacityError
+    return CapacityError(need, have, have, message=f"workspace of {have} bytes is smaller than the {need} bytes "
+                                                   "this call needs")
+
+
+class PreparedBackward:
+    """One layer's DP backward bound to fixed device buffers: calling it is a
+    single C-ABI call (no per-call planning or allocation in Python), which is
+    what a training loop or a CUDA graph capture wants.
+
+    grad_w / norms_sq are written in place; `device_step` (CUDA int64 scalar)
+    keys the noise so replays of a captured graph draw fresh noise."""
+
+    def __init__(self, kind: WorkflowKind, x: torch.Tensor, dy: torch.Tensor, cfg: Optional[DPConfig], *,
+                 grad_w: Optional[torch.Tensor] = None, norms_sq: Optional[torch.Tensor] = None,
+                 path: str = "auto", noise_impl: str = "keyed_f32", accumulate: bool = False,
+                 add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
+                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+        dims = _dims(x, dy)
+        if not (x.is_cuda and dy.is_cuda and x.is_contiguous() and dy.is_contiguous() and x.dtype == dy.dtype):
+            raise UsageError("PreparedBackward needs contiguous CUDA inputs of one dtype")
+        c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
+        self.kind = kind
+        self.x, self.dy = x, dy
+        self.desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=_input_dtype_code(x),
+                                   reduction=c.reduction, clip_c=c.clip_c, sigma=c.sigma, seed=c.seed,
+                                   layer_id=c.layer_id, step=c.step, rank=rank, world=world, mean_batch=mean_batch,
+                                   accumulate=accumulate, add_noise=add_noise, noise_impl=noise_impl, path=path,
+                                   device_step=_step_ptr(device_step))
+        self._device_step = device_step
+        lib = _lib.load()
+        self._lib = lib
+        self._k = _lib.KIND[kind.value]
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.fdp_workspace_bytes(ctypes.byref(self.desc), self._k, ctypes.byref(nbytes)))
+        dev = x.device
+        self.grad_w = grad_w if grad_w is not None else torch.zeros((dims.D, dims.P), dtype=torch.float32, device=dev)
+        self.norms_sq = None if kind == WorkflowKind.NON_DP else (
+            norms_sq if norms_sq is not None else torch.zeros(dims.B, dtype=torch.float32, device=dev))
+        if workspace is None:
+            workspace = torch.zeros(max(nbytes.value, 4096), dtype=torch.uint8, device=dev)
+        elif workspace.numel() * workspace.element_size() < nbytes.value:
+            raise fdp_capacity(nbytes.value, workspace.numel() * workspace.element_size())
+        self.workspace = workspace
+        self.workspace_bytes = nbytes.value
+        self._args = (self._k, ctypes.byref(self.desc), x.data_ptr(), dy.data_ptr(), self.grad_w.data_ptr(),
+                      self.norms_sq.data_ptr() if self.norms_sq is not None else None, workspace.data_ptr(),
+                      workspace.numel() * workspace.element_size())
+        self.plan = _lib.plan(self.desc, kind.value)
+
+    def set_step(self, step: int) -> None:
+        self.desc.step = _lib._wrap64(step)
+
+    def __call__(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
+        _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
 
 
 def backward_nondp(x, dy, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:

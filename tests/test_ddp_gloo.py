@@ -1,0 +1,70 @@
+"""World-size-2 data-parallel composition on CPU (gloo): per-rank contributions
+(clipped sum over the rank's samples / global B + noise on the rank's index
+slice, exactly what the kernel computes with rank/world/mean_batch) summed by
+paper_2507_01154_b200.ddp.allreduce_grads_ equal the single-process result."""
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import dp_oracle as O
+from paper_2507_01154_b200.ddp import allreduce_grads_, noise_partition
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_contribution(x, dy, cfg, rank, world):
+    """What rank `rank` of `world` produces for its batch slice (oracle arithmetic)."""
+    B = x.shape[0]
+    lo_b, hi_b = B * rank // world, B * (rank + 1) // world
+    n = dy.shape[2] * x.shape[2]
+    lo, hi = noise_partition(n, rank, world)
+    g, _ = O.dp_backward(x[lo_b:hi_b], dy[lo_b:hi_b], cfg, exact_noise=True, mean_batch=B, noise_lo=lo,
+                         noise_hi=hi)
+    return g
+
+
+def _worker(rank, world, port, x, dy, cfgs, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    grads = [torch.tensor(_rank_contribution(x, dy, c, rank, world)) for c in cfgs]
+    allreduce_grads_(grads, bucket_bytes=1024)  # several buckets
+    if rank == 0:
+        for i, g in enumerate(grads):
+            out[i] = g.numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_allreduce_equals_single_process():
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (6, 5, 12))
+    dy = rng.uniform(-1, 1, (6, 5, 7))
+    cfgs = [O.Cfg(0.7, 1.3, "mean", 5, 2, 9), O.Cfg(1e9, 0.5, "sum", 1, 0, 0), O.Cfg(0.1, 0.0, "mean", 0, 0, 0)]
+    world = 2
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, _free_port(), x, dy, cfgs, out), nprocs=world, join=True)
+        for i, c in enumerate(cfgs):
+            want, _ = O.dp_backward(x, dy, c, exact_noise=True)
+            assert np.max(np.abs(out[i] - want)) <= 1e-12 * max(1.0, np.max(np.abs(want))), i
+
+
+def test_partition_matches_kernel_partition():
+    # same slices as fdp_noise_partition (tests/test_host_api.py checks the C side)
+    for n in (1, 10, 65536, 999983):
+        for world in (1, 2, 3, 8):
+            sl = [noise_partition(n, r, world) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))

@@ -31,8 +31,9 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_desc_layout_matches_header():
-    # 4 x int64, 2 x int32, 2 x double, 3 x int64, 2 x int32, int64, 6 x int32
-    assert ctypes.sizeof(_lib.FdpDesc) == 4 * 8 + 2 * 4 + 2 * 8 + 3 * 8 + 2 * 4 + 8 + 6 * 4
+    # 4 x int64, 2 x int32, 2 x double, 3 x int64, 2 x int32, int64, 6 x int32, pointer
+    assert ctypes.sizeof(_lib.FdpDesc) == 4 * 8 + 2 * 4 + 2 * 8 + 3 * 8 + 2 * 4 + 8 + 6 * 4 + 8
+    assert _lib.FdpDesc.device_step.offset == ctypes.sizeof(_lib.FdpDesc) - 8
     assert ctypes.sizeof(_lib.FdpPlanInfo) == 11 * 4 + 4 + 8
 
 
