@@ -23,8 +23,11 @@ NOISE = {"keyed_f32": 0, "keyed_f64": 1, "philox": 2}
 PATH = {"auto": 0, "fused": 1, "two_phase": 2, "simt": 3}
 PATH_NAMES = {v: k for k, v in PATH.items()}
 KIND = {"non_dp": 0, "explicit_dp": 1, "implicit_dp": 2, "flashdp": 3}
+NORM_PHASE = {"auto": 0, "ghost": 1, "recompute": 2}
+NORM_PHASE_NAMES = {v: k for k, v in NORM_PHASE.items()}
 FLAG_SKIP_BARRIER = 1
 FLAG_TIMEOUT_SHORT = 2
+FLAG_TRACE = 4
 
 # Every symbol include/fdp.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
@@ -115,13 +118,17 @@ def check(rc: int) -> None:
 
 def make_desc(*, B, T, P, D, in_dtype=DTYPE_BF16, reduction="sum", clip_c=1.0, sigma=0.0, seed=0, layer_id=0,
               step=0, rank=0, world=1, mean_batch=0, accumulate=False, add_noise=True, noise_impl="keyed_f32",
-              path="auto", flags=0, norm_phase=0, device_step=None) -> FdpDesc:
+              path="auto", flags=0, norm_phase="auto", device_step=None) -> FdpDesc:
     if reduction not in REDUCE:
         raise UsageError(f"reduction must be one of {tuple(REDUCE)}, got {reduction!r}")
     if noise_impl not in NOISE:
         raise UsageError(f"noise_impl must be one of {tuple(NOISE)}, got {noise_impl!r}")
     if path not in PATH:
         raise UsageError(f"path must be one of {tuple(PATH)}, got {path!r}")
+    if isinstance(norm_phase, str):
+        if norm_phase not in NORM_PHASE:
+            raise UsageError(f"norm_phase must be one of {tuple(NORM_PHASE)}, got {norm_phase!r}")
+        norm_phase = NORM_PHASE[norm_phase]
     return FdpDesc(B=B, T=T, P=P, D=D, in_dtype=in_dtype, reduction=REDUCE[reduction], clip_c=float(clip_c),
                    sigma=float(sigma), seed=_wrap64(seed), layer_id=_wrap64(layer_id), step=_wrap64(step),
                    rank=rank, world=world, mean_batch=mean_batch, accumulate=int(bool(accumulate)),

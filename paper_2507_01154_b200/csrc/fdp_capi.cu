@@ -82,13 +82,13 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// bf16 (inner, T, B) tensor, box (64, kBK, 1), 128B swizzle.
-int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t T, int64_t B) {
+// bf16 (inner, T, B) tensor, box (64, box_rows, 1), 128B swizzle.
+int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t T, int64_t B, int box_rows = fdp::kBK) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(FDP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(B)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * 2), static_cast<cuuint64_t>(inner * T * 2)};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(fdp::kBK), 1};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -128,7 +128,8 @@ struct Plan {
   int path = FDP_PATH_SIMT;
   int norm_phase = FDP_NORMS_RECOMPUTE;
   int bn = 128;
-  int n_dt = 0, n_pt = 0, n_tiles = 0;
+  int cg = 1;
+  int n_dt = 0, n_pt = 0, n_tiles = 0, n_wtiles = 0;
   int groups = 1;
   int grid = 0;
   int launches = 0;
@@ -151,17 +152,46 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
+// Ghost norms cost ~T^2 (P + D) (1 + 1/nT) flops per sample, recomputing the
+// per-sample gradient 2 T P D: take the cheaper one unless the caller forces it.
+int choose_norm_phase(const fdp_desc* d) {
+  if (d->norm_phase == FDP_NORMS_GHOST || d->norm_phase == FDP_NORMS_RECOMPUTE) return d->norm_phase;
+  const double nT = static_cast<double>((d->T + 127) / 128);
+  const double ghost = static_cast<double>(d->T) * d->T * (d->P + d->D) * (1.0 + 1.0 / nT);
+  const double recompute = 2.0 * d->T * d->P * d->D;
+  return ghost < recompute ? FDP_NORMS_GHOST : FDP_NORMS_RECOMPUTE;
+}
+
 int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   const bool tc_dev = di.major == 10;  // sm_100 family
   const bool tc_ok = tc_dev && tc_shape_ok(d);
   const int want = d->path;
   pl = Plan();
   const int forced_bn = env_int("FDP_FORCE_BN", 0);
+  const int forced_cg = env_int("FDP_FORCE_CG", 0);
 
-  auto tiles_for = [&](int bn, int& ndt, int& npt) {
-    ndt = static_cast<int>((d->D + fdp::kBM - 1) / fdp::kBM);
+  // Work tile = cg x 128 d-rows x bn p-cols; returns the number of work tiles.
+  auto tiles_for = [&](int bn, int cg, int& ndt2, int& npt) {
+    const long long ndt = (d->D + fdp::kBM - 1) / fdp::kBM;
+    ndt2 = static_cast<int>((ndt + cg - 1) / cg);
     npt = static_cast<int>((d->P + bn - 1) / bn);
-    return static_cast<long long>(ndt) * npt;
+    return static_cast<long long>(ndt2) * npt;
+  };
+  // Preference order among equally good fills: CTA pairs (half the operand
+  // traffic per SM) and the 64-register accumulator width first.
+  const int cands[4][2] = {{128, 2}, {256, 2}, {256, 1}, {128, 1}};
+  auto allowed = [&](int bn, int cg) {
+    return (!forced_bn || bn == forced_bn) && (!forced_cg || cg == forced_cg);
+  };
+  auto persistent_choice = [&]() {
+    for (auto& cd : cands)
+      if (allowed(cd[0], cd[1]) && fdp::tc_max_coresident_ctas(cd[0], cd[1]) > 0) {
+        pl.bn = cd[0];
+        pl.cg = cd[1];
+        return;
+      }
+    pl.bn = 128;
+    pl.cg = 1;
   };
 
   if (kind == FDP_KIND_FLASHDP) {
@@ -173,53 +203,58 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     if (want == FDP_PATH_SIMT || !tc_ok) {
       pl.path = FDP_PATH_SIMT;
     } else {
-      // choose the tile width that best fills the SMs with co-resident CTAs
+      // choose the tile shape that best fills the SMs with co-resident CTAs
       double best = -1.0;
-      int best_bn = 0, best_groups = 1;
-      for (int bn : {256, 128}) {
-        if (forced_bn && bn != forced_bn) continue;
-        int ndt, npt;
-        const long long nt = tiles_for(bn, ndt, npt);
-        const int cores = fdp::tc_max_coresident(bn);
-        const long long cap = static_cast<long long>(di.sms) * (cores > 0 ? 1 : 0);
-        if (nt > cap || cap == 0) continue;
-        long long g = cap / nt;
+      int best_bn = 0, best_cg = 1, best_groups = 1;
+      for (auto& cd : cands) {
+        const int bn = cd[0], cg = cd[1];
+        if (!allowed(bn, cg)) continue;
+        int ndt2, npt;
+        const long long nwt = tiles_for(bn, cg, ndt2, npt);
+        const long long cap = fdp::tc_max_coresident_ctas(bn, cg);
+        const long long need = nwt * cg;
+        if (cap <= 0 || need > cap) continue;
+        long long g = cap / need;
         if (g > d->B) g = d->B;
         if (g > 8) g = 8;
-        const double util = static_cast<double>(nt * g) / di.sms;
-        if (util > best + 1e-9) {
+        const double util = static_cast<double>(need * g) / di.sms;
+        if (util > best + 0.02) {
           best = util;
           best_bn = bn;
+          best_cg = cg;
           best_groups = static_cast<int>(g);
         }
       }
       if (best_bn && want != FDP_PATH_TWO_PHASE) {
         pl.path = FDP_PATH_FUSED;
         pl.bn = best_bn;
+        pl.cg = best_cg;
         pl.groups = best_groups;
       } else {
         pl.path = FDP_PATH_TWO_PHASE;
-        pl.bn = forced_bn ? forced_bn : 256;
-        pl.norm_phase = FDP_NORMS_RECOMPUTE;
+        persistent_choice();
+        pl.norm_phase = choose_norm_phase(d);
       }
     }
   } else if (kind == FDP_KIND_IMPLICIT_DP) {
     pl.path = (tc_ok && want != FDP_PATH_SIMT) ? FDP_PATH_TWO_PHASE : FDP_PATH_SIMT;
-    pl.bn = forced_bn ? forced_bn : 256;
+    persistent_choice();
     pl.norm_phase = FDP_NORMS_RECOMPUTE;
   } else {  // NON_DP / EXPLICIT_DP: tensor-core GEMM stage when possible
     pl.path = (tc_ok && want != FDP_PATH_SIMT) ? FDP_PATH_FUSED : FDP_PATH_SIMT;
-    pl.bn = forced_bn ? forced_bn : 256;
+    persistent_choice();
   }
   pl.tc = pl.path != FDP_PATH_SIMT;
 
   if (pl.tc) {
-    tiles_for(pl.bn, pl.n_dt, pl.n_pt);
-    pl.n_tiles = pl.n_dt * pl.n_pt;
+    pl.n_wtiles = static_cast<int>(tiles_for(pl.bn, pl.cg, pl.n_dt, pl.n_pt));
+    pl.n_tiles = pl.n_wtiles * pl.cg;
   } else {
+    pl.cg = 1;
     pl.n_dt = static_cast<int>((d->D + 31) / 32);
     pl.n_pt = static_cast<int>((d->P + 31) / 32);
     pl.n_tiles = pl.n_dt * pl.n_pt;
+    pl.n_wtiles = pl.n_tiles;
   }
 
   // grid + launch count
@@ -227,7 +262,9 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     pl.grid = pl.n_tiles * pl.groups;
     pl.launches = 1;
   } else if (pl.tc) {
-    pl.grid = pl.n_tiles < di.sms ? pl.n_tiles : di.sms;
+    const int cap = fdp::tc_max_coresident_ctas(pl.bn, pl.cg);
+    const int max_clusters = (cap > 0 ? cap : di.sms) / pl.cg;
+    pl.grid = (pl.n_wtiles < max_clusters ? pl.n_wtiles : max_clusters) * pl.cg;
     if (kind == FDP_KIND_NON_DP) pl.launches = 1;
     else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;  // G, norms, reduce, clip, sum
     else pl.launches = 3;                                     // norms, reduce, reweight
@@ -241,6 +278,10 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   // workspace layout
   const long long B = d->B;
   pl.part_tiles = pl.n_tiles;
+  if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_GHOST) {
+    const long long nT = (d->T + 127) / 128;
+    pl.part_tiles = static_cast<int>(nT * (nT + 1) / 2);
+  }
   if (kind == FDP_KIND_EXPLICIT_DP) {
     pl.expl_chunks = 64;
     pl.part_tiles = pl.expl_chunks;
@@ -340,8 +381,9 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.T = static_cast<int>(d->T);
   p.P = static_cast<int>(d->P);
   p.D = static_cast<int>(d->D);
-  p.n_dt = pl.n_dt;
+  p.n_dt2 = pl.n_dt;
   p.n_pt = pl.n_pt;
+  p.n_wtiles = pl.n_wtiles;
   p.n_tiles = pl.n_tiles;
   p.groups = mode == fdp::MODE_FUSED ? pl.groups : 1;
   p.mode = mode;
@@ -435,7 +477,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
 
   if (kind == FDP_KIND_NON_DP) {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, nullptr, ws, fdp::MODE_NONDP);
-    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc nondp launch");
     return FDP_OK;
   }
@@ -447,7 +489,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     float* fac = ws_at<float>(ws, pl.off_factor);
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_STORE_G);
     p.g_out = g;
-    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc explicit G launch");
     fdp::SimtParams sp = simt_params(d, pl, c, x, dy, grad_w, norms, ws);
     if ((e = fdp::explicit_norms(g, sp.B, DP, part, pl.expl_chunks, s)) != cudaSuccess)
@@ -462,20 +504,42 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   }
   if (pl.path == FDP_PATH_FUSED) {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_FUSED);
-    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, true, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, true, s)) != cudaSuccess)
       return cuda_fail(e, "tc fused launch");
     return FDP_OK;
   }
-  // TWO_PHASE: norm phase (recompute), factors, one reweighted pass
+  // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass
   {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_NORMS);
-    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
-      return cuda_fail(e, "tc norm-phase launch");
-    if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pl.n_tiles, d->clip_c, p.clip_c2, c.inv_batch, norms,
-                                          ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
-      return cuda_fail(e, "factor reduce");
+    if (pl.norm_phase == FDP_NORMS_GHOST) {
+      CUtensorMap gx, gy;
+      if ((rc = make_tmap(&gx, x, d->P, d->T, d->B, 128))) return rc;
+      if ((rc = make_tmap(&gy, dy, d->D, d->T, d->B, 128))) return rc;
+      fdp::GhostParams g{};
+      g.B = p.B;
+      g.T = p.T;
+      g.P = p.P;
+      g.D = p.D;
+      g.nT = static_cast<int>((d->T + 127) / 128);
+      g.n_pairs = g.nT * (g.nT + 1) / 2;
+      g.n_items = g.n_pairs * g.B;
+      g.part = p.ws_part;
+      g.err = p.ws_ctrl + 1;
+      g.budget_ns = p.budget_ns;
+      const int grid = g.n_items < di.sms ? g.n_items : di.sms;
+      if ((e = fdp::launch_ghost(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
+      if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, g.n_pairs, d->clip_c, p.clip_c2, c.inv_batch, norms,
+                                            ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+        return cuda_fail(e, "factor reduce");
+    } else {
+      if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+        return cuda_fail(e, "tc norm-phase launch");
+      if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pl.n_tiles, d->clip_c, p.clip_c2, c.inv_batch, norms,
+                                            ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+        return cuda_fail(e, "factor reduce");
+    }
     fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
-    if ((e = fdp::launch_tc(pl.bn, tm_dy, tm_x, q, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, q, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc reweight launch");
   }
   return FDP_OK;
@@ -509,7 +573,7 @@ int fdp_plan(const fdp_desc* d, int32_t kind, fdp_plan_info* out) {
   if ((rc = make_plan(d, kind, di, pl))) return rc;
   out->path = pl.path;
   out->norm_phase = pl.path == FDP_PATH_TWO_PHASE ? pl.norm_phase : 0;
-  out->tile_d = pl.tc ? fdp::kBM : 32;
+  out->tile_d = pl.tc ? fdp::kBM * pl.cg : 32;
   out->tile_p = pl.tc ? pl.bn : 32;
   out->tile_t = pl.tc ? fdp::kBK : 32;
   out->n_d = pl.n_dt;

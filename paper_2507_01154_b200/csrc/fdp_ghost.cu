@@ -1,0 +1,190 @@
+// fdp_ghost.cu -- ghost-norm kernel: per-sample ||G_b||_F^2 without forming G_b.
+//
+// First phase of the TWO_PHASE path for layers whose per-sample gradient tiles
+// do not fit the co-resident grid (Llama shapes). Using
+//   ||dY_b^T X_b||_F^2 = < X_b X_b^T , dY_b dY_b^T >_F
+// each work item (b, i, j), i <= j, computes the 128x128 Gram tiles
+//   Gx = X_b[i] X_b[j]^T  (K = P)   and   Gy = dY_b[i] dY_b[j]^T  (K = D)
+// on tcgen05 (both operands K-major: rows of X / dY are contiguous in p / d),
+// keeps both in TMEM (2 x 128 columns, double-buffered), and reduces
+// w_ij * sum(Gx .* Gy) (w = 1 on the diagonal, 2 off it) to one partial per
+// (sample, tile pair). The partials are summed in a fixed order by
+// k_reduce_norms, which also forms the clip factors (dpcore.py:41-47).
+// Cost ~ T^2 (P + D) flops per sample versus 2 T P D for recomputing G_b, so
+// the layer is never differentiated twice (the reference's implicit workflow
+// recomputes: workflows.py:302-321).
+#include "fdp_internal.h"
+#include "fdp_ptx.cuh"
+
+namespace fdp {
+
+namespace {
+
+constexpr int kGT = 128;                       // Gram tile rows (t) = cols (s)
+constexpr int kGTileBytes = kGT * kBK * 2;     // 16 KB: 128 rows x 64 bf16 (one SW128 K-major atom column)
+constexpr int kGStageBytes = 2 * kGTileBytes;  // A + B
+constexpr int kGStages = 6;
+constexpr int kGNBuf = 2;                      // (Gx, Gy) accumulator pairs
+constexpr size_t kGSmem = 1024 + size_t(kGStages) * kGStageBytes + 1024;
+// kind::f16, bf16 x bf16 -> fp32, A and B K-major, M = N = 128
+constexpr uint32_t kGIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(128 >> 3) << 17) |
+                             (static_cast<uint32_t>(128 >> 4) << 24);
+
+// K-major SWIZZLE_128B canonical layout: 8-row core groups of 128 B rows,
+// SBO = 1024 B between 8-row groups; LBO unused (one 64-element atom in K).
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return make_sdesc_sw128(saddr, 16, 1024); }
+
+__device__ __forceinline__ void decode_item(int wi, int n_pairs, int nT, int& b, int& i, int& j) {
+  b = wi / n_pairs;
+  int r = wi % n_pairs;
+  // row-major upper triangle: row i has nT - i entries
+  i = 0;
+  while (r >= nT - i) {
+    r -= nT - i;
+    ++i;
+  }
+  j = i + r;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    ghost_norm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
+                      const GhostParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGStages * kGStageBytes);
+  uint64_t* empty = full + kGStages;
+  uint64_t* tfull = empty + kGStages;
+  uint64_t* tempty = tfull + kGNBuf;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + kGNBuf);
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned* err = p.err;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kGNBuf; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    prefetch_tmap(&tm_x);
+    prefetch_tmap(&tm_dy);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int nkx = (p.P + kBK - 1) / kBK, nky = (p.D + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
+        int b, i, j;
+        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        for (int k = 0; k < nkx + nky; ++k) {
+          const bool isx = k < nkx;
+          const CUtensorMap* m = isx ? &tm_x : &tm_dy;
+          const int kk = (isx ? k : k - nkx) * kBK;
+          mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x301);
+          uint8_t* sa = smem + stage * kGStageBytes;
+          mbar_arrive_expect_tx(&full[stage], i == j ? kGTileBytes : kGStageBytes);
+          tma_load_3d(sa, m, &full[stage], kk, i * kGT, b);
+          if (i != j) tma_load_3d(sa + kGTileBytes, m, &full[stage], kk, j * kGT, b);
+          if (++stage == kGStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
+        int b, i, j;
+        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        mbar_wait(&tempty[buf], tphase ^ 1, err, p.budget_ns, 0x302);
+        tc_fence_after();
+        for (int k = 0; k < nkx + nky; ++k) {
+          const bool isx = k < nkx;
+          const uint32_t dtm = tmem_base + buf * 256 + (isx ? 0 : 128);
+          mbar_wait(&full[stage], phase, err, p.budget_ns, 0x303);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + stage * kGStageBytes);
+          const uint32_t bb = (i == j) ? a : a + kGTileBytes;
+#pragma unroll
+          for (int kq = 0; kq < kBK / 16; ++kq)
+            tc_mma_f16(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kGIdesc,
+                       (k == 0 || k == nkx) && kq == 0 ? 0u : 1u);
+          tc_commit(&empty[stage]);
+          if (++stage == kGStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[buf]);
+        if (++buf == kGNBuf) { buf = 0; tphase ^= 1; }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
+    uint32_t buf = 0, tphase = 0;
+    for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
+      int b, i, j;
+      decode_item(wi, p.n_pairs, p.nT, b, i, j);
+      mbar_wait(&tfull[buf], tphase, err, p.budget_ns, 0x304);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + half * 64;
+      float part = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float gx[32], gy[32];
+        tmem_ld32(tb + c * 32, gx);
+        tmem_ld32(tb + 128 + c * 32, gy);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) part = fmaf(gx[e], gy[e], part);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (++buf == kGNBuf) { buf = 0; tphase ^= 1; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) red[ew] = part;
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (etid == 0) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kEpiWarps; ++w) s += red[w];
+        p.part[static_cast<long long>(b) * p.n_pairs + (wi % p.n_pairs)] = (i == j ? 1.0f : 2.0f) * s;
+      }
+      named_bar_sync(1, 32 * kEpiWarps);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem_base);
+}
+
+}  // namespace
+
+cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
+                         cudaStream_t stream) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !done[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(ghost_norm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGSmem));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev] = true;
+  }
+  ghost_norm_kernel<<<grid, kTcThreads, kGSmem, stream>>>(tm_x, tm_dy, p);
+  return cudaGetLastError();
+}
+
+}  // namespace fdp

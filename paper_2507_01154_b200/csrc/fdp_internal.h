@@ -23,7 +23,10 @@ enum TcMode : int {
 
 struct TcParams {
   int B, T, P, D;
-  int n_dt, n_pt, n_tiles;
+  int n_dt2;     // work-tile rows: ceil(ceil(D/128) / CG)   (a work tile is CG x 128 d-rows x BN p-cols)
+  int n_pt;      // work-tile columns: ceil(P / BN)
+  int n_wtiles;  // n_dt2 * n_pt
+  int n_tiles;   // CTA-level tiles = n_wtiles * CG (one norm partial per CTA tile and sample)
   int groups;  // sample groups per output tile (FUSED)
   int mode;
   int n_kb;
@@ -47,17 +50,32 @@ struct TcParams {
   unsigned* ws_cnt;        // [B]
   unsigned* ws_tile_cnt;   // [n_tiles]
   unsigned* ws_ctrl;       // [0] exit counter, [1] error word
-  float* ws_acc;           // [(groups-1)][n_tiles][kBM*BN]
+  float* ws_acc;           // [n_tiles][groups][kBM*BN]
   int skip_barrier;
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][128] phase timestamps or nullptr
 };
 
-// Launch the tcgen05 kernel (BN = 128 or 256). cooperative=true for MODE_FUSED.
-cudaError_t launch_tc(int bn, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
+// Launch the tcgen05 kernel: BN = 128 or 256 output columns per CTA, CG = 1 or
+// 2 CTAs per MMA (cta_group::2 pairs two SMs on a 256-row tile). cooperative=true
+// for MODE_FUSED (all CTAs must be co-resident for the in-kernel barriers).
+cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
                       bool cooperative, cudaStream_t stream);
-int tc_max_coresident(int bn);  // CTAs per SM that can be co-resident (0 if the kernel cannot run)
-size_t tc_smem_bytes(int bn);
+// Upper bound on co-resident CTAs of the (bn, cg) kernel on this device (0: cannot run).
+int tc_max_coresident_ctas(int bn, int cg);
+
+// ---- ghost norms (TWO_PHASE first phase): ||G_b||^2 = <X_b X_b^T, dY_b dY_b^T>
+struct GhostParams {
+  int B, T, P, D;
+  int nT;        // ceil(T / 128)
+  int n_pairs;   // nT (nT + 1) / 2 upper-triangle Gram tile pairs per sample
+  int n_items;   // B * n_pairs
+  float* part;   // [B][n_pairs] weighted partials
+  unsigned* err;
+  unsigned long long budget_ns;
+};
+cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
+                         cudaStream_t stream);
 
 // ---- SIMT (CUDA-core) kernels: generic shapes, fp32 inputs, explicit baseline
 struct SimtParams {

@@ -114,7 +114,7 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
          grad_out: Optional[torch.Tensor] = None, norms_out: Optional[torch.Tensor] = None,
          accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
          skip_barrier: bool = False, short_timeout: bool = False, workspace: Optional[torch.Tensor] = None,
-         device_step: Optional[torch.Tensor] = None) -> BackwardResult:
+         device_step: Optional[torch.Tensor] = None, norm_phase: str = "auto") -> BackwardResult:
     dims = _dims(x, dy)
     if kind != WorkflowKind.NON_DP and cfg is None:
         raise UsageError("DP workflows need a DPConfig")
@@ -132,7 +132,7 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=in_dtype, reduction=c.reduction,
                           clip_c=c.clip_c, sigma=c.sigma, seed=c.seed, layer_id=c.layer_id, step=c.step, rank=rank,
                           world=world, mean_batch=mean_batch, accumulate=accumulate, add_noise=add_noise,
-                          noise_impl=noise_impl, path=path, flags=flags,
+                          noise_impl=noise_impl, path=path, flags=flags, norm_phase=norm_phase,
                           device_step=_step_ptr(device_step))
     lib = _lib.load()
     k = _lib.KIND[kind.value]
@@ -215,7 +215,8 @@ class PreparedBackward:
                  grad_w: Optional[torch.Tensor] = None, norms_sq: Optional[torch.Tensor] = None,
                  path: str = "auto", noise_impl: str = "keyed_f32", accumulate: bool = False,
                  add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
-                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                 norm_phase: str = "auto"):
         dims = _dims(x, dy)
         if not (x.is_cuda and dy.is_cuda and x.is_contiguous() and dy.is_contiguous() and x.dtype == dy.dtype):
             raise UsageError("PreparedBackward needs contiguous CUDA inputs of one dtype")
@@ -226,7 +227,7 @@ class PreparedBackward:
                                    reduction=c.reduction, clip_c=c.clip_c, sigma=c.sigma, seed=c.seed,
                                    layer_id=c.layer_id, step=c.step, rank=rank, world=world, mean_batch=mean_batch,
                                    accumulate=accumulate, add_noise=add_noise, noise_impl=noise_impl, path=path,
-                                   device_step=_step_ptr(device_step))
+                                   norm_phase=norm_phase, device_step=_step_ptr(device_step))
         self._device_step = device_step
         lib = _lib.load()
         self._lib = lib
@@ -310,6 +311,7 @@ def execution_plan(x_shape, dy_shape, kind: WorkflowKind = WorkflowKind.FLASHDP,
     desc = _lib.make_desc(B=B, T=T, P=P, D=D, in_dtype=_lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F32,
                           path=path)
     info = _lib.plan(desc, kind.value)
-    return {"path": _lib.PATH_NAMES[info.path], "tile_d": info.tile_d, "tile_p": info.tile_p, "tile_t": info.tile_t,
+    return {"path": _lib.PATH_NAMES[info.path], "norm_phase": _lib.NORM_PHASE_NAMES.get(info.norm_phase, "auto"),
+            "tile_d": info.tile_d, "tile_p": info.tile_p, "tile_t": info.tile_t,
             "n_d": info.n_d, "n_p": info.n_p, "groups": info.groups, "grid": info.grid, "launches": info.launches,
             "sms": info.sms, "workspace_bytes": info.workspace_bytes}

@@ -16,12 +16,14 @@ for (B, T, P, D) in [(8, 1024, 4096, 4096), (4, 2048, 5120, 13824), (8, 1024, 76
     x2, y2 = x.view(-1, P), dy.view(-1, D)
     us = timed(lambda: torch.mm(y2.t(), x2, out_dtype=torch.float32))
     print(f"{B}x{T} {P}->{D} cublas {us:.1f}us {fl/us/1e6:.0f} TF", flush=True)
-    for bn in ("128", "256"):
+    for bn, cg in (("128", "1"), ("256", "1"), ("128", "2"), ("256", "2")):
         os.environ["FDP_FORCE_BN"] = bn
+        os.environ["FDP_FORCE_CG"] = cg
         c = fdp.PreparedBackward(fdp.WorkflowKind.NON_DP, x, dy, None)
         us = timed(c)
-        print(f"{B}x{T} {P}->{D} tcgen05 nondp bn{bn} grid{c.plan.grid} {us:.1f}us {fl/us/1e6:.0f} TF", flush=True)
+        print(f"{B}x{T} {P}->{D} tcgen05 nondp bn{bn} cg{cg} grid{c.plan.grid} {us:.1f}us {fl/us/1e6:.0f} TF", flush=True)
         c = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, fdp.DPConfig(1.0, 0.0), path="two_phase")
         us = timed(c)
-        print(f"{B}x{T} {P}->{D} two_phase bn{bn} {us:.1f}us {fl/us/1e6:.0f} TF(dW-equiv)", flush=True)
+        print(f"{B}x{T} {P}->{D} two_phase bn{bn} cg{cg} {us:.1f}us {fl/us/1e6:.0f} TF(dW-equiv)", flush=True)
     os.environ.pop("FDP_FORCE_BN")
+    os.environ.pop("FDP_FORCE_CG")

@@ -43,28 +43,30 @@ def main():
         nd = fdp.PreparedBackward(fdp.WorkflowKind.NON_DP, x, dy, None)
         us = timed(nd)
         out.append({"layer": name, "variant": "tcgen05_nondp", "us": round(us, 2), "tflops": round(flops / us / 1e6, 1)})
-        for bn in ("128", "256"):
+        for bn, cg in (("128", "1"), ("256", "1"), ("128", "2"), ("256", "2")):
             os.environ["FDP_FORCE_BN"] = bn
-            for noise, sigma in (("none", 0.0), ("keyed_f32", 1.0), ("philox", 1.0)):
+            os.environ["FDP_FORCE_CG"] = cg
+            for noise, sigma in (("none", 0.0), ("philox", 1.0)):
                 cfg = fdp.DPConfig(1.0, sigma, "mean", seed=1, layer_id=2)
                 try:
                     c = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, path="fused",
                                              noise_impl="keyed_f32" if noise == "none" else noise)
                     us = timed(c)
-                    out.append({"layer": name, "variant": f"fused_bn{bn}_{noise}", "us": round(us, 2),
+                    out.append({"layer": name, "variant": f"fused_bn{bn}_cg{cg}_{noise}", "us": round(us, 2),
                                 "tflops": round(flops / us / 1e6, 1), "groups": c.plan.groups, "grid": c.plan.grid})
                 except Exception as e:  # noqa: BLE001
-                    out.append({"layer": name, "variant": f"fused_bn{bn}_{noise}", "error": repr(e)[:200]})
+                    out.append({"layer": name, "variant": f"fused_bn{bn}_cg{cg}_{noise}", "error": repr(e)[:200]})
             cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=2)
             try:
                 c = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, path="two_phase", noise_impl="philox")
                 us = timed(c)
-                out.append({"layer": name, "variant": f"two_phase_bn{bn}_philox", "us": round(us, 2),
+                out.append({"layer": name, "variant": f"two_phase_bn{bn}_cg{cg}_philox", "us": round(us, 2),
                             "tflops": round(flops / us / 1e6, 1)})
             except Exception as e:  # noqa: BLE001
                 out.append({"layer": name, "variant": f"two_phase_bn{bn}", "error": repr(e)[:200]})
         os.environ.pop("FDP_FORCE_BN", None)
-        for r in out[-10:]:
+        os.environ.pop("FDP_FORCE_CG", None)
+        for r in out[-14:]:
             print(json.dumps(r), flush=True)
 
 
