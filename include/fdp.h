@@ -96,7 +96,11 @@ enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2,
                  /* record per-CTA phase timestamps (%globaltimer, ns) of the fused kernel
                     in the workspace tail: grid x 128 uint64 after fdp_plan_info.workspace_bytes
                     minus grid*1024 bytes (see paper_2507_01154_b200/trace.py) */
-                 FDP_FLAG_TRACE = 4 };
+                 FDP_FLAG_TRACE = 4,
+                 /* sum the sample groups' clipped tiles in a fixed order (slot
+                    reduce-scatter) instead of TMA reduce-add atomics: bitwise
+                    reproducible across runs, slower for layers that need groups */
+                 FDP_FLAG_DETERMINISTIC = 8 };
 
 /* Norm phase of the TWO_PHASE path. */
 enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2 };

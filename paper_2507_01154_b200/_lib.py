@@ -28,6 +28,7 @@ NORM_PHASE_NAMES = {v: k for k, v in NORM_PHASE.items()}
 FLAG_SKIP_BARRIER = 1
 FLAG_TIMEOUT_SHORT = 2
 FLAG_TRACE = 4
+FLAG_DETERMINISTIC = 8
 
 # Every symbol include/fdp.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (

@@ -97,6 +97,19 @@ int make_tmap(CUtensorMap* m, const void* ptr, int64_t inner, int64_t T, int64_t
   return FDP_OK;
 }
 
+// fp32 2-D/3-D maps for the fused epilogue's TMA stores (128B swizzle, 32-column boxes)
+int make_tmap_f32(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                  const cuuint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(FDP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FDP_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", static_cast<int>(r));
+  return FDP_OK;
+}
+
 int validate(const fdp_desc* d, int32_t kind) {
   if (!d) return fail(FDP_ERR_USAGE, "null descriptor");
   if (kind < FDP_KIND_NON_DP || kind > FDP_KIND_FLASHDP) return fail(FDP_ERR_USAGE, "unknown workflow kind %d", kind);
@@ -135,8 +148,8 @@ struct Plan {
   int launches = 0;
   bool tc = false;
   // workspace layout (byte offsets)
-  size_t off_ctrl = 0, off_cnt = 0, off_tile_cnt = 0, off_part = 0, off_factor = 0, off_acc = 0, off_g = 0,
-         off_gp = 0, total = 0;
+  size_t off_ctrl = 0, off_cnt = 0, off_tile_cnt = 0, off_part = 0, off_tag = 0, off_factor = 0, off_acc = 0,
+         off_g = 0, off_gp = 0, total = 0;
   int part_tiles = 0;  // partial norms per sample
   int expl_chunks = 0;
 };
@@ -217,6 +230,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
         long long g = cap / need;
         if (g > d->B) g = d->B;
         if (g > 8) g = 8;
+        while (g & (g - 1)) --g;  // 1, 2, 4 or 8: slices of 128 rows stay whole 8-row swizzle atoms
         const double util = static_cast<double>(need * g) / di.sms;
         if (util > best + 0.02) {
           best = util;
@@ -295,10 +309,12 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   off = align_up(off + 4ull * pl.n_tiles, 256);
   pl.off_part = off;
   off = align_up(off + 4ull * B * pl.part_tiles, 256);
+  pl.off_tag = off;
+  off = align_up(off + 8ull * B * pl.n_tiles, 256);
   pl.off_factor = off;
   off = align_up(off + 4 * B, 256);
   pl.off_acc = off;
-  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED && pl.groups > 1)
+  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED && pl.groups > 1 && (d->flags & FDP_FLAG_DETERMINISTIC))
     off = align_up(off + 4ull * pl.groups * pl.n_tiles * fdp::kBM * pl.bn, 256);
   pl.off_g = off;
   pl.off_gp = off;
@@ -408,10 +424,12 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.factors_in = ws_at<float>(ws, pl.off_factor);
   p.ws_part = ws_at<float>(ws, pl.off_part);
   p.ws_cnt = ws_at<unsigned>(ws, pl.off_cnt);
+  p.ws_tagged = ws_at<unsigned long long>(ws, pl.off_tag);
   p.ws_tile_cnt = ws_at<unsigned>(ws, pl.off_tile_cnt);
   p.ws_ctrl = ws_at<unsigned>(ws, pl.off_ctrl);
   p.ws_acc = ws_at<float>(ws, pl.off_acc);
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
+  p.deterministic = (d->flags & FDP_FLAG_DETERMINISTIC) ? 1 : 0;
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
   p.trace = (d->flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, pl.total - 1024ull * pl.grid) : nullptr;
   return p;
@@ -474,10 +492,33 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   CUtensorMap tm_dy, tm_x;
   if ((rc = make_tmap(&tm_dy, dy, d->D, d->T, d->B))) return rc;
   if ((rc = make_tmap(&tm_x, x, d->P, d->T, d->B))) return rc;
+  fdp::EpiMaps em;
+  em.gw = em.gw_slice = em.slot = em.slice = tm_dy;  // placeholders (unused outside MODE_FUSED)
+  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED) {
+    const cuuint64_t gdims[2] = {static_cast<cuuint64_t>(d->P), static_cast<cuuint64_t>(d->D)};
+    const cuuint64_t gstr[1] = {static_cast<cuuint64_t>(d->P * 4)};
+    const cuuint32_t gbox[2] = {32, static_cast<cuuint32_t>(fdp::kBM)};
+    if ((rc = make_tmap_f32(&em.gw, grad_w, 2, gdims, gstr, gbox))) return rc;
+    if (pl.groups > 1 && (d->flags & FDP_FLAG_DETERMINISTIC)) {
+      const cuuint32_t rows_own = static_cast<cuuint32_t>(fdp::kBM / pl.groups);
+      const cuuint32_t sbox[2] = {32, rows_own};
+      if ((rc = make_tmap_f32(&em.gw_slice, grad_w, 2, gdims, gstr, sbox))) return rc;
+      const cuuint64_t sdims[3] = {static_cast<cuuint64_t>(pl.bn), static_cast<cuuint64_t>(fdp::kBM),
+                                   static_cast<cuuint64_t>(pl.n_tiles) * pl.groups};
+      const cuuint64_t sstr[2] = {static_cast<cuuint64_t>(pl.bn * 4), static_cast<cuuint64_t>(pl.bn * 4 * fdp::kBM)};
+      const cuuint32_t box_full[3] = {32, static_cast<cuuint32_t>(fdp::kBM), 1};
+      const cuuint32_t box_sl[3] = {32, rows_own, 1};
+      float* slots = ws_at<float>(ws, pl.off_acc);
+      if ((rc = make_tmap_f32(&em.slot, slots, 3, sdims, sstr, box_full))) return rc;
+      if ((rc = make_tmap_f32(&em.slice, slots, 3, sdims, sstr, box_sl))) return rc;
+    }
+    if ((reinterpret_cast<uintptr_t>(grad_w) & 15u) != 0)
+      return fail(FDP_ERR_USAGE, "grad_w must be 16-byte aligned for the fused tensor-core path");
+  }
 
   if (kind == FDP_KIND_NON_DP) {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, nullptr, ws, fdp::MODE_NONDP);
-    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc nondp launch");
     return FDP_OK;
   }
@@ -489,7 +530,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     float* fac = ws_at<float>(ws, pl.off_factor);
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_STORE_G);
     p.g_out = g;
-    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc explicit G launch");
     fdp::SimtParams sp = simt_params(d, pl, c, x, dy, grad_w, norms, ws);
     if ((e = fdp::explicit_norms(g, sp.B, DP, part, pl.expl_chunks, s)) != cudaSuccess)
@@ -504,7 +545,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   }
   if (pl.path == FDP_PATH_FUSED) {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_FUSED);
-    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, true, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, true, s)) != cudaSuccess)
       return cuda_fail(e, "tc fused launch");
     return FDP_OK;
   }
@@ -532,14 +573,14 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
                                             ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     } else {
-      if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, p, pl.grid, false, s)) != cudaSuccess)
+      if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, false, s)) != cudaSuccess)
         return cuda_fail(e, "tc norm-phase launch");
       if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pl.n_tiles, d->clip_c, p.clip_c2, c.inv_batch, norms,
                                             ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     }
     fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
-    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, q, pl.grid, false, s)) != cudaSuccess)
+    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, q, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc reweight launch");
   }
   return FDP_OK;

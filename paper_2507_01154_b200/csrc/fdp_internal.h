@@ -10,7 +10,7 @@ namespace fdp {
 constexpr int kBM = 128;  // d rows per output tile (UMMA M, one TMEM lane per row)
 constexpr int kBK = 64;   // t extent of one pipeline stage (4 x UMMA K=16)
 constexpr int kEpiWarps = 8;
-constexpr int kEpiWarp0 = 4;                        // warpgroup 0: TMA, MMA, 2 spare warps
+constexpr int kEpiWarp0 = 4;  // warpgroup 0: warp 0 TMA producer, warp 1 MMA issuer, 2 spare
 constexpr int kTcThreads = 32 * kEpiWarp0 + 32 * kEpiWarps;  // warpgroups 1-2: epilogue
 
 enum TcMode : int {
@@ -46,12 +46,14 @@ struct TcParams {
   float* norms_out;
   float* g_out;
   const float* factors_in;
-  float* ws_part;          // [B][n_tiles]
+  float* ws_part;          // [B][n_tiles] (NORMS mode)
+  unsigned long long* ws_tagged;  // [B][n_tiles] {float partial, uint32 launch tag} (FUSED mode)
   unsigned* ws_cnt;        // [B]
   unsigned* ws_tile_cnt;   // [n_tiles]
   unsigned* ws_ctrl;       // [0] exit counter, [1] error word
   float* ws_acc;           // [n_tiles][groups][kBM*BN]
   int skip_barrier;
+  int deterministic;
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][128] phase timestamps or nullptr
 };
@@ -59,8 +61,13 @@ struct TcParams {
 // Launch the tcgen05 kernel: BN = 128 or 256 output columns per CTA, CG = 1 or
 // 2 CTAs per MMA (cta_group::2 pairs two SMs on a 256-row tile). cooperative=true
 // for MODE_FUSED (all CTAs must be co-resident for the in-kernel barriers).
-cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
-                      bool cooperative, cudaStream_t stream);
+// TMA maps of the fused epilogue: grad_w (D,P) fp32 with 32x128 and 32xrows_own
+// boxes, and the reduce-scatter slots [n_tiles*groups][128][BN] (full / slice boxes).
+struct EpiMaps {
+  CUtensorMap gw, gw_slice, slot, slice;
+};
+cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const EpiMaps& em,
+                      const TcParams& p, int grid, bool cooperative, cudaStream_t stream);
 // Upper bound on co-resident CTAs of the (bn, cg) kernel on this device (0: cannot run).
 int tc_max_coresident_ctas(int bn, int cg);
 

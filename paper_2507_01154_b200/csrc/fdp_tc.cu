@@ -55,7 +55,7 @@ struct TcCfg {
 template <int BN, int CG>
 __global__ void __launch_bounds__(kTcThreads, 1)
     dpdw_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
-                   const TcParams p) {
+                   const __grid_constant__ EpiMaps em, const TcParams p) {
   using C = TcCfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNBuf;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
+  uint64_t* rs_bar = tempty + C::kNBuf;  // reduce-scatter slice loads (one phase per launch)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rs_bar + 1);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps]
   float* bcast = red + kEpiWarps;                           // [1] (ordered by named barriers)
   float* stage_buf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + C::kBarBytes);
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
+    mbar_init(rs_bar, 1);
     fence_mbar_init();
     fence_proxy_async_smem();
     prefetch_tmap(&tm_dy);
@@ -226,8 +228,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const bool reduce_scatter = fused && p.groups > 1;
     // noise is pre-written into grad_w in chunks while the MMA / the norm
     // all-reduce are in flight; with sample groups each CTA draws only its slice.
-    const bool pre_noise = dp_sum && p.add_noise;
+    // grad_w rows are pre-filled (old value if accumulating, + noise) during the
+    // sample loop when noise is drawn, and always when sample groups combine their
+    // tiles with TMA reduce-add (every group then adds onto initialised rows).
+    const bool atomic_groups = reduce_scatter && !p.deterministic;
+    const bool pre_noise = (dp_sum && p.add_noise) || atomic_groups;
     const bool rmw_store = pre_noise || p.accumulate;
+    const bool draw_noise = dp_sum && p.add_noise;
+    // launch tag of the tagged norm-partial slots (bumped by the last CTA at exit)
+    unsigned tag = __ldcg(p.ws_ctrl + 2) + 1u;
+    if (tag == 0u) tag = 1u;
     const int n_units = per_sample ? (p.B - b0 + b_step - 1) / b_step : 1;
     const int own_r0 = reduce_scatter ? group * kBM / p.groups : 0;
     const int own_r1 = reduce_scatter ? (group + 1) * kBM / p.groups : kBM;
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const long long flat = static_cast<long long>(dd) * p.P + pp;
             float4* dst = reinterpret_cast<float4*>(p.grad_w + flat);
             float4 v = p.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (flat + 3 >= p.noise_lo && flat < p.noise_hi) {
+            if (draw_noise && flat + 3 >= p.noise_lo && flat < p.noise_hi) {
               const float4 n = noise_draw4(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
               const float s = p.noise_scale;
               if (flat + 0 >= p.noise_lo && flat + 0 < p.noise_hi) v.x += s * n.x;
@@ -294,12 +304,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float part = 0.0f;
         const uint32_t tb = taddr(b);
 #pragma unroll
-        for (int c = 0; c < C::kCPT / 32; ++c) {
-          float v[32];
-          tmem_ld32(tb + c * 32, v);
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tb + c * 16, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) part = fmaf(v[i], v[i], part);
+          for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -314,28 +324,50 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint64_t t0 = globaltimer_ns();
             while (globaltimer_ns() - t0 < 200000ull) __nanosleep(1000);
           }
-          p.ws_part[static_cast<long long>(ub) * p.n_tiles + tile] = s;
-          if (fused) red_release_add_u32(&p.ws_cnt[ub], 1u);
+          if (fused) {
+            // one 8-byte store carries the partial and this launch's tag: the
+            // readers need no separate counter or fence (single-copy atomic)
+            st_relaxed_u64(p.ws_tagged + static_cast<long long>(ub) * p.n_tiles + tile,
+                           (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s));
+          } else {
+            p.ws_part[static_cast<long long>(ub) * p.n_tiles + tile] = s;
+          }
         }
       };
       // inter-block all-reduce of sample ub, then the clip factor (workflows.py:394-403)
       auto wait_factor = [&](int ub) -> float {
         if (ew == 0) {
-          if (lane == 0) {
-            if (!p.skip_barrier) {
-              const uint64_t t0 = globaltimer_ns();
-              while (ld_acquire_u32(&p.ws_cnt[ub]) < static_cast<unsigned>(p.n_tiles)) {
-                if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
-                __nanosleep(32);
-              }
-            } else if (ld_acquire_u32(&p.ws_cnt[ub]) < static_cast<unsigned>(p.n_tiles)) {
-              atomicOr(err, 0x200u);  // ordering fault: clip reads an incomplete all-reduce
-            }
+          // lane l owns partial slots l, l+32, ...; spin on each until it carries this
+          // launch's tag, then sum in a fixed order (fp64) -> identical on every CTA
+          const unsigned long long* slots = p.ws_tagged + static_cast<long long>(ub) * p.n_tiles;
+          constexpr int kMaxPer = 5;  // fused grids have n_tiles <= 160 CTA tiles
+          unsigned long long v[kMaxPer];
+#pragma unroll
+          for (int k = 0; k < kMaxPer; ++k) {  // all loads in flight at once: one L2 round trip
+            const int i = lane + 32 * k;
+            v[k] = i < p.n_tiles ? ld_relaxed_u64(slots + i) : (static_cast<unsigned long long>(tag) << 32);
           }
-          __syncwarp();
+          bool stale = false;
+          if (!p.skip_barrier) {
+            const uint64_t t0 = globaltimer_ns();
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k) {
+              const int i = lane + 32 * k;
+              while (static_cast<unsigned>(v[k] >> 32) != tag) {
+                if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
+                v[k] = ld_relaxed_u64(slots + i);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k) stale |= static_cast<unsigned>(v[k] >> 32) != tag;
+          }
           double s = 0.0;
-          for (int i = lane; i < p.n_tiles; i += 32)
-            s += static_cast<double>(__ldcg(p.ws_part + static_cast<long long>(ub) * p.n_tiles + i));
+#pragma unroll
+          for (int k = 0; k < kMaxPer; ++k)
+            if (lane + 32 * k < p.n_tiles) s += static_cast<double>(__uint_as_float(static_cast<unsigned>(v[k])));
+          if (__any_sync(0xffffffffu, stale) && lane == 0)
+            atomicOr(err, 0x200u);  // ordering fault: clip reads an incomplete all-reduce
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
           if (lane == 0) {
@@ -352,37 +384,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       auto accumulate_scaled = [&](uint32_t b, float f) {
         const uint32_t tb = taddr(b);
 #pragma unroll
-        for (int c = 0; c < C::kCPT / 32; ++c) {
-          float v[32];
-          tmem_ld32(tb + c * 32, v);
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tb + c * 16, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fmaf(f, v[i], acc[c * 32 + i]);
+          for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
         }
       };
 
       FDP_TRACE(0);
       if (p.mode == MODE_FUSED) {
-        // software pipeline: sample u+1 is published and noise chunk u is drawn
-        // while the all-reduce of sample u is in flight
-        uint32_t bcur = wait_ready();
-        FDP_TRACE(9);
-        publish(b0, bcur);
+        // per sample: publish the norm partial, draw a noise chunk while the
+        // block-wise all-reduce is in flight, clip + accumulate, free the TMEM
+        // buffer (the MMA of the next samples proceeds meanwhile)
         for (int u = 0; u < n_units; ++u) {
           const int ub = b0 + u * b_step;
+          const uint32_t b = wait_ready();
+          FDP_TRACE(9 + 4 * u);
+          publish(ub, b);
           if (pre_noise) noise_chunk(u);
           FDP_TRACE(8 + 4 * u);
-          uint32_t bnext = 0;
-          if (u + 1 < n_units) {
-            bnext = wait_ready();
-            FDP_TRACE(13 + 4 * u);
-            publish(ub + b_step, bnext);
-          }
           const float f = wait_factor(ub);
           FDP_TRACE(10 + 4 * u);
-          accumulate_scaled(bcur, f);
-          release(bcur);
-          bcur = bnext;
+          accumulate_scaled(b, f);
+          release(b);
         }
       } else if (p.mode == MODE_REWEIGHT) {
         int u = 0;
@@ -432,59 +458,106 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       FDP_TRACE(1);
 
-      if (reduce_scatter) {
-        // ---- reduce-scatter of the clipped sums across the tile's sample groups:
-        // every group parks its partial tile (row-major, coalesced) in L2, then
-        // group g sums rows [g*BM/S, (g+1)*BM/S) of all S partials in a fixed
-        // order (deterministic), adds its pre-noised grad_w rows and writes them.
-        const long long tile_elems = static_cast<long long>(kBM) * BN;
-        float* slots = p.ws_acc + static_cast<long long>(tile) * p.groups * tile_elems;
-        store_tile(slots + group * tile_elems, BN, kBM, BN, false, acc);
-        __threadfence();
+      if (fused) {
+        // ---- epilogue I/O through TMA. The accumulator tile goes to shared memory
+        // (free now: every stage has been consumed) in 32-column boxes with the
+        // 128B swizzle, then bulk tensor stores move it. When grad_w already holds
+        // the noise (or the accumulated gradient) the store is a TMA reduce-add.
+        uint8_t* stg0 = smem;  // box kb at stg0 + kb * 16 KB: 128 rows x 128 B
+#pragma unroll
+        for (int c = 0; c < C::kCPT / 32; ++c) {
+          uint8_t* box = stg0 + (col0 / 32 + c) * (kBM * 128) + row * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) =
+                make_float4(acc[c * 32 + 4 * j], acc[c * 32 + 4 * j + 1], acc[c * 32 + 4 * j + 2],
+                            acc[c * 32 + 4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        if (rmw_store) __threadfence_block();  // noise chunks (generic) before the TMA reduce
         named_bar_sync(1, 32 * kEpiWarps);
+        if (reduce_scatter && !p.deterministic) {
+          // every group reduce-adds its whole clipped tile onto grad_w once all
+          // groups have initialised (pre-filled) their row slices
+          __threadfence();
+          named_bar_sync(1, 32 * kEpiWarps);
+          if (etid == 0) {
+            red_release_add_u32(&p.ws_tile_cnt[tile], 1u);
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_u32(&p.ws_tile_cnt[tile]) < static_cast<unsigned>(p.groups)) {
+              if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x106);
+              __nanosleep(64);
+            }
+            fence_proxy_async_global();
+            for (int kbx = 0; kbx < BN / 32; ++kbx)
+              tma_reduce_add_2d(&em.gw, stg0 + kbx * (kBM * 128), p0 + kbx * 32, d0);
+            bulk_commit();
+            bulk_wait_all();
+          }
+          FDP_TRACE(2);
+          continue;
+        }
+        if (!reduce_scatter) {
+          if (etid == 0) {
+            fence_proxy_async_global();
+            for (int kbx = 0; kbx < BN / 32; ++kbx) {
+              if (rmw_store) tma_reduce_add_2d(&em.gw, stg0 + kbx * (kBM * 128), p0 + kbx * 32, d0);
+              else tma_store_2d(&em.gw, stg0 + kbx * (kBM * 128), p0 + kbx * 32, d0);
+            }
+            bulk_commit();
+            bulk_wait_all();
+          }
+          FDP_TRACE(2);
+          continue;
+        }
+        // ---- reduce-scatter across the tile's sample groups (deterministic order):
+        // park the partial tile in L2, then group g sums rows [g*BM/S, (g+1)*BM/S)
+        // of all S partials and adds them onto its (pre-noised) rows of grad_w.
+        const int rows_own = own_r1 - own_r0;
+        const int slot0 = tile * p.groups;
         if (etid == 0) {
+          for (int kbx = 0; kbx < BN / 32; ++kbx) tma_store_3d(&em.slot, stg0 + kbx * (kBM * 128), kbx * 32, 0, slot0 + group);
+          bulk_commit();
+          bulk_wait_all();
+          fence_proxy_async_global();
           red_release_add_u32(&p.ws_tile_cnt[tile], 1u);
           const uint64_t t0 = globaltimer_ns();
           while (ld_acquire_u32(&p.ws_tile_cnt[tile]) < static_cast<unsigned>(p.groups)) {
             if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x106);
             __nanosleep(64);
           }
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(rs_bar, static_cast<uint32_t>(p.groups * (BN / 32) * rows_own * 128));
+          for (int g = 0; g < p.groups; ++g)
+            for (int kbx = 0; kbx < BN / 32; ++kbx)
+              tma_load_3d(stg0 + (g * (BN / 32) + kbx) * (rows_own * 128), &em.slice, rs_bar, kbx * 32, own_r0,
+                          slot0 + g);
         }
-        named_bar_sync(1, 32 * kEpiWarps);
-        const int n4 = (own_r1 - own_r0) * BN / 4;
-        constexpr int kU = 4;  // float4 groups in flight per thread
-        for (int base4 = etid; base4 < n4; base4 += kU * 32 * kEpiWarps) {
-          float4 s[kU], o[kU];
-          long long off[kU], flat[kU];
-          bool ok[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int e4 = base4 + u * 32 * kEpiWarps;
-            const int r = own_r0 + (e4 * 4) / BN, c = (e4 * 4) % BN;
-            ok[u] = e4 < n4 && d0 + r < p.D && p0 + c < p.P;  // P % 8 == 0: all-in or all-out
-            off[u] = static_cast<long long>(r) * BN + c;
-            flat[u] = static_cast<long long>(d0 + r) * p.P + p0 + c;
-            s[u] = ok[u] ? __ldcg(reinterpret_cast<const float4*>(slots + off[u])) : make_float4(0.f, 0.f, 0.f, 0.f);
-            o[u] = (ok[u] && rmw_store) ? __ldcg(reinterpret_cast<const float4*>(p.grad_w + flat[u]))
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+        mbar_wait(rs_bar, 0, err, p.budget_ns, 0x107);
+        const int n4 = rows_own * (BN / 4);  // float4 chunks of the slice
+        const int box_bytes = rows_own * 128;
+        for (int e4 = etid; e4 < n4; e4 += 32 * kEpiWarps) {
+          const int kbx = e4 / (rows_own * 8);
+          const int rem = e4 % (rows_own * 8);
+          const int r = rem >> 3, j = rem & 7;
+          const int off = kbx * box_bytes + r * 128 + ((j ^ (r & 7)) << 4);
+          float4 s = *reinterpret_cast<const float4*>(stg0 + off);
           for (int g = 1; g < p.groups; ++g) {
-            float4 t4[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-              t4[u] = ok[u] ? __ldcg(reinterpret_cast<const float4*>(slots + g * tile_elems + off[u]))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              s[u].x += t4[u].x; s[u].y += t4[u].y; s[u].z += t4[u].z; s[u].w += t4[u].w;
-            }
+            const float4 t4 = *reinterpret_cast<const float4*>(stg0 + g * (BN / 32) * box_bytes + off);
+            s.x += t4.x; s.y += t4.y; s.z += t4.z; s.w += t4.w;
           }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            if (!ok[u]) continue;
-            s[u].x += o[u].x; s[u].y += o[u].y; s[u].z += o[u].z; s[u].w += o[u].w;
-            *reinterpret_cast<float4*>(p.grad_w + flat[u]) = s[u];
+          *reinterpret_cast<float4*>(stg0 + off) = s;
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          fence_proxy_async_global();
+          for (int kbx = 0; kbx < BN / 32; ++kbx) {
+            if (rmw_store) tma_reduce_add_2d(&em.gw_slice, stg0 + kbx * box_bytes, p0 + kbx * 32, d0 + own_r0);
+            else tma_store_2d(&em.gw_slice, stg0 + kbx * box_bytes, p0 + kbx * 32, d0 + own_r0);
           }
+          bulk_commit();
+          bulk_wait_all();
         }
         FDP_TRACE(2);
         continue;
@@ -516,8 +589,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const unsigned old = atomicAdd(&p.ws_ctrl[0], 1u);
     if (old == gridDim.x - 1) {
       __threadfence();
-      for (int b = 0; b < p.B; ++b) p.ws_cnt[b] = 0u;
       for (int t = 0; t < p.n_tiles; ++t) p.ws_tile_cnt[t] = 0u;
+      unsigned tag = p.ws_ctrl[2] + 1u;
+      if (tag == 0u) tag = 1u;
+      p.ws_ctrl[2] = tag;  // the next fused launch on this workspace uses tag + 1
       p.ws_ctrl[0] = 0u;
       __threadfence();
     }
@@ -537,8 +612,8 @@ static cudaError_t set_attr_once() {
 }
 
 template <int BN, int CG>
-static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
-                                  bool cooperative, cudaStream_t stream) {
+static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const EpiMaps& em,
+                                  const TcParams& p, int grid, bool cooperative, cudaStream_t stream) {
   using C = TcCfg<BN, CG>;
   cudaError_t e = set_attr_once<BN, CG>();
   if (e != cudaSuccess) return e;
@@ -563,26 +638,26 @@ static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& t
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, p);
+  e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, em, p);
   if (e != cudaSuccess && cooperative && CG == 2) {
     // Some drivers reject cooperative + cluster launches. The grid never exceeds
     // the co-resident capacity (checked by the planner), so fall back to a plain
     // cluster launch; the in-kernel watchdog turns a broken assumption into an error.
     (void)cudaGetLastError();
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, p);
+    e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, em, p);
   }
   return e;
 }
 
-cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const TcParams& p, int grid,
-                      bool cooperative, cudaStream_t stream) {
+cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const EpiMaps& em,
+                      const TcParams& p, int grid, bool cooperative, cudaStream_t stream) {
   if (cg == 2) {
-    if (bn == 256) return launch_tc_impl<256, 2>(tm_dy, tm_x, p, grid, cooperative, stream);
-    return launch_tc_impl<128, 2>(tm_dy, tm_x, p, grid, cooperative, stream);
+    if (bn == 256) return launch_tc_impl<256, 2>(tm_dy, tm_x, em, p, grid, cooperative, stream);
+    return launch_tc_impl<128, 2>(tm_dy, tm_x, em, p, grid, cooperative, stream);
   }
-  if (bn == 256) return launch_tc_impl<256, 1>(tm_dy, tm_x, p, grid, cooperative, stream);
-  return launch_tc_impl<128, 1>(tm_dy, tm_x, p, grid, cooperative, stream);
+  if (bn == 256) return launch_tc_impl<256, 1>(tm_dy, tm_x, em, p, grid, cooperative, stream);
+  return launch_tc_impl<128, 1>(tm_dy, tm_x, em, p, grid, cooperative, stream);
 }
 
 template <int BN, int CG>

@@ -114,7 +114,8 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
          grad_out: Optional[torch.Tensor] = None, norms_out: Optional[torch.Tensor] = None,
          accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
          skip_barrier: bool = False, short_timeout: bool = False, workspace: Optional[torch.Tensor] = None,
-         device_step: Optional[torch.Tensor] = None, norm_phase: str = "auto") -> BackwardResult:
+         device_step: Optional[torch.Tensor] = None, norm_phase: str = "auto",
+         deterministic: bool = False) -> BackwardResult:
     dims = _dims(x, dy)
     if kind != WorkflowKind.NON_DP and cfg is None:
         raise UsageError("DP workflows need a DPConfig")
@@ -128,7 +129,8 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     in_dtype = _input_dtype_code(xd)
 
     c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
-    flags = (_lib.FLAG_SKIP_BARRIER if skip_barrier else 0) | (_lib.FLAG_TIMEOUT_SHORT if short_timeout else 0)
+    flags = ((_lib.FLAG_SKIP_BARRIER if skip_barrier else 0) | (_lib.FLAG_TIMEOUT_SHORT if short_timeout else 0)
+             | (_lib.FLAG_DETERMINISTIC if deterministic else 0))
     desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=in_dtype, reduction=c.reduction,
                           clip_c=c.clip_c, sigma=c.sigma, seed=c.seed, layer_id=c.layer_id, step=c.step, rank=rank,
                           world=world, mean_batch=mean_batch, accumulate=accumulate, add_noise=add_noise,
@@ -216,7 +218,7 @@ class PreparedBackward:
                  path: str = "auto", noise_impl: str = "keyed_f32", accumulate: bool = False,
                  add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
                  device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
-                 norm_phase: str = "auto"):
+                 norm_phase: str = "auto", deterministic: bool = False):
         dims = _dims(x, dy)
         if not (x.is_cuda and dy.is_cuda and x.is_contiguous() and dy.is_contiguous() and x.dtype == dy.dtype):
             raise UsageError("PreparedBackward needs contiguous CUDA inputs of one dtype")
@@ -227,7 +229,8 @@ class PreparedBackward:
                                    reduction=c.reduction, clip_c=c.clip_c, sigma=c.sigma, seed=c.seed,
                                    layer_id=c.layer_id, step=c.step, rank=rank, world=world, mean_batch=mean_batch,
                                    accumulate=accumulate, add_noise=add_noise, noise_impl=noise_impl, path=path,
-                                   norm_phase=norm_phase, device_step=_step_ptr(device_step))
+                                   norm_phase=norm_phase, device_step=_step_ptr(device_step),
+                                   flags=_lib.FLAG_DETERMINISTIC if deterministic else 0)
         self._device_step = device_step
         lib = _lib.load()
         self._lib = lib

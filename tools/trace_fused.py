@@ -47,13 +47,17 @@ def main():
            "loop_end_us_med_max": [float(np.nanmedian(rel[:, 1])), float(np.nanmax(rel[:, 1]))],
            "final_end_us_med_max": [float(np.nanmedian(rel[:, 2])), float(np.nanmax(rel[:, 2]))]}
     units = []
+    out["first_ready_med"] = round(float(np.nanmedian(rel[:, 9])), 2)
+
+    def med(col):
+        v = rel[:, col]
+        return round(float(np.nanmedian(v)), 2) if np.isfinite(v).any() else None
+
     for u in range(n_units):
-        pre, ready, passed = rel[:, 8 + 4 * u], rel[:, 9 + 4 * u], rel[:, 10 + 4 * u]
-        units.append({"u": u, "pre_med": round(float(np.nanmedian(pre)), 2),
-                      "mma_ready_med": round(float(np.nanmedian(ready)), 2),
-                      "mma_ready_max": round(float(np.nanmax(ready)), 2),
-                      "barrier_passed_med": round(float(np.nanmedian(passed)), 2),
-                      "barrier_passed_max": round(float(np.nanmax(passed)), 2)})
+        # slots: 9+4u sample u ready (MMA done), 8+4u published + noise chunk u done, 10+4u factor u known
+        units.append({"u": u, "ready": med(9 + 4 * u), "noise_done": med(8 + 4 * u),
+                      "factor": med(10 + 4 * u),
+                      "factor_max": round(float(np.nanmax(rel[:, 10 + 4 * u])), 2)})
     out["units"] = units
     print(json.dumps(out))
 
