@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--clip", type=float, default=1.0)
     ap.add_argument("--sigma", type=float, default=1.0)
-    ap.add_argument("--noise", default="keyed_f32", choices=["keyed_f32", "keyed_f64", "philox"])
+    ap.add_argument("--noise", default="philox", choices=["keyed_f32", "keyed_f64", "philox"],
+                    help="production noise: Philox (north star); keyed_f32 reproduces the reference draws")
     ap.add_argument("--path", default="auto")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

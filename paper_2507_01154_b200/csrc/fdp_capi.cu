@@ -5,6 +5,7 @@
 #include "fdp_internal.h"
 #include "fdp_rng.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -196,8 +197,9 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   auto allowed = [&](int bn, int cg) {
     return (!forced_bn || bn == forced_bn) && (!forced_cg || cg == forced_cg);
   };
+  const int pcands[4][2] = {{256, 2}, {256, 1}, {128, 2}, {128, 1}};  // persistent: widest tile first
   auto persistent_choice = [&]() {
-    for (auto& cd : cands)
+    for (auto& cd : pcands)
       if (allowed(cd[0], cd[1]) && fdp::tc_max_coresident_ctas(cd[0], cd[1]) > 0) {
         pl.bn = cd[0];
         pl.cg = cd[1];
@@ -216,8 +218,16 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     if (want == FDP_PATH_SIMT || !tc_ok) {
       pl.path = FDP_PATH_SIMT;
     } else {
-      // choose the tile shape that best fills the SMs with co-resident CTAs
-      double best = -1.0;
+      // Choose the tile shape with the smallest modelled time: per-CTA samples x
+      // one sample's MMA time at the measured per-SM rate of that shape, plus the
+      // cross-group reduction when samples are split over CTAs. Per-SM rates
+      // (TFLOP/s, B200, fused loop; tools/trace_fused.py): operand traffic per
+      // flop halves from a 128x128 single-CTA tile to a 256x256 CTA-pair tile.
+      auto sm_rate = [](int bn, int cg) {
+        if (bn == 256) return cg == 2 ? 9.6e12 : 7.4e12;
+        return cg == 2 ? 6.4e12 : 6.3e12;
+      };
+      double best = 1e300;
       int best_bn = 0, best_cg = 1, best_groups = 1;
       for (auto& cd : cands) {
         const int bn = cd[0], cg = cd[1];
@@ -231,14 +241,25 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
         if (g > d->B) g = d->B;
         if (g > 8) g = 8;
         while (g & (g - 1)) --g;  // 1, 2, 4 or 8: slices of 128 rows stay whole 8-row swizzle atoms
-        const double util = static_cast<double>(need * g) / di.sms;
-        if (util > best + 0.02) {
-          best = util;
+        const double units = static_cast<double>((d->B + g - 1) / g);
+        const double unit_flops = 2.0 * fdp::kBM * bn * static_cast<double>(d->T);
+        // a sample is never faster than one block-wise all-reduce round (~2.5 us)
+        const double unit_t = std::max(unit_flops / sm_rate(bn, cg), 2.5e-6);
+        const double est = units * unit_t + (g > 1 ? 4e-6 : 0.0) + 8e-6;
+        if (est < best * 0.97) {
+          best = est;
           best_bn = bn;
           best_cg = cg;
           best_groups = static_cast<int>(g);
         }
       }
+      // two-phase estimate: norm phase + one reweighted pass at the persistent rate
+      const double dw_flops = 2.0 * d->B * d->T * static_cast<double>(d->P) * d->D;
+      const double nT = static_cast<double>((d->T + 127) / 128);
+      const double ghost_flops = d->B * static_cast<double>(d->T) * d->T * (d->P + d->D) * (1.0 + 1.0 / nT);
+      const double norm_flops = std::min(ghost_flops, dw_flops);
+      const double two_phase_est = (norm_flops / 0.55e15) + dw_flops / 1.1e15 + 25e-6;
+      if (best_bn && want == FDP_PATH_AUTO && two_phase_est < 0.8 * best) best_bn = 0;
       if (best_bn && want != FDP_PATH_TWO_PHASE) {
         pl.path = FDP_PATH_FUSED;
         pl.bn = best_bn;

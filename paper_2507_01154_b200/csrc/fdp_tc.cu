@@ -191,6 +191,54 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
+  } else if (warp == 2 || warp == 3) {
+    // ======================= noise warps (warpgroup 0's spare warps) =======================
+    // Pre-fill this CTA's rows of grad_w with (accumulate ? grad_w : 0) + sigma*C*noise
+    // (rng.py keyed draws or Philox, 4 consecutive columns per thread) while the MMA
+    // and the epilogue run; the epilogue waits on named barrier 2 before its final
+    // (reduce-add) store. No accumulator registers live here.
+    const bool dp_sum = p.mode == MODE_FUSED || p.mode == MODE_REWEIGHT;
+    const bool reduce_scatter = fused && p.groups > 1;
+    const bool atomic_groups = reduce_scatter && !p.deterministic;
+    const bool pre_noise = (dp_sum && p.add_noise) || atomic_groups;
+    const bool draw_noise = dp_sum && p.add_noise;
+    if (pre_noise) {
+      uint64_t kb = p.key_base, kbg = p.key_base_g;
+      if (p.step_ptr) {
+        kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
+        kbg = kb + kGamma;
+      }
+      const int own_r0 = reduce_scatter ? group * kBM / p.groups : 0;
+      const int own_r1 = reduce_scatter ? (group + 1) * kBM / p.groups : kBM;
+      const int ntid = (warp - 2) * 32 + lane;
+      for (int wt = first_wt; wt < p.n_wtiles; wt += wt_stride) {
+        const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+        const int p0 = (wt % p.n_pt) * BN;
+        const int q_all = (own_r1 - own_r0) * (BN / 4);
+        for (int e4 = ntid; e4 < q_all; e4 += 64) {
+          const int dd = d0 + own_r0 + e4 / (BN / 4);
+          const int pp = p0 + (e4 % (BN / 4)) * 4;
+          if (dd < p.D && pp < p.P) {  // P % 8 == 0: a float4 never straddles a row or the tile edge
+            const long long flat = static_cast<long long>(dd) * p.P + pp;
+            float4* dst = reinterpret_cast<float4*>(p.grad_w + flat);
+            float4 v = p.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (draw_noise && flat + 3 >= p.noise_lo && flat < p.noise_hi) {
+              const float4 n = noise_draw4(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
+              const float s = p.noise_scale;
+              if (flat + 0 >= p.noise_lo && flat + 0 < p.noise_hi) v.x += s * n.x;
+              if (flat + 1 >= p.noise_lo && flat + 1 < p.noise_hi) v.y += s * n.y;
+              if (flat + 2 >= p.noise_lo && flat + 2 < p.noise_hi) v.z += s * n.z;
+              if (flat + 3 >= p.noise_lo && flat + 3 < p.noise_hi) v.w += s * n.w;
+            }
+            __stcg(dst, v);
+          }
+        }
+        __threadfence();
+        // bar.sync (not arrive): the noise warps must not run a whole tile ahead
+        // of the epilogue in persistent modes, or barrier generations would mix
+        named_bar_sync(2, 32 * (2 + kEpiWarps));
+      }
+    }
   } else if (warp >= kEpiWarp0) {
     // ======================= epilogue (8 warps per CTA) =======================
     const int ew = warp - kEpiWarp0;
@@ -220,21 +268,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     auto taddr = [&](uint32_t b) { return tmem_base + (static_cast<uint32_t>(q * 32) << 16) + b * BN + col0; };
 
     const bool dp_sum = p.mode == MODE_FUSED || p.mode == MODE_REWEIGHT;
-    uint64_t kb = p.key_base, kbg = p.key_base_g;
-    if (p.step_ptr) {
-      kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
-      kbg = kb + kGamma;
-    }
     const bool reduce_scatter = fused && p.groups > 1;
-    // noise is pre-written into grad_w in chunks while the MMA / the norm
-    // all-reduce are in flight; with sample groups each CTA draws only its slice.
-    // grad_w rows are pre-filled (old value if accumulating, + noise) during the
-    // sample loop when noise is drawn, and always when sample groups combine their
+    // grad_w rows are pre-filled by the noise warps (old value if accumulating,
+    // + noise) when noise is drawn, and always when sample groups combine their
     // tiles with TMA reduce-add (every group then adds onto initialised rows).
     const bool atomic_groups = reduce_scatter && !p.deterministic;
     const bool pre_noise = (dp_sum && p.add_noise) || atomic_groups;
     const bool rmw_store = pre_noise || p.accumulate;
-    const bool draw_noise = dp_sum && p.add_noise;
     // launch tag of the tagged norm-partial slots (bumped by the last CTA at exit)
     unsigned tag = __ldcg(p.ws_ctrl + 2) + 1u;
     if (tag == 0u) tag = 1u;
@@ -272,31 +312,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
           __syncwarp();
-        }
-      };
-      auto noise_chunk = [&](int unit) {
-        // grad_w = (accumulate ? grad_w : 0) + sigma*C*n(flat) over chunk `unit` of
-        // this CTA's rows, 4 consecutive columns per thread (P % 8 == 0)
-        const int q_all = (own_r1 - own_r0) * (BN / 4);
-        const int q_lo = static_cast<int>((static_cast<long long>(unit) * q_all) / n_units);
-        const int q_hi = static_cast<int>((static_cast<long long>(unit + 1) * q_all) / n_units);
-        for (int e4 = q_lo + etid; e4 < q_hi; e4 += 32 * kEpiWarps) {
-          const int dd = d0 + own_r0 + e4 / (BN / 4);
-          const int pp = p0 + (e4 % (BN / 4)) * 4;
-          if (dd < p.D && pp < p.P) {
-            const long long flat = static_cast<long long>(dd) * p.P + pp;
-            float4* dst = reinterpret_cast<float4*>(p.grad_w + flat);
-            float4 v = p.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (draw_noise && flat + 3 >= p.noise_lo && flat < p.noise_hi) {
-              const float4 n = noise_draw4(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
-              const float s = p.noise_scale;
-              if (flat + 0 >= p.noise_lo && flat + 0 < p.noise_hi) v.x += s * n.x;
-              if (flat + 1 >= p.noise_lo && flat + 1 < p.noise_hi) v.y += s * n.y;
-              if (flat + 2 >= p.noise_lo && flat + 2 < p.noise_hi) v.z += s * n.z;
-              if (flat + 3 >= p.noise_lo && flat + 3 < p.noise_hi) v.w += s * n.w;
-            }
-            __stcg(dst, v);
-          }
         }
       };
       // pass 1 + publish: intra-block reduce of ||G_b||^2 (workflows.py:387-389)
@@ -355,6 +370,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               const int i = lane + 32 * k;
               while (static_cast<unsigned>(v[k] >> 32) != tag) {
                 if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
+                __nanosleep(32);
                 v[k] = ld_relaxed_u64(slots + i);
               }
             }
@@ -403,7 +419,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t b = wait_ready();
           FDP_TRACE(9 + 4 * u);
           publish(ub, b);
-          if (pre_noise) noise_chunk(u);
           FDP_TRACE(8 + 4 * u);
           const float f = wait_factor(ub);
           FDP_TRACE(10 + 4 * u);
@@ -413,7 +428,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       } else if (p.mode == MODE_REWEIGHT) {
         int u = 0;
         for (int ub = b0; ub < p.B; ub += b_step, ++u) {
-          if (pre_noise) noise_chunk(u);
           const uint32_t b = wait_ready();
           accumulate_scaled(b, p.factors_in[ub]);
           release(b);
@@ -457,6 +471,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         release(b);
       }
       FDP_TRACE(1);
+      // grad_w rows pre-filled by the noise warps (generic stores, fenced) before
+      // any store / TMA reduce-add of this tile
+      if (pre_noise) named_bar_sync(2, 32 * (2 + kEpiWarps));
 
       if (fused) {
         // ---- epilogue I/O through TMA. The accumulator tile goes to shared memory
@@ -563,12 +580,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         continue;
       }
 
-      // ---- finalize: mean is folded into the clip factor; the noise (if any) is
-      // already in grad_w from the noise chunks (written by other threads: sync first).
-      if (pre_noise) {
-        __threadfence_block();
-        named_bar_sync(1, 32 * kEpiWarps);
-      }
+      // ---- finalize (persistent modes): mean is folded into the clip factor; the
+      // noise (if any) is already in grad_w.
       store_tile(p.grad_w + static_cast<long long>(d0) * p.P + p0, p.P, p.D - d0, p.P - p0, rmw_store, acc);
       FDP_TRACE(2);
     }

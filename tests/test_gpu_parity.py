@@ -369,7 +369,7 @@ def test_dplinear_autograd_matches_oracle():
     want, wn = O.dp_backward(host(x.detach()), host(dy.to(torch.bfloat16)), O.Cfg(0.5, 0.0, "mean"))
     assert rel(host(lin.weight.grad), want) < BF16_TOL
     assert rel(host(lin.last_norms_sq), wn) < BF16_TOL
-    dx_want = (dy.float() @ lin.weight.float()).to(torch.bfloat16)
+    dx_want = (dy.float() @ lin.weight.detach().float()).to(torch.bfloat16)
     assert rel(host(x.grad), host(dx_want)) < 1e-2
     # bias: per-sample sum_t dY, clipped at C, mean over the batch
     gb = host(dy.float()).sum(axis=1)
@@ -392,3 +392,13 @@ def test_dplinear_micro_batches_add_noise_once():
         lin(xi).backward(dy[2 * i:2 * i + 2])
     want, _ = O.dp_backward(host(x), host(dy), O.Cfg(1.0, 1.0, "mean", 0, 1, 7), exact_noise=False)
     assert rel(host(lin.weight.grad), want) < BF16_TOL
+
+
+@pytest.mark.parametrize("norm_phase", ["ghost", "recompute"])
+def test_two_phase_many_tiles_per_cta(norm_phase):
+    """Persistent two-phase launch: several output tiles per CTA and several
+    samples per tile (noise warps, TMEM buffers and barriers cycle across tiles)."""
+    x, dy = randn(6, 256, 2048, 2048, seed=21, scale_dy=1e-2)
+    cfg = fdp.DPConfig(0.05, 1.0, "mean", seed=9, layer_id=4, step=2)
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase=norm_phase)
+    check(r, x, dy, cfg, BF16_TOL)
