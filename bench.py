@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nondp", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
+    ap.add_argument("--per-layer", action="store_true",
+                    help="one fused launch per layer instead of one multi-layer launch per step")
     return ap.parse_args()
 
 
@@ -235,12 +237,31 @@ def main():
                                  device_step=device_step, workspace=shared_ws)
         calls.append((name, c))
     plans = {n: c.plan for n, c in calls[:4]}
+    group = None
+    if not a.per_layer:
+        glayers = [(xs[name], dys[name], fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234,
+                                                      layer_id=lid, step=0)) for lid, name, P, D in layers]
+        group = fdp.PreparedGroup(glayers, grads=[c.grad_w for _, c in calls], noise_impl=a.noise, rank=rank,
+                                  world=world, mean_batch=global_B, device_step=device_step)
 
     stream = torch.cuda.current_stream(dev)
     dominant = "h0.c_fc"  # largest per-launch work; every block's c_fc is timed
     dom_events = []
 
     def step(record=False):
+        if group is not None:
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                group(stream)
+                e1.record(stream)
+                dom_events.append((e0, e1))
+            else:
+                group(stream)
+            device_step.add_(1)
+            if world > 1:
+                dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+            return
         for name, c in calls:
             if record and name.endswith(".c_fc"):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -295,7 +316,7 @@ def main():
 
     # dominant kernel: fused DP-dW launch of the c_fc layers, CUDA events on the launch stream
     dom_ms = [e0.elapsed_time(e1) for e0, e1 in dom_events] if dom_events else []
-    dom_flops = 2 * B * T * 768 * 3072
+    dom_flops = flops_per_step_rank if group is not None else 2 * B * T * 768 * 3072
     peaks, peak_kind = load_peaks()
     dom_avg_s = (statistics.mean(dom_ms) * 1e-3) if dom_ms else None
     achieved = dom_flops / dom_avg_s / 1e12 if dom_avg_s else None
@@ -311,11 +332,27 @@ def main():
                 "peak_source": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)",
                 "frac_of_sustained": (achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
                 if achieved else None,
-                "kernel": "dpdw_tc_kernel (MODE_FUSED) on c_fc: B=%d T=%d P=768 D=3072" % (B, T),
+                "kernel": ("dpdw_group_kernel: fused DP backward of all 48 layers in one launch, B=%d T=%d" % (B, T))
+                if group is not None else "dpdw_tc_kernel (MODE_FUSED) on c_fc: B=%d T=%d P=768 D=3072" % (B, T),
                 "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_avg_s * 1e3 if dom_avg_s else None,
                 "launches_timed": len(dom_ms)}
 
     extra = {}
+    if group is not None:
+        def per_layer_step():
+            for _, c in calls:
+                c(stream)
+        for _ in range(3):
+            per_layer_step()
+        torch.cuda.synchronize()
+        p0e, p1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0e.record(stream)
+        n_pl = max(10, a.steps // 4)
+        for _ in range(n_pl):
+            per_layer_step()
+        p1e.record(stream)
+        torch.cuda.synchronize()
+        extra["per_layer_launches_ms_per_step"] = p0e.elapsed_time(p1e) / n_pl
     # ---- non-DP baseline (same layers, plain bf16 dW GEMM): cuBLAS and our tcgen05 kernel
     if not a.no_nondp:
         def nondp_cublas():
@@ -417,7 +454,7 @@ def main():
                        "graph": bool(graph is not None)},
             "tflops_per_gpu": flops_per_step_rank / (ms_per_step * 1e-3) / 1e12,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": (len(calls) * a.steps),
+            "gpu_launches": (a.steps if group is not None else len(calls) * a.steps),
             "plans": {k: {"path": fdp._lib.PATH_NAMES[v.path], "tile": [v.tile_d, v.tile_p], "groups": v.groups,
                           "grid": v.grid} for k, v in plans.items()},
         }

@@ -163,6 +163,18 @@ FDP_API int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const v
 FDP_API int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
            void* ws, size_t ws_bytes, void* stream);
 
+/* The fused DP backward of n layers (n <= 48) in ONE persistent cooperative
+ * launch: the training-step batching of Algorithm 1 (every layer keeps its own
+ * DPConfig, noise key, per-sample norms and outputs; the producer/MMA/epilogue
+ * pipelines never drain between layers). Every layer must be tensor-core
+ * eligible (bf16, P % 8 == 0, D % 8 == 0) and fit the co-resident fused grid;
+ * otherwise FDP_ERR_USAGE (call fdp_backward per layer instead). The arrays
+ * hold one device pointer per layer; the workspace is shared by all layers. */
+FDP_API int fdp_group_workspace_bytes(int32_t n, const fdp_desc* descs, size_t* bytes);
+FDP_API int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, const void* const* dy,
+                               float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes,
+                               void* stream);
+
 /* dpcore.noise_for_indices for flat indices [lo, hi) scaled by `scale`
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -607,6 +608,77 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   return FDP_OK;
 }
 
+
+// ---- multi-layer fused launch
+struct GroupPlan {
+  int bn = 0, cg = 1, grid = 0;
+  std::vector<int> groups, n_dt2, n_pt, n_wtiles;
+  std::vector<size_t> off_tagged, off_tile_cnt;
+  size_t total = 0;
+};
+
+int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl) {
+  if (n < 1 || n > fdp::kMaxGroupLayers)
+    return fail(FDP_ERR_USAGE, "fdp_backward_group takes 1..%d layers, got %d", fdp::kMaxGroupLayers, n);
+  if (di.major != 10) return fail(FDP_ERR_USAGE, "fdp_backward_group needs an sm_100 device");
+  for (int l = 0; l < n; ++l) {
+    int rc = validate(&descs[l], FDP_KIND_FLASHDP);
+    if (rc) return rc;
+    if (!tc_shape_ok(&descs[l]))
+      return fail(FDP_ERR_USAGE, "layer %d is not tensor-core eligible (bf16, P %% 8 == 0, D %% 8 == 0)", l);
+  }
+  const int cands[4][2] = {{256, 2}, {128, 2}, {256, 1}, {128, 1}};
+  const int forced_bn = env_int("FDP_FORCE_BN", 0), forced_cg = env_int("FDP_FORCE_CG", 0);
+  double best = 1e300;
+  for (auto& cd : cands) {
+    const int bn = cd[0], cg = cd[1];
+    if ((forced_bn && bn != forced_bn) || (forced_cg && cg != forced_cg)) continue;
+    const long long cap = fdp::tc_max_coresident_ctas(bn, cg);
+    if (cap <= 0) continue;
+    const double rate = bn == 256 ? (cg == 2 ? 9.6e12 : 7.4e12) : (cg == 2 ? 6.4e12 : 6.3e12);
+    double est = 0.0;
+    bool ok = true;
+    GroupPlan cand;
+    cand.bn = bn;
+    cand.cg = cg;
+    for (int l = 0; l < n && ok; ++l) {
+      const fdp_desc* d = &descs[l];
+      const long long ndt = (d->D + fdp::kBM - 1) / fdp::kBM;
+      const int ndt2 = static_cast<int>((ndt + cg - 1) / cg);
+      const int npt = static_cast<int>((d->P + bn - 1) / bn);
+      const long long need = static_cast<long long>(ndt2) * npt * cg;
+      if (need > cap) { ok = false; break; }
+      long long g = cap / need;
+      if (g > d->B) g = d->B;
+      if (g > 8) g = 8;
+      while (g & (g - 1)) --g;
+      const double units = static_cast<double>((d->B + g - 1) / g);
+      est += units * std::max(2.0 * fdp::kBM * bn * static_cast<double>(d->T) / rate, 2.5e-6) + (g > 1 ? 3e-6 : 0.0);
+      cand.groups.push_back(static_cast<int>(g));
+      cand.n_dt2.push_back(ndt2);
+      cand.n_pt.push_back(npt);
+      cand.n_wtiles.push_back(ndt2 * npt);
+      cand.grid = std::max(cand.grid, static_cast<int>(need * g));
+    }
+    if (ok && est < best * 0.97) {
+      best = est;
+      gpl = cand;
+    }
+  }
+  if (!gpl.bn) return fail(FDP_ERR_USAGE, "a layer does not fit the co-resident fused grid; use fdp_backward per layer");
+  size_t off = 256;  // control words
+  for (int l = 0; l < n; ++l) {
+    const long long ntiles = static_cast<long long>(gpl.n_wtiles[l]) * gpl.cg;
+    gpl.off_tagged.push_back(off);
+    off = align_up(off + 8ull * descs[l].B * ntiles, 256);
+    gpl.off_tile_cnt.push_back(off);
+    off = align_up(off + 4ull * ntiles, 256);
+  }
+  if (descs[0].flags & FDP_FLAG_TRACE) off += 2048ull * gpl.grid;  // [grid][256] u64
+  gpl.total = off;
+  return FDP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -673,6 +745,82 @@ int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const void* dy,
 int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq, void* ws,
            size_t ws_bytes, void* stream) {
   return run(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+
+int fdp_group_workspace_bytes(int32_t n, const fdp_desc* descs, size_t* bytes) {
+  if (!descs || !bytes) return fail(FDP_ERR_USAGE, "null argument");
+  DevInfo di;
+  int rc = get_dev(di);
+  if (rc) return rc;
+  GroupPlan gpl;
+  if ((rc = plan_group(n, descs, di, gpl))) return rc;
+  *bytes = gpl.total;
+  return FDP_OK;
+}
+
+int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, const void* const* dy,
+                       float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes, void* stream) {
+  if (!descs || !x || !dy || !grad_w || !norms_sq) return fail(FDP_ERR_USAGE, "null argument");
+  DevInfo di;
+  int rc = get_dev(di);
+  if (rc) return rc;
+  GroupPlan gpl;
+  if ((rc = plan_group(n, descs, di, gpl))) return rc;
+  if (!ws || ws_bytes < gpl.total)
+    return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
+                gpl.total);
+  static thread_local fdp::GroupParams gp;  // ~28 KB: keep it off the stack
+  std::memset(&gp, 0, sizeof(gp));
+  for (int l = 0; l < n; ++l) {
+    const fdp_desc* d = &descs[l];
+    if (!x[l] || !dy[l] || !grad_w[l] || !norms_sq[l]) return fail(FDP_ERR_USAGE, "null tensor pointer (layer %d)", l);
+    if (!(aligned16(x[l]) && aligned16(dy[l]) && aligned16(grad_w[l])))
+      return fail(FDP_ERR_USAGE, "layer %d: x, dy and grad_w must be 16-byte aligned", l);
+    fdp::GLayer& L = gp.L[l];
+    if ((rc = make_tmap(&L.tm_dy, dy[l], d->D, d->T, d->B))) return rc;
+    if ((rc = make_tmap(&L.tm_x, x[l], d->P, d->T, d->B))) return rc;
+    const cuuint64_t gdims[2] = {static_cast<cuuint64_t>(d->P), static_cast<cuuint64_t>(d->D)};
+    const cuuint64_t gstr[1] = {static_cast<cuuint64_t>(d->P * 4)};
+    const cuuint32_t gbox[2] = {32, static_cast<cuuint32_t>(fdp::kBM)};
+    if ((rc = make_tmap_f32(&L.gw, grad_w[l], 2, gdims, gstr, gbox))) return rc;
+    const Common c = common_of(d);
+    L.grad_w = grad_w[l];
+    L.norms_out = norms_sq[l];
+    L.tagged = ws_at<unsigned long long>(ws, gpl.off_tagged[l]);
+    L.tile_cnt = ws_at<unsigned>(ws, gpl.off_tile_cnt[l]);
+    L.key_base = c.key_base;
+    L.key_base_g = c.key_base_g;
+    L.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+    L.seed_u = static_cast<uint64_t>(d->seed);
+    L.layer_u = static_cast<uint64_t>(d->layer_id);
+    L.noise_lo = c.noise_lo;
+    L.noise_hi = c.noise_hi;
+    L.clip_c = d->clip_c;
+    L.clip_c2 = d->clip_c * d->clip_c;
+    L.inv_batch = c.inv_batch;
+    L.noise_scale = c.noise_scale;
+    L.B = static_cast<int>(d->B);
+    L.T = static_cast<int>(d->T);
+    L.P = static_cast<int>(d->P);
+    L.D = static_cast<int>(d->D);
+    L.n_dt2 = gpl.n_dt2[l];
+    L.n_pt = gpl.n_pt[l];
+    L.n_wtiles = gpl.n_wtiles[l];
+    L.n_tiles = gpl.n_wtiles[l] * gpl.cg;
+    L.groups = gpl.groups[l];
+    L.n_kb = static_cast<int>((d->T + fdp::kBK - 1) / fdp::kBK);
+    L.accumulate = d->accumulate;
+    L.add_noise = c.add_noise;
+    L.noise_impl = d->noise_impl;
+  }
+  gp.ctrl = ws_at<unsigned>(ws, 0);
+  gp.budget_ns = (descs[0].flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+  gp.trace = (descs[0].flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, gpl.total - 2048ull * gpl.grid) : nullptr;
+  gp.n_layers = n;
+  cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "group launch");
+  return FDP_OK;
 }
 
 int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream) {

@@ -1,0 +1,412 @@
+// fdp_group.cu -- the fused DP weight-gradient backward of a LIST of layers in one
+// persistent cooperative launch.
+//
+// Same per-layer algorithm as dpdw_tc_kernel's MODE_FUSED (Algorithm 1,
+// PAPER.md:109-137; workflows.py:340-421), but the TMA producer, the MMA issuer,
+// the noise warps and the epilogue all walk the layer list in the same order,
+// so the pipelines never drain between layers: layer l+1's operand loads and
+// first MMAs run while layer l's epilogue finishes its last norm all-reduce and
+// its TMA stores. Every layer keeps its own tagged norm-partial slots and tile
+// counters; a CTA whose cluster id is beyond a layer's work simply skips it.
+// Layer descriptors (with their TMA maps) are a __grid_constant__ parameter
+// block, so the launch is CUDA-graph capturable with no host->device copy.
+#include <cstdio>
+#include <cstdlib>
+
+#include "fdp_internal.h"
+#include "fdp_ptx.cuh"
+#include "fdp_rng.cuh"
+
+namespace fdp {
+
+template <int BN, int CG>
+struct GCfg {
+  static constexpr int kBCols = BN / CG;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = kBCols * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStgBytes = 2 * kBM * 128;  // two 32-column fp32 boxes (one per column half)
+  static constexpr int kStages = (232448 - 2048 - kStgBytes) / kStageBytes;
+  static constexpr int kNBuf = 512 / BN;
+  static constexpr int kCPT = BN / 2;
+  static constexpr int kBarBytes = 1024;
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + kStgBytes + kBarBytes;
+  static constexpr uint32_t kIdesc = make_idesc_bf16_mn(kBM * CG, BN);
+};
+
+#define GTRACE(slot)                                                                                 \
+  do {                                                                                               \
+    if (gp.trace && etid == 0 && (slot) < 256) gp.trace[blockIdx.x * 256 + (slot)] = globaltimer_ns(); \
+  } while (0)
+
+template <int BN, int CG>
+__global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_constant__ GroupParams gp) {
+  using C = GCfg<BN, CG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = smem + C::kStages * C::kStageBytes;  // 1024-aligned: two 16 KB swizzled boxes
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::kStgBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kNBuf;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);
+  float* bcast = red + kEpiWarps;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned* err = gp.ctrl + 1;
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / CG;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < C::kNBuf; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps * CG);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair<512>(tmem_holder);
+    else tmem_alloc<512>(tmem_holder);
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  unsigned tag = __ldcg(gp.ctrl + 2) + 1u;
+  if (tag == 0u) tag = 1u;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int l = 0; l < gp.n_layers; ++l) {
+        const GLayer& L = gp.L[l];
+        if (cid >= L.n_wtiles * L.groups) continue;
+        const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
+        const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
+        const int p0 = (wt % L.n_pt) * BN + rank * C::kBCols;
+        for (int b = group; b < L.B; b += L.groups) {
+          for (int kb = 0; kb < L.n_kb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1, err, gp.budget_ns, 0x401);
+            uint8_t* sa = smem + stage * C::kStageBytes;
+            uint8_t* sb = sa + C::kABytes;
+            if constexpr (CG == 2) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], C::kStageBytes * CG);
+              tma_load_3d_pair(sa, &L.tm_dy, &full[stage], d0, kb * kBK, b);
+              tma_load_3d_pair(sa + 8192, &L.tm_dy, &full[stage], d0 + 64, kb * kBK, b);
+#pragma unroll
+              for (int j = 0; j < C::kBCols / 64; ++j)
+                tma_load_3d_pair(sb + j * 8192, &L.tm_x, &full[stage], p0 + 64 * j, kb * kBK, b);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+              tma_load_3d(sa, &L.tm_dy, &full[stage], d0, kb * kBK, b);
+              tma_load_3d(sa + 8192, &L.tm_dy, &full[stage], d0 + 64, kb * kBK, b);
+#pragma unroll
+              for (int j = 0; j < C::kBCols / 64; ++j)
+                tma_load_3d(sb + j * 8192, &L.tm_x, &full[stage], p0 + 64 * j, kb * kBK, b);
+            }
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA) =======================
+    if (lane == 0 && leader) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      for (int l = 0; l < gp.n_layers; ++l) {
+        const GLayer& L = gp.L[l];
+        if (cid >= L.n_wtiles * L.groups) continue;
+        const int group = cid / L.n_wtiles;
+        for (int b = group; b < L.B; b += L.groups) {
+          mbar_wait(&tempty[buf], tphase ^ 1, err, gp.budget_ns, 0x402);
+          tc_fence_after();
+          const uint32_t dtm = tmem_base + buf * BN;
+          for (int kb = 0; kb < L.n_kb; ++kb) {
+            mbar_wait(&full[stage], phase, err, gp.budget_ns, 0x403);
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t b_base = a_base + C::kABytes;
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ad = make_sdesc_sw128(a_base + k * 2048, 8192, 1024);
+              const uint64_t bd = make_sdesc_sw128(b_base + k * 2048, 8192, 1024);
+              if constexpr (CG == 2) tc_mma_f16_pair(dtm, ad, bd, C::kIdesc, (kb | k) != 0);
+              else tc_mma_f16(dtm, ad, bd, C::kIdesc, (kb | k) != 0);
+            }
+            if constexpr (CG == 2) tc_commit_pair(&empty[stage]);
+            else tc_commit(&empty[stage]);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
+          if constexpr (CG == 2) tc_commit_pair(&tfull[buf]);
+          else tc_commit(&tfull[buf]);
+          if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ======================= noise warps: pre-fill this CTA's grad_w rows =======================
+    const int ntid = (warp - 2) * 32 + lane;
+    for (int l = 0; l < gp.n_layers; ++l) {
+      const GLayer& L = gp.L[l];
+      if (cid >= L.n_wtiles * L.groups) continue;
+      const bool draw = L.add_noise != 0;
+      const bool prefill = draw || L.groups > 1;
+      if (!prefill) continue;
+      uint64_t kb = L.key_base, kbg = L.key_base_g;
+      if (L.step_ptr) {
+        kb = absorb3(L.seed_u, L.layer_u, static_cast<uint64_t>(*L.step_ptr));
+        kbg = kb + kGamma;
+      }
+      const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
+      const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
+      const int p0 = (wt % L.n_pt) * BN;
+      const int r0 = group * kBM / L.groups, r1 = (group + 1) * kBM / L.groups;
+      const int q_all = (r1 - r0) * (BN / 4);
+      for (int e4 = ntid; e4 < q_all; e4 += 64) {
+        const int dd = d0 + r0 + e4 / (BN / 4);
+        const int pp = p0 + (e4 % (BN / 4)) * 4;
+        if (dd < L.D && pp < L.P) {
+          const long long flat = static_cast<long long>(dd) * L.P + pp;
+          float4* dst = reinterpret_cast<float4*>(L.grad_w + flat);
+          float4 v = L.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (draw && flat + 3 >= L.noise_lo && flat < L.noise_hi) {
+            const float4 n = noise_draw4(L.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
+            const float s = L.noise_scale;
+            if (flat + 0 >= L.noise_lo && flat + 0 < L.noise_hi) v.x += s * n.x;
+            if (flat + 1 >= L.noise_lo && flat + 1 < L.noise_hi) v.y += s * n.y;
+            if (flat + 2 >= L.noise_lo && flat + 2 < L.noise_hi) v.z += s * n.z;
+            if (flat + 3 >= L.noise_lo && flat + 3 < L.noise_hi) v.w += s * n.w;
+          }
+          __stcg(dst, v);
+        }
+      }
+      __threadfence();
+      named_bar_sync(2, 32 * (2 + kEpiWarps));
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ======================= epilogue =======================
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
+    const int row = q * 32 + lane, col0 = half * C::kCPT;
+    uint32_t rbuf = 0, rph = 0;
+    for (int l = 0; l < gp.n_layers; ++l) {
+      const GLayer& L = gp.L[l];
+      if (cid >= L.n_wtiles * L.groups) continue;
+      const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
+      const int tile = wt * CG + rank;
+      const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
+      const int p0 = (wt % L.n_pt) * BN;
+      const bool prefill = L.add_noise != 0 || L.groups > 1;
+      const bool rmw = prefill || L.accumulate;
+      float acc[C::kCPT];
+#pragma unroll
+      for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
+
+      bool first = true;
+      for (int b = group; b < L.B; b += L.groups) {
+        mbar_wait(&tfull[rbuf], rph, err, gp.budget_ns, 0x404);
+        tc_fence_after();
+        if (first) GTRACE(3 * l);  // layer l: first sample's MMA done
+        first = false;
+        const uint32_t buf = rbuf;
+        if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
+        // intra-block reduce of ||G_b||^2, published as one tagged 8-byte store
+        float part = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tb + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) red[ew] = part;
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          float s = 0.0f;
+#pragma unroll
+          for (int w = 0; w < kEpiWarps; ++w) s += red[w];
+          st_relaxed_u64(L.tagged + static_cast<long long>(b) * L.n_tiles + tile,
+                         (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s));
+        }
+        // block-wise all-reduce: fixed-order fp64 sum of the tagged partials
+        if (ew == 0) {
+          const unsigned long long* slots = L.tagged + static_cast<long long>(b) * L.n_tiles;
+          constexpr int kMaxPer = 5;
+          unsigned long long v[kMaxPer];
+#pragma unroll
+          for (int k = 0; k < kMaxPer; ++k) {
+            const int i = lane + 32 * k;
+            v[k] = i < L.n_tiles ? ld_relaxed_u64(slots + i) : (static_cast<unsigned long long>(tag) << 32);
+          }
+          const uint64_t t0 = globaltimer_ns();
+#pragma unroll
+          for (int k = 0; k < kMaxPer; ++k) {
+            while (static_cast<unsigned>(v[k] >> 32) != tag) {
+              if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x405);
+              __nanosleep(32);
+              v[k] = ld_relaxed_u64(slots + lane + 32 * k);
+            }
+          }
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < kMaxPer; ++k)
+            if (lane + 32 * k < L.n_tiles) s += static_cast<double>(__uint_as_float(static_cast<unsigned>(v[k])));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) {
+            const double cf = (s <= L.clip_c2) ? 1.0 : L.clip_c / sqrt(s);  // dpcore.py:41-47
+            *bcast = static_cast<float>(cf) * L.inv_batch;
+            if (tile == 0) L.norms_out[b] = static_cast<float>(s);
+          }
+        }
+        named_bar_sync(1, 32 * kEpiWarps);
+        const float f = *bcast;
+#pragma unroll
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tb + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_leader(&tempty[buf]);
+          else mbar_arrive(&tempty[buf]);
+        }
+      }
+
+      GTRACE(3 * l + 1);  // layer l: last clip factor applied
+      // ---- finalize: wait for the noise warps' pre-fill (and, with sample groups,
+      // for every group's pre-fill), then TMA store / reduce-add in 32-column boxes
+      if (prefill) named_bar_sync(2, 32 * (2 + kEpiWarps));
+      if (L.groups > 1) {
+        __threadfence();
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          red_release_add_u32(&L.tile_cnt[tile], 1u);
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire_u32(&L.tile_cnt[tile]) < static_cast<unsigned>(L.groups)) {
+            if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x406);
+            __nanosleep(64);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C::kCPT / 32; ++c) {
+        if (etid == 0) bulk_wait_read_all();  // the previous boxes have left the staging buffer
+        named_bar_sync(1, 32 * kEpiWarps);
+        uint8_t* box = stg + half * (kBM * 128) + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) =
+              make_float4(acc[c * 32 + 4 * j], acc[c * 32 + 4 * j + 1], acc[c * 32 + 4 * j + 2],
+                          acc[c * 32 + 4 * j + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          fence_proxy_async_global();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = p0 + h * C::kCPT + c * 32;
+            if (rmw) tma_reduce_add_2d(&L.gw, stg + h * (kBM * 128), col, d0);
+            else tma_store_2d(&L.gw, stg + h * (kBM * 128), col, d0);
+          }
+          bulk_commit();
+        }
+      }
+      GTRACE(3 * l + 2);  // layer l: stores issued
+    }
+    if (etid == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(&gp.ctrl[0], 1u);
+    if (old == gridDim.x - 1) {
+      __threadfence();
+      for (int l = 0; l < gp.n_layers; ++l)
+        for (int t = 0; t < gp.L[l].n_tiles; ++t) gp.L[l].tile_cnt[t] = 0u;
+      unsigned nt = gp.ctrl[2] + 1u;
+      if (nt == 0u) nt = 1u;
+      gp.ctrl[2] = nt;
+      gp.ctrl[0] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+template <int BN, int CG>
+static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream_t stream) {
+  using C = GCfg<BN, CG>;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(dpdw_group_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CG;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  attr[na].id = cudaLaunchAttributeCooperative;
+  attr[na].val.cooperative = 1;
+  ++na;
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
+  if (e != cudaSuccess && CG == 2) {
+    if (std::getenv("FDP_DEBUG")) std::fprintf(stderr, "fdp: cooperative cluster launch rejected (%s); plain cluster launch\n", cudaGetErrorString(e));
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;  // cluster launch without the cooperative attribute (grid <= co-resident capacity)
+    e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
+  }
+  return e;
+}
+
+cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream) {
+  if (cg == 2) {
+    if (bn == 256) return launch_group_impl<256, 2>(gp, grid, stream);
+    return launch_group_impl<128, 2>(gp, grid, stream);
+  }
+  if (bn == 256) return launch_group_impl<256, 1>(gp, grid, stream);
+  return launch_group_impl<128, 1>(gp, grid, stream);
+}
+
+}  // namespace fdp

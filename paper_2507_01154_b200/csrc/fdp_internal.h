@@ -71,6 +71,32 @@ cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMa
 // Upper bound on co-resident CTAs of the (bn, cg) kernel on this device (0: cannot run).
 int tc_max_coresident_ctas(int bn, int cg);
 
+// ---- multi-layer fused launch (fdp_group.cu)
+struct GLayer {
+  CUtensorMap tm_dy, tm_x, gw;  // operand maps (box 64x64 bf16) and the grad_w store map (32x128 fp32)
+  float* grad_w;
+  float* norms_out;
+  unsigned long long* tagged;   // [B][n_tiles] tagged norm partials
+  unsigned* tile_cnt;           // [n_tiles] sample-group arrivals
+  uint64_t key_base, key_base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long noise_lo, noise_hi;
+  double clip_c, clip_c2;
+  float inv_batch, noise_scale;
+  int B, T, P, D, n_dt2, n_pt, n_wtiles, n_tiles, groups, n_kb;
+  int accumulate, add_noise, noise_impl, pad_;
+};
+constexpr int kMaxGroupLayers = 48;  // keeps the parameter block under 32 KB
+struct GroupParams {
+  GLayer L[kMaxGroupLayers];
+  unsigned* ctrl;  // [0] exit counter, [1] error word, [2] launch epoch
+  unsigned long long budget_ns;
+  unsigned long long* trace;  // [grid][256] per-layer phase timestamps (FDP_FLAG_TRACE) or nullptr
+  int n_layers;
+};
+cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
+
 // ---- ghost norms (TWO_PHASE first phase): ||G_b||^2 = <X_b X_b^T, dY_b dY_b^T>
 struct GhostParams {
   int B, T, P, D;

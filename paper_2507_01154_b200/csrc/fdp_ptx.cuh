@@ -292,3 +292,8 @@ __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads)
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 }  // namespace fdp
+
+namespace fdp {
+// the smem sources of all committed bulk stores have been read (buffer reusable)
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+}  // namespace fdp

@@ -26,6 +26,9 @@
 // The other modes reuse the pipeline: NORMS (norm partials only), REWEIGHT
 // (clip factors precomputed: the second phase of the two-phase path), STORE_G
 // (explicit baseline stage 1), NONDP (plain dW GEMM accumulated in TMEM).
+#include <cstdio>
+#include <cstdlib>
+
 #include "fdp_internal.h"
 #include "fdp_ptx.cuh"
 #include "fdp_rng.cuh"
@@ -656,6 +659,7 @@ static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& t
     // Some drivers reject cooperative + cluster launches. The grid never exceeds
     // the co-resident capacity (checked by the planner), so fall back to a plain
     // cluster launch; the in-kernel watchdog turns a broken assumption into an error.
+    if (std::getenv("FDP_DEBUG")) std::fprintf(stderr, "fdp: cooperative cluster launch rejected (%s); plain cluster launch\n", cudaGetErrorString(e));
     (void)cudaGetLastError();
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, em, p);

@@ -260,6 +260,64 @@ class PreparedBackward:
         _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
 
 
+class PreparedGroup:
+    """The fused DP backward of several layers in ONE persistent launch
+    (fdp_backward_group): e.g. every linear layer of a model after the
+    activation-gradient pass. Each layer keeps its own DPConfig (clip C, sigma,
+    noise key = layer_id), norms and outputs; results equal per-layer
+    backward_flashdp calls (up to fp32 summation order across sample groups).
+
+    layers: sequence of (x, dy, cfg) with contiguous bf16 CUDA tensors."""
+
+    def __init__(self, layers, *, grads=None, norms=None, noise_impl: str = "keyed_f32", accumulate: bool = False,
+                 add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
+                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+        n = len(layers)
+        if n < 1:
+            raise UsageError("PreparedGroup needs at least one layer")
+        self.layers = list(layers)
+        descs = (_lib.FdpDesc * n)()
+        self.grads, self.norms = [], []
+        xs, dys, gs, ns = [], [], [], []
+        for i, (x, dy, cfg) in enumerate(self.layers):
+            dims = _dims(x, dy)
+            if not (x.is_cuda and dy.is_cuda and x.dtype == torch.bfloat16 and dy.dtype == torch.bfloat16
+                    and x.is_contiguous() and dy.is_contiguous()):
+                raise UsageError(f"layer {i}: PreparedGroup needs contiguous bf16 CUDA inputs")
+            descs[i] = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, reduction=cfg.reduction,
+                                      clip_c=cfg.clip_c, sigma=cfg.sigma, seed=cfg.seed, layer_id=cfg.layer_id,
+                                      step=cfg.step, rank=rank, world=world, mean_batch=mean_batch,
+                                      accumulate=accumulate, add_noise=add_noise, noise_impl=noise_impl,
+                                      device_step=_step_ptr(device_step))
+            g = grads[i] if grads is not None else torch.zeros((dims.D, dims.P), dtype=torch.float32, device=x.device)
+            nrm = norms[i] if norms is not None else torch.zeros(dims.B, dtype=torch.float32, device=x.device)
+            self.grads.append(g)
+            self.norms.append(nrm)
+            xs.append(x.data_ptr())
+            dys.append(dy.data_ptr())
+            gs.append(g.data_ptr())
+            ns.append(nrm.data_ptr())
+        self.descs = descs
+        arr = ctypes.c_void_p * n
+        self._ptrs = (arr(*xs), arr(*dys), arr(*gs), arr(*ns))
+        lib = _lib.load()
+        self._lib = lib
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.fdp_group_workspace_bytes(n, descs, ctypes.byref(nbytes)))
+        if workspace is None:
+            workspace = torch.zeros(max(nbytes.value, 4096), dtype=torch.uint8, device=self.layers[0][0].device)
+        elif workspace.numel() * workspace.element_size() < nbytes.value:
+            raise fdp_capacity(nbytes.value, workspace.numel() * workspace.element_size())
+        self.workspace = workspace
+        self._n = n
+
+    def __call__(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.layers[0][0].device)
+        xs, dys, gs, ns = self._ptrs
+        _lib.check(self._lib.fdp_backward_group(self._n, self.descs, xs, dys, gs, ns, self.workspace.data_ptr(),
+                                                self.workspace.numel(), s.cuda_stream))
+
+
 def backward_nondp(x, dy, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:
     """grad_w = sum_b sum_t dY^T X; no per-sample quantity (workflows.py:121-150)."""
     return _run(WorkflowKind.NON_DP, x, dy, None, spec, None, **opts)

@@ -402,3 +402,30 @@ def test_two_phase_many_tiles_per_cta(norm_phase):
     cfg = fdp.DPConfig(0.05, 1.0, "mean", seed=9, layer_id=4, step=2)
     r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase=norm_phase)
     check(r, x, dy, cfg, BF16_TOL)
+
+
+def test_group_launch_matches_per_layer_calls():
+    """fdp_backward_group: GPT-2-like layer list in one persistent launch == per-layer results."""
+    shapes = [(768, 2304), (768, 768), (768, 3072), (3072, 768), (256, 512)]
+    B, T = 4, 256
+    layers, singles = [], []
+    for i, (P, D) in enumerate(shapes):
+        x, dy = randn(B, T, P, D, seed=100 + i, scale_dy=1e-2)
+        cfg = fdp.DPConfig(0.05 * (i + 1), 1.0, "mean", seed=3, layer_id=i, step=5)
+        layers.append((x, dy, cfg))
+        singles.append(fdp.backward_flashdp(x, dy, cfg, path="fused", noise_impl="philox"))
+    grp = fdp.PreparedGroup(layers, noise_impl="philox")
+    for rep in range(2):  # the workspace is reusable call after call
+        grp()
+        torch.cuda.synchronize()
+        for i, (x, dy, cfg) in enumerate(layers):
+            assert rel(host(grp.grads[i]), host(singles[i].grad_w)) < 1e-5, (rep, i)
+            assert rel(host(grp.norms[i]), host(singles[i].per_sample_norms_sq)) < 1e-5, (rep, i)
+    # and against the oracle with keyed noise
+    grp2 = fdp.PreparedGroup(layers, noise_impl="keyed_f32")
+    grp2()
+    torch.cuda.synchronize()
+    for i, (x, dy, cfg) in enumerate(layers):
+        want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=False)
+        assert rel(host(grp2.grads[i]), want) < BF16_TOL, i
+        assert rel(host(grp2.norms[i]), wn) < BF16_TOL, i

@@ -1,0 +1,62 @@
+"""Per-layer timeline of the multi-layer fused launch (FDP_FLAG_TRACE).
+
+    python tools/trace_group.py [noise] [B] [T]
+"""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2507_01154_b200 as fdp  # noqa: E402
+from paper_2507_01154_b200 import _lib  # noqa: E402
+
+GPT2 = [("c_attn", 768, 2304), ("attn_proj", 768, 768), ("c_fc", 768, 3072), ("mlp_proj", 3072, 768)]
+
+
+def main():
+    noise = sys.argv[1] if len(sys.argv) > 1 else "philox"
+    B = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    T = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
+    g = torch.Generator(device="cuda").manual_seed(0)
+    layers = []
+    for blk in range(2):
+        for j, (name, P, D) in enumerate(GPT2):
+            x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
+            dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+            layers.append((x, dy, fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=blk * 4 + j)))
+    grp = fdp.PreparedGroup(layers, noise_impl=noise)
+    for i in range(len(layers)):
+        grp.descs[i].flags = _lib.FLAG_TRACE
+    nbytes = ctypes.c_size_t()
+    _lib.check(_lib.load().fdp_group_workspace_bytes(len(layers), grp.descs, ctypes.byref(nbytes)))
+    grp.workspace = torch.zeros(nbytes.value, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        grp()
+    torch.cuda.synchronize()
+    grid = 148
+    raw = grp.workspace[nbytes.value - 2048 * grid:].view(torch.int64).cpu().numpy()
+    # the trace region is sized for the launch grid; infer it from the nonzero rows
+    tr = raw.reshape(-1, 256)
+    tr = tr[(tr[:, 0] > 0) | (tr[:, 3] > 0)]
+    t0 = tr[tr > 0].min()
+    rel = np.where(tr > 0, (tr - t0) / 1e3, np.nan)
+    out = []
+    for l in range(len(layers)):
+        cols = rel[:, 3 * l:3 * l + 3]
+        if not np.isfinite(cols).any():
+            continue
+        out.append({"layer": l, "name": GPT2[l % 4][0],
+                    "first_ready_med": round(float(np.nanmedian(cols[:, 0])), 2),
+                    "loop_end_med": round(float(np.nanmedian(cols[:, 1])), 2),
+                    "stored_med": round(float(np.nanmedian(cols[:, 2])), 2),
+                    "stored_max": round(float(np.nanmax(cols[:, 2])), 2),
+                    "ctas": int(np.isfinite(cols[:, 0]).sum())})
+    print(json.dumps({"noise": noise, "B": B, "T": T, "layers": out}))
+
+
+if __name__ == "__main__":
+    main()
