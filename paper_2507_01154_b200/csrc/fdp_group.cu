@@ -25,7 +25,7 @@ struct GCfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = kBCols * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStgBytes = 2 * kBM * 128;  // two 32-column fp32 boxes (one per column half)
+  static constexpr int kStgBytes = 4 * kBM * 128;  // 2 buffers x two 32-column fp32 boxes (one per column half)
   static constexpr int kStages = (232448 - 2048 - kStgBytes) / kStageBytes;
   static constexpr int kNBuf = 512 / BN;
   static constexpr int kCPT = BN / 2;
@@ -191,6 +191,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         }
       }
       __threadfence();
+      // the pre-fill of this group's rows is globally visible: count it right away,
+      // so the groups' reduce-adds never wait on another group's epilogue
+      asm volatile("bar.sync 3, 64;" ::: "memory");
+      if (L.groups > 1 && ntid == 0) red_release_add_u32(&L.tile_cnt[(cid % L.n_wtiles) * CG + rank], 1u);
+      if (gp.trace && ntid == 0 && l < 16) gp.trace[blockIdx.x * 256 + 8 * l + 6] = globaltimer_ns();
       named_bar_sync(2, 32 * (2 + kEpiWarps));
     }
   } else if (warp >= kEpiWarp0) {
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       for (int b = group; b < L.B; b += L.groups) {
         mbar_wait(&tfull[rbuf], rph, err, gp.budget_ns, 0x404);
         tc_fence_after();
-        if (first) GTRACE(3 * l);  // layer l: first sample's MMA done
+        if (first && l < 16) GTRACE(8 * l);  // layer l: first sample's MMA done
         first = false;
         const uint32_t buf = rbuf;
         if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
@@ -253,13 +258,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
             v[k] = i < L.n_tiles ? ld_relaxed_u64(slots + i) : (static_cast<unsigned long long>(tag) << 32);
           }
           const uint64_t t0 = globaltimer_ns();
+          while (true) {  // re-poll every stale slot at once: one L2 round trip per iteration
+            bool all = true;
 #pragma unroll
-          for (int k = 0; k < kMaxPer; ++k) {
-            while (static_cast<unsigned>(v[k] >> 32) != tag) {
-              if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x405);
-              __nanosleep(32);
-              v[k] = ld_relaxed_u64(slots + lane + 32 * k);
-            }
+            for (int k = 0; k < kMaxPer; ++k) all &= static_cast<unsigned>(v[k] >> 32) == tag;
+            if (all) break;
+            if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x405);
+            __nanosleep(20);
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k)
+              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = ld_relaxed_u64(slots + lane + 32 * k);
           }
           double s = 0.0;
 #pragma unroll
@@ -291,15 +299,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         }
       }
 
-      GTRACE(3 * l + 1);  // layer l: last clip factor applied
+      if (l < 16) GTRACE(8 * l + 1);  // layer l: last clip factor applied
       // ---- finalize: wait for the noise warps' pre-fill (and, with sample groups,
       // for every group's pre-fill), then TMA store / reduce-add in 32-column boxes
       if (prefill) named_bar_sync(2, 32 * (2 + kEpiWarps));
+      if (l < 16) GTRACE(8 * l + 2);
       if (L.groups > 1) {
-        __threadfence();
-        named_bar_sync(1, 32 * kEpiWarps);
-        if (etid == 0) {
-          red_release_add_u32(&L.tile_cnt[tile], 1u);
+        if (etid == 0) {  // every group's rows are pre-filled (counted by the noise warps)
           const uint64_t t0 = globaltimer_ns();
           while (ld_acquire_u32(&L.tile_cnt[tile]) < static_cast<unsigned>(L.groups)) {
             if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x406);
@@ -307,11 +313,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
           }
         }
       }
+      if (l < 16) GTRACE(8 * l + 3);
 #pragma unroll
       for (int c = 0; c < C::kCPT / 32; ++c) {
-        if (etid == 0) bulk_wait_read_all();  // the previous boxes have left the staging buffer
+        uint8_t* sbuf = stg + (c & 1) * (2 * kBM * 128);
+        if (etid == 0) bulk_wait_read_le1();  // the boxes issued two rounds ago have left this buffer
         named_bar_sync(1, 32 * kEpiWarps);
-        uint8_t* box = stg + half * (kBM * 128) + row * 128;
+        uint8_t* box = sbuf + half * (kBM * 128) + row * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) =
@@ -324,13 +332,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int col = p0 + h * C::kCPT + c * 32;
-            if (rmw) tma_reduce_add_2d(&L.gw, stg + h * (kBM * 128), col, d0);
-            else tma_store_2d(&L.gw, stg + h * (kBM * 128), col, d0);
+            if (rmw) tma_reduce_add_2d(&L.gw, sbuf + h * (kBM * 128), col, d0);
+            else tma_store_2d(&L.gw, sbuf + h * (kBM * 128), col, d0);
           }
           bulk_commit();
         }
+        if (l < 16 && c == 0) GTRACE(8 * l + 4);
       }
-      GTRACE(3 * l + 2);  // layer l: stores issued
+      if (l < 16) GTRACE(8 * l + 5);  // layer l: stores issued
     }
     if (etid == 0) bulk_wait_all();
   }
@@ -385,9 +394,11 @@ static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  attr[na].id = cudaLaunchAttributeCooperative;
-  attr[na].val.cooperative = 1;
-  ++na;
+  if (!std::getenv("FDP_NO_COOP")) {  // see fdp_tc.cu
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);

@@ -297,3 +297,8 @@ namespace fdp {
 // the smem sources of all committed bulk stores have been read (buffer reusable)
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 }  // namespace fdp
+
+namespace fdp {
+// at most one committed bulk group may still be reading its smem source
+__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+}  // namespace fdp

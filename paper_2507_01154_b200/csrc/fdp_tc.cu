@@ -237,6 +237,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
         __threadfence();
+        if (atomic_groups) {  // count this group's pre-fill right away (see the epilogue's reduce-add)
+          asm volatile("bar.sync 3, 64;" ::: "memory");
+          if (ntid == 0) red_release_add_u32(&p.ws_tile_cnt[wt * CG + rank], 1u);
+        }
         // bar.sync (not arrive): the noise warps must not run a whole tile ahead
         // of the epilogue in persistent modes, or barrier generations would mix
         named_bar_sync(2, 32 * (2 + kEpiWarps));
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           __syncwarp();
         }
       };
+      int trace_u = -1;
       // pass 1 + publish: intra-block reduce of ||G_b||^2 (workflows.py:387-389)
       auto publish = [&](int ub, uint32_t b) {
         float part = 0.0f;
@@ -329,10 +334,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
         }
+        if (trace_u >= 0) FDP_TRACE(64 + 4 * trace_u);  // pass-1 TMEM reads + FMAs done
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         if (lane == 0) red[ew] = part;
         named_bar_sync(1, 32 * kEpiWarps);
+        if (trace_u >= 0) FDP_TRACE(65 + 4 * trace_u);  // block reduce done
         if (etid == 0) {
           float s = 0.0f;
 #pragma unroll
@@ -367,16 +374,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           bool stale = false;
           if (!p.skip_barrier) {
-            const uint64_t t0 = globaltimer_ns();
+          const uint64_t t0 = globaltimer_ns();
+          while (true) {  // re-poll every stale slot at once: one L2 round trip per iteration
+            bool all = true;
 #pragma unroll
-            for (int k = 0; k < kMaxPer; ++k) {
-              const int i = lane + 32 * k;
-              while (static_cast<unsigned>(v[k] >> 32) != tag) {
-                if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
-                __nanosleep(32);
-                v[k] = ld_relaxed_u64(slots + i);
-              }
-            }
+            for (int k = 0; k < kMaxPer; ++k) all &= static_cast<unsigned>(v[k] >> 32) == tag;
+            if (all) break;
+            if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
+            __nanosleep(20);
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k)
+              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = ld_relaxed_u64(slots + lane + 32 * k);
+          }
           } else {
 #pragma unroll
             for (int k = 0; k < kMaxPer; ++k) stale |= static_cast<unsigned>(v[k] >> 32) != tag;
@@ -421,11 +430,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int ub = b0 + u * b_step;
           const uint32_t b = wait_ready();
           FDP_TRACE(9 + 4 * u);
+          trace_u = u < 16 ? u : -1;
           publish(ub, b);
           FDP_TRACE(8 + 4 * u);
           const float f = wait_factor(ub);
           FDP_TRACE(10 + 4 * u);
           accumulate_scaled(b, f);
+          if (trace_u >= 0) FDP_TRACE(66 + 4 * trace_u);  // pass 2 done
+          trace_u = -1;
           release(b);
         }
       } else if (p.mode == MODE_REWEIGHT) {
@@ -498,11 +510,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         named_bar_sync(1, 32 * kEpiWarps);
         if (reduce_scatter && !p.deterministic) {
           // every group reduce-adds its whole clipped tile onto grad_w once all
-          // groups have initialised (pre-filled) their row slices
-          __threadfence();
-          named_bar_sync(1, 32 * kEpiWarps);
+          // groups have initialised (pre-filled) their row slices (the noise warps
+          // count each pre-fill as soon as it is visible)
           if (etid == 0) {
-            red_release_add_u32(&p.ws_tile_cnt[tile], 1u);
             const uint64_t t0 = globaltimer_ns();
             while (ld_acquire_u32(&p.ws_tile_cnt[tile]) < static_cast<unsigned>(p.groups)) {
               if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x106);
@@ -647,7 +657,9 @@ static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& t
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (cooperative) {
+  // FDP_NO_COOP=1: plain launch (profilers that cannot replay cooperative cluster
+  // launches); the grid never exceeds the co-resident capacity either way
+  if (cooperative && !std::getenv("FDP_NO_COOP")) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;

@@ -55,8 +55,8 @@ def main():
 
     for u in range(n_units):
         # slots: 9+4u sample u ready (MMA done), 8+4u published + noise chunk u done, 10+4u factor u known
-        units.append({"u": u, "ready": med(9 + 4 * u), "noise_done": med(8 + 4 * u),
-                      "factor": med(10 + 4 * u),
+        units.append({"u": u, "ready": med(9 + 4 * u), "pass1": med(64 + 4 * u), "block_red": med(65 + 4 * u),
+                      "published": med(8 + 4 * u), "factor": med(10 + 4 * u), "pass2": med(66 + 4 * u),
                       "factor_max": round(float(np.nanmax(rel[:, 10 + 4 * u])), 2)})
     out["units"] = units
     print(json.dumps(out))
