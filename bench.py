@@ -320,11 +320,15 @@ def main():
     peaks, peak_kind = load_peaks()
     dom_avg_s = (statistics.mean(dom_ms) * 1e-3) if dom_ms else None
     achieved = dom_flops / dom_avg_s / 1e12 if dom_avg_s else None
+    # algorithmic bytes of the same launch: bf16 X and dY read once, fp32 grad_w written, fp32 norms
+    dom_layers = layers if group is not None else [(0, "c_fc", 768, 3072)]
+    dom_bytes = sum(2 * B * T * (P + D) + 4 * D * P + 4 * B for _, _, P, D in dom_layers)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("fused_c_fc_dram_bytes")
+            traffic = json.load(open(tpath)).get("group_kernel_dram_bytes" if group is not None
+                                                 else "fused_c_fc_dram_bytes")
         except Exception:  # noqa: BLE001
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
@@ -334,7 +338,8 @@ def main():
                 if achieved else None,
                 "kernel": ("dpdw_group_kernel: fused DP backward of all 48 layers in one launch, B=%d T=%d" % (B, T))
                 if group is not None else "dpdw_tc_kernel (MODE_FUSED) on c_fc: B=%d T=%d P=768 D=3072" % (B, T),
-                "algorithmic_flops_per_launch": dom_flops, "avg_launch_ms": dom_avg_s * 1e3 if dom_avg_s else None,
+                "algorithmic_flops_per_launch": dom_flops, "algorithmic_bytes_per_launch": dom_bytes,
+                "avg_launch_ms": dom_avg_s * 1e3 if dom_avg_s else None,
                 "launches_timed": len(dom_ms)}
 
     extra = {}

@@ -15,6 +15,7 @@
 
 #include "fdp_internal.h"
 #include "fdp_ptx.cuh"
+#include "fdp_prefill.cuh"
 #include "fdp_rng.cuh"
 
 namespace fdp {
@@ -171,29 +172,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
       const int p0 = (wt % L.n_pt) * BN;
       const int r0 = group * kBM / L.groups, r1 = (group + 1) * kBM / L.groups;
-      const int q_all = (r1 - r0) * (BN / 4);
-      for (int e4 = ntid; e4 < q_all; e4 += 64) {
-        const int dd = d0 + r0 + e4 / (BN / 4);
-        const int pp = p0 + (e4 % (BN / 4)) * 4;
-        if (dd < L.D && pp < L.P) {
-          const long long flat = static_cast<long long>(dd) * L.P + pp;
-          float4* dst = reinterpret_cast<float4*>(L.grad_w + flat);
-          float4 v = L.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (draw && flat + 3 >= L.noise_lo && flat < L.noise_hi) {
-            const float4 n = noise_draw4(L.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
-            const float s = L.noise_scale;
-            if (flat + 0 >= L.noise_lo && flat + 0 < L.noise_hi) v.x += s * n.x;
-            if (flat + 1 >= L.noise_lo && flat + 1 < L.noise_hi) v.y += s * n.y;
-            if (flat + 2 >= L.noise_lo && flat + 2 < L.noise_hi) v.z += s * n.z;
-            if (flat + 3 >= L.noise_lo && flat + 3 < L.noise_hi) v.w += s * n.w;
-          }
-          __stcg(dst, v);
-        }
-      }
+      prefill_rows<BN>(L.grad_w, L.D, L.P, d0 + r0, d0 + r1, p0, L.accumulate != 0, draw, L.noise_impl, kbg, kb,
+                       L.noise_scale, L.noise_lo, L.noise_hi, ntid);
       __threadfence();
       // the pre-fill of this group's rows is globally visible: count it right away,
       // so the groups' reduce-adds never wait on another group's epilogue
-      asm volatile("bar.sync 3, 64;" ::: "memory");
+      named_bar_sync(3, 64);
       if (L.groups > 1 && ntid == 0) red_release_add_u32(&L.tile_cnt[(cid % L.n_wtiles) * CG + rank], 1u);
       if (gp.trace && ntid == 0 && l < 16) gp.trace[blockIdx.x * 256 + 8 * l + 6] = globaltimer_ns();
       named_bar_sync(2, 32 * (2 + kEpiWarps));

@@ -155,8 +155,12 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_mn(int M, int N) {
 }
 
 // ---------------------------------------------------------------- named barriers / misc
+// Non-.aligned barrier forms: threads may arrive individually (a warp whose
+// lane 0 ran a divergent branch is still counted correctly). bar.sync is
+// barrier.sync.aligned and requires warp-convergent execution.
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -289,7 +293,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 
 namespace fdp {
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 }  // namespace fdp
 

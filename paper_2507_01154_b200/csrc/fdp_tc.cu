@@ -31,6 +31,7 @@
 
 #include "fdp_internal.h"
 #include "fdp_ptx.cuh"
+#include "fdp_prefill.cuh"
 #include "fdp_rng.cuh"
 
 namespace fdp {
@@ -217,28 +218,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int wt = first_wt; wt < p.n_wtiles; wt += wt_stride) {
         const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
         const int p0 = (wt % p.n_pt) * BN;
-        const int q_all = (own_r1 - own_r0) * (BN / 4);
-        for (int e4 = ntid; e4 < q_all; e4 += 64) {
-          const int dd = d0 + own_r0 + e4 / (BN / 4);
-          const int pp = p0 + (e4 % (BN / 4)) * 4;
-          if (dd < p.D && pp < p.P) {  // P % 8 == 0: a float4 never straddles a row or the tile edge
-            const long long flat = static_cast<long long>(dd) * p.P + pp;
-            float4* dst = reinterpret_cast<float4*>(p.grad_w + flat);
-            float4 v = p.accumulate ? __ldcg(dst) : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (draw_noise && flat + 3 >= p.noise_lo && flat < p.noise_hi) {
-              const float4 n = noise_draw4(p.noise_impl, kbg, kb, static_cast<uint64_t>(flat >> 2));
-              const float s = p.noise_scale;
-              if (flat + 0 >= p.noise_lo && flat + 0 < p.noise_hi) v.x += s * n.x;
-              if (flat + 1 >= p.noise_lo && flat + 1 < p.noise_hi) v.y += s * n.y;
-              if (flat + 2 >= p.noise_lo && flat + 2 < p.noise_hi) v.z += s * n.z;
-              if (flat + 3 >= p.noise_lo && flat + 3 < p.noise_hi) v.w += s * n.w;
-            }
-            __stcg(dst, v);
-          }
-        }
+        prefill_rows<BN>(p.grad_w, p.D, p.P, d0 + own_r0, d0 + own_r1, p0, p.accumulate != 0, draw_noise,
+                         p.noise_impl, kbg, kb, p.noise_scale, p.noise_lo, p.noise_hi, ntid);
         __threadfence();
         if (atomic_groups) {  // count this group's pre-fill right away (see the epilogue's reduce-add)
-          asm volatile("bar.sync 3, 64;" ::: "memory");
+          named_bar_sync(3, 64);
           if (ntid == 0) red_release_add_u32(&p.ws_tile_cnt[wt * CG + rank], 1u);
         }
         // bar.sync (not arrive): the noise warps must not run a whole tile ahead

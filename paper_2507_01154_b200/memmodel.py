@@ -81,27 +81,35 @@ def ledger(kind: str, B: int, T: int, P: int, D: int, width: int, plan=None, dp:
     Derived from the dataflow of workflows.py (loads of X/dY once per fused
     pass, norm/accumulator round trips, per-sample G materialisation); the
     formulas are cross-checked against the reference simulator in the tests.
-    ``plan`` (a BlockPlan) only matters for flashdp (norm reloads per (p,d)
-    block and one accumulator spill per batch chunk). ``dp`` False drops the
-    finalize flops (non-DP has no emit step).
+    ``plan`` (a BlockPlan) sets the flashdp norm reloads per (p,d) block and
+    accumulator spills per batch chunk, and every kind's peak scratch: the
+    simulator's high-water mark is one input tile pair b·t·(p+d), plus the
+    per-sample tile b·d·p where one is materialised (explicit, implicit,
+    flashdp) and flashdp's b norm partials, or the d·p output tile when that is
+    larger (pinned on all golden ledgers). Without a plan, peak scratch is 0.
+    ``dp`` False drops the finalize flops (non-DP has no emit step).
     """
     inputs = B * T * (P + D)
     g = B * D * P
     dp_elems = D * P
     grad_flops = 2 * B * T * D * P
+    tile_in = tile_g = tile_out = 0
+    if plan is not None:
+        tile_in, tile_g, tile_out = plan.b * plan.t * (plan.p + plan.d), plan.b * plan.d * plan.p, plan.d * plan.p
     if kind == "non_dp":
         return TrafficReport(bytes_loaded=inputs * width, bytes_stored=dp_elems * width, flops=grad_flops,
-                             kernel_launches=1)
+                             kernel_launches=1, peak_scratch_bytes=max(tile_in, tile_out) * width)
     emit = dp_elems
     if kind == "explicit_dp":
         return TrafficReport(bytes_loaded=(inputs + 3 * g + B) * width,
                              bytes_stored=(2 * g + B + dp_elems) * width,
                              flops=grad_flops + 4 * g + emit, kernel_launches=4,
-                             per_sample_grad_bytes_stored=2 * g * width)
+                             per_sample_grad_bytes_stored=2 * g * width,
+                             peak_scratch_bytes=max(tile_in + tile_g, tile_out) * width)
     if kind == "implicit_dp":
         return TrafficReport(bytes_loaded=(2 * inputs + B) * width, bytes_stored=(B + dp_elems) * width,
                              flops=2 * grad_flops + 4 * g + emit, redundant_flops=grad_flops,
-                             kernel_launches=2)
+                             kernel_launches=2, peak_scratch_bytes=max(tile_in + tile_g, tile_out) * width)
     if kind == "flashdp":
         if plan is None:
             raise UsageError("flashdp ledger needs the block plan")

@@ -177,7 +177,7 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
                                 "completed (barrier skipped)")
 
     wplan = plan
-    if kind == WorkflowKind.FLASHDP and wplan is None:
+    if wplan is None:  # the reference plans every kind from the spec (workflows.py:437-438)
         wplan = plan_blocks(dims, spec or B200_SPEC)
     width = (spec or B200_SPEC).dtype_width_bytes
     report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)

@@ -309,8 +309,11 @@ def test_device_step_counter_keys_noise():
     x, dy = randn(2, 64, 128, 128, seed=1)
     step = torch.tensor([5], dtype=torch.int64, device="cuda")
     cfg = fdp.DPConfig(1.0, 1.0, seed=3, layer_id=1, step=5)
-    a = fdp.backward_flashdp(x, dy, fdp.DPConfig(1.0, 1.0, seed=3, layer_id=1, step=0), device_step=step).grad_w
-    b = fdp.backward_flashdp(x, dy, cfg).grad_w
+    # deterministic: sample-group partial sums are combined in a fixed order, so
+    # the two launches must agree bitwise (atomic group reduce-adds would not)
+    a = fdp.backward_flashdp(x, dy, fdp.DPConfig(1.0, 1.0, seed=3, layer_id=1, step=0), device_step=step,
+                             deterministic=True).grad_w
+    b = fdp.backward_flashdp(x, dy, cfg, deterministic=True).grad_w
     assert torch.equal(a, b)
 
 

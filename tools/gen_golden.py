@@ -89,6 +89,17 @@ def gen_config1():
     np.savez_compressed(OUT / "config1.npz", **out)
 
 
+def gen_report():
+    """The reference's own scenario report (run_scenario + render_report, bench.py:274-335)
+    for the config-1 cell, whole batch and 2x2 micro-batches."""
+    from dpflows.bench import MicroBatchSpec, ScenarioConfig, render_report, run_scenario
+    for tag, micro in (("report_c1", None), ("report_c1_micro", MicroBatchSpec(2, 2))):
+        cfg = ScenarioConfig(layers=(LayerSpec("l", 128, 256, 256),), batch_sizes=(4,),
+                             workflows=tuple(WorkflowKind(k) for k in KINDS), mem=MemSpec(228 * 1024, 2),
+                             dp=DPConfig(clip_c=1.0, sigma=0.0, seed=0), micro_batch=micro)
+        (OUT / f"{tag}.csv").write_text(render_report(run_scenario(cfg), "csv"))
+
+
 def gen_random():
     """Small random instances with random valid plans (test_acceptance.py:38-58 style)."""
     r = random.Random(20817)
@@ -160,6 +171,7 @@ def main():
     gen_rng()
     gen_worked()
     gen_config1()
+    gen_report()
     gen_random()
     gen_ledgers()
     gen_micro()
