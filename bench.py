@@ -411,14 +411,16 @@ def main():
         h2d = sum(B * T * (P + D) * 2 for _, _, P, D in layers)
         d2h = sum(P * D * 4 + B * 4 for _, _, P, D in layers)
 
+        streamer = fdp.HostStreamedBackward(dev, noise_impl=a.noise, rank=rank, world=world, mean_batch=global_B)
+
         def e2e_step(step_idx):
+            batch = []
             for lid, name, P, D in layers:
                 xh, yh = host[name.split(".")[1]]
-                cfg = fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234, layer_id=lid,
-                                   step=step_idx)
-                res = fdp.run_backward(fdp.WorkflowKind.FLASHDP, xh, yh, cfg, rank=rank, world=world,
-                                       mean_batch=global_B, noise_impl=a.noise)
-                assert res.grad_w.device.type == "cpu"
+                batch.append((xh, yh, fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234,
+                                                    layer_id=lid, step=step_idx)))
+            res = streamer(batch)
+            assert res[-1].grad_w.device.type == "cpu"
 
         e2e_step(0)
         torch.cuda.synchronize()
@@ -435,7 +437,7 @@ def main():
             e2e_s = float(tt.item())
         e2e = {"value": tokens_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s * 1e3,
-               "api": "paper_2507_01154_b200.run_backward(WorkflowKind.FLASHDP, pinned host bf16 X/dY) per layer"}
+               "api": "paper_2507_01154_b200.HostStreamedBackward (per-layer fdp_backward; pinned host bf16 X/dY in, fp32 grad_w + norms out; H2D/kernel/D2H overlapped on 3 streams)"}
 
     # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
     cpu = None

@@ -818,6 +818,7 @@ int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, c
   gp.budget_ns = (descs[0].flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
   gp.trace = (descs[0].flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, gpl.total - 2048ull * gpl.grid) : nullptr;
   gp.n_layers = n;
+  gp.nosync = env_int("FDP_DEBUG_NOSYNC", 0);
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
             bool all = true;
 #pragma unroll
             for (int k = 0; k < kMaxPer; ++k) all &= static_cast<unsigned>(v[k] >> 32) == tag;
-            if (all) break;
+            if (all || gp.nosync) break;
             if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x405);
             __nanosleep(20);
 #pragma unroll

@@ -94,6 +94,7 @@ struct GroupParams {
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][256] per-layer phase timestamps (FDP_FLAG_TRACE) or nullptr
   int n_layers;
+  int nosync;  // debug (FDP_DEBUG_NOSYNC): clip factors from whatever partials are present, no wait
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
 

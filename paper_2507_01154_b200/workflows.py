@@ -318,6 +318,98 @@ class PreparedGroup:
                                                 self.workspace.numel(), s.cuda_stream))
 
 
+class HostStreamedBackward:
+    """DP backward of a list of layers whose inputs live in HOST memory (the
+    reference's calling convention: run_backward on host arrays, once per layer,
+    workflows.py:427-440), pipelined over three CUDA streams:
+
+        copy-in   layer i+1's X/dY host->device into one of two device slots
+        compute   layer i's fused DP backward (fdp_backward, one launch)
+        copy-out  layer i-1's grad_w / norms device->host
+
+    so the PCIe transfers in both directions overlap each other and the kernels;
+    the step costs ~max(H2D bytes / PCIe bandwidth, kernel time). Results are
+    identical to per-layer run_backward calls (same kernels, same descriptors).
+
+    layers: sequence of (x_host, dy_host, cfg); x_host (B,T,P) / dy_host (B,T,D)
+    CPU torch tensors (bf16 or fp32; pinned for asynchronous copies). Returns one
+    BackwardResult per layer with host grad_w (D,P) fp32 and norms (B,) fp32."""
+
+    def __init__(self, device: Optional[torch.device] = None, *, noise_impl: str = "keyed_f32", path: str = "auto",
+                 rank: int = 0, world: int = 1, mean_batch: int = 0, deterministic: bool = False):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.opts = dict(noise_impl=noise_impl, path=path, rank=rank, world=world, mean_batch=mean_batch,
+                         flags=_lib.FLAG_DETERMINISTIC if deterministic else 0)
+        self._in = torch.cuda.Stream(self.device)
+        self._out = torch.cuda.Stream(self.device)
+        self._slots: list = [None, None]
+        self._lib = _lib.load()
+
+    def _slot(self, i: int, nx: int, ny: int, dtype: torch.dtype):
+        s = self._slots[i]
+        if s is None or s[0].numel() < nx or s[1].numel() < ny or s[0].dtype != dtype:
+            s = (torch.empty(nx, dtype=dtype, device=self.device), torch.empty(ny, dtype=dtype, device=self.device))
+            self._slots[i] = s
+        return s
+
+    def __call__(self, layers, kind: WorkflowKind = WorkflowKind.FLASHDP, spec: Optional[MemSpec] = None):
+        dev = self.device
+        comp = torch.cuda.current_stream(dev)
+        lib = self._lib
+        k = _lib.KIND[kind.value]
+        n = len(layers)
+        in_done = [torch.cuda.Event() for _ in range(n)]
+        comp_done = [torch.cuda.Event() for _ in range(n)]
+        results = []
+        pending = []  # device tensors kept alive until the copy-out stream is synchronised
+        for i, (x, dy, cfg) in enumerate(layers):
+            dims = _dims(x, dy)
+            if not (isinstance(x, torch.Tensor) and isinstance(dy, torch.Tensor)) or x.is_cuda or dy.is_cuda:
+                raise UsageError("HostStreamedBackward takes host (CPU) torch tensors")
+            if x.dtype != dy.dtype or x.dtype not in (torch.bfloat16, torch.float32):
+                raise UsageError(f"x and dy must share a dtype in (bfloat16, float32), got {x.dtype}, {dy.dtype}")
+            if kind != WorkflowKind.NON_DP and cfg is None:
+                raise UsageError("DP workflows need a DPConfig")
+            xs, ys = x.contiguous(), dy.contiguous()
+            xd, yd = self._slot(i % 2, xs.numel(), ys.numel(), xs.dtype)
+            xd, yd = xd[:xs.numel()], yd[:ys.numel()]
+            with torch.cuda.stream(self._in):
+                if i >= 2:  # slot reuse: layer i-2's kernel has consumed it
+                    self._in.wait_event(comp_done[i - 2])
+                xd.copy_(xs.view(-1), non_blocking=True)
+                yd.copy_(ys.view(-1), non_blocking=True)
+                in_done[i].record(self._in)
+            c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
+            desc = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=_input_dtype_code(xd),
+                                  reduction=c.reduction, clip_c=c.clip_c, sigma=c.sigma, seed=c.seed,
+                                  layer_id=c.layer_id, step=c.step, **self.opts)
+            ws_bytes = ctypes.c_size_t()
+            _lib.check(lib.fdp_workspace_bytes(ctypes.byref(desc), k, ctypes.byref(ws_bytes)))
+            ws = _POOL.get(ws_bytes.value, dev, comp)
+            grad = torch.empty((dims.D, dims.P), dtype=torch.float32, device=dev)
+            norms = torch.empty(dims.B, dtype=torch.float32, device=dev)
+            comp.wait_event(in_done[i])
+            _lib.check(lib.fdp_backward(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                                        norms.data_ptr() if kind != WorkflowKind.NON_DP else None, ws.data_ptr(),
+                                        ws.numel(), comp.cuda_stream))
+            comp_done[i].record(comp)
+            g_host = torch.empty((dims.D, dims.P), dtype=torch.float32, pin_memory=True)
+            n_host = torch.empty(dims.B, dtype=torch.float32, pin_memory=True)
+            with torch.cuda.stream(self._out):
+                self._out.wait_event(comp_done[i])
+                g_host.copy_(grad, non_blocking=True)
+                if kind != WorkflowKind.NON_DP:
+                    n_host.copy_(norms, non_blocking=True)
+            pending.append((grad, norms))
+            width = (spec or B200_SPEC).dtype_width_bytes
+            report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=plan_blocks(dims, spec or B200_SPEC))
+            results.append(BackwardResult(g_host, report, n_host if kind != WorkflowKind.NON_DP else torch.zeros(0)))
+        self._out.synchronize()
+        comp.wait_stream(self._out)  # later device work on these buffers (caching allocator reuse) orders after
+        del pending
+        return results
+
+
 def backward_nondp(x, dy, spec: Optional[MemSpec] = None, *, sim=None, **opts) -> BackwardResult:
     """grad_w = sum_b sum_t dY^T X; no per-sample quantity (workflows.py:121-150)."""
     return _run(WorkflowKind.NON_DP, x, dy, None, spec, None, **opts)

@@ -432,3 +432,25 @@ def test_group_launch_matches_per_layer_calls():
         want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=False)
         assert rel(host(grp2.grads[i]), want) < BF16_TOL, i
         assert rel(host(grp2.norms[i]), wn) < BF16_TOL, i
+
+
+def test_host_streamed_matches_per_layer_and_oracle():
+    """HostStreamedBackward (pinned host inputs, H2D / kernel / D2H on three
+    streams) returns exactly what per-layer run_backward calls return, and the
+    oracle agrees on the reference-keyed noise (sigma > 0)."""
+    shapes = [(4, 128, 256, 512), (4, 128, 512, 256), (2, 64, 128, 384), (4, 128, 256, 512)]
+    layers, dev = [], []
+    for i, (B, T, P, D) in enumerate(shapes):
+        x, dy = randn(B, T, P, D, seed=40 + i)
+        cfg = fdp.DPConfig(0.5, 1.0, "mean", seed=9, layer_id=i, step=3)
+        layers.append((x.cpu().pin_memory(), dy.cpu().pin_memory(), cfg))
+        dev.append((x, dy, cfg))
+    streamed = fdp.HostStreamedBackward(noise_impl="keyed_f64", deterministic=True)(layers)
+    for (x, dy, cfg), r in zip(dev, streamed):
+        assert r.grad_w.device.type == "cpu" and r.per_sample_norms_sq.device.type == "cpu"
+        one = fdp.run_backward(W.FLASHDP, x, dy, cfg, noise_impl="keyed_f64", deterministic=True)
+        assert torch.equal(r.grad_w, one.grad_w.cpu())
+        assert torch.equal(r.per_sample_norms_sq, one.per_sample_norms_sq.cpu())
+        want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True)
+        assert rel(r.grad_w.double().numpy(), want) < BF16_TOL
+        assert rel(r.per_sample_norms_sq.double().numpy(), wn) < BF16_TOL
