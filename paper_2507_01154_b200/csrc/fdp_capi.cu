@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <map>
 #include <vector>
 
 namespace {
@@ -452,6 +453,9 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.ws_acc = ws_at<float>(ws, pl.off_acc);
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
   p.deterministic = (d->flags & FDP_FLAG_DETERMINISTIC) ? 1 : 0;
+  p.poll_ns = env_int("FDP_POLL_NS", 0);
+  p.pub_mode = env_int("FDP_PUB_MODE", 1);
+  p.poll_mode = env_int("FDP_POLL_MODE", 0);
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
   p.trace = (d->flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, pl.total - 1024ull * pl.grid) : nullptr;
   return p;
@@ -612,12 +616,57 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
 // ---- multi-layer fused launch
 struct GroupPlan {
   int bn = 0, cg = 1, grid = 0;
-  std::vector<int> groups, n_dt2, n_pt, n_wtiles;
+  std::vector<int> groups, c_off, n_dt2, n_pt, n_wtiles;
   std::vector<size_t> off_tagged, off_tile_cnt;
   size_t total = 0;
 };
 
+int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl);
+
+// The packing search costs milliseconds; a training loop calls the same layer
+// list every step, so plans are cached by (device, layer extents, flags, env).
 int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl) {
+  static std::mutex mu;
+  static std::map<std::vector<long long>, GroupPlan> cache;
+  std::vector<long long> key;
+  key.reserve(4 * n + 8);
+  key.push_back(di.dev);
+  key.push_back(n);
+  key.push_back(env_int("FDP_FORCE_BN", 0));
+  key.push_back(env_int("FDP_FORCE_CG", 0));
+  key.push_back(env_int("FDP_NO_PACK", 0));
+  if (n > 0 && n <= fdp::kMaxGroupLayers) {
+    key.push_back(descs[0].flags & FDP_FLAG_TRACE);
+    for (int l = 0; l < n; ++l) {
+      key.push_back(descs[l].B);
+      key.push_back(descs[l].T);
+      key.push_back(descs[l].P);
+      key.push_back(descs[l].D);
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      // extents match a validated plan; the per-call descriptor fields are still checked
+      for (int l = 0; l < n; ++l) {
+        int rc = validate(&descs[l], FDP_KIND_FLASHDP);
+        if (rc) return rc;
+      }
+      gpl = it->second;
+      return FDP_OK;
+    }
+  }
+  int rc = plan_group_uncached(n, descs, di, gpl);
+  if (rc == FDP_OK) {
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 256) cache.clear();
+    cache[key] = gpl;
+  }
+  return rc;
+}
+
+int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl) {
   if (n < 1 || n > fdp::kMaxGroupLayers)
     return fail(FDP_ERR_USAGE, "fdp_backward_group takes 1..%d layers, got %d", fdp::kMaxGroupLayers, n);
   if (di.major != 10) return fail(FDP_ERR_USAGE, "fdp_backward_group needs an sm_100 device");
@@ -629,14 +678,22 @@ int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& g
   }
   const int cands[4][2] = {{256, 2}, {128, 2}, {256, 1}, {128, 1}};
   const int forced_bn = env_int("FDP_FORCE_BN", 0), forced_cg = env_int("FDP_FORCE_CG", 0);
+  const bool no_pack = env_int("FDP_NO_PACK", 0) != 0;
   double best = 1e300;
   for (auto& cd : cands) {
     const int bn = cd[0], cg = cd[1];
     if ((forced_bn && bn != forced_bn) || (forced_cg && cg != forced_cg)) continue;
     const long long cap = fdp::tc_max_coresident_ctas(bn, cg);
     if (cap <= 0) continue;
+    const int K = static_cast<int>(cap / cg);  // co-resident clusters
     const double rate = bn == 256 ? (cg == 2 ? 9.6e12 : 7.4e12) : (cg == 2 ? 6.4e12 : 6.3e12);
-    double est = 0.0;
+    // Pack layers onto cluster ranges: every cluster walks the layers in order,
+    // so a layer's finish time on a cluster is (that cluster's load) + (its units'
+    // time). For each layer pick the sample-group count g and the cyclic range
+    // start that minimise the layer's finish time (ties: least idle time inside
+    // the range, then fewer groups), e.g. GPT-2's c_attn (27 tiles x 2 groups)
+    // and attn_proj (9 tiles x 2 groups) side by side on 54 + 18 clusters.
+    std::vector<double> load(K, 0.0);
     bool ok = true;
     GroupPlan cand;
     cand.bn = bn;
@@ -646,21 +703,44 @@ int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& g
       const long long ndt = (d->D + fdp::kBM - 1) / fdp::kBM;
       const int ndt2 = static_cast<int>((ndt + cg - 1) / cg);
       const int npt = static_cast<int>((d->P + bn - 1) / bn);
-      const long long need = static_cast<long long>(ndt2) * npt * cg;
-      if (need > cap) { ok = false; break; }
-      long long g = cap / need;
-      if (g > d->B) g = d->B;
-      if (g > 8) g = 8;
-      while (g & (g - 1)) --g;
-      const double units = static_cast<double>((d->B + g - 1) / g);
-      est += units * std::max(2.0 * fdp::kBM * bn * static_cast<double>(d->T) / rate, 2.5e-6) + (g > 1 ? 3e-6 : 0.0);
-      cand.groups.push_back(static_cast<int>(g));
+      const int nwt = ndt2 * npt;
+      if (nwt > K) { ok = false; break; }
+      const double unit = std::max(2.0 * fdp::kBM * bn * static_cast<double>(d->T) / rate, 2.5e-6);
+      double bfin = 1e300, bidle = 1e300;
+      int bg = 0, boff = 0;
+      const int gmax = static_cast<int>(std::min<long long>(std::min<long long>(d->B, 8), K / nwt));
+      for (int g = 1; g <= gmax; ++g) {
+        if (no_pack && (g & (g - 1))) continue;
+        const int nc = nwt * g;
+        const double t = static_cast<double>((d->B + g - 1) / g) * unit + (g > 1 ? 3e-6 : 0.0);
+        for (int off = 0; off < (no_pack ? 1 : K); ++off) {
+          double m = 0.0, sum = 0.0;
+          for (int i = 0; i < nc; ++i) {
+            const double v = load[(off + i) % K];
+            m = std::max(m, v);
+            sum += v;
+          }
+          const double fin = m + t, idle = m * nc - sum;
+          if (fin < bfin * (1 - 1e-9) || (fin <= bfin * (1 + 1e-9) && idle < bidle * (1 - 1e-9) - 1e-12)) {
+            bfin = fin;
+            bidle = idle;
+            bg = g;
+            boff = off;
+          }
+        }
+      }
+      if (no_pack && !bg) { ok = false; break; }
+      for (int i = 0; i < nwt * bg; ++i) load[(boff + i) % K] = bfin;
+      cand.groups.push_back(bg);
+      cand.c_off.push_back(boff);
       cand.n_dt2.push_back(ndt2);
       cand.n_pt.push_back(npt);
-      cand.n_wtiles.push_back(ndt2 * npt);
-      cand.grid = std::max(cand.grid, static_cast<int>(need * g));
+      cand.n_wtiles.push_back(nwt);
+      cand.grid = std::max(cand.grid, (boff + nwt * bg > K ? K : boff + nwt * bg) * cg);
     }
-    if (ok && est < best * 0.97) {
+    if (!ok) continue;
+    const double est = *std::max_element(load.begin(), load.end());
+    if (est < best * 0.97) {
       best = est;
       gpl = cand;
     }
@@ -809,6 +889,7 @@ int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, c
     L.n_wtiles = gpl.n_wtiles[l];
     L.n_tiles = gpl.n_wtiles[l] * gpl.cg;
     L.groups = gpl.groups[l];
+    L.c_off = gpl.c_off[l];
     L.n_kb = static_cast<int>((d->T + fdp::kBK - 1) / fdp::kBK);
     L.accumulate = d->accumulate;
     L.add_noise = c.add_noise;
@@ -819,6 +900,10 @@ int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, c
   gp.trace = (descs[0].flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, gpl.total - 2048ull * gpl.grid) : nullptr;
   gp.n_layers = n;
   gp.nosync = env_int("FDP_DEBUG_NOSYNC", 0);
+  gp.dbg_noise = env_int("FDP_DEBUG_NOISE", 0);
+  gp.poll_ns = env_int("FDP_POLL_NS", 0);
+  gp.pub_mode = env_int("FDP_PUB_MODE", 1);
+  gp.poll_mode = env_int("FDP_POLL_MODE", 0);
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

@@ -10,6 +10,16 @@
 // counters; a CTA whose cluster id is beyond a layer's work simply skips it.
 // Layer descriptors (with their TMA maps) are a __grid_constant__ parameter
 // block, so the launch is CUDA-graph capturable with no host->device copy.
+//
+// Layer packing: layer l occupies the cluster range [c_off, c_off + n_wtiles *
+// groups) (mod the cluster count); the host planner packs small layers next to
+// each other (e.g. GPT-2's c_attn on 54 clusters and attn_proj on the other 18),
+// so every cluster carries the same number of sample units per step. Norm
+// all-reduces only couple the clusters of one layer.
+//
+// The noise warps run ahead of the epilogue across layers (the layers' grad_w
+// rows are disjoint); a shared-memory counter tells the epilogue which layers'
+// pre-fills are complete.
 #include <cstdio>
 #include <cstdlib>
 
@@ -53,6 +63,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);
   float* bcast = red + kEpiWarps;
+  volatile unsigned* pf_done = reinterpret_cast<volatile unsigned*>(bcast + 1);  // layers pre-filled so far
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -60,6 +71,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
   const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
   const bool leader = rank == 0;
   const int cid = blockIdx.x / CG;
+  const int n_clusters = static_cast<int>(gridDim.x) / CG;
+  // this cluster's index within layer L's cluster range (>= L.n_wtiles * L.groups: idle)
+  auto lcid = [&](const GLayer& L) {
+    const int c = cid - L.c_off;
+    return c < 0 ? c + n_clusters : c;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -70,6 +87,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
+    *pf_done = 0u;
     fence_mbar_init();
     fence_proxy_async_smem();
   }
@@ -91,8 +109,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       uint32_t stage = 0, phase = 0;
       for (int l = 0; l < gp.n_layers; ++l) {
         const GLayer& L = gp.L[l];
-        if (cid >= L.n_wtiles * L.groups) continue;
-        const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
+        const int lc = lcid(L);
+        if (lc >= L.n_wtiles * L.groups) continue;
+        const int wt = lc % L.n_wtiles, group = lc / L.n_wtiles;
         const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
         const int p0 = (wt % L.n_pt) * BN + rank * C::kBCols;
         for (int b = group; b < L.B; b += L.groups) {
@@ -126,8 +145,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
       for (int l = 0; l < gp.n_layers; ++l) {
         const GLayer& L = gp.L[l];
-        if (cid >= L.n_wtiles * L.groups) continue;
-        const int group = cid / L.n_wtiles;
+        const int lc = lcid(L);
+        if (lc >= L.n_wtiles * L.groups) continue;
+        const int group = lc / L.n_wtiles;
         for (int b = group; b < L.B; b += L.groups) {
           mbar_wait(&tempty[buf], tphase ^ 1, err, gp.budget_ns, 0x402);
           tc_fence_after();
@@ -156,31 +176,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     }
   } else if (warp == 2 || warp == 3) {
     // ======================= noise warps: pre-fill this CTA's grad_w rows =======================
+    // (accumulate ? old : 0) + sigma*C*noise, or zeros when only sample groups need
+    // initialised rows for their reduce-adds. Runs ahead across layers.
     const int ntid = (warp - 2) * 32 + lane;
     for (int l = 0; l < gp.n_layers; ++l) {
       const GLayer& L = gp.L[l];
-      if (cid >= L.n_wtiles * L.groups) continue;
-      const bool draw = L.add_noise != 0;
-      const bool prefill = draw || L.groups > 1;
-      if (!prefill) continue;
-      uint64_t kb = L.key_base, kbg = L.key_base_g;
-      if (L.step_ptr) {
-        kb = absorb3(L.seed_u, L.layer_u, static_cast<uint64_t>(*L.step_ptr));
-        kbg = kb + kGamma;
+      const int lc = lcid(L);
+      const bool draw = L.add_noise != 0 && gp.dbg_noise != 1;
+      if (lc < L.n_wtiles * L.groups && (L.add_noise != 0 || L.groups > 1)) {
+        uint64_t kb = L.key_base, kbg = L.key_base_g;
+        if (L.step_ptr) {
+          kb = absorb3(L.seed_u, L.layer_u, static_cast<uint64_t>(*L.step_ptr));
+          kbg = kb + kGamma;
+        }
+        const int wt = lc % L.n_wtiles, group = lc / L.n_wtiles;
+        const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
+        const int p0 = (wt % L.n_pt) * BN;
+        const int r0 = group * kBM / L.groups, r1 = (group + 1) * kBM / L.groups;
+        prefill_rows<BN>(L.grad_w, L.D, L.P, d0 + r0, d0 + r1, p0, L.accumulate != 0, draw, L.noise_impl, kbg, kb,
+                         gp.dbg_noise == 2 ? 0.0f : L.noise_scale, L.noise_lo, L.noise_hi, ntid);
+        __threadfence();
+        named_bar_sync(3, 64);
+        // this group's rows are globally visible: count them right away, so the
+        // groups' reduce-adds never wait on another group's epilogue
+        if (L.groups > 1 && ntid == 0) red_release_add_u32(&L.tile_cnt[(lc % L.n_wtiles) * CG + rank], 1u);
+        if (gp.trace && ntid == 0 && l < 16) gp.trace[blockIdx.x * 256 + 8 * l + 6] = globaltimer_ns();
       }
-      const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
-      const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
-      const int p0 = (wt % L.n_pt) * BN;
-      const int r0 = group * kBM / L.groups, r1 = (group + 1) * kBM / L.groups;
-      prefill_rows<BN>(L.grad_w, L.D, L.P, d0 + r0, d0 + r1, p0, L.accumulate != 0, draw, L.noise_impl, kbg, kb,
-                       L.noise_scale, L.noise_lo, L.noise_hi, ntid);
-      __threadfence();
-      // the pre-fill of this group's rows is globally visible: count it right away,
-      // so the groups' reduce-adds never wait on another group's epilogue
-      named_bar_sync(3, 64);
-      if (L.groups > 1 && ntid == 0) red_release_add_u32(&L.tile_cnt[(cid % L.n_wtiles) * CG + rank], 1u);
-      if (gp.trace && ntid == 0 && l < 16) gp.trace[blockIdx.x * 256 + 8 * l + 6] = globaltimer_ns();
-      named_bar_sync(2, 32 * (2 + kEpiWarps));
+      if (ntid == 0) *pf_done = static_cast<unsigned>(l + 1);
     }
   } else if (warp >= kEpiWarp0) {
     // ======================= epilogue =======================
@@ -190,8 +212,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     uint32_t rbuf = 0, rph = 0;
     for (int l = 0; l < gp.n_layers; ++l) {
       const GLayer& L = gp.L[l];
-      if (cid >= L.n_wtiles * L.groups) continue;
-      const int wt = cid % L.n_wtiles, group = cid / L.n_wtiles;
+      const int lc = lcid(L);
+      if (lc >= L.n_wtiles * L.groups) continue;
+      const int wt = lc % L.n_wtiles, group = lc / L.n_wtiles;
       const int tile = wt * CG + rank;
       const int d0 = ((wt / L.n_pt) * CG + rank) * kBM;
       const int p0 = (wt % L.n_pt) * BN;
@@ -228,8 +251,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
           float s = 0.0f;
 #pragma unroll
           for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-          st_relaxed_u64(L.tagged + static_cast<long long>(b) * L.n_tiles + tile,
-                         (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s));
+          publish_u64(L.tagged + static_cast<long long>(b) * L.n_tiles + tile,
+                      (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s), gp.pub_mode);
         }
         // block-wise all-reduce: fixed-order fp64 sum of the tagged partials
         if (ew == 0) {
@@ -239,7 +262,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
 #pragma unroll
           for (int k = 0; k < kMaxPer; ++k) {
             const int i = lane + 32 * k;
-            v[k] = i < L.n_tiles ? ld_relaxed_u64(slots + i) : (static_cast<unsigned long long>(tag) << 32);
+            v[k] = i < L.n_tiles ? poll_u64(slots + i, gp.poll_mode) : (static_cast<unsigned long long>(tag) << 32);
           }
           const uint64_t t0 = globaltimer_ns();
           while (true) {  // re-poll every stale slot at once: one L2 round trip per iteration
@@ -248,10 +271,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
             for (int k = 0; k < kMaxPer; ++k) all &= static_cast<unsigned>(v[k] >> 32) == tag;
             if (all || gp.nosync) break;
             if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x405);
-            __nanosleep(20);
+            if (gp.poll_ns) __nanosleep(gp.poll_ns);
 #pragma unroll
             for (int k = 0; k < kMaxPer; ++k)
-              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = ld_relaxed_u64(slots + lane + 32 * k);
+              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = poll_u64(slots + lane + 32 * k, gp.poll_mode);
           }
           double s = 0.0;
 #pragma unroll
@@ -286,7 +309,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       if (l < 16) GTRACE(8 * l + 1);  // layer l: last clip factor applied
       // ---- finalize: wait for the noise warps' pre-fill (and, with sample groups,
       // for every group's pre-fill), then TMA store / reduce-add in 32-column boxes
-      if (prefill) named_bar_sync(2, 32 * (2 + kEpiWarps));
+      if (prefill && etid == 0) {  // this CTA's pre-fill of layer l is complete and visible
+        const uint64_t t0 = globaltimer_ns();
+        while (*pf_done < static_cast<unsigned>(l + 1)) {
+          if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x407);
+          __nanosleep(32);
+        }
+        __threadfence();
+      }
       if (l < 16) GTRACE(8 * l + 2);
       if (L.groups > 1) {
         if (etid == 0) {  // every group's rows are pre-filled (counted by the noise warps)

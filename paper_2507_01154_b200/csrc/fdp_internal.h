@@ -54,6 +54,10 @@ struct TcParams {
   float* ws_acc;           // [n_tiles][groups][kBM*BN]
   int skip_barrier;
   int deterministic;
+  // publish the tagged norm partial with an L2 atomic exchange (1, default: reaches L2 at once;
+  // 0 = st.relaxed, 2 = st.release) and poll with ld.relaxed (0) / volatile (1) / acquire (2)
+  int pub_mode, poll_mode;
+  int poll_ns;  // back-off between polls of the norm partials (FDP_POLL_NS, default 0: spin)
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][128] phase timestamps or nullptr
 };
@@ -85,7 +89,8 @@ struct GLayer {
   double clip_c, clip_c2;
   float inv_batch, noise_scale;
   int B, T, P, D, n_dt2, n_pt, n_wtiles, n_tiles, groups, n_kb;
-  int accumulate, add_noise, noise_impl, pad_;
+  int accumulate, add_noise, noise_impl;
+  int c_off;  // first cluster of this layer's range (layers are packed onto cluster ranges, fdp_capi.cu)
 };
 constexpr int kMaxGroupLayers = 48;  // keeps the parameter block under 32 KB
 struct GroupParams {
@@ -94,6 +99,8 @@ struct GroupParams {
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][256] per-layer phase timestamps (FDP_FLAG_TRACE) or nullptr
   int n_layers;
+  int dbg_noise;  // debug (FDP_DEBUG_NOISE): 1 = no draws (zero pre-fill), 2 = draws scaled by 0
+  int pub_mode, poll_mode, poll_ns;  // experiments (FDP_PUB_MODE, FDP_POLL_MODE, FDP_POLL_NS)
   int nosync;  // debug (FDP_DEBUG_NOSYNC): clip factors from whatever partials are present, no wait
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);

@@ -273,6 +273,24 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Publish / poll variants of the tagged norm-partial slots (experiments: FDP_PUB_MODE / FDP_POLL_MODE).
+__device__ __forceinline__ void publish_u64(unsigned long long* p, unsigned long long v, int mode) {
+  if (mode == 1) {
+    unsigned long long old;
+    asm volatile("atom.relaxed.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  } else if (mode == 2) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  } else {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  }
+}
+__device__ __forceinline__ unsigned long long poll_u64(const unsigned long long* p, int mode) {
+  unsigned long long v;
+  if (mode == 1) asm volatile("ld.volatile.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else if (mode == 2) asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 }  // namespace fdp
 
 namespace fdp {

@@ -64,15 +64,21 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 
 // Philox noise: flat indices are grouped in aligned blocks of 4; block g uses
 // one Philox4x32-10 call (counter = g) whose 4 words feed two Box-Muller pairs
-// (cos and sin branches). u1 = (w + 1) 2^-32 in (0, 1], u2 = w 2^-32.
+// (cos and sin branches). u1 = (w + 1) 2^-32 in (0, 1], angle = 2 pi w 2^-32 - pi.
+// The transform uses the SFU approximations (MUFU lg2 / rsqrt / sin / cos,
+// ~2^-21 relative): this mode is checked statistically, and every path (fused
+// epilogues, fdp_noise) uses this one function, so draws agree bit for bit.
 __device__ __forceinline__ float4 philox_normal4(uint64_t base, uint64_t block) {
   uint32_t c[4] = {static_cast<uint32_t>(block), static_cast<uint32_t>(block >> 32), 0x44504E5Au, 0u};
   philox4x32_10(c, static_cast<uint32_t>(base), static_cast<uint32_t>(base >> 32));
-  const float r0 = sqrtf(-2.0f * logf((__uint2float_rn(c[0]) + 1.0f) * 0x1p-32f));
-  const float r1 = sqrtf(-2.0f * logf((__uint2float_rn(c[2]) + 1.0f) * 0x1p-32f));
+  constexpr float kM2Ln2 = -1.3862943611198906f;  // -2 ln 2: -2 ln u = -2 ln2 * log2 u
+  const float t0 = fmaxf(kM2Ln2 * __log2f((__uint2float_rn(c[0]) + 1.0f) * 0x1p-32f), 1e-30f);
+  const float t1 = fmaxf(kM2Ln2 * __log2f((__uint2float_rn(c[2]) + 1.0f) * 0x1p-32f), 1e-30f);
+  const float r0 = t0 * rsqrtf(t0), r1 = t1 * rsqrtf(t1);
+  constexpr float kPi = 3.14159265358979f;
   float s0, c0, s1, c1;
-  sincospif(__uint2float_rn(c[1]) * 0x1p-31f, &s0, &c0);
-  sincospif(__uint2float_rn(c[3]) * 0x1p-31f, &s1, &c1);
+  __sincosf(fmaf(__uint2float_rn(c[1]), 0x1p-31f * kPi, -kPi), &s0, &c0);
+  __sincosf(fmaf(__uint2float_rn(c[3]), 0x1p-31f * kPi, -kPi), &s1, &c1);
   return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
 }
 

@@ -336,8 +336,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (fused) {
             // one 8-byte store carries the partial and this launch's tag: the
             // readers need no separate counter or fence (single-copy atomic)
-            st_relaxed_u64(p.ws_tagged + static_cast<long long>(ub) * p.n_tiles + tile,
-                           (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s));
+            publish_u64(p.ws_tagged + static_cast<long long>(ub) * p.n_tiles + tile,
+                        (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s), p.pub_mode);
           } else {
             p.ws_part[static_cast<long long>(ub) * p.n_tiles + tile] = s;
           }
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int k = 0; k < kMaxPer; ++k) {  // all loads in flight at once: one L2 round trip
             const int i = lane + 32 * k;
-            v[k] = i < p.n_tiles ? ld_relaxed_u64(slots + i) : (static_cast<unsigned long long>(tag) << 32);
+            v[k] = i < p.n_tiles ? poll_u64(slots + i, p.poll_mode) : (static_cast<unsigned long long>(tag) << 32);
           }
           bool stale = false;
           if (!p.skip_barrier) {
@@ -365,11 +365,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int k = 0; k < kMaxPer; ++k) all &= static_cast<unsigned>(v[k] >> 32) == tag;
             if (all) break;
             if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x105);
-            __nanosleep(20);
+            if (p.poll_ns) __nanosleep(p.poll_ns);
 #pragma unroll
             for (int k = 0; k < kMaxPer; ++k)
-              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = ld_relaxed_u64(slots + lane + 32 * k);
+              if (static_cast<unsigned>(v[k] >> 32) != tag) v[k] = poll_u64(slots + lane + 32 * k, p.poll_mode);
           }
+          if (trace_u >= 0) FDP_TRACE(67 + 4 * trace_u);  // every partial of the sample seen
           } else {
 #pragma unroll
             for (int k = 0; k < kMaxPer; ++k) stale |= static_cast<unsigned>(v[k] >> 32) != tag;

@@ -43,11 +43,15 @@ def main():
                          (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16))
                         for _ in range(12)]
     cases = {"all48": [(name, blk) for blk in range(12) for name, _, _ in TYPES]}
-    for name, _, _ in TYPES:
+    if os.environ.get("EXP_ONLY48"):
+        TYPES_ = []
+    else:
+        TYPES_ = TYPES
+    for name, _, _ in TYPES_:
         cases[name + "x12"] = [(name, blk) for blk in range(12)]
     for case, items in cases.items():
         flops = sum(2 * B * T * inputs[n][b][0].shape[2] * inputs[n][b][1].shape[2] for n, b in items)
-        for sigma in (0.0, 1.0):
+        for sigma in [float(v) for v in os.environ.get("EXP_SIGMAS", "0,1").split(",")]:
             layers = [(inputs[n][b][0], inputs[n][b][1], fdp.DPConfig(1.0, sigma, "mean", seed=1, layer_id=i))
                       for i, (n, b) in enumerate(items)]
             grp = fdp.PreparedGroup(layers, noise_impl="philox")

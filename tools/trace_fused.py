@@ -56,11 +56,14 @@ def main():
     for u in range(n_units):
         # slots: 9+4u sample u ready (MMA done), 8+4u published + noise chunk u done, 10+4u factor u known
         units.append({"u": u, "ready": med(9 + 4 * u), "pass1": med(64 + 4 * u), "block_red": med(65 + 4 * u),
-                      "published": med(8 + 4 * u), "factor": med(10 + 4 * u), "pass2": med(66 + 4 * u),
+                      "published": med(8 + 4 * u), "factor": med(10 + 4 * u), "pass2": med(66 + 4 * u), "poll_exit": med(67 + 4 * u),
                       "factor_max": round(float(np.nanmax(rel[:, 10 + 4 * u])), 2),
                       "ready_max": round(float(np.nanmax(rel[:, 9 + 4 * u])), 2),
                       "published_max": round(float(np.nanmax(rel[:, 8 + 4 * u])), 2),
-                      "last_publisher_cta": int(np.nanargmax(rel[:, 8 + 4 * u]))})
+                      "ready_min": round(float(np.nanmin(rel[:, 9 + 4 * u])), 2),
+                      "published_min": round(float(np.nanmin(rel[:, 8 + 4 * u])), 2),
+                      "published_p90": round(float(np.nanpercentile(rel[:, 8 + 4 * u], 90)), 2),
+                      "late_ctas": [int(i) for i in np.argsort(np.nan_to_num(rel[:, 8 + 4 * u], nan=-1))[-4:]]})
     out["units"] = units
     print(json.dumps(out))
 

@@ -21,13 +21,14 @@ def main():
     noise = sys.argv[1] if len(sys.argv) > 1 else "philox"
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     T = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
+    sigma = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
     g = torch.Generator(device="cuda").manual_seed(0)
     layers = []
     for blk in range(2):
         for j, (name, P, D) in enumerate(GPT2):
             x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
             dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
-            layers.append((x, dy, fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=blk * 4 + j)))
+            layers.append((x, dy, fdp.DPConfig(1.0, sigma, "mean", seed=1, layer_id=blk * 4 + j)))
     grp = fdp.PreparedGroup(layers, noise_impl=noise)
     for i in range(len(layers)):
         grp.descs[i].flags = _lib.FLAG_TRACE
@@ -55,8 +56,10 @@ def main():
         for k, nm in enumerate(names):
             v = cols[:, k]
             row[nm] = round(float(np.nanmedian(v)), 2) if np.isfinite(v).any() else None
+            if nm in ("loop_end", "noise_signal", "stored"):
+                row[nm + "_max"] = round(float(np.nanmax(v)), 2) if np.isfinite(v).any() else None
         out.append(row)
-    print(json.dumps({"noise": noise, "B": B, "T": T, "layers": out}))
+    print(json.dumps({"noise": noise, "sigma": sigma, "B": B, "T": T, "layers": out}))
 
 
 if __name__ == "__main__":
