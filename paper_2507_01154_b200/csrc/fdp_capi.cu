@@ -519,12 +519,19 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   if ((rc = make_tmap(&tm_dy, dy, d->D, d->T, d->B))) return rc;
   if ((rc = make_tmap(&tm_x, x, d->P, d->T, d->B))) return rc;
   fdp::EpiMaps em;
-  em.gw = em.gw_slice = em.slot = em.slice = tm_dy;  // placeholders (unused outside MODE_FUSED)
-  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED) {
+  em.gw = em.gw_slice = em.slot = em.slice = tm_dy;  // placeholders (unused by the modes that skip them)
+  if (kind != FDP_KIND_EXPLICIT_DP) {
+    // grad_w store / reduce-add map: the TMA epilogue of the fused, reweight and non-DP modes
+    if ((reinterpret_cast<uintptr_t>(grad_w) & 15u) != 0)
+      return fail(FDP_ERR_USAGE, "grad_w must be 16-byte aligned for the tensor-core path");
     const cuuint64_t gdims[2] = {static_cast<cuuint64_t>(d->P), static_cast<cuuint64_t>(d->D)};
     const cuuint64_t gstr[1] = {static_cast<cuuint64_t>(d->P * 4)};
     const cuuint32_t gbox[2] = {32, static_cast<cuuint32_t>(fdp::kBM)};
     if ((rc = make_tmap_f32(&em.gw, grad_w, 2, gdims, gstr, gbox))) return rc;
+  }
+  if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED) {
+    const cuuint64_t gdims[2] = {static_cast<cuuint64_t>(d->P), static_cast<cuuint64_t>(d->D)};
+    const cuuint64_t gstr[1] = {static_cast<cuuint64_t>(d->P * 4)};
     if (pl.groups > 1 && (d->flags & FDP_FLAG_DETERMINISTIC)) {
       const cuuint32_t rows_own = static_cast<cuuint32_t>(fdp::kBM / pl.groups);
       const cuuint32_t sbox[2] = {32, rows_own};

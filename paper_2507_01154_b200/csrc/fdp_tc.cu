@@ -42,12 +42,16 @@ struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 2;           // 16 KB: two 64-wide d atoms x 64 t rows
   static constexpr int kBBytes = kBCols * kBK * 2;        // kBCols/64 atoms x 8 KB
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (192 * 1024) / kStageBytes;
   static constexpr int kNBuf = 512 / BN;                  // TMEM accumulator buffers
   static constexpr int kCPT = BN / 2;                     // accumulator columns per epilogue thread
   static constexpr int kBarBytes = 1024;
-  static constexpr int kStgBytes = kEpiWarps * 32 * 33 * 4;  // per-warp 32x33 transpose buffers
-  static constexpr size_t kSmem = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + kBarBytes + kStgBytes;
+  // epilogue staging: two buffers x two 128-row x 32-column fp32 boxes (TMA store /
+  // reduce-add of a persistent tile while the next tile's MMAs run); MODE_STORE_G
+  // reuses it as per-warp 32x33 transpose buffers
+  static constexpr int kStgBytes = 4 * kBM * 128;
+  static_assert(kStgBytes >= kEpiWarps * 32 * 33 * 4, "transpose buffers must fit the staging area");
+  static constexpr int kStages = (232448 - 1024 - kBarBytes - kStgBytes) / kStageBytes;
+  static constexpr size_t kSmem = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + kStgBytes + kBarBytes;
   static constexpr uint32_t kIdesc = make_idesc_bf16_mn(kBM * CG, BN);
 };
 
@@ -63,7 +67,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   using C = TcCfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* stg = smem + C::kStages * C::kStageBytes;  // 1024-aligned staging boxes (kStgBytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::kStgBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNBuf;
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rs_bar + 1);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps]
   float* bcast = red + kEpiWarps;                           // [1] (ordered by named barriers)
-  float* stage_buf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + C::kBarBytes);
+  float* stage_buf = reinterpret_cast<float*>(stg);  // MODE_STORE_G transpose buffers
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int etid = ew * 32 + lane;     // 0..255
     const int row = q * 32 + lane;       // tile-local d
     const int col0 = half * C::kCPT;     // tile-local first p
-    float* stg = stage_buf + ew * (32 * 33);  // this warp's 32x33 transpose buffer
+    float* tbuf = stage_buf + ew * (32 * 33);  // this warp's 32x33 transpose buffer (MODE_STORE_G)
     uint32_t rbuf = 0, rph = 0;          // next TMEM buffer to wait for (buffers complete in order)
 
     auto wait_ready = [&]() -> uint32_t {
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int c = 0; c < C::kCPT / 32; ++c) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = vals[c * 32 + i];
+          for (int i = 0; i < 32; ++i) tbuf[lane * 33 + i] = vals[c * 32 + i];
           __syncwarp();
           const int cc = col0 + c * 32 + lane;
 #pragma unroll 4
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int rr = q * 32 + r;
             if (rr < nrow && cc < ncol) {
               float* g = dst + static_cast<long long>(rr) * ld + cc;
-              float v = stg[r * 33 + lane];
+              float v = tbuf[r * 33 + lane];
               if (add_old) v += __ldcg(g);
               __stcg(g, v);
             }
@@ -578,13 +583,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         continue;
       }
 
-      // ---- finalize (persistent modes): mean is folded into the clip factor; the
-      // noise (if any) is already in grad_w.
-      store_tile(p.grad_w + static_cast<long long>(d0) * p.P + p0, p.P, p.D - d0, p.P - p0, rmw_store, acc);
+      // ---- finalize (persistent modes: REWEIGHT, NONDP): mean is folded into the
+      // clip factor; the noise (if any) is already in grad_w. The tile leaves through
+      // TMA in 32-column boxes, double-buffered, so the next tile's MMAs (already
+      // running into the free TMEM buffer) never wait on the stores; rows / columns
+      // beyond (D, P) are clipped by the tensor map.
+#pragma unroll
+      for (int c = 0; c < C::kCPT / 32; ++c) {
+        uint8_t* sbuf = stg + (c & 1) * (2 * kBM * 128);
+        if (etid == 0) bulk_wait_read_le1();  // the boxes issued two rounds ago have left this buffer
+        named_bar_sync(1, 32 * kEpiWarps);
+        uint8_t* box = sbuf + half * (kBM * 128) + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) =
+              make_float4(acc[c * 32 + 4 * j], acc[c * 32 + 4 * j + 1], acc[c * 32 + 4 * j + 2],
+                          acc[c * 32 + 4 * j + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          fence_proxy_async_global();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = p0 + h * C::kCPT + c * 32;
+            if (rmw_store) tma_reduce_add_2d(&em.gw, sbuf + h * (kBM * 128), col, d0);
+            else tma_store_2d(&em.gw, sbuf + h * (kBM * 128), col, d0);
+          }
+          bulk_commit();
+        }
+      }
       FDP_TRACE(2);
     }
   }
 
+  if (warp >= kEpiWarp0 && threadIdx.x == 32 * kEpiWarp0) bulk_wait_all();  // staging reads + stores complete
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();  // the leader's MMAs wrote the peer's TMEM / read its smem
   else __syncthreads();
