@@ -178,6 +178,32 @@ int choose_norm_phase(const fdp_desc* d) {
   return ghost < recompute ? FDP_NORMS_GHOST : FDP_NORMS_RECOMPUTE;
 }
 
+// Ghost-norm kernel variant: 256-row Gram tiles on CTA pairs (half the operand
+// bytes per flop) or 128-row tiles on single CTAs (finer work items). Both take
+// the same time per wave of work items at the rates measured on B200 (the
+// single-CTA tile is bound by shared-memory fill at ~half the pair's per-SM
+// rate, so a pair wave costs ~1.2 single waves), so the cheaper schedule wins.
+struct GhostShape {
+  bool pair;
+  int nT, n_pairs, parts;  // parts: norm partials per sample
+};
+GhostShape ghost_shape(const fdp_desc* d, int sms) {
+  const long long nT2 = (d->T + 255) / 256, np2 = nT2 * (nT2 + 1) / 2;
+  const long long nT1 = (d->T + 127) / 128, np1 = nT1 * (nT1 + 1) / 2;
+  const long long clusters = sms / 2 > 0 ? sms / 2 : 1;
+  const long long waves2 = (d->B * np2 + clusters - 1) / clusters;
+  const long long waves1 = (d->B * np1 + sms - 1) / (sms > 0 ? sms : 1);
+  int forced = env_int("FDP_GHOST_PAIR", -1);
+  // a wave of 256-row pair items takes ~1.2x a wave of 128-row single-CTA items (measured, K = P + D = 8192)
+  const bool pair = forced >= 0 ? forced != 0 : 6 * waves2 < 5 * waves1;
+  GhostShape g;
+  g.pair = pair;
+  g.nT = static_cast<int>(pair ? nT2 : nT1);
+  g.n_pairs = static_cast<int>(pair ? np2 : np1);
+  g.parts = pair ? 2 * g.n_pairs : g.n_pairs;
+  return g;
+}
+
 int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   const bool tc_dev = di.major == 10;  // sm_100 family
   const bool tc_ok = tc_dev && tc_shape_ok(d);
@@ -315,10 +341,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   // workspace layout
   const long long B = d->B;
   pl.part_tiles = pl.n_tiles;
-  if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_GHOST) {
-    const long long nT = (d->T + 127) / 128;
-    pl.part_tiles = static_cast<int>(nT * (nT + 1) / 2);
-  }
+  if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_GHOST) pl.part_tiles = ghost_shape(d, di.sms).parts;
   if (kind == FDP_KIND_EXPLICIT_DP) {
     pl.expl_chunks = 64;
     pl.part_tiles = pl.expl_chunks;
@@ -454,6 +477,9 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
   p.deterministic = (d->flags & FDP_FLAG_DETERMINISTIC) ? 1 : 0;
   p.poll_ns = env_int("FDP_POLL_NS", 0);
+  // epilogue-drawn noise for the reweight pass: measured faster with <= 2 samples per
+  // tile (5120x13824, B=2: 496 -> 433 us), slower from 4 up (the SFU burst per tile)
+  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", d->B <= 2 ? 1 : 0)) ? 1 : 0;
   p.pub_mode = env_int("FDP_PUB_MODE", 1);
   p.poll_mode = env_int("FDP_POLL_MODE", 0);
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
@@ -589,20 +615,27 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       CUtensorMap gx, gy;
       if ((rc = make_tmap(&gx, x, d->P, d->T, d->B, 128))) return rc;
       if ((rc = make_tmap(&gy, dy, d->D, d->T, d->B, 128))) return rc;
+      const GhostShape gs = ghost_shape(d, di.sms);
       fdp::GhostParams g{};
       g.B = p.B;
       g.T = p.T;
       g.P = p.P;
       g.D = p.D;
-      g.nT = static_cast<int>((d->T + 127) / 128);
-      g.n_pairs = g.nT * (g.nT + 1) / 2;
+      g.nT = gs.nT;
+      g.n_pairs = gs.n_pairs;
       g.n_items = g.n_pairs * g.B;
       g.part = p.ws_part;
       g.err = p.ws_ctrl + 1;
       g.budget_ns = p.budget_ns;
-      const int grid = g.n_items < di.sms ? g.n_items : di.sms;
-      if ((e = fdp::launch_ghost(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
-      if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, g.n_pairs, d->clip_c, p.clip_c2, c.inv_batch, norms,
+      if (gs.pair) {
+        const int clusters = di.sms / 2;
+        const int grid = 2 * (g.n_items < clusters ? g.n_items : clusters);
+        if ((e = fdp::launch_ghost_pair(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
+      } else {
+        const int grid = g.n_items < di.sms ? g.n_items : di.sms;
+        if ((e = fdp::launch_ghost(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
+      }
+      if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, gs.parts, d->clip_c, p.clip_c2, c.inv_batch, norms,
                                             ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     } else {

@@ -170,7 +170,196 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem_base);
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// Work item (b, i, j), i <= j over 256-row blocks of t: a 2-CTA cluster computes
+// the 256x256 Gram tiles with tcgen05.mma.cta_group::2 (M = 256: CTA r owns rows
+// i*256 + r*128 .. +128 of the tile; N = 256: each CTA stages 128 of the j-block
+// rows), Gx into TMEM columns [0, 256) and Gy into [256, 512). The epilogue pulls
+// Gx into registers as soon as it is complete (so the next item's Gx MMAs can
+// start while Gy is still accumulating), then reduces Gx .* Gy against Gy. Per
+// SM this halves the operand bytes per flop of the 128x128 single-CTA kernel,
+// which is bound by shared-memory fill. Partials: [B][n_pairs][2] (one per CTA).
+constexpr int kPT = 256;                               // Gram tile rows per pair
+constexpr int kPHalf = 128;                            // rows staged per CTA
+constexpr int kPTileBytes = kPHalf * kBK * 2;          // 16 KB
+constexpr int kPStageBytes = 2 * kPTileBytes;          // A + B halves
+constexpr int kPStages = 6;
+constexpr size_t kPSmem = 1024 + size_t(kPStages) * kPStageBytes + 1024;
+// kind::f16, bf16 x bf16 -> fp32, A and B K-major, M = 256 (pair), N = 256
+constexpr uint32_t kPIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kPT >> 3) << 17) |
+                             (static_cast<uint32_t>(kPT >> 4) << 24);
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    ghost_norm_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
+                           const GhostParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes);
+  uint64_t* empty = full + kPStages;
+  uint64_t* tfull = empty + kPStages;  // [0] Gx done, [1] Gy done
+  uint64_t* tempty = tfull + 2;        // [0] Gx read, [1] Gy read
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned* err = p.err;
+  const int rank = static_cast<int>(cluster_ctarank());
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps * 2);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    prefetch_tmap(&tm_x);
+    prefetch_tmap(&tm_dy);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int nkx = (p.P + kBK - 1) / kBK, nky = (p.D + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int wi = cid; wi < p.n_items; wi += n_clusters) {
+        int b, i, j;
+        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        const int ra = i * kPT + rank * kPHalf, rb = j * kPT + rank * kPHalf;
+        for (int k = 0; k < nkx + nky; ++k) {
+          const bool isx = k < nkx;
+          const CUtensorMap* m = isx ? &tm_x : &tm_dy;
+          const int kk = (isx ? k : k - nkx) * kBK;
+          mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x311);
+          uint8_t* sa = smem + stage * kPStageBytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (i == j ? kPTileBytes : kPStageBytes));
+          tma_load_3d_pair(sa, m, &full[stage], kk, ra, b);
+          if (i != j) tma_load_3d_pair(sa + kPTileBytes, m, &full[stage], kk, rb, b);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      uint32_t stage = 0, phase = 0, tph = 0;
+      for (int wi = cid; wi < p.n_items; wi += n_clusters) {
+        int b, i, j;
+        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        for (int k = 0; k < nkx + nky; ++k) {
+          const bool isx = k < nkx;
+          if (k == 0 || k == nkx) {  // Gx / Gy accumulator of the previous item has been read out
+            mbar_wait(&tempty[isx ? 0 : 1], tph ^ 1, err, p.budget_ns, 0x312);
+            tc_fence_after();
+          }
+          const uint32_t dtm = tmem_base + (isx ? 0u : static_cast<uint32_t>(kPT));
+          mbar_wait(&full[stage], phase, err, p.budget_ns, 0x313);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + stage * kPStageBytes);
+          const uint32_t bb = (i == j) ? a : a + kPTileBytes;
+#pragma unroll
+          for (int kq = 0; kq < kBK / 16; ++kq)
+            tc_mma_f16_pair(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kPIdesc,
+                            (k == 0 || k == nkx) && kq == 0 ? 0u : 1u);
+          tc_commit_pair(&empty[stage]);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+          if (k == nkx - 1) tc_commit_pair(&tfull[0]);
+        }
+        tc_commit_pair(&tfull[1]);
+        tph ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
+    uint32_t tph = 0;
+    for (int wi = cid; wi < p.n_items; wi += n_clusters) {
+      int b, i, j;
+      decode_item(wi, p.n_pairs, p.nT, b, i, j);
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
+      float gx[128];
+      mbar_wait(&tfull[0], tph, err, p.budget_ns, 0x314);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float v[16];
+        tmem_ld16(tb + c * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) gx[c * 16 + e] = v[e];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[0]);
+      mbar_wait(&tfull[1], tph, err, p.budget_ns, 0x315);
+      tc_fence_after();
+      float part = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float v[16];
+        tmem_ld16(tb + kPT + c * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) part = fmaf(gx[c * 16 + e], v[e], part);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[1]);
+      tph ^= 1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) red[ew] = part;
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (etid == 0) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kEpiWarps; ++w) s += red[w];
+        p.part[(static_cast<long long>(b) * p.n_pairs + (wi % p.n_pairs)) * 2 + rank] = (i == j ? 1.0f : 2.0f) * s;
+      }
+      named_bar_sync(1, 32 * kEpiWarps);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+}
+
 }  // namespace
+
+cudaError_t launch_ghost_pair(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
+                              cudaStream_t stream) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(ghost_norm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kPSmem));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = kPSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ghost_norm_pair_kernel, tm_x, tm_dy, p);
+}
 
 cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
                          cudaStream_t stream) {

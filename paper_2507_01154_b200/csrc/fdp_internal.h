@@ -54,6 +54,7 @@ struct TcParams {
   float* ws_acc;           // [n_tiles][groups][kBM*BN]
   int skip_barrier;
   int deterministic;
+  int epi_noise;  // MODE_REWEIGHT: draw Philox noise in the epilogue (no grad_w pre-fill)
   // publish the tagged norm partial with an L2 atomic exchange (1, default: reaches L2 at once;
   // 0 = st.relaxed, 2 = st.release) and poll with ld.relaxed (0) / volatile (1) / acquire (2)
   int pub_mode, poll_mode;
@@ -117,6 +118,9 @@ struct GhostParams {
 };
 cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
                          cudaStream_t stream);
+// CTA-pair variant: 256x256 Gram tiles (nT = ceil(T/256)), partials [B][n_pairs][2], grid = 2 x clusters.
+cudaError_t launch_ghost_pair(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
+                              cudaStream_t stream);
 
 // ---- SIMT (CUDA-core) kernels: generic shapes, fp32 inputs, explicit baseline
 struct SimtParams {

@@ -206,11 +206,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // (rng.py keyed draws or Philox, 4 consecutive columns per thread) while the MMA
     // and the epilogue run; the epilogue waits on named barrier 2 before its final
     // (reduce-add) store. No accumulator registers live here.
-    const bool dp_sum = p.mode == MODE_FUSED || p.mode == MODE_REWEIGHT;
+    // (the persistent reweight pass draws Philox noise in its epilogue instead)
     const bool reduce_scatter = fused && p.groups > 1;
     const bool atomic_groups = reduce_scatter && !p.deterministic;
-    const bool pre_noise = (dp_sum && p.add_noise) || atomic_groups;
-    const bool draw_noise = dp_sum && p.add_noise;
+    const bool draw_noise = (fused || (p.mode == MODE_REWEIGHT && !p.epi_noise)) && p.add_noise;
+    const bool pre_noise = draw_noise || atomic_groups;
     if (pre_noise) {
       uint64_t kb = p.key_base, kbg = p.key_base_g;
       if (p.step_ptr) {
@@ -263,14 +263,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     };
     auto taddr = [&](uint32_t b) { return tmem_base + (static_cast<uint32_t>(q * 32) << 16) + b * BN + col0; };
 
-    const bool dp_sum = p.mode == MODE_FUSED || p.mode == MODE_REWEIGHT;
     const bool reduce_scatter = fused && p.groups > 1;
     // grad_w rows are pre-filled by the noise warps (old value if accumulating,
     // + noise) when noise is drawn, and always when sample groups combine their
     // tiles with TMA reduce-add (every group then adds onto initialised rows).
     const bool atomic_groups = reduce_scatter && !p.deterministic;
-    const bool pre_noise = (dp_sum && p.add_noise) || atomic_groups;
+    const bool pre_noise = ((fused || (p.mode == MODE_REWEIGHT && !p.epi_noise)) && p.add_noise) || atomic_groups;
     const bool rmw_store = pre_noise || p.accumulate;
+    // MODE_REWEIGHT with p.epi_noise (Philox, <= 2 samples per tile; host choice):
+    // the epilogue starts each tile's accumulator at sigma*C*N(key, d*P + p), so
+    // the tile leaves with a plain TMA store and no grad_w pre-fill. With more
+    // samples per tile the noise warps' pre-fill + TMA reduce-add is cheaper.
+    const bool epi_noise = p.mode == MODE_REWEIGHT && p.add_noise && p.epi_noise;
+    uint64_t nkb = p.key_base;
+    if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     // launch tag of the tagged norm-partial slots (bumped by the last CTA at exit)
     unsigned tag = __ldcg(p.ws_ctrl + 2) + 1u;
     if (tag == 0u) tag = 1u;
@@ -285,6 +291,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float acc[C::kCPT];
 #pragma unroll
       for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
+      // Philox noise of this thread's 128 columns is the accumulator's initial value
+      // (drawn while the tile's first MMAs run; the rank's slice only)
+      if (epi_noise) {
+        const long long frow = static_cast<long long>(d0 + row) * p.P;
+        const bool row_ok = d0 + row < p.D;
+#pragma unroll
+        for (int q4 = 0; q4 < C::kCPT / 4; ++q4) {
+          const int col = p0 + col0 + 4 * q4;
+          const long long f = frow + col;
+          if (row_ok && col < p.P && f + 3 >= p.noise_lo && f < p.noise_hi) {  // P % 8 == 0: quads stay in a row
+            const float4 n = philox_normal4(nkb, static_cast<uint64_t>(f >> 2));
+            acc[4 * q4 + 0] = (f + 0 >= p.noise_lo && f + 0 < p.noise_hi) ? p.noise_scale * n.x : 0.0f;
+            acc[4 * q4 + 1] = (f + 1 >= p.noise_lo && f + 1 < p.noise_hi) ? p.noise_scale * n.y : 0.0f;
+            acc[4 * q4 + 2] = (f + 2 >= p.noise_lo && f + 2 < p.noise_hi) ? p.noise_scale * n.z : 0.0f;
+            acc[4 * q4 + 3] = (f + 3 >= p.noise_lo && f + 3 < p.noise_hi) ? p.noise_scale * n.w : 0.0f;
+          }
+        }
+      }
 
       // Coalesced write of this warp's 32 rows x kCPT accumulator columns via a
       // 32x33 smem transpose: every store instruction covers 128 contiguous bytes

@@ -454,3 +454,37 @@ def test_host_streamed_matches_per_layer_and_oracle():
         want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True)
         assert rel(r.grad_w.double().numpy(), want) < BF16_TOL
         assert rel(r.per_sample_norms_sq.double().numpy(), wn) < BF16_TOL
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("B,T,P,D", [(3, 200, 512, 1024), (1, 100, 256, 128), (16, 520, 384, 256), (2, 1024, 1024, 512)])
+def test_ghost_variants_against_oracle(pair, B, T, P, D, monkeypatch):
+    """Ghost-norm phase on single CTAs (128-row Gram tiles) and on CTA pairs
+    (256-row tiles, cta_group::2): norms, clip factors and the clipped sum agree
+    with the oracle; ragged T and several items per cluster included."""
+    monkeypatch.setenv("FDP_GHOST_PAIR", pair)
+    x, dy = randn(B, T, P, D, seed=T + P + int(pair))
+    cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=3, layer_id=5, step=2)
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase="ghost")
+    check(r, x, dy, cfg, BF16_TOL)
+
+
+@pytest.mark.parametrize("epi", ["0", "1"])
+@pytest.mark.parametrize("rank,world", [(0, 1), (1, 2)])
+def test_reweight_noise_placement(epi, rank, world, monkeypatch):
+    """Two-phase reweight pass with Philox noise drawn in the epilogue (accumulator
+    initial value, plain TMA store) or pre-filled by the noise warps (TMA
+    reduce-add): out(sigma) - out(0) is exactly the rank's slice of sigma*C*noise."""
+    monkeypatch.setenv("FDP_EPI_NOISE", epi)
+    B, T, P, D = 2, 256, 1024, 768
+    x, dy = randn(B, T, P, D, seed=31, scale_dy=1e-2)
+    cfg0 = fdp.DPConfig(1.0, 0.0, "mean", seed=5, layer_id=9, step=3)
+    cfg1 = fdp.DPConfig(1.0, 1.5, "mean", seed=5, layer_id=9, step=3)
+    kw = dict(path="two_phase", noise_impl="philox", rank=rank, world=world)
+    g0 = fdp.backward_flashdp(x, dy, cfg0, **kw).grad_w
+    g1 = fdp.backward_flashdp(x, dy, cfg1, **kw).grad_w
+    n = fdp.noise_range(cfg1, 0, P * D, 1.5, noise_impl="philox").view(D, P)
+    lo, hi = P * D * rank // world, P * D * (rank + 1) // world
+    mask = torch.zeros(P * D, device="cuda")
+    mask[lo:hi] = 1.0
+    assert rel(host(g1 - g0), host(n * mask.view(D, P))) < 1e-5
