@@ -436,6 +436,46 @@ fdp::SimtParams simt_params(const fdp_desc* d, const Plan& pl, const Common& c, 
   return s;
 }
 
+fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common& c, float* grad_w, void* ws,
+                                bool reweight) {
+  fdp::StreamParams p{};
+  p.B = static_cast<int>(d->B);
+  p.P = static_cast<int>(d->P);
+  p.D = static_cast<int>(d->D);
+  p.n_pt = pl.n_pt;
+  p.n_wtiles = pl.n_wtiles;
+  p.n_kb = static_cast<int>((d->T + fdp::kBK - 1) / fdp::kBK);
+  p.reweight = reweight ? 1 : 0;
+  p.accumulate = d->accumulate;
+  p.add_noise = reweight ? c.add_noise : 0;
+  // epilogue-drawn Philox noise for tiles held whole: measured faster with <= 2
+  // samples per tile (5120x13824, B=2: 496 -> 433 us), slower from 4 up
+  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", d->B <= 2 ? 1 : 0)) ? 1 : 0;
+  p.noise_impl = d->noise_impl;
+  p.noise_scale = c.noise_scale;
+  p.key_base = c.key_base;
+  p.key_base_g = c.key_base_g;
+  p.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+  p.seed_u = static_cast<uint64_t>(d->seed);
+  p.layer_u = static_cast<uint64_t>(d->layer_id);
+  p.noise_lo = c.noise_lo;
+  p.noise_hi = c.noise_hi;
+  p.grad_w = grad_w;
+  p.factors_in = ws_at<float>(ws, pl.off_factor);
+  p.tile_cnt = ws_at<unsigned>(ws, pl.off_tile_cnt);
+  p.ctrl = ws_at<unsigned>(ws, pl.off_ctrl);
+  p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+  return p;
+}
+
+// Grid of the stream-K kernel: every co-resident cluster, capped by the unit count.
+int stream_grid(const fdp_desc* d, const Plan& pl, const DevInfo& di) {
+  const int cap = fdp::tc_max_coresident_ctas(pl.bn, pl.cg);
+  const long long clusters = (cap > 0 ? cap : di.sms) / pl.cg;
+  const long long units = static_cast<long long>(pl.n_wtiles) * d->B;
+  return static_cast<int>((units < clusters ? units : clusters) * pl.cg);
+}
+
 fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, float* grad_w, float* norms, void* ws,
                         int mode) {
   fdp::TcParams p{};
@@ -575,7 +615,14 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       return fail(FDP_ERR_USAGE, "grad_w must be 16-byte aligned for the fused tensor-core path");
   }
 
+  const bool use_stream = env_int("FDP_STREAMK", 1) != 0;
   if (kind == FDP_KIND_NON_DP) {
+    if (use_stream) {
+      fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, false);
+      if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
+        return cuda_fail(e, "stream-K nondp launch");
+      return FDP_OK;
+    }
     fdp::TcParams p = tc_params(d, pl, c, grad_w, nullptr, ws, fdp::MODE_NONDP);
     if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, false, s)) != cudaSuccess)
       return cuda_fail(e, "tc nondp launch");
@@ -645,9 +692,15 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
                                             ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     }
-    fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
-    if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, q, pl.grid, false, s)) != cudaSuccess)
-      return cuda_fail(e, "tc reweight launch");
+    if (use_stream) {  // stream-K over (tile, sample) units: no partial last wave
+      fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, true);
+      if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
+        return cuda_fail(e, "stream-K reweight launch");
+    } else {
+      fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
+      if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, q, pl.grid, false, s)) != cudaSuccess)
+        return cuda_fail(e, "tc reweight launch");
+    }
   }
   return FDP_OK;
 }

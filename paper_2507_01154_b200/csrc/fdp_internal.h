@@ -76,6 +76,26 @@ cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMa
 // Upper bound on co-resident CTAs of the (bn, cg) kernel on this device (0: cannot run).
 int tc_max_coresident_ctas(int bn, int cg);
 
+// ---- stream-K persistent kernel (fdp_stream.cu): two-phase reweight pass and non-DP dW
+struct StreamParams {
+  int B, P, D, n_pt, n_wtiles, n_kb;
+  int reweight;     // 1: acc += factors_in[b] * G_b per sample; 0: plain sum over samples (non-DP)
+  int accumulate, add_noise, epi_noise, noise_impl;
+  float noise_scale;
+  uint64_t key_base, key_base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long noise_lo, noise_hi;
+  float* grad_w;
+  const float* factors_in;  // [B] clip factor x mean scale
+  unsigned* tile_cnt;       // [n_wtiles * CG] row-initialisation flags (left zeroed)
+  unsigned* ctrl;           // [0] exit counter, [1] error word
+  unsigned long long budget_ns;
+};
+// grid <= co-resident CTAs (split tiles wait on the cluster that initialises them)
+cudaError_t launch_stream(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
+                          const StreamParams& p, int grid, cudaStream_t stream);
+
 // ---- multi-layer fused launch (fdp_group.cu)
 struct GLayer {
   CUtensorMap tm_dy, tm_x, gw;  // operand maps (box 64x64 bf16) and the grad_w store map (32x128 fp32)

@@ -1,0 +1,383 @@
+// fdp_stream.cu -- stream-K persistent tcgen05 kernel for the second phase of the
+// two-phase DP backward (reweight: grad_w = sum_b c_b dY_b^T X_b + noise, with the
+// clip factors c_b from the norm phase) and for the non-DP dW GEMM.
+//
+// Work is a list of (work tile, sample) units on the K co-resident clusters: whole
+// tiles in wave order while full waves last, then the units of the last partial
+// wave split evenly (stream-K), so every cluster carries the same work whatever
+// the tile count (a 4096x4096 layer has 256 pair tiles on 74 clusters: 3 waves +
+// 34 tiles x B samples shared by all). A cluster's work is a list of segments
+// (tile, samples [bb, be)); a tile split across
+// clusters is combined with TMA reduce-adds onto rows initialised once by the
+// noise warps of the cluster holding the tile's first samples (old value when
+// accumulating, + sigma*C*noise), signalled through a per-CTA-tile counter.
+// A tile held whole by one cluster leaves with a plain TMA store (or a reduce-add
+// when accumulating); its Philox noise can start the accumulator instead.
+//
+// Reference: the recompute / reweight half of workflows.py:246-324 (implicit) and
+// the non-DP sum workflows.py:121-150; finalize and noise dpcore.py:60-73.
+#include <cstdio>
+#include <cstdlib>
+
+#include "fdp_internal.h"
+#include "fdp_prefill.cuh"
+#include "fdp_ptx.cuh"
+#include "fdp_rng.cuh"
+
+namespace fdp {
+
+template <int BN, int CG>
+struct SCfg {
+  static constexpr int kBCols = BN / CG;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = kBCols * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStgBytes = 4 * kBM * 128;  // 2 buffers x two 128-row x 32-column fp32 boxes
+  static constexpr int kBarBytes = 1024;
+  static constexpr int kStages = (232448 - 1024 - kBarBytes - kStgBytes) / kStageBytes;
+  static constexpr int kNBuf = 512 / BN;
+  static constexpr int kCPT = BN / 2;
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + kStgBytes + kBarBytes;
+  static constexpr uint32_t kIdesc = make_idesc_bf16_mn(kBM * CG, BN);
+};
+
+// Segment walk of one cluster: the first floor(n_wtiles / K) waves hand out whole
+// tiles in wave order (tile w*K + c), so the clusters of a wave work on
+// neighbouring tiles whose operand rows share L2; the units of the remaining
+// R = n_wtiles mod K tiles (tile-major, R*B of them) are split evenly, cluster c
+// taking [R B c / K, R B (c+1) / K).
+struct SegWalk {
+  int cid, K, B, waves, w;
+  long long u, hi, tail0;
+  __device__ __forceinline__ SegWalk(int cid_, int K_, int B_, int n_wtiles) : cid(cid_), K(K_), B(B_), w(0) {
+    waves = n_wtiles / K_;
+    tail0 = static_cast<long long>(waves) * K_;
+    const long long tail_units = (static_cast<long long>(n_wtiles) - tail0) * B_;
+    u = tail_units * cid_ / K_;
+    hi = tail_units * (cid_ + 1) / K_;
+  }
+  __device__ __forceinline__ bool next(int& wt, int& bb, int& be) {
+    if (w < waves) {
+      wt = w * K + cid;
+      bb = 0;
+      be = B;
+      ++w;
+      return true;
+    }
+    if (u >= hi) return false;
+    wt = static_cast<int>(tail0 + u / B);
+    bb = static_cast<int>(u % B);
+    const long long left = hi - u;
+    be = left < static_cast<long long>(B - bb) ? bb + static_cast<int>(left) : B;
+    u += be - bb;
+    return true;
+  }
+};
+
+template <int BN, int CG>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    dpdw_stream_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
+                       const __grid_constant__ CUtensorMap tm_gw, const StreamParams p) {
+  using C = SCfg<BN, CG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::kStgBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kNBuf;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned* err = p.ctrl + 1;
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+  const bool per_unit = p.reweight != 0;  // one TMEM accumulation per sample (scaled by c_b) vs per segment
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < C::kNBuf; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps * CG);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    prefetch_tmap(&tm_dy);
+    prefetch_tmap(&tm_x);
+  }
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair<512>(tmem_holder);
+    else tmem_alloc<512>(tmem_holder);
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // noise of a whole tile drawn into the accumulator (Philox) instead of pre-filled
+  const bool epi_noise = p.add_noise && p.epi_noise && p.noise_impl == 2;
+  // does tile (split or whole) get its rows initialised by a pre-fill?
+  auto tile_prefilled = [&](bool whole) {
+    return whole ? (p.add_noise && !epi_noise) : (!p.accumulate || p.add_noise);
+  };
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+      int wt, bb, be;
+      while (w.next(wt, bb, be)) {
+        const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+        const int p0 = (wt % p.n_pt) * BN + rank * C::kBCols;
+        for (int b = bb; b < be; ++b) {
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x501);
+            uint8_t* sa = smem + stage * C::kStageBytes;
+            uint8_t* sb = sa + C::kABytes;
+            if constexpr (CG == 2) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], C::kStageBytes * CG);
+              tma_load_3d_pair(sa, &tm_dy, &full[stage], d0, kb * kBK, b);
+              tma_load_3d_pair(sa + 8192, &tm_dy, &full[stage], d0 + 64, kb * kBK, b);
+#pragma unroll
+              for (int j = 0; j < C::kBCols / 64; ++j)
+                tma_load_3d_pair(sb + j * 8192, &tm_x, &full[stage], p0 + 64 * j, kb * kBK, b);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+              tma_load_3d(sa, &tm_dy, &full[stage], d0, kb * kBK, b);
+              tma_load_3d(sa + 8192, &tm_dy, &full[stage], d0 + 64, kb * kBK, b);
+#pragma unroll
+              for (int j = 0; j < C::kBCols / 64; ++j)
+                tma_load_3d(sb + j * 8192, &tm_x, &full[stage], p0 + 64 * j, kb * kBK, b);
+            }
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA) =======================
+    if (lane == 0 && leader) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+      int wt, bb, be;
+      while (w.next(wt, bb, be)) {
+        for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
+          const int ue = per_unit ? ub + 1 : be;
+          mbar_wait(&tempty[buf], tphase ^ 1, err, p.budget_ns, 0x502);
+          tc_fence_after();
+          const uint32_t dtm = tmem_base + buf * BN;
+          uint32_t accum = 0;
+          for (int b = ub; b < ue; ++b) {
+            for (int kb = 0; kb < p.n_kb; ++kb) {
+              mbar_wait(&full[stage], phase, err, p.budget_ns, 0x503);
+              tc_fence_after();
+              const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
+              const uint32_t b_base = a_base + C::kABytes;
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint64_t ad = make_sdesc_sw128(a_base + k * 2048, 8192, 1024);
+                const uint64_t bd = make_sdesc_sw128(b_base + k * 2048, 8192, 1024);
+                if constexpr (CG == 2) tc_mma_f16_pair(dtm, ad, bd, C::kIdesc, accum);
+                else tc_mma_f16(dtm, ad, bd, C::kIdesc, accum);
+                accum = 1;
+              }
+              if constexpr (CG == 2) tc_commit_pair(&empty[stage]);
+              else tc_commit(&empty[stage]);
+              if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            }
+          }
+          if constexpr (CG == 2) tc_commit_pair(&tfull[buf]);
+          else tc_commit(&tfull[buf]);
+          if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ======================= noise warps: initialise the rows of tiles this cluster opens =======================
+    // Runs ahead of the epilogue (rows of different tiles are disjoint); each
+    // initialisation is published through the CTA tile's counter.
+    const int ntid = (warp - 2) * 32 + lane;
+    uint64_t kb = p.key_base, kbg = p.key_base_g;
+    if (p.step_ptr) {
+      kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
+      kbg = kb + kGamma;
+    }
+    SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+    int wt, bb, be;
+    while (w.next(wt, bb, be)) {
+      const bool whole = bb == 0 && be == p.B;
+      if (bb != 0 || !tile_prefilled(whole)) continue;
+      const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+      const int p0 = (wt % p.n_pt) * BN;
+      prefill_rows<BN>(p.grad_w, p.D, p.P, d0, d0 + kBM, p0, p.accumulate != 0, p.add_noise != 0, p.noise_impl,
+                       kbg, kb, p.noise_scale, p.noise_lo, p.noise_hi, ntid);
+      __threadfence();
+      named_bar_sync(3, 64);
+      if (ntid == 0) red_release_add_u32(&p.tile_cnt[wt * CG + rank], 1u);
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ======================= epilogue =======================
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
+    const int row = q * 32 + lane, col0 = half * C::kCPT;
+    uint64_t nkb = p.key_base;
+    if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
+    uint32_t rbuf = 0, rph = 0;
+    SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+    int wt, bb, be;
+    while (w.next(wt, bb, be)) {
+      const bool whole = bb == 0 && be == p.B;
+      const int tile = wt * CG + rank;
+      const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+      const int p0 = (wt % p.n_pt) * BN;
+      float acc[C::kCPT];
+#pragma unroll
+      for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
+      if (epi_noise && whole) {  // the tile's Philox noise starts the accumulator (rank slice only)
+        const long long frow = static_cast<long long>(d0 + row) * p.P;
+        const bool row_ok = d0 + row < p.D;
+#pragma unroll
+        for (int q4 = 0; q4 < C::kCPT / 4; ++q4) {
+          const int col = p0 + col0 + 4 * q4;
+          const long long f = frow + col;
+          if (row_ok && col < p.P && f + 3 >= p.noise_lo && f < p.noise_hi) {  // P % 8 == 0: quads stay in a row
+            const float4 n = philox_normal4(nkb, static_cast<uint64_t>(f >> 2));
+            acc[4 * q4 + 0] = (f + 0 >= p.noise_lo && f + 0 < p.noise_hi) ? p.noise_scale * n.x : 0.0f;
+            acc[4 * q4 + 1] = (f + 1 >= p.noise_lo && f + 1 < p.noise_hi) ? p.noise_scale * n.y : 0.0f;
+            acc[4 * q4 + 2] = (f + 2 >= p.noise_lo && f + 2 < p.noise_hi) ? p.noise_scale * n.z : 0.0f;
+            acc[4 * q4 + 3] = (f + 3 >= p.noise_lo && f + 3 < p.noise_hi) ? p.noise_scale * n.w : 0.0f;
+          }
+        }
+      }
+      for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
+        mbar_wait(&tfull[rbuf], rph, err, p.budget_ns, 0x504);
+        tc_fence_after();
+        const uint32_t buf = rbuf;
+        if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
+        const float f = per_unit ? p.factors_in[ub] : 1.0f;
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
+#pragma unroll
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tb + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_leader(&tempty[buf]);
+          else mbar_arrive(&tempty[buf]);
+        }
+      }
+      // ---- finalize: reduce-add onto initialised rows (split tiles, accumulation,
+      // pre-filled noise) or plain store; 32-column boxes, double-buffered
+      const bool rmw = !whole || p.accumulate || (p.add_noise && !epi_noise);
+      if (tile_prefilled(whole) && etid == 0) {
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_u32(&p.tile_cnt[tile]) < 1u) {
+          if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x505);
+          __nanosleep(64);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C::kCPT / 32; ++c) {
+        uint8_t* sbuf = stg + (c & 1) * (2 * kBM * 128);
+        if (etid == 0) bulk_wait_read_le1();
+        named_bar_sync(1, 32 * kEpiWarps);
+        uint8_t* box = sbuf + half * (kBM * 128) + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) =
+              make_float4(acc[c * 32 + 4 * j], acc[c * 32 + 4 * j + 1], acc[c * 32 + 4 * j + 2],
+                          acc[c * 32 + 4 * j + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          fence_proxy_async_global();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = p0 + h * C::kCPT + c * 32;
+            if (rmw) tma_reduce_add_2d(&tm_gw, sbuf + h * (kBM * 128), col, d0);
+            else tma_store_2d(&tm_gw, sbuf + h * (kBM * 128), col, d0);
+          }
+          bulk_commit();
+        }
+      }
+    }
+    if (etid == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
+  }
+  if (threadIdx.x == 0) {  // last CTA out re-arms the tile counters
+    __threadfence();
+    const unsigned old = atomicAdd(&p.ctrl[0], 1u);
+    if (old == gridDim.x - 1) {
+      __threadfence();
+      for (int t = 0; t < p.n_wtiles * CG; ++t) p.tile_cnt[t] = 0u;
+      p.ctrl[0] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+template <int BN, int CG>
+static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
+                                      const StreamParams& p, int grid, cudaStream_t stream) {
+  using C = SCfg<BN, CG>;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(dpdw_stream_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (CG == 2) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  // Split tiles wait on the cluster that initialises them, which is resident:
+  // the grid never exceeds the co-resident capacity (host planner).
+  return cudaLaunchKernelEx(&cfg, dpdw_stream_kernel<BN, CG>, tm_dy, tm_x, tm_gw, p);
+}
+
+cudaError_t launch_stream(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
+                          const StreamParams& p, int grid, cudaStream_t stream) {
+  if (cg == 2) {
+    if (bn == 256) return launch_stream_impl<256, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
+    return launch_stream_impl<128, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  }
+  if (bn == 256) return launch_stream_impl<256, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  return launch_stream_impl<128, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+}
+
+}  // namespace fdp

@@ -488,3 +488,29 @@ def test_reweight_noise_placement(epi, rank, world, monkeypatch):
     mask = torch.zeros(P * D, device="cuda")
     mask[lo:hi] = 1.0
     assert rel(host(g1 - g0), host(n * mask.view(D, P))) < 1e-5
+
+
+@pytest.mark.parametrize("streamk", ["0", "1"])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_two_phase_split_tiles_accumulate(streamk, accumulate, monkeypatch):
+    """Stream-K reweight pass: 32 pair tiles x 3 samples on the co-resident
+    clusters split tiles across clusters (reduce-adds onto rows initialised once);
+    with accumulate=True the result lands on top of grad_out; reference-keyed noise
+    makes sigma > 0 exact."""
+    monkeypatch.setenv("FDP_STREAMK", streamk)
+    B, T, P, D = 3, 256, 2048, 1024
+    x, dy = randn(B, T, P, D, seed=51, scale_dy=1e-2)
+    cfg = fdp.DPConfig(0.7, 1.0, "mean", seed=8, layer_id=2, step=5)
+    g0 = torch.randn(D, P, device="cuda")
+    out = g0.clone()
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", noise_impl="keyed_f64", grad_out=out,
+                             accumulate=accumulate)
+    want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True)
+    if accumulate:
+        want = want + host(g0)
+    assert rel(host(r.grad_w), want) < BF16_TOL
+    assert rel(host(r.per_sample_norms_sq), wn) < BF16_TOL
+    nd = g0.clone()
+    fdp.run_backward(W.NON_DP, x, dy, None, grad_out=nd, accumulate=accumulate)
+    want_nd = O.nondp_backward(host(x), host(dy)) + (host(g0) if accumulate else 0.0)
+    assert rel(host(nd), want_nd) < BF16_TOL
