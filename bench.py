@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
     ap.add_argument("--per-layer", action="store_true",
                     help="one fused launch per layer instead of one multi-layer launch per step")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="N>1: layer chunks whose all-reduce overlaps the next chunk's launch")
+    ap.add_argument("--comm-sms", type=int, default=16, help="N>1: SMs left free for the NCCL kernel")
     return ap.parse_args()
 
 
@@ -241,8 +244,15 @@ def main():
     if not a.per_layer:
         glayers = [(xs[name], dys[name], fdp.DPConfig(clip_c=a.clip, sigma=a.sigma, reduction="mean", seed=1234,
                                                       layer_id=lid, step=0)) for lid, name, P, D in layers]
-        group = fdp.PreparedGroup(glayers, grads=[c.grad_w for _, c in calls], noise_impl=a.noise, rank=rank,
-                                  world=world, mean_batch=global_B, device_step=device_step)
+        if world > 1:
+            from paper_2507_01154_b200.ddp import ChunkedAllReduceBackward
+
+            group = ChunkedAllReduceBackward(glayers, flat, n_chunks=a.chunks, comm_sms=a.comm_sms,
+                                             noise_impl=a.noise, rank=rank, world=world, mean_batch=global_B,
+                                             device_step=device_step)
+        else:
+            group = fdp.PreparedGroup(glayers, grads=[c.grad_w for _, c in calls], noise_impl=a.noise, rank=rank,
+                                      world=world, mean_batch=global_B, device_step=device_step)
 
     stream = torch.cuda.current_stream(dev)
     dominant = "h0.c_fc"  # largest per-launch work; every block's c_fc is timed
@@ -258,9 +268,7 @@ def main():
                 dom_events.append((e0, e1))
             else:
                 group(stream)
-            device_step.add_(1)
-            if world > 1:
-                dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+            device_step.add_(1)  # N>1: the chunked group already all-reduced every bucket
             return
         for name, c in calls:
             if record and name.endswith(".c_fc"):
@@ -374,6 +382,7 @@ def main():
                 c(stream)
 
         def timeit(fn, n):
+            time.sleep(1.0)  # same idle start for every arm (clock / power state)
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
@@ -385,16 +394,36 @@ def main():
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / n
 
-        try:
-            nd_ms = timeit(nondp_cublas, max(10, a.steps // 4))
-        except Exception as e:  # noqa: BLE001
-            nd_ms = None
-            extra["nondp_cublas_error"] = repr(e)[:200]
-        nd_ours_ms = timeit(nondp_ours, max(10, a.steps // 4))
+        # paired comparison: DP step and non-DP dW timed alike, alternating, best of 3
+        n_cmp = max(20, a.steps // 2)
+        dp_t, nd_t, nd_own_t = [], [], []
+        nd_err = None
+        def dp_kernels():  # the DP backward alone (collectives excluded on both sides)
+            if group is not None:
+                group(stream)
+            else:
+                for _, c in calls:
+                    c(stream)
+            device_step.add_(1)
+
+        for _ in range(3):
+            dp_t.append(timeit(dp_kernels, n_cmp))
+            try:
+                nd_t.append(timeit(nondp_cublas, n_cmp))
+            except Exception as e:  # noqa: BLE001
+                nd_err = repr(e)[:200]
+            nd_own_t.append(timeit(nondp_ours, n_cmp))
+        nd_ms = min(nd_t) if nd_t else None
+        dp_ms = min(dp_t)
+        nd_ours_ms = min(nd_own_t)
+        if nd_err:
+            extra["nondp_cublas_error"] = nd_err
         extra["nondp"] = {
-            "cublas_ms_per_step": nd_ms, "tcgen05_nondp_ms_per_step": nd_ours_ms,
-            "dp_over_nondp_pct_vs_cublas": (100.0 * nd_ms / ms_per_step) if nd_ms else None,
-            "dp_over_nondp_pct_vs_own": 100.0 * nd_ours_ms / ms_per_step,
+            "method": "DP step, cuBLAS non-DP dW and our non-DP dW each timed over %d steps after 1 s idle, "
+                      "alternating, best of 3" % n_cmp,
+            "dp_ms_per_step": dp_ms, "cublas_ms_per_step": nd_ms, "tcgen05_nondp_ms_per_step": nd_ours_ms,
+            "dp_over_nondp_pct_vs_cublas": (100.0 * nd_ms / dp_ms) if nd_ms else None,
+            "dp_over_nondp_pct_vs_own": 100.0 * nd_ours_ms / dp_ms,
             "nondp_tflops_cublas": flops_per_step_rank / (nd_ms * 1e-3) / 1e12 if nd_ms else None,
         }
         # restore DP grads (non-DP calls overwrote them); not part of any timing

@@ -175,6 +175,15 @@ FDP_API int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* con
                                float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes,
                                void* stream);
 
+/* Same as fdp_group_workspace_bytes / fdp_backward_group with the launch limited
+ * to at most `max_ctas` CTAs (0 = all co-resident CTAs): the remaining SMs stay
+ * free for a kernel running concurrently on another stream, e.g. the NCCL
+ * all-reduce of the previous layer chunk under data parallelism. */
+FDP_API int fdp_group_workspace_bytes_ex(int32_t n, const fdp_desc* descs, int32_t max_ctas, size_t* bytes);
+FDP_API int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x, const void* const* dy,
+                                  float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes,
+                                  int32_t max_ctas, void* stream);
+
 /* dpcore.noise_for_indices for flat indices [lo, hi) scaled by `scale`
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);

@@ -34,7 +34,7 @@ FLAG_DETERMINISTIC = 8
 EXPORTED_SYMBOLS = (
     "fdp_abi_version", "fdp_last_error", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes",
     "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_partition",
-    "fdp_group_workspace_bytes", "fdp_backward_group",
+    "fdp_group_workspace_bytes", "fdp_backward_group", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex",
 )
 
 
@@ -101,7 +101,12 @@ def load() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_size_t)]
     lib.fdp_backward_group.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc)] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [
         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-    for name in ("fdp_group_workspace_bytes", "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
+    lib.fdp_group_workspace_bytes_ex.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc), ctypes.c_int32,
+                                                 ctypes.POINTER(ctypes.c_size_t)]
+    lib.fdp_backward_group_ex.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc)] + [
+        ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p]
+    for name in ("fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
+                 "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
                  "fdp_dw", "fdp_noise", "fdp_noise_partition"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib

@@ -714,11 +714,11 @@ struct GroupPlan {
   size_t total = 0;
 };
 
-int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl);
+int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, int max_ctas, GroupPlan& gpl);
 
 // The packing search costs milliseconds; a training loop calls the same layer
 // list every step, so plans are cached by (device, layer extents, flags, env).
-int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl) {
+int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, int max_ctas, GroupPlan& gpl) {
   static std::mutex mu;
   static std::map<std::vector<long long>, GroupPlan> cache;
   std::vector<long long> key;
@@ -728,6 +728,7 @@ int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& g
   key.push_back(env_int("FDP_FORCE_BN", 0));
   key.push_back(env_int("FDP_FORCE_CG", 0));
   key.push_back(env_int("FDP_NO_PACK", 0));
+  key.push_back(max_ctas);
   if (n > 0 && n <= fdp::kMaxGroupLayers) {
     key.push_back(descs[0].flags & FDP_FLAG_TRACE);
     for (int l = 0; l < n; ++l) {
@@ -750,7 +751,7 @@ int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& g
       return FDP_OK;
     }
   }
-  int rc = plan_group_uncached(n, descs, di, gpl);
+  int rc = plan_group_uncached(n, descs, di, max_ctas, gpl);
   if (rc == FDP_OK) {
     std::lock_guard<std::mutex> g(mu);
     if (cache.size() > 256) cache.clear();
@@ -759,7 +760,7 @@ int plan_group(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& g
   return rc;
 }
 
-int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, GroupPlan& gpl) {
+int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, int max_ctas, GroupPlan& gpl) {
   if (n < 1 || n > fdp::kMaxGroupLayers)
     return fail(FDP_ERR_USAGE, "fdp_backward_group takes 1..%d layers, got %d", fdp::kMaxGroupLayers, n);
   if (di.major != 10) return fail(FDP_ERR_USAGE, "fdp_backward_group needs an sm_100 device");
@@ -776,8 +777,9 @@ int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, Gro
   for (auto& cd : cands) {
     const int bn = cd[0], cg = cd[1];
     if ((forced_bn && bn != forced_bn) || (forced_cg && cg != forced_cg)) continue;
-    const long long cap = fdp::tc_max_coresident_ctas(bn, cg);
-    if (cap <= 0) continue;
+    long long cap = fdp::tc_max_coresident_ctas(bn, cg);
+    if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;  // SMs left free (e.g. for a concurrent NCCL kernel)
+    if (cap < cg) continue;
     const int K = static_cast<int>(cap / cg);  // co-resident clusters
     const double rate = bn == 256 ? (cg == 2 ? 9.6e12 : 7.4e12) : (cg == 2 ? 6.4e12 : 6.3e12);
     // Pack layers onto cluster ranges: every cluster walks the layers in order,
@@ -921,25 +923,37 @@ int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, floa
 }
 
 
-int fdp_group_workspace_bytes(int32_t n, const fdp_desc* descs, size_t* bytes) {
+int fdp_group_workspace_bytes_ex(int32_t n, const fdp_desc* descs, int32_t max_ctas, size_t* bytes) {
   if (!descs || !bytes) return fail(FDP_ERR_USAGE, "null argument");
+  if (max_ctas < 0) return fail(FDP_ERR_USAGE, "max_ctas must be >= 0, got %d", max_ctas);
   DevInfo di;
   int rc = get_dev(di);
   if (rc) return rc;
   GroupPlan gpl;
-  if ((rc = plan_group(n, descs, di, gpl))) return rc;
+  if ((rc = plan_group(n, descs, di, max_ctas, gpl))) return rc;
   *bytes = gpl.total;
   return FDP_OK;
 }
 
+int fdp_group_workspace_bytes(int32_t n, const fdp_desc* descs, size_t* bytes) {
+  return fdp_group_workspace_bytes_ex(n, descs, 0, bytes);
+}
+
 int fdp_backward_group(int32_t n, const fdp_desc* descs, const void* const* x, const void* const* dy,
                        float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes, void* stream) {
+  return fdp_backward_group_ex(n, descs, x, dy, grad_w, norms_sq, ws, ws_bytes, 0, stream);
+}
+
+int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x, const void* const* dy,
+                          float* const* grad_w, float* const* norms_sq, void* ws, size_t ws_bytes, int32_t max_ctas,
+                          void* stream) {
   if (!descs || !x || !dy || !grad_w || !norms_sq) return fail(FDP_ERR_USAGE, "null argument");
+  if (max_ctas < 0) return fail(FDP_ERR_USAGE, "max_ctas must be >= 0, got %d", max_ctas);
   DevInfo di;
   int rc = get_dev(di);
   if (rc) return rc;
   GroupPlan gpl;
-  if ((rc = plan_group(n, descs, di, gpl))) return rc;
+  if ((rc = plan_group(n, descs, di, max_ctas, gpl))) return rc;
   if (!ws || ws_bytes < gpl.total)
     return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
                 gpl.total);

@@ -267,12 +267,17 @@ class PreparedGroup:
     noise key = layer_id), norms and outputs; results equal per-layer
     backward_flashdp calls (up to fp32 summation order across sample groups).
 
-    layers: sequence of (x, dy, cfg) with contiguous bf16 CUDA tensors."""
+    layers: sequence of (x, dy, cfg) with contiguous bf16 CUDA tensors.
+    max_ctas > 0 caps the launch (SMs left free for a concurrent collective)."""
 
     def __init__(self, layers, *, grads=None, norms=None, noise_impl: str = "keyed_f32", accumulate: bool = False,
                  add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
-                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+                 device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                 max_ctas: int = 0):
         n = len(layers)
+        if max_ctas < 0:
+            raise UsageError(f"max_ctas must be >= 0, got {max_ctas}")
+        self.max_ctas = int(max_ctas)
         if n < 1:
             raise UsageError("PreparedGroup needs at least one layer")
         self.layers = list(layers)
@@ -303,7 +308,7 @@ class PreparedGroup:
         lib = _lib.load()
         self._lib = lib
         nbytes = ctypes.c_size_t()
-        _lib.check(lib.fdp_group_workspace_bytes(n, descs, ctypes.byref(nbytes)))
+        _lib.check(lib.fdp_group_workspace_bytes_ex(n, descs, self.max_ctas, ctypes.byref(nbytes)))
         if workspace is None:
             workspace = torch.zeros(max(nbytes.value, 4096), dtype=torch.uint8, device=self.layers[0][0].device)
         elif workspace.numel() * workspace.element_size() < nbytes.value:
@@ -314,8 +319,8 @@ class PreparedGroup:
     def __call__(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         s = stream if stream is not None else torch.cuda.current_stream(self.layers[0][0].device)
         xs, dys, gs, ns = self._ptrs
-        _lib.check(self._lib.fdp_backward_group(self._n, self.descs, xs, dys, gs, ns, self.workspace.data_ptr(),
-                                                self.workspace.numel(), s.cuda_stream))
+        _lib.check(self._lib.fdp_backward_group_ex(self._n, self.descs, xs, dys, gs, ns, self.workspace.data_ptr(),
+                                                   self.workspace.numel(), self.max_ctas, s.cuda_stream))
 
 
 class HostStreamedBackward:

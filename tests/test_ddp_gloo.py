@@ -68,3 +68,44 @@ def test_partition_matches_kernel_partition():
             sl = [noise_partition(n, r, world) for r in range(world)]
             assert sl[0][0] == 0 and sl[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+
+
+def _chunk_worker(rank, world, port, x, dy, cfgs, out):
+    """ChunkedAllReduceBackward on CPU: each chunk's 'launch' writes the rank's
+    oracle contribution into its slices of the flat buffer; the chunk buckets are
+    all-reduced (gloo) as they complete."""
+    from paper_2507_01154_b200.ddp import ChunkedAllReduceBackward
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    xt, dyt = torch.tensor(x), torch.tensor(dy)
+    layers = [(xt, dyt, c) for c in cfgs]
+    n_el = sum(dy.shape[2] * x.shape[2] for _ in cfgs)
+    flat = torch.zeros(n_el, dtype=torch.float64)
+
+    def make_group(chunk_layers, grads, cap):
+        def run():
+            for (_, _, c), g in zip(chunk_layers, grads):
+                g.copy_(torch.tensor(_rank_contribution(x, dy, c, rank, world)))
+        return run
+
+    step = ChunkedAllReduceBackward(layers, flat, n_chunks=2, world=world, make_group=make_group)
+    assert len(step.chunks) == 2
+    step()
+    if rank == 0:
+        out["flat"] = flat.numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_chunked_allreduce_backward_two_ranks():
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (4, 3, 8))
+    dy = rng.uniform(-1, 1, (4, 3, 6))
+    cfgs = [O.Cfg(0.5, 1.0, "mean", 7, l, 3) for l in range(3)]
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_chunk_worker, args=(2, _free_port(), x, dy, cfgs, out), nprocs=2, join=True)
+        want = np.concatenate([O.dp_backward(x, dy, c, exact_noise=True)[0].reshape(-1) for c in cfgs])
+        assert np.max(np.abs(out["flat"] - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
