@@ -102,8 +102,11 @@ enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2,
                     reproducible across runs, slower for layers that need groups */
                  FDP_FLAG_DETERMINISTIC = 8 };
 
-/* Norm phase of the TWO_PHASE path. */
-enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2 };
+/* Norm phase of the TWO_PHASE path. SINGLE (B == 1, no accumulation): the only
+ * sample's gradient IS the layer's GEMM, so it is computed once (stream-K
+ * tcgen05, per-tile sums of squares in the epilogue) and one elementwise pass
+ * applies the clip factor and the noise. */
+enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2, FDP_NORMS_SINGLE = 3 };
 
 typedef struct fdp_desc {
   int64_t B, T, P, D;       /* X (B,T,P), dY (B,T,D)                          */

@@ -137,6 +137,10 @@ int validate(const fdp_desc* d, int32_t kind) {
   if (d->noise_impl < FDP_NOISE_KEYED_F32 || d->noise_impl > FDP_NOISE_PHILOX)
     return fail(FDP_ERR_USAGE, "unknown noise_impl %d", d->noise_impl);
   if (d->path < FDP_PATH_AUTO || d->path > FDP_PATH_SIMT) return fail(FDP_ERR_USAGE, "unknown path %d", d->path);
+  if (d->norm_phase < FDP_NORMS_AUTO || d->norm_phase > FDP_NORMS_SINGLE)
+    return fail(FDP_ERR_USAGE, "unknown norm_phase %d", d->norm_phase);
+  if (d->norm_phase == FDP_NORMS_SINGLE && (d->B != 1 || d->accumulate))
+    return fail(FDP_ERR_USAGE, "norm_phase single needs B == 1 and accumulate == 0");
   return FDP_OK;
 }
 
@@ -170,8 +174,11 @@ int env_int(const char* name, int dflt) {
 
 // Ghost norms cost ~T^2 (P + D) (1 + 1/nT) flops per sample, recomputing the
 // per-sample gradient 2 T P D: take the cheaper one unless the caller forces it.
+bool single_ok(const fdp_desc* d) { return d->B == 1 && !d->accumulate; }
+
 int choose_norm_phase(const fdp_desc* d) {
-  if (d->norm_phase == FDP_NORMS_GHOST || d->norm_phase == FDP_NORMS_RECOMPUTE) return d->norm_phase;
+  if (d->norm_phase != FDP_NORMS_AUTO) return d->norm_phase;
+  if (single_ok(d)) return FDP_NORMS_SINGLE;
   const double nT = static_cast<double>((d->T + 127) / 128);
   const double ghost = static_cast<double>(d->T) * d->T * (d->P + d->D) * (1.0 + 1.0 / nT);
   const double recompute = 2.0 * d->T * d->P * d->D;
@@ -285,7 +292,10 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
       const double dw_flops = 2.0 * d->B * d->T * static_cast<double>(d->P) * d->D;
       const double nT = static_cast<double>((d->T + 127) / 128);
       const double ghost_flops = d->B * static_cast<double>(d->T) * d->T * (d->P + d->D) * (1.0 + 1.0 / nT);
-      const double norm_flops = std::min(ghost_flops, dw_flops);
+      const double norm_flops = (single_ok(d) && d->norm_phase != FDP_NORMS_GHOST &&
+                                 d->norm_phase != FDP_NORMS_RECOMPUTE)
+                                    ? 0.0
+                                    : std::min(ghost_flops, dw_flops);
       const double two_phase_est = (norm_flops / 0.55e15) + dw_flops / 1.1e15 + 25e-6;
       if (best_bn && want == FDP_PATH_AUTO && two_phase_est < 0.8 * best) best_bn = 0;
       if (best_bn && want != FDP_PATH_TWO_PHASE) {
@@ -330,6 +340,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     pl.grid = (pl.n_wtiles < max_clusters ? pl.n_wtiles : max_clusters) * pl.cg;
     if (kind == FDP_KIND_NON_DP) pl.launches = 1;
     else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;  // G, norms, reduce, clip, sum
+    else if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_SINGLE) pl.launches = 2;  // GEMM, finalize
     else pl.launches = 3;                                     // norms, reduce, reweight
   } else {
     pl.grid = pl.n_tiles;
@@ -653,6 +664,22 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_FUSED);
     if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, true, s)) != cudaSuccess)
       return cuda_fail(e, "tc fused launch");
+    return FDP_OK;
+  }
+  // TWO_PHASE, B == 1: the sample's gradient is the GEMM itself; its norm comes from
+  // the GEMM epilogue and one elementwise pass applies the clip factor and the noise
+  if (pl.norm_phase == FDP_NORMS_SINGLE) {
+    fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, false);
+    q.norm_part = ws_at<float>(ws, pl.off_part);
+    if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
+      return cuda_fail(e, "stream-K single-sample GEMM launch");
+    if ((e = fdp::single_sample_finalize(grad_w, d->D * d->P, q.norm_part, pl.n_tiles, d->clip_c,
+                                         d->clip_c * d->clip_c, c.inv_batch, norms, c.add_noise, d->noise_impl,
+                                         c.noise_scale, c.key_base, c.key_base_g,
+                                         reinterpret_cast<const long long*>(d->device_step),
+                                         static_cast<uint64_t>(d->seed), static_cast<uint64_t>(d->layer_id),
+                                         c.noise_lo, c.noise_hi, s)) != cudaSuccess)
+      return cuda_fail(e, "single-sample finalize");
     return FDP_OK;
   }
   // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass

@@ -89,6 +89,7 @@ struct StreamParams {
   float* grad_w;
   const float* factors_in;  // [B] clip factor x mean scale
   unsigned* tile_cnt;       // [n_wtiles * CG] row-initialisation flags (left zeroed)
+  float* norm_part;         // B == 1 single-sample path: sum of squares of each CTA tile ([n_wtiles * CG]) or null
   unsigned* ctrl;           // [0] exit counter, [1] error word
   unsigned long long budget_ns;
 };
@@ -177,6 +178,13 @@ cudaError_t explicit_norms(const float* g, int B, long long DP, float* part, int
 cudaError_t explicit_clip(const float* g, float* gp, const float* factors, int B, long long DP, cudaStream_t s);
 cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int P, const SimtParams& p,
                                   cudaStream_t s);
+
+// B == 1 second pass: ||G||^2 from the per-tile partials (fixed order), then
+// grad_w = grad_w * min(1, C/||G||) * inv_batch (+ sigma*C*noise on [lo, hi)).
+cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part, int n_parts, double clip_c,
+                                   double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl,
+                                   float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
+                                   uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s);
 
 cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int impl, uint64_t base,
                        uint64_t base_g, cudaStream_t s);

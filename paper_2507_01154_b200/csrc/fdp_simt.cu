@@ -199,6 +199,62 @@ __global__ void k_noise_fill(float* out, long long lo, long long hi, float scale
   }
 }
 
+__global__ void __launch_bounds__(256)
+    k_single_finalize(float* __restrict__ g, long long n, const float* __restrict__ part, int n_parts, double clip_c,
+                      double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl, float scale,
+                      uint64_t base, uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u,
+                      long long lo, long long hi) {
+  __shared__ float s_f;
+  if (threadIdx.x < 32) {  // every block sums the partials in the same fixed order
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n_parts; i += 32) t += static_cast<double>(part[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      const double cf = (t <= clip_c2) ? 1.0 : clip_c / sqrt(t);  // dpcore.py:41-47
+      s_f = static_cast<float>(cf) * inv_batch;
+      if (blockIdx.x == 0 && norms_out) norms_out[0] = static_cast<float>(t);
+    }
+  }
+  __syncthreads();
+  const float f = s_f;
+  if (step_ptr) {
+    base = absorb3(seed_u, layer_u, static_cast<uint64_t>(*step_ptr));
+    base_g = base + kGamma;
+  }
+  float4* g4 = reinterpret_cast<float4*>(g);
+  const long long n4 = n >> 2;  // n = D * P, P % 8 == 0
+  constexpr int kU = 4;         // float4 per thread per iteration: loads in flight, independent Philox chains
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n4; i0 += stride * kU) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n4) v[u] = g4[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= n4) continue;
+      v[u].x *= f;
+      v[u].y *= f;
+      v[u].z *= f;
+      v[u].w *= f;
+      const long long e = i << 2;
+      if (add_noise && e + 3 >= lo && e < hi) {
+        const float4 z = impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
+                                   : noise_draw4(impl, base_g, base, static_cast<uint64_t>(i));
+        if (e + 0 >= lo && e + 0 < hi) v[u].x += scale * z.x;
+        if (e + 1 >= lo && e + 1 < hi) v[u].y += scale * z.y;
+        if (e + 2 >= lo && e + 2 < hi) v[u].z += scale * z.z;
+        if (e + 3 >= lo && e + 3 < hi) v[u].w += scale * z.w;
+      }
+      g4[i] = v[u];
+    }
+  }
+}
+
 int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -207,6 +263,16 @@ int grid_for(long long n, int threads) {
 }
 
 }  // namespace
+
+cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part, int n_parts, double clip_c,
+                                   double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl,
+                                   float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
+                                   uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s) {
+  k_single_finalize<<<grid_for(n / 16, 256), 256, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch,
+                                                         norms_out, add_noise, impl, noise_scale, base, base_g,
+                                                         step_ptr, seed_u, layer_u, lo, hi);
+  return cudaGetLastError();
+}
 
 cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s) {
   k_partial_norms<<<dim3(p.n_pt, p.n_dt, p.B), 256, 0, s>>>(p);

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNBuf;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps] tile sum-of-squares partials
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -276,6 +277,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) {
           if constexpr (CG == 2) mbar_arrive_leader(&tempty[buf]);
           else mbar_arrive(&tempty[buf]);
+        }
+      }
+      if (p.norm_part) {  // single-sample path: this CTA tile's ||G||^2 partial (tiles are whole)
+        float sq = 0.0f;
+#pragma unroll
+        for (int i = 0; i < C::kCPT; ++i) sq = fmaf(acc[i], acc[i], sq);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[ew] = sq;
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          float t = 0.0f;
+#pragma unroll
+          for (int k = 0; k < kEpiWarps; ++k) t += red[k];
+          p.norm_part[tile] = t;
         }
       }
       // ---- finalize: reduce-add onto initialised rows (split tiles, accumulation,

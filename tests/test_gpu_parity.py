@@ -514,3 +514,28 @@ def test_two_phase_split_tiles_accumulate(streamk, accumulate, monkeypatch):
     fdp.run_backward(W.NON_DP, x, dy, None, grad_out=nd, accumulate=accumulate)
     want_nd = O.nondp_backward(host(x), host(dy)) + (host(g0) if accumulate else 0.0)
     assert rel(host(nd), want_nd) < BF16_TOL
+
+
+@pytest.mark.parametrize("B,T,P,D,red", [(1, 512, 1024, 768, "mean"), (1, 200, 2048, 2048, "sum"),
+                                         (1, 64, 128, 384, "mean")])
+def test_single_sample_path_against_oracle(B, T, P, D, red):
+    """B == 1 two-phase path: the GEMM's epilogue gives ||G||^2 and one elementwise
+    pass applies the clip and the noise (reference-keyed: exact), incl. a rank slice."""
+    x, dy = randn(B, T, P, D, seed=P + T, scale_dy=1e-2)
+    cfg = fdp.DPConfig(0.3, 1.0, red, seed=6, layer_id=1, step=2)
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", noise_impl="keyed_f64")
+    assert fdp.execution_plan(tuple(x.shape), tuple(dy.shape), path="two_phase")["norm_phase"] == "single"
+    want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True)
+    assert rel(host(r.grad_w), want) < BF16_TOL
+    assert rel(host(r.per_sample_norms_sq), wn) < BF16_TOL
+    # rank 1 of 2 adds the noise of its slice only
+    r1 = fdp.backward_flashdp(x, dy, cfg, path="two_phase", noise_impl="keyed_f64", rank=1, world=2)
+    n = P * D
+    want1, _ = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True, noise_lo=n // 2, noise_hi=n)
+    assert rel(host(r1.grad_w), want1) < BF16_TOL
+
+
+def test_single_sample_norm_phase_needs_one_sample():
+    x, dy = randn(2, 64, 128, 128, seed=1)
+    with pytest.raises(fdp.UsageError):
+        fdp.backward_flashdp(x, dy, fdp.DPConfig(1.0, 0.0), path="two_phase", norm_phase="single")
