@@ -143,17 +143,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     // ======================= MMA issuer (leader CTA) =======================
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      // FDP_FLAG_TRACE: where the MMA issuer waits (ns): on a TMEM buffer (epilogue
+      // behind) and on operand stages (TMA behind); slots 248-251 of the CTA's row
+      const bool tr = gp.trace != nullptr;
+      uint64_t w_tmem = 0, w_full = 0, t_first = 0, units = 0;
       for (int l = 0; l < gp.n_layers; ++l) {
         const GLayer& L = gp.L[l];
         const int lc = lcid(L);
         if (lc >= L.n_wtiles * L.groups) continue;
         const int group = lc / L.n_wtiles;
         for (int b = group; b < L.B; b += L.groups) {
+          uint64_t t0 = tr ? globaltimer_ns() : 0;
+          if (tr && !t_first) t_first = t0;
           mbar_wait(&tempty[buf], tphase ^ 1, err, gp.budget_ns, 0x402);
+          if (tr) w_tmem += globaltimer_ns() - t0;
+          ++units;
           tc_fence_after();
           const uint32_t dtm = tmem_base + buf * BN;
           for (int kb = 0; kb < L.n_kb; ++kb) {
+            if (tr) t0 = globaltimer_ns();
             mbar_wait(&full[stage], phase, err, gp.budget_ns, 0x403);
+            if (tr) w_full += globaltimer_ns() - t0;
             tc_fence_after();
             const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
             const uint32_t b_base = a_base + C::kABytes;
@@ -172,6 +182,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
           else tc_commit(&tfull[buf]);
           if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
         }
+      }
+      if (tr) {
+        unsigned long long* row = gp.trace + blockIdx.x * 256;
+        row[248] = w_tmem;
+        row[249] = w_full;
+        row[250] = globaltimer_ns() - t_first;  // first unit's wait .. last MMA issued
+        row[251] = units;
       }
     }
   } else if (warp == 2 || warp == 3) {
@@ -210,6 +227,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
     const int row = q * 32 + lane, col0 = half * C::kCPT;
     uint32_t rbuf = 0, rph = 0;
+    // pass 1 of sample b's unit in TMEM buffer `buf`: intra-block reduce of
+    // ||G_b||^2 over this CTA tile, published as one tagged 8-byte atomic
+    auto pass1_publish = [&](const GLayer& Lx, int bx, int tilex, uint32_t bufx) {
+      const uint32_t tbx = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bufx * BN + col0;
+      float part = 0.0f;
+#pragma unroll
+      for (int c = 0; c < C::kCPT / 16; ++c) {
+        float v[16];
+        tmem_ld16(tbx + c * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) red[ew] = part;
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (etid == 0) {
+        float sx = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kEpiWarps; ++w) sx += red[w];
+        publish_u64(Lx.tagged + static_cast<long long>(bx) * Lx.n_tiles + tilex,
+                    (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(sx), gp.pub_mode);
+      }
+    };
     for (int l = 0; l < gp.n_layers; ++l) {
       const GLayer& L = gp.L[l];
       const int lc = lcid(L);
@@ -228,32 +270,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       for (int b = group; b < L.B; b += L.groups) {
         mbar_wait(&tfull[rbuf], rph, err, gp.budget_ns, 0x404);
         tc_fence_after();
-        if (first && l < 16) GTRACE(8 * l);  // layer l: first sample's MMA done
-        first = false;
         const uint32_t buf = rbuf;
         if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
+        pass1_publish(L, b, tile, buf);
+        if (first && l < 16) GTRACE(8 * l);  // layer l: first sample published
+        first = false;
         const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
-        // intra-block reduce of ||G_b||^2, published as one tagged 8-byte store
-        float part = 0.0f;
-#pragma unroll
-        for (int c = 0; c < C::kCPT / 16; ++c) {
-          float v[16];
-          tmem_ld16(tb + c * 16, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) red[ew] = part;
-        named_bar_sync(1, 32 * kEpiWarps);
-        if (etid == 0) {
-          float s = 0.0f;
-#pragma unroll
-          for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-          publish_u64(L.tagged + static_cast<long long>(b) * L.n_tiles + tile,
-                      (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(s), gp.pub_mode);
-        }
         // block-wise all-reduce: fixed-order fp64 sum of the tagged partials
         if (ew == 0) {
           const unsigned long long* slots = L.tagged + static_cast<long long>(b) * L.n_tiles;

@@ -24,7 +24,7 @@ def main():
     sigma = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
     g = torch.Generator(device="cuda").manual_seed(0)
     layers = []
-    for blk in range(2):
+    for blk in range(int(os.environ.get("TG_BLOCKS", "2"))):
         for j, (name, P, D) in enumerate(GPT2):
             x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
             dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
@@ -59,7 +59,14 @@ def main():
             if nm in ("loop_end", "noise_signal", "stored"):
                 row[nm + "_max"] = round(float(np.nanmax(v)), 2) if np.isfinite(v).any() else None
         out.append(row)
-    print(json.dumps({"noise": noise, "sigma": sigma, "B": B, "T": T, "layers": out}))
+    mma = raw.reshape(-1, 256)[:grid, 248:252]
+    lead = mma[mma[:, 3] > 0]
+    mma_stats = {"ctas": int(len(lead)),
+                 "wait_tmem_us_med": round(float(np.median(lead[:, 0])) / 1e3, 2),
+                 "wait_operands_us_med": round(float(np.median(lead[:, 1])) / 1e3, 2),
+                 "issue_span_us_med": round(float(np.median(lead[:, 2])) / 1e3, 2),
+                 "units_med": float(np.median(lead[:, 3]))} if len(lead) else {}
+    print(json.dumps({"noise": noise, "sigma": sigma, "B": B, "T": T, "layers": out, "mma_issuer": mma_stats}))
 
 
 if __name__ == "__main__":
