@@ -54,8 +54,9 @@ enum fdp_status {
   FDP_ERR_CUDA = 4
 };
 
-/* Input element type of X and dY. Accumulation is always fp32. */
-enum fdp_dtype { FDP_DTYPE_BF16 = 0, FDP_DTYPE_F32 = 1 };
+/* Input element type of X and dY. Accumulation is always fp32. F64 is accepted
+ * only by the optimizer steps (parameter / moment state). */
+enum fdp_dtype { FDP_DTYPE_BF16 = 0, FDP_DTYPE_F32 = 1, FDP_DTYPE_F64 = 2 };
 
 /* dpcore.REDUCTIONS (dpcore.py:20) */
 enum fdp_reduction { FDP_REDUCE_SUM = 0, FDP_REDUCE_MEAN = 1 };
@@ -190,6 +191,19 @@ FDP_API int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* 
 /* dpcore.noise_for_indices for flat indices [lo, hi) scaled by `scale`
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);
+
+/* Optimizer steps on a finalized DP gradient, in place, fp32 or fp64 state
+ * (dtype FDP_DTYPE_F32 / FDP_DTYPE_F64); reference dpcore.dp_sgd_step /
+ * dp_adam_step (dpcore.py:131-156: Adam without bias correction, post-update v).
+ * `noise` (optional, NULL = none): add sigma*clip_c*N(seed, layer_id, step,
+ * noise_offset + i) to grad[i] first (noise_impl / device_step / add_noise of the
+ * descriptor apply) -- the reduce-scatter form of data parallelism, where a
+ * rank adds the noise of the shard it owns right before its optimizer step. */
+FDP_API int fdp_sgd_step(int32_t dtype, void* theta, const void* grad, int64_t n, double eta, const fdp_desc* noise,
+                         int64_t noise_offset, void* stream);
+FDP_API int fdp_adam_step(int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n, double eta,
+                          double beta1, double beta2, double eps, const fdp_desc* noise, int64_t noise_offset,
+                          void* stream);
 
 /* Noise slice [lo, hi) of [0, n) owned by `rank` of `world` (data-parallel
  * noise-once partition). Pure host arithmetic. */

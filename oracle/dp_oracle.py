@@ -14,6 +14,8 @@ A float64 numpy restatement of the reference algorithm
   dp backward          oracle.py:49-65  clip-sum-noise
   flashdp workflow     workflows.py:340-421 (same arithmetic, tiling-invariant)
   micro-batching       dpcore.py:90-104, bench.py:244-271
+  optimizer steps      dpcore.py:131-156 (SGD; Adam without bias correction, post-update v)
+  training demo        bench.py:409-458 train_demo (least-squares linear layer)
   input generator      bench.py:234-241 cell_inputs, rng.py:88-94
 
 Parity is pinned: tests/test_oracle_golden.py checks every function here
@@ -211,6 +213,43 @@ def micro_batched(x: np.ndarray, dy: np.ndarray, cfg: Cfg, size: int, exact_nois
         part, _ = dp_backward(x[i:i + size], dy[i:i + size], micro)
         acc += part
     return finalize(acc, B, cfg, exact_noise)
+
+
+def sgd_step(theta: np.ndarray, grad: np.ndarray, eta: float) -> np.ndarray:
+    """dpcore.py:131-136."""
+    return theta - eta * grad
+
+
+def adam_step(theta, m, v, grad, eta, beta1=0.9, beta2=0.999, eps=1e-8):
+    """dpcore.py:139-156: no bias correction, post-update v. Returns (theta, m, v)."""
+    m = beta1 * m + (1.0 - beta1) * grad
+    v = beta2 * v + (1.0 - beta2) * (grad * grad)
+    theta = theta - (eta / (np.sqrt(v) + eps)) * m
+    return theta, m, v
+
+
+def train_demo(x, w0, y_target, sigma: float, steps: int, eta: float, optimizer: str = "sgd", clip_c: float = 1.0,
+               seed: int = 2024, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> np.ndarray:
+    """bench.py:409-458: least-squares training of one linear layer; the loss is
+    recorded before each update; the DP gradient is clip-sum-noise (reduction sum)
+    keyed on (seed, layer 0, step)."""
+    B, T, _ = x.shape
+    D = w0.shape[0]
+    denom = B * T * D
+    theta = np.array(w0, dtype=np.float64)
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    losses = []
+    for step in range(steps):
+        resid = np.einsum("btp,dp->btd", x, theta) - y_target
+        losses.append(float((resid * resid).sum() / denom))
+        dy = (2.0 / denom) * resid
+        grad, _ = dp_backward(x, dy, Cfg(clip_c, sigma, "sum", seed, 0, step))
+        if optimizer == "adam":
+            theta, m, v = adam_step(theta, m, v, grad, eta, beta1, beta2, eps)
+        else:
+            theta = sgd_step(theta, grad, eta)
+    return np.array(losses)
 
 
 def cell_inputs(seed: int, layer_index: int, B: int, T: int, P: int, D: int) -> tuple[np.ndarray, np.ndarray]:

@@ -17,7 +17,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "_fdp.so"
 
 FDP_OK, FDP_ERR_SHAPE, FDP_ERR_USAGE, FDP_ERR_CAPACITY, FDP_ERR_CUDA = range(5)
-DTYPE_BF16, DTYPE_F32 = 0, 1
+DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
 REDUCE = {"sum": 0, "mean": 1}
 NOISE = {"keyed_f32": 0, "keyed_f64": 1, "philox": 2}
 PATH = {"auto": 0, "fused": 1, "two_phase": 2, "simt": 3}
@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "fdp_abi_version", "fdp_last_error", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes",
     "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_partition",
     "fdp_group_workspace_bytes", "fdp_backward_group", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex",
+    "fdp_sgd_step", "fdp_adam_step",
 )
 
 
@@ -105,7 +106,12 @@ def load() -> ctypes.CDLL:
                                                  ctypes.POINTER(ctypes.c_size_t)]
     lib.fdp_backward_group_ex.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc)] + [
         ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p]
-    for name in ("fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
+    lib.fdp_sgd_step.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                 ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+    lib.fdp_adam_step.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+    for name in ("fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
                  "fdp_dw", "fdp_noise", "fdp_noise_partition"):
         getattr(lib, name).restype = ctypes.c_int

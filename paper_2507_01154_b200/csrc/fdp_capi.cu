@@ -1056,6 +1056,48 @@ int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scal
   return FDP_OK;
 }
 
+static int optim_common(int adam, int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n,
+                        double eta, double b1, double b2, double eps, const fdp_desc* noise, int64_t noise_offset,
+                        void* stream) {
+  if (dtype != FDP_DTYPE_F32 && dtype != FDP_DTYPE_F64)
+    return fail(FDP_ERR_USAGE, "optimizer state must be fp32 (1) or fp64 (2), got dtype %d", dtype);
+  if (n < 0) return fail(FDP_ERR_SHAPE, "negative element count %lld", (long long)n);
+  if (n > 0 && (!theta || !grad || (adam && (!m || !v)))) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if (!(eta == eta) || !std::isfinite(eta)) return fail(FDP_ERR_USAGE, "eta must be finite");
+  if (adam && !(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0))
+    return fail(FDP_ERR_USAGE, "beta1 and beta2 must lie in [0, 1), got %g, %g", b1, b2);
+  fdp::OptimNoise nz{};
+  if (noise) {
+    int rc = validate(noise, FDP_KIND_FLASHDP);
+    if (rc) return rc;
+    if (noise_offset < 0) return fail(FDP_ERR_USAGE, "noise_offset must be >= 0");
+    const Common c = common_of(noise);
+    nz.on = c.add_noise;
+    nz.impl = noise->noise_impl;
+    nz.scale = c.noise_scale;
+    nz.base = c.key_base;
+    nz.base_g = c.key_base_g;
+    nz.step_ptr = reinterpret_cast<const long long*>(noise->device_step);
+    nz.seed_u = static_cast<uint64_t>(noise->seed);
+    nz.layer_u = static_cast<uint64_t>(noise->layer_id);
+    nz.offset = noise_offset;
+  }
+  cudaError_t e = fdp::optim_step(adam, dtype == FDP_DTYPE_F64, theta, m, v, grad, n, eta, b1, b2, eps, nz,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, adam ? "adam step" : "sgd step");
+  return FDP_OK;
+}
+
+int fdp_sgd_step(int32_t dtype, void* theta, const void* grad, int64_t n, double eta, const fdp_desc* noise,
+                 int64_t noise_offset, void* stream) {
+  return optim_common(0, dtype, theta, nullptr, nullptr, grad, n, eta, 0.0, 0.0, 0.0, noise, noise_offset, stream);
+}
+
+int fdp_adam_step(int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n, double eta,
+                  double beta1, double beta2, double eps, const fdp_desc* noise, int64_t noise_offset, void* stream) {
+  return optim_common(1, dtype, theta, m, v, grad, n, eta, beta1, beta2, eps, noise, noise_offset, stream);
+}
+
 int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi) {
   if (n < 0 || world < 1 || rank < 0 || rank >= world) return fail(FDP_ERR_USAGE, "bad partition arguments");
   if (lo) *lo = n * rank / world;

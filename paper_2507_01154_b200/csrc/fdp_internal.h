@@ -186,6 +186,18 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
                                    uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s);
 
+// ---- optimizer steps (fdp_optim.cu)
+struct OptimNoise {
+  int on, impl;
+  float scale;
+  uint64_t base, base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long offset;
+};
+cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const void* g, long long n, double eta,
+                       double b1, double b2, double eps, const OptimNoise& nz, cudaStream_t s);
+
 cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int impl, uint64_t base,
                        uint64_t base_g, cudaStream_t s);
 

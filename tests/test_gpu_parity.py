@@ -539,3 +539,75 @@ def test_single_sample_norm_phase_needs_one_sample():
     x, dy = randn(2, 64, 128, 128, seed=1)
     with pytest.raises(fdp.UsageError):
         fdp.backward_flashdp(x, dy, fdp.DPConfig(1.0, 0.0), path="two_phase", norm_phase="single")
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-12), (torch.float32, 2e-5)])  # fp32: 1 - 0.999f is off by 1.3e-5
+def test_adam_kernel_hand_check(dtype, tol):
+    """fdp_adam_step vs the reference's hand-derived Adam steps (criterion 10)."""
+    st = fdp.OptimizerState.fresh(torch.ones(1, dtype=dtype, device="cuda"), eta=0.1)
+    expected = [(0.1, 0.001, 0.6837723339831304), (0.19, 0.001999, 0.2588132602301777),
+                (0.271, 0.002997001, -0.23621018409018568)]
+    for m_want, v_want, t_want in expected:
+        st = fdp.dp_adam_step(st, torch.ones(1, dtype=dtype, device="cuda"))
+        assert abs(float(st.m[0]) - m_want) <= tol * max(1.0, abs(m_want))
+        assert abs(float(st.v[0]) - v_want) <= tol * max(1.0, abs(v_want))
+        assert abs(float(st.theta[0]) - t_want) <= tol * max(1.0, abs(t_want))
+    assert st.step == 3
+
+
+@pytest.mark.parametrize("opt,eta", [("sgd", 0.05), ("adam", 0.02)])
+def test_train_demo_parity_on_gpu(opt, eta):
+    """The reference's training demo (bench.py:409-458, criterion 9) run on the
+    GPU: DP gradient from backward_flashdp (reference-keyed noise), update by the
+    fdp_sgd_step / fdp_adam_step kernels; the loss curve tracks the reference's own
+    (golden) curve in fp32."""
+    g = golden("train.npz")
+    x = torch.tensor(g["x"], dtype=torch.float32, device="cuda")
+    y = torch.tensor(g["y"], dtype=torch.float32, device="cuda")
+    B, T, D = y.shape
+    denom = B * T * D
+    for sigma in (0.1, 0.5, 1.0):
+        theta = torch.tensor(g["w0"], dtype=torch.float32, device="cuda")
+        st = fdp.OptimizerState.fresh(theta, eta=eta)
+        losses = []
+        for step in range(50):
+            th = st.theta if opt == "adam" else theta
+            resid = torch.einsum("btp,dp->btd", x, th) - y
+            losses.append(float((resid * resid).sum() / denom))
+            dy = (2.0 / denom) * resid
+            cfg = fdp.DPConfig(1.0, sigma, "sum", seed=2024, layer_id=0, step=step)
+            grad = fdp.backward_flashdp(x, dy.contiguous(), cfg, noise_impl="keyed_f64").grad_w
+            if opt == "adam":
+                st = fdp.dp_adam_step_(st, grad)
+            else:
+                fdp.dp_sgd_step_(theta, grad, eta)
+        want = g[f"{opt}_{sigma}_flashdp"]
+        assert np.max(np.abs(np.array(losses) - want) / np.abs(want)) < 1e-4, (opt, sigma)
+
+
+def test_optimizer_adds_shard_noise_once():
+    """Reduce-scatter form of data parallelism: a clipped sum WITHOUT noise, then
+    each shard's optimizer step adding that shard's noise, equals the clipped sum
+    WITH noise followed by a plain step."""
+    x, dy = randn(4, 128, 256, 512, seed=61, scale_dy=1e-2)
+    cfg = fdp.DPConfig(0.5, 1.0, "mean", seed=3, layer_id=6, step=9)
+    g_noised = fdp.backward_flashdp(x, dy, cfg, noise_impl="philox").grad_w.reshape(-1)
+    g_clean = fdp.backward_flashdp(x, dy, cfg, noise_impl="philox", add_noise=False).grad_w.reshape(-1)
+    n = g_clean.numel()
+    theta0 = torch.randn(n, device="cuda")
+    a = fdp.OptimizerState.fresh(theta0.clone(), eta=0.01)
+    a = fdp.dp_adam_step_(a, g_noised)
+    b = fdp.OptimizerState.fresh(theta0.clone(), eta=0.01)
+    half = n // 2
+    shards = []
+    for lo, hi in ((0, half), (half, n)):
+        s = fdp.OptimizerState.fresh(theta0[lo:hi].clone(), eta=0.01)
+        shards.append(fdp.dp_adam_step_(s, g_clean[lo:hi].contiguous(), noise=cfg, noise_offset=lo,
+                                        noise_impl="philox", layer_numel=n))
+    theta_b = torch.cat([s.theta for s in shards])
+    assert rel(host(theta_b - theta0), host(a.theta - theta0)) < 1e-4
+    sgd_a = theta0.clone()
+    fdp.dp_sgd_step_(sgd_a, g_noised, 0.1)
+    sgd_b = theta0.clone()
+    fdp.dp_sgd_step_(sgd_b, g_clean, 0.1, noise=cfg, noise_impl="philox", layer_numel=n)
+    assert rel(host(sgd_b - theta0), host(sgd_a - theta0)) < 1e-5

@@ -166,8 +166,34 @@ def gen_micro():
                         cfg=np.array([0.5, 0.7, 1, 5, 1, 0]))
 
 
+def gen_train():
+    """The reference's train_demo (bench.py:409-458) with SGD and Adam: inputs,
+    initial weights, targets and the per-step loss curves of explicit_dp and
+    flashdp at three noise levels (acceptance criterion 9, test_acceptance.py:231-251)."""
+    from dpflows.bench import TrainDemoConfig, train_demo
+
+    out = {}
+    for opt in ("sgd", "adam"):
+        train = {"dims": {"B": 4, "T": 4, "P": 8, "D": 4}, "steps": 50, "workflows": ["explicit_dp", "flashdp"],
+                 "sigmas": [0.1, 0.5, 1.0], "eta": 0.05}
+        if opt == "adam":
+            train.update({"optimizer": "adam", "eta": 0.02, "beta1": 0.9, "beta2": 0.999, "eps_adam": 1e-8})
+        cfg = TrainDemoConfig.from_dict({"train": train, "mem": {"scratchpad_capacity_bytes": 8192},
+                                         "dp": {"clip_c": 1.0, "sigma": 0.0, "seed": 2024}})
+        res = train_demo(cfg)
+        for sigma, per_wf in res.items():
+            for wf, losses in per_wf.items():
+                out[f"{opt}_{sigma}_{wf}"] = np.array(losses)
+    d = (4, 4, 8, 4)
+    out["x"] = rng.keyed_uniform_array((2024, 11), d[0] * d[1] * d[2]).reshape(d[0], d[1], d[2])
+    out["w0"] = rng.keyed_uniform_array((2024, 12), d[3] * d[2], -0.5, 0.5).reshape(d[3], d[2])
+    out["y"] = rng.keyed_uniform_array((2024, 13), d[0] * d[1] * d[3]).reshape(d[0], d[1], d[3])
+    np.savez_compressed(OUT / "train.npz", **out)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    gen_train()
     gen_rng()
     gen_worked()
     gen_config1()
