@@ -46,6 +46,13 @@ class _DPLinearFn(torch.autograd.Function):
         dy3 = dy.reshape(B, -1, D)
         cdt = torch.bfloat16 if m.compute_dtype == torch.bfloat16 else torch.float32
         cfg = m.dp_config()
+        collector = _ACTIVE_GROUP[0]
+        if collector is not None and cdt == torch.bfloat16:
+            # deferred: the weight gradient comes from the collector's single multi-layer launch
+            collector._record(m, x3.to(cdt).contiguous(), dy3.to(cdt).contiguous(), cfg, m._noise_now,
+                              m.logical_batch or B)
+            gb = m._bias_grad(dy3.float()).to(weight.dtype) if ctx.has_bias else None
+            return dx, None, gb, None
         res = _run(WorkflowKind.FLASHDP, x3.to(cdt).contiguous(), dy3.to(cdt).contiguous(), cfg, None, None,
                    add_noise=m._noise_now, mean_batch=m.logical_batch or B, rank=m.rank, world=m.world,
                    noise_impl=m.noise_impl)
@@ -55,6 +62,82 @@ class _DPLinearFn(torch.autograd.Function):
         if ctx.has_bias:
             gb = m._bias_grad(dy3.float()).to(weight.dtype)
         return dx, gw, gb, None
+
+
+_ACTIVE_GROUP: list = [None]
+
+
+class GroupedDPBackward:
+    """Context manager that defers the DP weight gradients of every DPLinear whose
+    backward runs inside it and computes them in ONE persistent multi-layer launch
+    (PreparedGroup / fdp_backward_group) when the context exits -- the
+    training-step form of Algorithm 1: no per-layer launch, pipelines that never
+    drain between layers, small layers packed side by side on the SMs.
+
+        with GroupedDPBackward():
+            loss.backward()          # dX as usual; dW of DPLinear layers deferred
+        # every DPLinear.weight.grad now holds its DP gradient (accumulated into an
+        # existing .grad, as autograd would for micro-batches)
+
+    Each layer keeps its own DPConfig (C, sigma, layer_id noise key, step). The
+    (X, dY) pairs of the layers are held until the context exits. Layers the
+    fused multi-layer launch cannot take (fp32 compute dtype, shapes over the
+    co-resident grid) run through the per-layer kernels instead."""
+
+    def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0):
+        self.noise_impl = noise_impl
+        self.max_ctas = max_ctas
+        self._pending: list = []
+        self.last_groups = 0
+
+    def __enter__(self):
+        if _ACTIVE_GROUP[0] is not None:
+            raise RuntimeError("GroupedDPBackward contexts do not nest")
+        _ACTIVE_GROUP[0] = self
+        self._pending = []
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        _ACTIVE_GROUP[0] = None
+        if exc_type is None:
+            self.flush()
+        self._pending = []
+        return False
+
+    def _record(self, module, x3, dy3, cfg, add_noise, mean_batch):
+        self._pending.append((module, x3, dy3, cfg, add_noise, mean_batch))
+
+    def flush(self) -> None:
+        from .workflows import PreparedGroup, WorkflowKind, _run
+        from .errors import UsageError
+
+        buckets: dict = {}
+        for item in self._pending:  # one launch per (noise on/off, mean divisor, partition, noise generator)
+            m, _, _, _, add_noise, mean_batch = item
+            key = (add_noise, mean_batch, m.rank, m.world, self.noise_impl or m.noise_impl)
+            buckets.setdefault(key, []).append(item)
+        self.last_groups = 0
+        for (add_noise, mean_batch, rank, world, impl), items in buckets.items():
+            grads = None
+            for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
+                chunk = items[lo:lo + 48]
+                try:
+                    grp = PreparedGroup([(x, dy, cfg) for _, x, dy, cfg, _, _ in chunk], noise_impl=impl,
+                                        add_noise=add_noise, rank=rank, world=world, mean_batch=mean_batch,
+                                        max_ctas=self.max_ctas)
+                    grp()
+                    grads = grp.grads
+                    self.last_groups += 1
+                except UsageError:  # per-layer kernels (two-phase for layers over the co-resident grid)
+                    grads = [_run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise,
+                                  mean_batch=mean_batch, rank=rank, world=world, noise_impl=impl).grad_w
+                             for _, x, dy, cfg, _, _ in chunk]
+                for (m, _, _, _, _, _), gw in zip(chunk, grads):
+                    gw = gw.to(m.weight.dtype)
+                    if m.weight.grad is None:
+                        m.weight.grad = gw
+                    else:
+                        m.weight.grad += gw
 
 
 class DPLinear(torch.nn.Module):

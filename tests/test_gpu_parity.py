@@ -611,3 +611,45 @@ def test_optimizer_adds_shard_noise_once():
     sgd_b = theta0.clone()
     fdp.dp_sgd_step_(sgd_b, g_clean, 0.1, noise=cfg, noise_impl="philox", layer_numel=n)
     assert rel(host(sgd_b - theta0), host(sgd_a - theta0)) < 1e-5
+
+
+def test_grouped_dp_backward_matches_per_layer():
+    """GroupedDPBackward: the DPLinear weight gradients of a whole backward pass in
+    ONE multi-layer launch equal the per-layer kernels' (same DP configs and noise
+    keys); dX / biases are unchanged; micro-batches accumulate into .grad."""
+    from paper_2507_01154_b200.dplinear import DPLinear, GroupedDPBackward
+
+    torch.manual_seed(3)
+    dims = [256, 512, 768, 256]
+    layers = [DPLinear(dims[i], dims[i + 1], bias=(i != 1), clip_c=0.3 + 0.2 * i, sigma=1.0, reduction="mean",
+                       layer_id=i, noise_impl="keyed_f64").cuda() for i in range(3)]
+    x = torch.randn(4, 64, dims[0], device="cuda").to(torch.bfloat16)
+
+    def run(grouped, micro):
+        for m in layers:
+            m.weight.grad = None
+            if m.bias is not None:
+                m.bias.grad = None
+        for i in range(micro):
+            xi = x[i * (4 // micro):(i + 1) * (4 // micro)]
+            for m in layers:
+                m.set_step(5, last_micro_batch=(i == micro - 1), logical_batch=4)
+            h = xi
+            for m in layers:
+                h = torch.nn.functional.gelu(m(h).float()).to(torch.bfloat16)
+            loss = (h.float() ** 2).mean()
+            if grouped:
+                with GroupedDPBackward() as gctx:
+                    loss.backward()
+                assert gctx.last_groups == 1
+            else:
+                loss.backward()
+        return [m.weight.grad.clone() for m in layers], [m.bias.grad.clone() for m in layers if m.bias is not None]
+
+    for micro in (1, 2):
+        wa, ba = run(False, micro)
+        wb, bb = run(True, micro)
+        for a, b in zip(wa, wb):
+            assert rel(host(b), host(a)) < 1e-4
+        for a, b in zip(ba, bb):
+            assert rel(host(b), host(a)) < 1e-6
