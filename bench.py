@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nondp", action="store_true")
+    ap.add_argument("--no-train", action="store_true",
+                    help="skip the GPT-2 training-step comparison (DP linear layers vs nn.Linear)")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
     ap.add_argument("--per-layer", action="store_true",
                     help="one fused launch per layer instead of one multi-layer launch per step")
@@ -476,6 +478,27 @@ def main():
                "sample": cpu_sample_desc(B).replace("each step times one of the 4 GPT-2 layer types in rotation",
                                                     "one pass over the 4 GPT-2 layer types")}
 
+    # ---- whole training step of the same model (N=1): DP linear layers through
+    # GroupedDPBackward vs plain nn.Linear, same optimizer (tools/train_gpt2.py)
+    train = None
+    if not a.no_train and world == 1:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import train_gpt2 as tg
+
+            targs = argparse.Namespace(batch=B, seq=T, steps=10, warmup=3)
+            nd_t = tg.run(False, targs)
+            dp_t = tg.run(True, targs)
+            train = {"model": "gpt2-small (124M) training step, random init, synthetic tokens, bf16 autocast, "
+                              "fused AdamW", "dp_tokens_per_s": dp_t["tokens_per_s"],
+                     "non_dp_tokens_per_s": nd_t["tokens_per_s"], "dp_ms_per_step": dp_t["ms_per_step"],
+                     "non_dp_ms_per_step": nd_t["ms_per_step"],
+                     "dp_pct_of_non_dp": 100.0 * dp_t["tokens_per_s"] / nd_t["tokens_per_s"],
+                     "dp_scope": "per-layer clipped + noised weight gradients of the 48 linear layers (+ their "
+                                 "biases); embeddings / LayerNorm not DP (as in the reference, SPEC.md:8)"}
+        except Exception as e:  # noqa: BLE001
+            train = {"error": repr(e)[:300]}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -495,6 +518,8 @@ def main():
                           "grid": v.grid} for k, v in plans.items()},
         }
         line.update(extra)
+        if train is not None:
+            line["train_step"] = train
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -30,16 +30,24 @@ class _DPLinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, weight, bias, module):
         ctx.module = module
-        ctx.save_for_backward(x, weight)
         ctx.has_bias = bias is not None
-        y = torch.nn.functional.linear(x, weight.to(x.dtype), None if bias is None else bias.to(x.dtype))
+        ctx.x_dtype = x.dtype
+        # compute dtype: autocast's when enabled (bf16 GEMMs, bf16 saved input -- what
+        # the DP kernel consumes, no second cast in backward), else the input's
+        cdt = torch.get_autocast_dtype("cuda") if torch.is_autocast_enabled("cuda") else x.dtype
+        with torch.autocast("cuda", enabled=False):
+            xc = x.to(cdt)
+            wc = weight.to(cdt)
+            y = torch.nn.functional.linear(xc, wc, None if bias is None else bias.to(cdt))
+        ctx.save_for_backward(xc, wc)
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x, weight = ctx.saved_tensors
+        x, wc = ctx.saved_tensors
         m: DPLinear = ctx.module
-        dx = dy @ weight.to(dy.dtype) if ctx.needs_input_grad[0] else None
+        weight = m.weight
+        dx = (dy.to(wc.dtype) @ wc).to(ctx.x_dtype) if ctx.needs_input_grad[0] else None
         B = x.shape[0]
         P, D = weight.shape[1], weight.shape[0]
         x3 = x.reshape(B, -1, P)
@@ -51,7 +59,7 @@ class _DPLinearFn(torch.autograd.Function):
             # deferred: the weight gradient comes from the collector's single multi-layer launch
             collector._record(m, x3.to(cdt).contiguous(), dy3.to(cdt).contiguous(), cfg, m._noise_now,
                               m.logical_batch or B)
-            gb = m._bias_grad(dy3.float()).to(weight.dtype) if ctx.has_bias else None
+            gb = m._bias_grad(dy3).to(weight.dtype) if ctx.has_bias else None
             return dx, None, gb, None
         res = _run(WorkflowKind.FLASHDP, x3.to(cdt).contiguous(), dy3.to(cdt).contiguous(), cfg, None, None,
                    add_noise=m._noise_now, mean_batch=m.logical_batch or B, rank=m.rank, world=m.world,
@@ -60,7 +68,7 @@ class _DPLinearFn(torch.autograd.Function):
         gw = res.grad_w.to(weight.dtype)
         gb = None
         if ctx.has_bias:
-            gb = m._bias_grad(dy3.float()).to(weight.dtype)
+            gb = m._bias_grad(dy3).to(weight.dtype)
         return dx, gw, gb, None
 
 
@@ -89,6 +97,7 @@ class GroupedDPBackward:
         self.max_ctas = max_ctas
         self._pending: list = []
         self.last_groups = 0
+        self._ws = None
 
     def __enter__(self):
         if _ACTIVE_GROUP[0] is not None:
@@ -109,7 +118,7 @@ class GroupedDPBackward:
 
     def flush(self) -> None:
         from .workflows import PreparedGroup, WorkflowKind, _run
-        from .errors import UsageError
+        from .errors import CapacityError, UsageError
 
         buckets: dict = {}
         for item in self._pending:  # one launch per (noise on/off, mean divisor, partition, noise generator)
@@ -122,9 +131,18 @@ class GroupedDPBackward:
             for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
                 chunk = items[lo:lo + 48]
                 try:
-                    grp = PreparedGroup([(x, dy, cfg) for _, x, dy, cfg, _, _ in chunk], noise_impl=impl,
-                                        add_noise=add_noise, rank=rank, world=world, mean_batch=mean_batch,
-                                        max_ctas=self.max_ctas)
+                    # every element of a fresh (non-accumulating) group output is written by the
+                    # kernel: no zero-fill; the workspace is kept (the kernel leaves it zeroed)
+                    grads_out = [torch.empty(dy.shape[2], x.shape[2], dtype=torch.float32, device=x.device)
+                                 for _, x, dy, _, _, _ in chunk]
+                    glayers = [(x, dy, cfg) for _, x, dy, cfg, _, _ in chunk]
+                    kw = dict(grads=grads_out, noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
+                              mean_batch=mean_batch, max_ctas=self.max_ctas)
+                    try:
+                        grp = PreparedGroup(glayers, workspace=self._ws, **kw)
+                    except CapacityError:  # cached workspace too small for this layer list: grow it
+                        grp = PreparedGroup(glayers, **kw)
+                    self._ws = grp.workspace
                     grp()
                     grads = grp.grads
                     self.last_groups += 1
@@ -175,7 +193,7 @@ class DPLinear(torch.nn.Module):
         self.logical_batch = logical_batch
 
     def _bias_grad(self, dy3: torch.Tensor) -> torch.Tensor:
-        g = dy3.sum(dim=1)                                   # (B, D) per-sample bias gradients
+        g = dy3.sum(dim=1, dtype=torch.float32)              # (B, D) per-sample bias gradients, fp32 accumulate
         ns = (g.double() * g.double()).sum(dim=1)
         f = torch.where(ns <= self.clip_c ** 2, torch.ones_like(ns), self.clip_c / ns.clamp_min(1e-300).sqrt())
         s = (f.float()[:, None] * g).sum(dim=0)

@@ -1,0 +1,94 @@
+"""GPT-2 small with DP linear layers: the consumer of the hot path in a training step.
+
+Only the four linear layers of every block (attention c_attn / c_proj, MLP c_fc /
+c_proj) are the reference's hot path (per-layer DP weight gradients,
+workflows.py:340-421); they are ``DPLinear`` modules whose weight gradients
+come from ONE multi-layer persistent launch per backward
+(``GroupedDPBackward``). Everything else (embeddings, LayerNorm, attention core,
+LM head) is plain PyTorch and, like in the reference, not clipped
+per sample. ``dp=False`` builds the same model with ``nn.Linear`` -- the non-DP
+baseline of "% of non-DP training throughput".
+
+Random-init weights, synthetic token ids; bf16 compute, fp32 master weights.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from .dplinear import DPLinear
+
+
+@dataclass
+class GPT2Config:
+    vocab: int = 50257
+    seq: int = 1024
+    d: int = 768
+    heads: int = 12
+    layers: int = 12
+    mlp: int = 3072
+
+
+def _linear(cin: int, cout: int, dp: bool, layer_id: int, clip_c: float, sigma: float, noise_impl: str):
+    if dp:
+        return DPLinear(cin, cout, bias=True, clip_c=clip_c, sigma=sigma, reduction="mean", layer_id=layer_id,
+                        noise_impl=noise_impl)
+    return torch.nn.Linear(cin, cout, bias=True)
+
+
+class Block(torch.nn.Module):
+    def __init__(self, cfg: GPT2Config, idx: int, dp: bool, clip_c: float, sigma: float, noise_impl: str):
+        super().__init__()
+        self.ln1 = torch.nn.LayerNorm(cfg.d)
+        self.ln2 = torch.nn.LayerNorm(cfg.d)
+        base = 4 * idx
+        self.c_attn = _linear(cfg.d, 3 * cfg.d, dp, base + 0, clip_c, sigma, noise_impl)
+        self.attn_proj = _linear(cfg.d, cfg.d, dp, base + 1, clip_c, sigma, noise_impl)
+        self.c_fc = _linear(cfg.d, cfg.mlp, dp, base + 2, clip_c, sigma, noise_impl)
+        self.mlp_proj = _linear(cfg.mlp, cfg.d, dp, base + 3, clip_c, sigma, noise_impl)
+        self.heads = cfg.heads
+
+    def forward(self, x):
+        B, T, C = x.shape
+        qkv = self.c_attn(self.ln1(x))
+        q, k, v = qkv.split(C, dim=2)
+        q = q.view(B, T, self.heads, C // self.heads).transpose(1, 2)
+        k = k.view(B, T, self.heads, C // self.heads).transpose(1, 2)
+        v = v.view(B, T, self.heads, C // self.heads).transpose(1, 2)
+        y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + self.attn_proj(y.transpose(1, 2).reshape(B, T, C))
+        return x + self.mlp_proj(F.gelu(self.c_fc(self.ln2(x)), approximate="tanh"))
+
+
+class GPT2(torch.nn.Module):
+    def __init__(self, cfg: GPT2Config, *, dp: bool = True, clip_c: float = 1.0, sigma: float = 1.0,
+                 noise_impl: str = "philox"):
+        super().__init__()
+        self.cfg = cfg
+        self.wte = torch.nn.Embedding(cfg.vocab, cfg.d)
+        self.wpe = torch.nn.Embedding(cfg.seq, cfg.d)
+        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl) for i in range(cfg.layers))
+        self.ln_f = torch.nn.LayerNorm(cfg.d)
+        self.dp = dp
+        for p in self.parameters():
+            if p.dim() >= 2:
+                torch.nn.init.normal_(p, std=0.02 / math.sqrt(2 * cfg.layers) if p.shape[0] == cfg.d else 0.02)
+
+    def dp_layers(self):
+        return [m for m in self.modules() if isinstance(m, DPLinear)]
+
+    def forward(self, idx):
+        B, T = idx.shape
+        x = self.wte(idx) + self.wpe(torch.arange(T, device=idx.device))[None]
+        for blk in self.blocks:
+            x = blk(x)
+        return F.linear(self.ln_f(x), self.wte.weight)  # tied LM head
+
+    def loss(self, idx, targets):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = self(idx)
+        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))
