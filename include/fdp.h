@@ -192,6 +192,16 @@ FDP_API int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* 
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);
 
+/* DP gradient of a linear layer's bias (B, T, D) -> (D): per-sample g_b = sum_t dY[b,t,:],
+ * clipped at the descriptor's clip_c with its own norm (per-layer clipping of the
+ * bias as its own group), summed (or /mean_batch) + sigma*C*N(seed, layer_id, step, d)
+ * on the rank's slice. Uses d->B, T, D (P ignored), in_dtype, reduction, noise
+ * fields. `ws` needs fdp_bias_workspace_bytes(d) bytes (no zeroing needed);
+ * norms_sq (B,) may be NULL. */
+FDP_API int fdp_bias_workspace_bytes(const fdp_desc* d, size_t* bytes);
+FDP_API int fdp_bias_dw(const fdp_desc* d, const void* dy, float* grad_b, float* norms_sq, void* ws, size_t ws_bytes,
+                        void* stream);
+
 /* Optimizer steps on a finalized DP gradient, in place, fp32 or fp64 state
  * (dtype FDP_DTYPE_F32 / FDP_DTYPE_F64); reference dpcore.dp_sgd_step /
  * dp_adam_step (dpcore.py:131-156: Adam without bias correction, post-update v).

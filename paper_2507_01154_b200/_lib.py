@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "fdp_abi_version", "fdp_last_error", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes",
     "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_partition",
     "fdp_group_workspace_bytes", "fdp_backward_group", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex",
-    "fdp_sgd_step", "fdp_adam_step",
+    "fdp_sgd_step", "fdp_adam_step", "fdp_bias_workspace_bytes", "fdp_bias_dw",
 )
 
 
@@ -111,7 +111,10 @@ def load() -> ctypes.CDLL:
     lib.fdp_adam_step.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
-    for name in ("fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
+    lib.fdp_bias_workspace_bytes.argtypes = [ctypes.POINTER(FdpDesc), ctypes.POINTER(ctypes.c_size_t)]
+    lib.fdp_bias_dw.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    for name in ("fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
                  "fdp_dw", "fdp_noise", "fdp_noise_partition"):
         getattr(lib, name).restype = ctypes.c_int

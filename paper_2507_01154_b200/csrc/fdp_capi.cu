@@ -1056,6 +1056,36 @@ int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scal
   return FDP_OK;
 }
 
+int fdp_bias_workspace_bytes(const fdp_desc* d, size_t* bytes) {
+  int rc = validate(d, FDP_KIND_FLASHDP);
+  if (rc) return rc;
+  if (!bytes) return fail(FDP_ERR_USAGE, "null output");
+  if (d->B > (1 << 24) || d->D > (1 << 30)) return fail(FDP_ERR_SHAPE, "extent too large");
+  *bytes = fdp::bias_dp_work_bytes(static_cast<int>(d->B), static_cast<int>(d->D));
+  return FDP_OK;
+}
+
+int fdp_bias_dw(const fdp_desc* d, const void* dy, float* grad_b, float* norms_sq, void* ws, size_t ws_bytes,
+                void* stream) {
+  size_t need = 0;
+  int rc = fdp_bias_workspace_bytes(d, &need);
+  if (rc) return rc;
+  if (!dy || !grad_b) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if (!ws || ws_bytes < need)
+    return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
+                need);
+  const Common c = common_of(d);
+  // the bias noise slice is [D*rank/world, D*(rank+1)/world) of its own index space
+  const long long lo = d->D * d->rank / d->world, hi = d->D * (d->rank + 1) / d->world;
+  cudaError_t e = fdp::bias_dp(dy, d->in_dtype == FDP_DTYPE_F32, static_cast<int>(d->B), static_cast<int>(d->T),
+                               static_cast<int>(d->D), static_cast<float*>(ws), d->clip_c, c.inv_batch, grad_b,
+                               norms_sq, c.add_noise, d->noise_impl, c.noise_scale, c.key_base, c.key_base_g,
+                               reinterpret_cast<const long long*>(d->device_step), static_cast<uint64_t>(d->seed),
+                               static_cast<uint64_t>(d->layer_id), lo, hi, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "bias dp");
+  return FDP_OK;
+}
+
 static int optim_common(int adam, int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n,
                         double eta, double b1, double b2, double eps, const fdp_desc* noise, int64_t noise_offset,
                         void* stream) {

@@ -186,6 +186,13 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
                                    uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s);
 
+// ---- DP bias gradient (fdp_simt.cu): per-sample sums over t, per-sample clip, batch sum, noise
+cudaError_t bias_dp(const void* dy, int in_f32, int B, int T, int D, float* work, double clip_c, float inv_batch,
+                    float* out, float* norms_out, int add_noise, int impl, float scale, uint64_t base,
+                    uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u, long long lo,
+                    long long hi, cudaStream_t s);
+size_t bias_dp_work_bytes(int B, int D);
+
 // ---- optimizer steps (fdp_optim.cu)
 struct OptimNoise {
   int on, impl;

@@ -12,17 +12,21 @@ call ``set_step(step, last_micro_batch=...)`` before each micro-batch; noise is
 added only on the last micro-batch and ``mean`` divides by the logical batch.
 
 The bias (if any) is clipped as its own per-layer group with the same C:
-its per-sample gradient is sum_t dY_b (B x D, tiny), handled with torch ops,
-noise keyed on a distinct layer id (layer_id + 2**32).
+its per-sample gradient is sum_t dY_b (B x D, tiny), computed, clipped, summed
+and noised by one fused CUDA pass pair (fdp_bias_dw), noise keyed on a
+distinct layer id (layer_id + 2**32).
 """
 
 from __future__ import annotations
 
 from typing import Optional
 
+import ctypes
+
 import torch
 
-from .dpcore import DPConfig, noise_range
+from . import _lib
+from .dpcore import DPConfig
 from .workflows import WorkflowKind, _run
 
 
@@ -193,22 +197,26 @@ class DPLinear(torch.nn.Module):
         self.logical_batch = logical_batch
 
     def _bias_grad(self, dy3: torch.Tensor) -> torch.Tensor:
-        g = dy3.sum(dim=1, dtype=torch.float32)              # (B, D) per-sample bias gradients, fp32 accumulate
-        ns = (g.double() * g.double()).sum(dim=1)
-        f = torch.where(ns <= self.clip_c ** 2, torch.ones_like(ns), self.clip_c / ns.clamp_min(1e-300).sqrt())
-        s = (f.float()[:, None] * g).sum(dim=0)
-        if self.reduction == "mean":
-            s = s / float(self.logical_batch or g.shape[0])
-        if self._noise_now and self.sigma > 0:
-            cfg = DPConfig(self.clip_c, self.sigma, self.reduction, self.seed, self.layer_id + (1 << 32), self.step)
-            n = s.numel()
-            lo, hi = n * self.rank // self.world, n * (self.rank + 1) // self.world
-            noise = torch.zeros_like(s)
-            if hi > lo:
-                noise[lo:hi] = noise_range(cfg, lo, hi, self.sigma * self.clip_c, noise_impl=self.noise_impl,
-                                           device=s.device)
-            s = s + noise
-        return s
+        """The bias as its own per-layer clipping group (fdp_bias_dw, one fused CUDA
+        pass pair): per-sample g_b = sum_t dY_b, clip at C, sum / logical batch, +
+        sigma*C noise keyed on layer_id + 2**32 over the rank's slice of [0, D)."""
+        B, T, D = dy3.shape
+        if dy3.dtype not in (torch.bfloat16, torch.float32):
+            dy3 = dy3.float()
+        dy3 = dy3.contiguous()
+        desc = _lib.make_desc(B=B, T=T, P=8, D=D, in_dtype=_lib.DTYPE_BF16 if dy3.dtype == torch.bfloat16
+                              else _lib.DTYPE_F32, reduction=self.reduction, clip_c=self.clip_c, sigma=self.sigma,
+                              seed=self.seed, layer_id=self.layer_id + (1 << 32), step=self.step, rank=self.rank,
+                              world=self.world, mean_batch=self.logical_batch or B, add_noise=self._noise_now,
+                              noise_impl=self.noise_impl)
+        lib = _lib.load()
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.fdp_bias_workspace_bytes(ctypes.byref(desc), ctypes.byref(nbytes)))
+        ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dy3.device)
+        out = torch.empty(D, dtype=torch.float32, device=dy3.device)
+        _lib.check(lib.fdp_bias_dw(ctypes.byref(desc), dy3.data_ptr(), out.data_ptr(), None, ws.data_ptr(),
+                                   ws.numel(), torch.cuda.current_stream(dy3.device).cuda_stream))
+        return out
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return _DPLinearFn.apply(x, self.weight, self.bias, self)

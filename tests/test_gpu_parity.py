@@ -653,3 +653,36 @@ def test_grouped_dp_backward_matches_per_layer():
             assert rel(host(b), host(a)) < 1e-4
         for a, b in zip(ba, bb):
             assert rel(host(b), host(a)) < 1e-6
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("rank,world", [(0, 1), (1, 3)])
+def test_bias_dw_against_oracle(dtype, rank, world):
+    """fdp_bias_dw: per-sample bias gradients sum_t dY_b, per-sample clip at C, mean,
+    reference-keyed noise on the rank's slice of [0, D) (keyed_f64: exact)."""
+    import ctypes
+    from paper_2507_01154_b200 import _lib
+
+    B, T, D = 5, 70, 777
+    g = torch.Generator().manual_seed(7)
+    dy = (torch.randn(B, T, D, generator=g) * 0.1).to(dtype).cuda()
+    lid = 3 + (1 << 32)
+    desc = _lib.make_desc(B=B, T=T, P=8, D=D, in_dtype=_lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F32,
+                          reduction="mean", clip_c=0.8, sigma=1.3, seed=11, layer_id=lid, step=4, rank=rank,
+                          world=world, noise_impl="keyed_f64")
+    lib = _lib.load()
+    nb = ctypes.c_size_t()
+    _lib.check(lib.fdp_bias_workspace_bytes(ctypes.byref(desc), ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    out = torch.empty(D, device="cuda")
+    norms = torch.empty(B, device="cuda")
+    _lib.check(lib.fdp_bias_dw(ctypes.byref(desc), dy.data_ptr(), out.data_ptr(), norms.data_ptr(), ws.data_ptr(),
+                               ws.numel(), None))
+    gb = host(dy).sum(axis=1)
+    ns = (gb ** 2).sum(axis=1)
+    f = np.array([O.clip_factor(v, 0.8) for v in ns])
+    want = (f[:, None] * gb).sum(0) / B
+    lo, hi = D * rank // world, D * (rank + 1) // world
+    want[lo:hi] += 0.8 * 1.3 * O.keyed_normal_array(11, lid, 4, np.arange(lo, hi))
+    assert rel(host(out), want) < 1e-5
+    assert rel(host(norms), ns) < 1e-5
