@@ -54,8 +54,12 @@ enum fdp_status {
   FDP_ERR_CUDA = 4
 };
 
-/* Input element type of X and dY. Accumulation is always fp32. F64 is accepted
- * only by the optimizer steps (parameter / moment state). */
+/* Input element type of X and dY. bf16 / f32: fp32 accumulation and fp32
+ * grad_w / norms_sq. F64 (the reference's own precision): the fp64 parity path --
+ * X, dY are double and grad_w / norms_sq point to DOUBLE arrays (cast through
+ * the float* parameters), fp64 FMA on the CUDA cores, keyed noise transformed in
+ * fp64; every workflow kind computes the same quantity. Also the optimizer
+ * steps' fp64 state. */
 enum fdp_dtype { FDP_DTYPE_BF16 = 0, FDP_DTYPE_F32 = 1, FDP_DTYPE_F64 = 2 };
 
 /* dpcore.REDUCTIONS (dpcore.py:20) */

@@ -121,8 +121,8 @@ int validate(const fdp_desc* d, int32_t kind) {
                 (long long)d->T, (long long)d->P, (long long)d->D);
   if (d->B > (1ll << 30) || d->T > (1ll << 30) || d->P > (1ll << 30) || d->D > (1ll << 30))
     return fail(FDP_ERR_SHAPE, "extent too large");
-  if (d->in_dtype != FDP_DTYPE_BF16 && d->in_dtype != FDP_DTYPE_F32)
-    return fail(FDP_ERR_USAGE, "in_dtype must be bf16 (0) or f32 (1), got %d", d->in_dtype);
+  if (d->in_dtype != FDP_DTYPE_BF16 && d->in_dtype != FDP_DTYPE_F32 && d->in_dtype != FDP_DTYPE_F64)
+    return fail(FDP_ERR_USAGE, "in_dtype must be bf16 (0), f32 (1) or f64 (2), got %d", d->in_dtype);
   if (kind != FDP_KIND_NON_DP) {
     if (!(d->clip_c > 0.0) || !std::isfinite(d->clip_c))
       return fail(FDP_ERR_USAGE, "clip_c must be positive, got %g", d->clip_c);
@@ -353,7 +353,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   const long long B = d->B;
   pl.part_tiles = pl.n_tiles;
   if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_GHOST) pl.part_tiles = ghost_shape(d, di.sms).parts;
-  if (kind == FDP_KIND_EXPLICIT_DP) {
+  if (kind == FDP_KIND_EXPLICIT_DP && d->in_dtype != FDP_DTYPE_F64) {
     pl.expl_chunks = 64;
     pl.part_tiles = pl.expl_chunks;
   }
@@ -364,18 +364,19 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   off = align_up(off + 4 * B, 256);
   pl.off_tile_cnt = off;
   off = align_up(off + 4ull * pl.n_tiles, 256);
+  const size_t esz = d->in_dtype == FDP_DTYPE_F64 ? 8 : 4;  // fp64 parity path keeps partials / factors in fp64
   pl.off_part = off;
-  off = align_up(off + 4ull * B * pl.part_tiles, 256);
+  off = align_up(off + esz * B * pl.part_tiles, 256);
   pl.off_tag = off;
   off = align_up(off + 8ull * B * pl.n_tiles, 256);
   pl.off_factor = off;
-  off = align_up(off + 4 * B, 256);
+  off = align_up(off + esz * B, 256);
   pl.off_acc = off;
   if (kind == FDP_KIND_FLASHDP && pl.path == FDP_PATH_FUSED && pl.groups > 1 && (d->flags & FDP_FLAG_DETERMINISTIC))
     off = align_up(off + 4ull * pl.groups * pl.n_tiles * fdp::kBM * pl.bn, 256);
   pl.off_g = off;
   pl.off_gp = off;
-  if (kind == FDP_KIND_EXPLICIT_DP) {
+  if (kind == FDP_KIND_EXPLICIT_DP && d->in_dtype != FDP_DTYPE_F64) {
     const size_t gbytes = 4ull * B * d->D * d->P;
     pl.off_gp = align_up(off + gbytes, 256);
     off = align_up(pl.off_gp + gbytes, 256);
@@ -557,6 +558,40 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     return fail(FDP_ERR_USAGE, "x and dy must be 16-byte aligned for the tensor-core path");
   const Common c = common_of(d);
   cudaError_t e;
+
+  if (d->in_dtype == FDP_DTYPE_F64) {  // fp64 parity path: every workflow kind computes the same quantity
+    fdp::F64Params q{};
+    q.B = static_cast<int>(d->B);
+    q.T = static_cast<int>(d->T);
+    q.P = static_cast<int>(d->P);
+    q.D = static_cast<int>(d->D);
+    q.n_dt = static_cast<int>((d->D + 31) / 32);
+    q.n_pt = static_cast<int>((d->P + 31) / 32);
+    q.n_tiles = q.n_dt * q.n_pt;
+    q.x = static_cast<const double*>(x);
+    q.dy = static_cast<const double*>(dy);
+    q.grad_w = reinterpret_cast<double*>(grad_w);
+    q.norms_out = reinterpret_cast<double*>(norms);
+    q.part = ws_at<double>(ws, pl.off_part);
+    q.factor = ws_at<double>(ws, pl.off_factor);
+    q.with_clip = kind != FDP_KIND_NON_DP;
+    q.clip_c = d->clip_c;
+    const long long mb = d->mean_batch > 0 ? d->mean_batch : d->B;
+    q.inv_batch = (q.with_clip && d->reduction == FDP_REDUCE_MEAN) ? 1.0 / static_cast<double>(mb) : 1.0;
+    q.add_noise = c.add_noise;
+    q.noise_impl = d->noise_impl;
+    q.noise_scale = d->sigma * d->clip_c;
+    q.key_base = c.key_base;
+    q.key_base_g = c.key_base_g;
+    q.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+    q.seed_u = static_cast<uint64_t>(d->seed);
+    q.layer_u = static_cast<uint64_t>(d->layer_id);
+    q.noise_lo = c.noise_lo;
+    q.noise_hi = c.noise_hi;
+    q.accumulate = d->accumulate;
+    if ((e = fdp::f64_backward(q, s)) != cudaSuccess) return cuda_fail(e, "fp64 backward");
+    return FDP_OK;
+  }
 
   if (!pl.tc) {
     fdp::SimtParams sp = simt_params(d, pl, c, x, dy, grad_w, norms, ws);

@@ -186,6 +186,24 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
                                    uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s);
 
+// ---- fp64 parity path (fdp_f64.cu): in_dtype FDP_DTYPE_F64, fp64 in / out
+struct F64Params {
+  int B, T, P, D, n_dt, n_pt, n_tiles;
+  const double* x;
+  const double* dy;
+  double* grad_w;
+  double* norms_out;
+  double* part;    // [B][n_tiles]
+  double* factor;  // [B]
+  int with_clip, add_noise, noise_impl, accumulate;
+  double clip_c, inv_batch, noise_scale;
+  uint64_t key_base, key_base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long noise_lo, noise_hi;
+};
+cudaError_t f64_backward(const F64Params& p, cudaStream_t s);
+
 // ---- DP bias gradient (fdp_simt.cu): per-sample sums over t, per-sample clip, batch sum, noise
 cudaError_t bias_dp(const void* dy, int in_f32, int B, int T, int D, float* work, double clip_c, float inv_batch,
                     float* out, float* norms_out, int add_noise, int impl, float scale, uint64_t base,

@@ -91,13 +91,15 @@ def _to_device(t, dtype, device) -> tuple[torch.Tensor, bool]:
         if dtype is not None and t.dtype != dtype:
             t = t.to(dtype)
         return t.contiguous(), False
-    if isinstance(t, torch.Tensor):  # host torch tensor (bf16 allowed): one H2D copy
-        target = dtype if dtype is not None else (t.dtype if t.dtype in (torch.bfloat16, torch.float32)
-                                                  else torch.float32)
+    # host inputs keep their precision: float64 (the reference's Tensor / numpy
+    # arrays) takes the fp64 parity path, bf16 / fp32 the fast paths
+    keep = (torch.bfloat16, torch.float32, torch.float64)
+    if isinstance(t, torch.Tensor):  # host torch tensor: one H2D copy
+        target = dtype if dtype is not None else (t.dtype if t.dtype in keep else torch.float32)
         return t.detach().to(device=device, dtype=target, non_blocking=t.is_pinned()).contiguous(), True
     arr = t.array if isinstance(t, Tensor) else np.asarray(t)
     host = torch.from_numpy(np.ascontiguousarray(arr))
-    target = dtype if dtype is not None else (torch.bfloat16 if host.dtype == torch.bfloat16 else torch.float32)
+    target = dtype if dtype is not None else (host.dtype if host.dtype in keep else torch.float32)
     return host.to(device=device, dtype=target, non_blocking=False).contiguous(), True
 
 
@@ -106,7 +108,9 @@ def _input_dtype_code(t: torch.Tensor) -> int:
         return _lib.DTYPE_BF16
     if t.dtype == torch.float32:
         return _lib.DTYPE_F32
-    raise UsageError(f"inputs must be bfloat16 or float32 on the device, got {t.dtype}")
+    if t.dtype == torch.float64:
+        return _lib.DTYPE_F64
+    raise UsageError(f"inputs must be bfloat16, float32 or float64 on the device, got {t.dtype}")
 
 
 def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemSpec], plan: Optional[BlockPlan], *,
@@ -141,18 +145,19 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     ws_bytes = ctypes.c_size_t()
     _lib.check(lib.fdp_workspace_bytes(ctypes.byref(desc), k, ctypes.byref(ws_bytes)))
 
+    out_dtype = torch.float64 if in_dtype == _lib.DTYPE_F64 else torch.float32  # fp64 path: fp64 outputs
     if grad_out is None:
-        grad = (torch.zeros if accumulate else torch.empty)((dims.D, dims.P), dtype=torch.float32, device=device)
+        grad = (torch.zeros if accumulate else torch.empty)((dims.D, dims.P), dtype=out_dtype, device=device)
     else:
-        if tuple(grad_out.shape) != (dims.D, dims.P) or grad_out.dtype != torch.float32 or not grad_out.is_contiguous():
-            raise ShapeError(f"grad_out must be a contiguous float32 ({dims.D}, {dims.P}) tensor")
+        if tuple(grad_out.shape) != (dims.D, dims.P) or grad_out.dtype != out_dtype or not grad_out.is_contiguous():
+            raise ShapeError(f"grad_out must be a contiguous {out_dtype} ({dims.D}, {dims.P}) tensor")
         grad = grad_out
     if kind == WorkflowKind.NON_DP:
         norms = None
     elif norms_out is not None:
         norms = norms_out
     else:
-        norms = torch.empty(dims.B, dtype=torch.float32, device=device)
+        norms = torch.empty(dims.B, dtype=out_dtype, device=device)
 
     stream = torch.cuda.current_stream(device)
     if workspace is not None:

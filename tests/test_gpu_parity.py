@@ -686,3 +686,65 @@ def test_bias_dw_against_oracle(dtype, rank, world):
     want[lo:hi] += 0.8 * 1.3 * O.keyed_normal_array(11, lid, 4, np.arange(lo, hi))
     assert rel(host(out), want) < 1e-5
     assert rel(host(norms), ns) < 1e-5
+
+
+# ---------------------------------------------------------------- fp64 parity path: the reference's own bar
+
+F64_TOL = 1e-12
+
+
+def test_fp64_worked_pair_and_random_instances_at_reference_tolerance():
+    """in_dtype F64 through the C ABI: the reference's golden outputs (worked pair,
+    60 random instances with random plans, every workflow kind, sigma > 0 with the
+    reference's keyed noise) reproduced to 1e-12 -- the reference's acceptance bar
+    (test_acceptance.py:38-58), through the drop-in path with reference Tensor
+    inputs (host float64 -> fp64 path -> host Tensor results)."""
+    g = golden("worked.npz")
+    x, dy = fdp.Tensor(g["x"].shape, g["x"]), fdp.Tensor(g["dy"].shape, g["dy"])
+    for tag, cfg in {"c10_sum": fdp.DPConfig(10.0, 0.0), "c10_mean": fdp.DPConfig(10.0, 0.0, "mean"),
+                     "c1e9": fdp.DPConfig(1e9, 0.0),
+                     "c10_s07": fdp.DPConfig(10.0, 0.7, seed=11, layer_id=2, step=5)}.items():
+        for kind in ("non_dp", "explicit_dp", "implicit_dp", "flashdp"):
+            r = fdp.run_backward(W(kind), x, dy, cfg)
+            assert rel(r.grad_w.array, g[f"{tag}_{kind}_grad"]) < F64_TOL, (tag, kind)
+            if kind != "non_dp":
+                assert rel(r.per_sample_norms_sq, g[f"{tag}_{kind}_norms"]) < F64_TOL
+    g = golden("random.npz")
+    for i in range(int(g["count"][0])):
+        x, dy = fdp.Tensor(g[f"x{i}"].shape, g[f"x{i}"]), fdp.Tensor(g[f"dy{i}"].shape, g[f"dy{i}"])
+        c, s, mean, seed, layer, step = g[f"cfg{i}"].tolist()
+        cfg = fdp.DPConfig(c, s, "mean" if mean else "sum", int(seed), int(layer), int(step))
+        r = fdp.backward_flashdp(x, dy, cfg)
+        assert rel(r.grad_w.array, g[f"grad{i}"]) < F64_TOL, i
+        assert rel(r.per_sample_norms_sq, g[f"norms{i}"]) < F64_TOL, i
+
+
+@pytest.mark.parametrize("tag", ["c1_s0", "c1_s1", "cmed_s0", "c1e9_s0", "c1_s1_mean_l3"])
+def test_fp64_config1_at_reference_tolerance(tag):
+    """BASELINE config 1 (B=4, T=128, 256->256) in fp64 on the GPU vs the reference's
+    own output, 1e-12 (sigma = 1 included: keyed noise in fp64)."""
+    g = golden("config1.npz")
+    x64, dy64 = O.cell_inputs(0, 0, 4, 128, 256, 256)
+    c, s, mean, seed, layer, step = g[f"{tag}_cfg"].tolist()
+    cfg = fdp.DPConfig(c, s, "mean" if mean else "sum", int(seed), int(layer), int(step))
+    r = fdp.backward_flashdp(torch.tensor(x64).cuda(), torch.tensor(dy64).cuda(), cfg, noise_impl="keyed_f64")
+    assert r.grad_w.dtype == torch.float64
+    assert rel(host(r.grad_w), g[f"{tag}_grad"]) < F64_TOL
+    assert rel(host(r.per_sample_norms_sq), g[f"{tag}_norms"]) < F64_TOL
+
+
+def test_fp64_random_stream_against_oracle():
+    """Acceptance criterion 1 analogue: 200 random instances (shapes, C, sigma,
+    reduction, keys) in fp64 on the GPU vs the fp64 oracle at 1e-12."""
+    rng = np.random.default_rng(99)
+    for i in range(200):
+        B, T, P, D = (int(v) for v in rng.integers(1, 9, size=4))
+        x = rng.uniform(-1, 1, (B, T, P))
+        dy = rng.uniform(-1, 1, (B, T, D))
+        cfg = fdp.DPConfig(float(10.0 ** rng.uniform(-1, 1)), float(rng.choice([0.0, 1.0])),
+                           str(rng.choice(["sum", "mean"])), seed=int(rng.integers(0, 1 << 31)),
+                           layer_id=int(rng.integers(0, 50)), step=int(rng.integers(0, 1000)))
+        r = fdp.backward_flashdp(torch.tensor(x).cuda(), torch.tensor(dy).cuda(), cfg, noise_impl="keyed_f64")
+        want, wn = O.dp_backward(x, dy, ocfg(cfg), exact_noise=True)
+        assert rel(host(r.grad_w), want) < F64_TOL, i
+        assert rel(host(r.per_sample_norms_sq), wn) < F64_TOL, i
