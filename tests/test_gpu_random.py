@@ -87,3 +87,21 @@ def test_random_group_parity(seed):
                                  exact_noise=True)
         assert _rel(gw.double().cpu().numpy(), want) < TOL
         assert _rel(nrm.double().cpu().numpy(), wn) < TOL
+
+
+@pytest.mark.parametrize("B,T,P,D,path", [
+    (64, 1, 256, 256, "fused"), (64, 3, 512, 128, "two_phase"), (1, 4096, 8, 8, "auto"),
+    (3, 5000, 64, 72, "auto"), (2, 33, 8, 4096, "auto"), (2, 33, 4096, 8, "auto"),
+    (128, 16, 128, 128, "fused"), (96, 8, 384, 256, "two_phase"), (1, 1, 8, 8, "auto")])
+def test_extreme_shapes(B, T, P, D, path):
+    """Degenerate and extreme extents: single tokens, one sample, very long or very
+    short sequences, skinny layers, many samples per tile (several sample groups)."""
+    g = torch.Generator().manual_seed(B * 7 + T)
+    x = torch.randn(B, T, P, generator=g).to(torch.bfloat16).cuda()
+    dy = (torch.randn(B, T, D, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    cfg = fdp.DPConfig(0.2, 1.0, "mean", seed=4, layer_id=1, step=2)
+    r = fdp.backward_flashdp(x, dy, cfg, path=path, noise_impl="keyed_f64")
+    want, wn = O.dp_backward(x.double().cpu().numpy(), dy.double().cpu().numpy(),
+                             O.Cfg(0.2, 1.0, "mean", 4, 1, 2), exact_noise=True)
+    assert _rel(r.grad_w.double().cpu().numpy(), want) < TOL
+    assert _rel(r.per_sample_norms_sq.double().cpu().numpy(), wn) < TOL
