@@ -125,3 +125,76 @@ class ChunkedAllReduceBackward:
                 dist.all_reduce(bucket, op=dist.ReduceOp.SUM, group=self.group)
         if cuda and self.world > 1:
             stream.wait_stream(self.comm)
+
+
+class ShardedDPAdam:
+    """ZeRO-1 style data parallelism for the DP step (the 13B layout):
+    every rank computes its clipped sums WITHOUT noise (scaled by 1/B_global), the
+    per-layer gradients are reduce-scattered (sum) so rank r owns a contiguous
+    shard of the flat parameter vector, rank r adds the DP noise of exactly that
+    shard inside its Adam step (fdp_adam_step with the layer's noise key and the
+    shard's flat offset within the layer) and updates its shard of the fp32
+    master weights + moments, then the updated parameters are all-gathered.
+    Noise is added exactly once per element, so the result equals the
+    single-process DP-Adam step.
+
+    layers: sequence of (n_elements, DPConfig) in flat order (the DPConfig keys the
+    noise: seed, layer_id, step, sigma, clip_c); params: the flat fp32 master
+    parameters (replicated), updated in place by step(grad_flat)."""
+
+    def __init__(self, layers, params: torch.Tensor, *, eta: float, beta1: float = 0.9, beta2: float = 0.999,
+                 eps: float = 1e-8, noise_impl: str = "philox", rank: int = 0, world: int = 1, group=None):
+        self.layers = list(layers)
+        self.params = params
+        self.n = sum(n for n, _ in self.layers)
+        if params.numel() != self.n:
+            raise ValueError("params must hold every layer's elements")
+        self.rank, self.world, self.group = rank, world, group
+        self.noise_impl = noise_impl
+        # equal (padded) shards for the collective: rank r owns [r*per, (r+1)*per) ∩ [0, n)
+        self.per = -(-self.n // world)
+        self.lo, self.hi = min(rank * self.per, self.n), min((rank + 1) * self.per, self.n)
+        self.m = torch.zeros(self.hi - self.lo, dtype=params.dtype, device=params.device)
+        self.v = torch.zeros_like(self.m)
+        self.eta, self.beta1, self.beta2, self.eps = eta, beta1, beta2, eps
+
+    def _shard_of(self, full: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return full
+        pad = torch.zeros(self.per * self.world, dtype=full.dtype, device=full.device)
+        pad[:self.n] = full
+        if dist.get_backend(self.group) == "nccl":
+            out = torch.empty(self.per, dtype=full.dtype, device=full.device)
+            dist.reduce_scatter_tensor(out, pad, op=dist.ReduceOp.SUM, group=self.group)
+        else:  # gloo has no reduce-scatter: all-reduce and keep this rank's slice
+            dist.all_reduce(pad, op=dist.ReduceOp.SUM, group=self.group)
+            out = pad[self.rank * self.per:(self.rank + 1) * self.per].clone()
+        return out
+
+    def step(self, grad_flat: torch.Tensor, cfg_step: int) -> None:
+        from dataclasses import replace
+
+        from .dpcore import OptimizerState, dp_adam_step_
+
+        own_lo, own_hi = self.lo, self.hi
+        shard = self._shard_of(grad_flat)[:own_hi - own_lo]
+        theta = self.params[own_lo:own_hi].clone()
+        off = 0
+        for n, cfg in self.layers:  # per (layer ∩ shard) segment: that layer's noise key and in-layer offset
+            a, b = max(off, own_lo), min(off + n, own_hi)
+            if a < b:
+                st = OptimizerState(theta=theta[a - own_lo:b - own_lo], m=self.m[a - own_lo:b - own_lo],
+                                    v=self.v[a - own_lo:b - own_lo], eta=self.eta, beta1=self.beta1,
+                                    beta2=self.beta2, eps_adam=self.eps)
+                dp_adam_step_(st, shard[a - own_lo:b - own_lo].contiguous(), noise=replace(cfg, step=cfg_step),
+                              noise_offset=a - off, noise_impl=self.noise_impl, layer_numel=n)
+            off += n
+        if self.world == 1:
+            self.params.copy_(theta)
+            return
+        pieces = [torch.empty(self.per, dtype=self.params.dtype, device=self.params.device)
+                  for _ in range(self.world)]
+        mine = torch.zeros(self.per, dtype=self.params.dtype, device=self.params.device)
+        mine[:own_hi - own_lo] = theta
+        dist.all_gather(pieces, mine, group=self.group)
+        self.params.copy_(torch.cat(pieces)[:self.n])

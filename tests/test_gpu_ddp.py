@@ -91,3 +91,52 @@ def test_group_cta_cap_matches_uncapped():
     torch.cuda.synchronize()
     for a, b in zip(full.grads, capped.grads):
         assert torch.allclose(a, b, rtol=1e-5, atol=1e-6 * float(a.abs().max()))
+
+
+def _zero1_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2507_01154_b200 as fdp
+    from paper_2507_01154_b200.ddp import ShardedDPAdam
+
+    data = _inputs()
+    B = data[0][0].shape[0]
+    lo, hi = B * rank // world, B * (rank + 1) // world
+    grads = []
+    for i, (x, dy) in enumerate(data):  # clipped sums of this rank's samples, no noise, / global B
+        r = fdp.backward_flashdp(x[lo:hi].contiguous().cuda(), dy[lo:hi].contiguous().cuda(), _cfg(i),
+                                 add_noise=False, mean_batch=B)
+        grads.append(r.grad_w.reshape(-1))
+    flat = torch.cat(grads)
+    params = torch.linspace(-1, 1, flat.numel(), device="cuda")
+    opt = ShardedDPAdam([(P * D, _cfg(i)) for i, (P, D) in enumerate(SHAPES)], params, eta=0.01,
+                        noise_impl="keyed_f64", rank=rank, world=world)
+    opt.step(flat, cfg_step=4)
+    torch.cuda.synchronize()
+    if rank == 0:
+        out["params"] = params.cpu().numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_zero1_sharded_adam_two_ranks_equals_single_gpu():
+    """ZeRO-1 form of 8e: noise-free clipped sums reduce-scattered, each rank adds
+    its shard's DP noise inside its Adam step, params all-gathered == one-process
+    DP gradient (noise included) followed by Adam."""
+    import paper_2507_01154_b200 as fdp
+
+    with mp.get_context("spawn").Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_zero1_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+        got = out["params"]
+    grads = []
+    for i, (x, dy) in enumerate(_inputs()):
+        grads.append(fdp.backward_flashdp(x.cuda(), dy.cuda(), _cfg(i), noise_impl="keyed_f64").grad_w.reshape(-1))
+    flat = torch.cat(grads)
+    st = fdp.OptimizerState.fresh(torch.linspace(-1, 1, flat.numel(), device="cuda"), eta=0.01)
+    st = fdp.dp_adam_step_(st, flat)
+    want = st.theta.cpu().numpy()
+    start = np.linspace(-1, 1, flat.numel())
+    assert np.max(np.abs((got - start) - (want - start))) / np.max(np.abs(want - start)) < 1e-4
