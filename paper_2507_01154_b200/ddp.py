@@ -70,7 +70,7 @@ class ChunkedAllReduceBackward:
     replace the device launch (tests on CPU pass a callable computing the same
     contribution)."""
 
-    def __init__(self, layers, flat_grad: torch.Tensor, *, n_chunks: int = 4, comm_sms: int = 16,
+    def __init__(self, layers, flat_grad: torch.Tensor, *, n_chunks: int = 4, comm_sms: int = 4,
                  noise_impl: str = "philox", rank: int = 0, world: int = 1, mean_batch: int = 0,
                  device_step: "torch.Tensor | None" = None, group=None, make_group=None):
         if n_chunks < 1:
