@@ -35,11 +35,15 @@ def timed(fn, n=5):
 def main():
     T = 2048
     g = torch.Generator(device="cuda").manual_seed(0)
-    for name, (d, ff) in MODELS.items():
-        shapes = [("q", d, d), ("k", d, d), ("v", d, d), ("o", d, d), ("gate", d, ff), ("up", d, ff),
-                  ("down", ff, d)]
+    variants = {"separate": lambda d, ff: [("q", d, d), ("k", d, d), ("v", d, d), ("o", d, d), ("gate", d, ff),
+                                           ("up", d, ff), ("down", ff, d)],
+                # fused projections (one clip group each, like GPT-2's c_attn): qkv and gate_up
+                "fused_qkv_gateup": lambda d, ff: [("qkv", d, 3 * d), ("o", d, d), ("gate_up", d, 2 * ff),
+                                                   ("down", ff, d)]}
+    for (name, (d, ff)), (vname, vshapes) in [(m, v) for m in MODELS.items() for v in variants.items()]:
+        shapes = vshapes(d, ff)
         for B in (1, 2, 4):
-            row = {"model": name, "B": B, "T": T, "layers": {}}
+            row = {"model": name, "projections": vname, "B": B, "T": T, "layers": {}}
             dp_total = nd_total = 0.0
             flops = 0.0
             for lname, P, D in shapes:
