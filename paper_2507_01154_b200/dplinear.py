@@ -204,15 +204,25 @@ class DPLinear(torch.nn.Module):
         if dy3.dtype not in (torch.bfloat16, torch.float32):
             dy3 = dy3.float()
         dy3 = dy3.contiguous()
-        desc = _lib.make_desc(B=B, T=T, P=8, D=D, in_dtype=_lib.DTYPE_BF16 if dy3.dtype == torch.bfloat16
-                              else _lib.DTYPE_F32, reduction=self.reduction, clip_c=self.clip_c, sigma=self.sigma,
-                              seed=self.seed, layer_id=self.layer_id + (1 << 32), step=self.step, rank=self.rank,
-                              world=self.world, mean_batch=self.logical_batch or B, add_noise=self._noise_now,
-                              noise_impl=self.noise_impl)
         lib = _lib.load()
-        nbytes = ctypes.c_size_t()
-        _lib.check(lib.fdp_bias_workspace_bytes(ctypes.byref(desc), ctypes.byref(nbytes)))
-        ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dy3.device)
+        key = (B, T, D, dy3.dtype, self.reduction, self.clip_c, self.sigma, self.seed, self.rank, self.world,
+               self.noise_impl)
+        cached = getattr(self, "_bias_cache", None)
+        if cached is None or cached[0] != key:  # descriptor + workspace size, rebuilt only when the shape changes
+            desc = _lib.make_desc(B=B, T=T, P=8, D=D, in_dtype=_lib.DTYPE_BF16 if dy3.dtype == torch.bfloat16
+                                  else _lib.DTYPE_F32, reduction=self.reduction, clip_c=self.clip_c,
+                                  sigma=self.sigma, seed=self.seed, layer_id=self.layer_id + (1 << 32),
+                                  rank=self.rank, world=self.world, noise_impl=self.noise_impl)
+            nbytes = ctypes.c_size_t()
+            _lib.check(lib.fdp_bias_workspace_bytes(ctypes.byref(desc), ctypes.byref(nbytes)))
+            cached = (key, desc, nbytes.value)
+            self._bias_cache = cached
+        _, desc, ws_bytes = cached
+        desc.step = _lib._wrap64(self.step)
+        desc.layer_id = _lib._wrap64(self.layer_id + (1 << 32))
+        desc.mean_batch = self.logical_batch or B
+        desc.add_noise = int(bool(self._noise_now))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dy3.device)
         out = torch.empty(D, dtype=torch.float32, device=dy3.device)
         _lib.check(lib.fdp_bias_dw(ctypes.byref(desc), dy3.data_ptr(), out.data_ptr(), None, ws.data_ptr(),
                                    ws.numel(), torch.cuda.current_stream(dy3.device).cuda_stream))
