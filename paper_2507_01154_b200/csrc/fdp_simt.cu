@@ -199,11 +199,30 @@ __global__ void k_noise_fill(float* out, long long lo, long long hi, float scale
   }
 }
 
-__global__ void __launch_bounds__(256)
+// kMode: 0 = any noise impl (per-element range checks), 1 = Philox with the whole
+// range noised, 2 = no noise. The Philox / no-noise variants are lean enough
+// to keep 48 warps per SM streaming, which the elementwise pass needs to reach
+// HBM bandwidth with the Philox arithmetic interleaved.
+template <int kMode>
+__global__ void __launch_bounds__(256, kMode == 0 ? 1 : 6)
     k_single_finalize(float* __restrict__ g, long long n, const float* __restrict__ part, int n_parts, double clip_c,
                       double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl, float scale,
                       uint64_t base, uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u,
                       long long lo, long long hi) {
+  float4* g4 = reinterpret_cast<float4*>(g);
+  const long long n4 = n >> 2;  // n = D * P, P % 8 == 0
+  constexpr int kU = kMode == 0 ? 4 : 2;  // float4 per thread per iteration: loads in flight
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  float4 v[kU];
+  auto load = [&]() {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n4) v[u] = __ldcs(g4 + i);
+    }
+  };
+  load();  // the first loads are in flight while warp 0 forms the clip factor
   __shared__ float s_f;
   if (threadIdx.x < 32) {  // every block sums the partials in the same fixed order
     double t = 0.0;
@@ -222,17 +241,7 @@ __global__ void __launch_bounds__(256)
     base = absorb3(seed_u, layer_u, static_cast<uint64_t>(*step_ptr));
     base_g = base + kGamma;
   }
-  float4* g4 = reinterpret_cast<float4*>(g);
-  const long long n4 = n >> 2;  // n = D * P, P % 8 == 0
-  constexpr int kU = 4;         // float4 per thread per iteration: loads in flight, independent Philox chains
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n4; i0 += stride * kU) {
-    float4 v[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const long long i = i0 + u * stride;
-      if (i < n4) v[u] = g4[i];
-    }
+  for (; i0 < n4; i0 += stride * kU, load()) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const long long i = i0 + u * stride;
@@ -241,16 +250,24 @@ __global__ void __launch_bounds__(256)
       v[u].y *= f;
       v[u].z *= f;
       v[u].w *= f;
-      const long long e = i << 2;
-      if (add_noise && e + 3 >= lo && e < hi) {
-        const float4 z = impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
-                                   : noise_draw4(impl, base_g, base, static_cast<uint64_t>(i));
-        if (e + 0 >= lo && e + 0 < hi) v[u].x += scale * z.x;
-        if (e + 1 >= lo && e + 1 < hi) v[u].y += scale * z.y;
-        if (e + 2 >= lo && e + 2 < hi) v[u].z += scale * z.z;
-        if (e + 3 >= lo && e + 3 < hi) v[u].w += scale * z.w;
+      if constexpr (kMode == 1) {
+        const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
+        v[u].x += scale * z.x;
+        v[u].y += scale * z.y;
+        v[u].z += scale * z.z;
+        v[u].w += scale * z.w;
+      } else if constexpr (kMode == 0) {
+        const long long e = i << 2;
+        if (add_noise && e + 3 >= lo && e < hi) {
+          const float4 z = impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
+                                     : noise_draw4(impl, base_g, base, static_cast<uint64_t>(i));
+          if (e + 0 >= lo && e + 0 < hi) v[u].x += scale * z.x;
+          if (e + 1 >= lo && e + 1 < hi) v[u].y += scale * z.y;
+          if (e + 2 >= lo && e + 2 < hi) v[u].z += scale * z.z;
+          if (e + 3 >= lo && e + 3 < hi) v[u].w += scale * z.w;
+        }
       }
-      g4[i] = v[u];
+      __stcs(g4 + i, v[u]);
     }
   }
 }
@@ -268,9 +285,24 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
                                    double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl,
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,
                                    uint64_t seed_u, uint64_t layer_u, long long lo, long long hi, cudaStream_t s) {
-  k_single_finalize<<<grid_for(n / 16, 256), 256, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch,
-                                                         norms_out, add_noise, impl, noise_scale, base, base_g,
-                                                         step_ptr, seed_u, layer_u, lo, hi);
+  // Philox over the whole tensor (the common case) or no noise: the lean variants
+  const int mode = !add_noise || hi <= lo ? 2 : (impl == 2 && lo <= 0 && hi >= n) ? 1 : 0;
+  const int threads = 256;
+  if (mode == 0) {
+    k_single_finalize<0><<<grid_for(n / 16, threads), threads, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2,
+                                                                         inv_batch, norms_out, add_noise, impl,
+                                                                         noise_scale, base, base_g, step_ptr, seed_u,
+                                                                         layer_u, lo, hi);
+  } else {
+    long long blocks = (n / 8 + threads - 1) / threads;
+    const long long cap = 148LL * 6 * 4;  // 6 resident blocks per SM, a few rounds each
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    auto k = mode == 1 ? k_single_finalize<1> : k_single_finalize<2>;
+    k<<<static_cast<int>(blocks), threads, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch, norms_out,
+                                                  add_noise, impl, noise_scale, base, base_g, step_ptr, seed_u,
+                                                  layer_u, lo, hi);
+  }
   return cudaGetLastError();
 }
 

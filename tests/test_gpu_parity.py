@@ -535,6 +535,30 @@ def test_single_sample_path_against_oracle(B, T, P, D, red):
     assert rel(host(r1.grad_w), want1) < BF16_TOL
 
 
+@pytest.mark.parametrize("rank,world", [(0, 1), (1, 2)])
+def test_single_sample_philox_finalize(rank, world):
+    """B == 1 finalize with Philox noise (the lean whole-range variant at world 1,
+    the range-checked one for a rank slice) and with sigma = 0 (the no-noise
+    variant): out(sigma) - out(0) is exactly the rank's slice of sigma*C*noise and
+    out(0) is the clipped mean gradient of the oracle."""
+    B, T, P, D = 1, 384, 1024, 768
+    x, dy = randn(B, T, P, D, seed=77, scale_dy=1e-2)
+    cfg0 = fdp.DPConfig(0.5, 0.0, "mean", seed=5, layer_id=2, step=4)
+    cfg1 = fdp.DPConfig(0.5, 1.5, "mean", seed=5, layer_id=2, step=4)
+    kw = dict(path="two_phase", noise_impl="philox", rank=rank, world=world)
+    r0 = fdp.backward_flashdp(x, dy, cfg0, **kw)
+    r1 = fdp.backward_flashdp(x, dy, cfg1, **kw)
+    assert fdp.execution_plan(tuple(x.shape), tuple(dy.shape), path="two_phase")["norm_phase"] == "single"
+    want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg0), exact_noise=True)
+    assert rel(host(r0.grad_w), want) < BF16_TOL
+    assert rel(host(r0.per_sample_norms_sq), wn) < BF16_TOL
+    n = fdp.noise_range(cfg1, 0, P * D, 0.75, noise_impl="philox").view(D, P)
+    lo, hi = P * D * rank // world, P * D * (rank + 1) // world
+    mask = torch.zeros(P * D, device="cuda")
+    mask[lo:hi] = 1.0
+    assert rel(host(r1.grad_w - r0.grad_w), host(n * mask.view(D, P))) < 1e-5
+
+
 def test_single_sample_norm_phase_needs_one_sample():
     x, dy = randn(2, 64, 128, 128, seed=1)
     with pytest.raises(fdp.UsageError):
