@@ -491,7 +491,7 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "tools"))
             import train_gpt2 as tg
 
-            targs = argparse.Namespace(batch=B, seq=T, steps=10, warmup=3)
+            targs = argparse.Namespace(batch=B, seq=T, steps=10, warmup=3, full=False)
             nd_t = tg.run(False, targs)
             dp_t = tg.run(True, targs)
             train = {"model": "gpt2-small (124M) training step, random init, synthetic tokens, bf16 autocast, "

@@ -196,15 +196,33 @@ FDP_API int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* 
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);
 
-/* DP gradient of a linear layer's bias (B, T, D) -> (D): per-sample g_b = sum_t dY[b,t,:],
- * clipped at the descriptor's clip_c with its own norm (per-layer clipping of the
- * bias as its own group), summed (or /mean_batch) + sigma*C*N(seed, layer_id, step, d)
- * on the rank's slice. Uses d->B, T, D (P ignored), in_dtype, reduction, noise
- * fields. `ws` needs fdp_bias_workspace_bytes(d) bytes (no zeroing needed);
- * norms_sq (B,) may be NULL. */
+/* Non-linear parameter groups (the reference clips linear
+ * weights only). Each group is clipped per sample with its own norm at
+ * the descriptor's clip_c (per-layer clipping), summed (or /mean_batch), and gets
+ * sigma*C*N(seed, layer_id, step, i) on the rank's slice of its own index space
+ * [0, L); accumulate adds onto `grad`. norms_sq (B,) may be NULL; `ws` needs the
+ * matching *_workspace_bytes (no zeroing needed). in_dtype bf16 or fp32. */
+enum fdp_vec_kind {
+  FDP_VEC_BIAS = 0,      /* g_b = sum_t dY[b,t,:]                                L = D   */
+  FDP_VEC_RMSNORM = 1,   /* g_b = sum_t dY[b,t,:] * xhat[b,t,:]  (gamma)         L = D   */
+  FDP_VEC_LAYERNORM = 2  /* g_b = [sum_t dY * xhat (gamma), sum_t dY (beta)]    L = 2 D */
+};
+/* Vector groups: dY, xhat (B, T, D) row-major (xhat = the normalised input, unused
+ * for FDP_VEC_BIAS); uses d->B, T, D (P ignored). */
+FDP_API int fdp_vec_workspace_bytes(const fdp_desc* d, int32_t kind, size_t* bytes);
+FDP_API int fdp_vec_dw(const fdp_desc* d, int32_t kind, const void* dy, const void* xhat, float* grad, float* norms_sq,
+                       void* ws, size_t ws_bytes, void* stream);
+/* fdp_vec_dw(kind = FDP_VEC_BIAS): the bias of a linear layer as its own group. */
 FDP_API int fdp_bias_workspace_bytes(const fdp_desc* d, size_t* bytes);
 FDP_API int fdp_bias_dw(const fdp_desc* d, const void* dy, float* grad_b, float* norms_sq, void* ws, size_t ws_bytes,
                         void* stream);
+/* Embedding table (V, D) = (d->P, d->D): tokens (B, T) int64, dY (B, T, D); the
+ * per-sample gradient scatters dY rows onto the sample's token rows, its norm is
+ * the token-equality Gram; every row of `grad` is written (flat index v*D + c for
+ * the noise). Token ids outside [0, V) contribute nothing. T <= 16384. */
+FDP_API int fdp_embedding_workspace_bytes(const fdp_desc* d, size_t* bytes);
+FDP_API int fdp_embedding_dw(const fdp_desc* d, const int64_t* tokens, const void* dy, float* grad, float* norms_sq,
+                             void* ws, size_t ws_bytes, void* stream);
 
 /* Optimizer steps on a finalized DP gradient, in place, fp32 or fp64 state
  * (dtype FDP_DTYPE_F32 / FDP_DTYPE_F64); reference dpcore.dp_sgd_step /

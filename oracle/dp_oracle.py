@@ -204,6 +204,69 @@ def nondp_backward(x: np.ndarray, dy: np.ndarray) -> np.ndarray:
     return per_sample_grads(x, dy).sum(axis=0)
 
 
+# ------------------------------------------------------------------ non-linear parameter groups
+# SURVEY 8f rank 3. Not in the reference (SPEC.md:8 clips linear weights only); the
+# per-sample gradients below are the textbook ones and everything after them (norm,
+# clip_factors, sum / mean, keyed noise on [lo, hi) of the group's own index space)
+# is the reference's per-layer arithmetic (oracle.py:49-65, dpcore.py:41-73).
+
+def vector_per_sample_grads(dy: np.ndarray, xhat: np.ndarray | None, kind: str) -> np.ndarray:
+    """(B, L): bias g_b = sum_t dY; rmsnorm g_b = sum_t dY * xhat (gamma);
+    layernorm g_b = [sum_t dY * xhat (gamma), sum_t dY (beta)] (L = 2 D)."""
+    dy = np.asarray(dy, dtype=np.float64)
+    if kind == "bias":
+        return dy.sum(axis=1)
+    gam = (dy * np.asarray(xhat, dtype=np.float64)).sum(axis=1)
+    if kind == "rmsnorm":
+        return gam
+    if kind == "layernorm":
+        return np.concatenate([gam, dy.sum(axis=1)], axis=1)
+    raise ValueError(kind)
+
+
+def dp_vector_backward(dy, xhat, kind: str, cfg: Cfg, exact_noise: bool = True, *, noise_lo: int = 0,
+                       noise_hi: int | None = None, mean_batch: int | None = None):
+    """Clip-sum-noise of a bias / RMSNorm / LayerNorm parameter group. Returns (grad (L,), norms_sq (B,))."""
+    g = vector_per_sample_grads(dy, xhat, kind)
+    norms = (g * g).sum(axis=1)
+    acc = (clip_factors(norms, cfg.clip_c)[:, None] * g).sum(axis=0)
+    batch = g.shape[0] if mean_batch is None else mean_batch
+    return finalize(acc, batch, cfg, exact_noise, noise_lo, noise_hi), norms
+
+
+def embedding_per_sample_grads(tokens: np.ndarray, dy: np.ndarray, vocab: int) -> np.ndarray:
+    """(B, V, d): G_b[v] = sum over positions t with tokens[b, t] == v of dY[b, t]."""
+    tokens = np.asarray(tokens)
+    dy = np.asarray(dy, dtype=np.float64)
+    B, T, d = dy.shape
+    g = np.zeros((B, vocab, d))
+    for b in range(B):
+        np.add.at(g[b], tokens[b], dy[b])
+    return g
+
+
+def embedding_norms_gram(tokens: np.ndarray, dy: np.ndarray) -> np.ndarray:
+    """||G_b||^2 without G: sum over position pairs with equal tokens of <dY_t, dY_s>
+    (the token-equality Gram of SURVEY 8f rank 3) -- a cross-check of the above."""
+    dy = np.asarray(dy, dtype=np.float64)
+    out = np.zeros(dy.shape[0])
+    for b in range(dy.shape[0]):
+        eq = (tokens[b][:, None] == tokens[b][None, :]).astype(np.float64)
+        out[b] = float(np.einsum("ts,td,sd->", eq, dy[b], dy[b]))
+    return out
+
+
+def dp_embedding_backward(tokens, dy, vocab: int, cfg: Cfg, exact_noise: bool = True, *, noise_lo: int = 0,
+                          noise_hi: int | None = None, mean_batch: int | None = None):
+    """Clip-sum-noise of an embedding table (V, d): noise on every row (untouched
+    rows included), flat index v * d + col. Returns (grad (V, d), norms_sq (B,))."""
+    g = embedding_per_sample_grads(tokens, dy, vocab)
+    norms = np.einsum("bvd,bvd->b", g, g)
+    acc = np.einsum("b,bvd->vd", clip_factors(norms, cfg.clip_c), g)
+    batch = g.shape[0] if mean_batch is None else mean_batch
+    return finalize(acc, batch, cfg, exact_noise, noise_lo, noise_hi), norms
+
+
 def micro_batched(x: np.ndarray, dy: np.ndarray, cfg: Cfg, size: int, exact_noise: bool = True) -> np.ndarray:
     """bench.py:244-271: sigma=0/sum micro runs, one finalize for the logical batch."""
     B = x.shape[0]

@@ -35,8 +35,10 @@ EXPORTED_SYMBOLS = (
     "fdp_abi_version", "fdp_last_error", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes",
     "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_partition",
     "fdp_group_workspace_bytes", "fdp_backward_group", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex",
-    "fdp_sgd_step", "fdp_adam_step", "fdp_bias_workspace_bytes", "fdp_bias_dw",
+    "fdp_sgd_step", "fdp_adam_step", "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_vec_workspace_bytes",
+    "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
 )
+VEC_KIND = {"bias": 0, "rmsnorm": 1, "layernorm": 2}
 
 
 class FdpDesc(ctypes.Structure):
@@ -114,7 +116,14 @@ def load() -> ctypes.CDLL:
     lib.fdp_bias_workspace_bytes.argtypes = [ctypes.POINTER(FdpDesc), ctypes.POINTER(ctypes.c_size_t)]
     lib.fdp_bias_dw.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-    for name in ("fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
+    lib.fdp_vec_workspace_bytes.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+    lib.fdp_vec_dw.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_int32] + [ctypes.c_void_p] * 5 + [
+        ctypes.c_size_t, ctypes.c_void_p]
+    lib.fdp_embedding_workspace_bytes.argtypes = [ctypes.POINTER(FdpDesc), ctypes.POINTER(ctypes.c_size_t)]
+    lib.fdp_embedding_dw.argtypes = [ctypes.POINTER(FdpDesc)] + [ctypes.c_void_p] * 5 + [ctypes.c_size_t,
+                                                                                        ctypes.c_void_p]
+    for name in ("fdp_vec_workspace_bytes", "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
+                 "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
                  "fdp_dw", "fdp_noise", "fdp_noise_partition"):
         getattr(lib, name).restype = ctypes.c_int

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_fdp.so"
 OBJ = PKG / "build_obj"
-SOURCES = ["fdp_tc.cu", "fdp_group.cu", "fdp_stream.cu", "fdp_optim.cu", "fdp_f64.cu", "fdp_ghost.cu", "fdp_simt.cu", "fdp_capi.cu"]
+SOURCES = ["fdp_tc.cu", "fdp_group.cu", "fdp_stream.cu", "fdp_optim.cu", "fdp_f64.cu", "fdp_ghost.cu", "fdp_simt.cu", "fdp_params.cu", "fdp_capi.cu"]
 HEADERS = ["fdp_internal.h", "fdp_ptx.cuh", "fdp_rng.cuh", "fdp_prefill.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

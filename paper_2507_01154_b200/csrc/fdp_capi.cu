@@ -1091,33 +1091,101 @@ int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scal
   return FDP_OK;
 }
 
-int fdp_bias_workspace_bytes(const fdp_desc* d, size_t* bytes) {
+// ---- non-linear parameter groups (fdp_params.cu)
+namespace {
+fdp::NoiseKey group_noise(const fdp_desc* d, long long L) {
+  const Common c = common_of(d);
+  fdp::NoiseKey nk{};
+  nk.add_noise = c.add_noise;
+  nk.impl = d->noise_impl;
+  nk.scale = c.noise_scale;
+  nk.base = c.key_base;
+  nk.base_g = c.key_base_g;
+  nk.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+  nk.seed_u = static_cast<uint64_t>(d->seed);
+  nk.layer_u = static_cast<uint64_t>(d->layer_id);
+  nk.lo = L * d->rank / d->world;  // the rank's slice of the group's own index space
+  nk.hi = L * (d->rank + 1) / d->world;
+  return nk;
+}
+
+int group_validate(const fdp_desc* d) {
   int rc = validate(d, FDP_KIND_FLASHDP);
   if (rc) return rc;
-  if (!bytes) return fail(FDP_ERR_USAGE, "null output");
-  if (d->B > (1 << 24) || d->D > (1 << 30)) return fail(FDP_ERR_SHAPE, "extent too large");
-  *bytes = fdp::bias_dp_work_bytes(static_cast<int>(d->B), static_cast<int>(d->D));
+  if (d->in_dtype != FDP_DTYPE_BF16 && d->in_dtype != FDP_DTYPE_F32)
+    return fail(FDP_ERR_USAGE, "parameter-group gradients take bf16 (0) or f32 (1) inputs, got dtype %d", d->in_dtype);
+  if (d->B > (1 << 24) || d->T > (1 << 30) || d->D > (1 << 28)) return fail(FDP_ERR_SHAPE, "extent too large");
   return FDP_OK;
+}
+
+int check_ws(void* ws, size_t ws_bytes, size_t need) {
+  if (!ws || ws_bytes < need)
+    return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
+                need);
+  return FDP_OK;
+}
+}  // namespace
+
+int fdp_vec_workspace_bytes(const fdp_desc* d, int32_t kind, size_t* bytes) {
+  int rc = group_validate(d);
+  if (rc) return rc;
+  if (kind < FDP_VEC_BIAS || kind > FDP_VEC_LAYERNORM) return fail(FDP_ERR_USAGE, "unknown vector group kind %d", kind);
+  if (!bytes) return fail(FDP_ERR_USAGE, "null output");
+  *bytes = fdp::vec_dp_work_bytes(kind, static_cast<int>(d->B), static_cast<int>(d->T), static_cast<int>(d->D));
+  return FDP_OK;
+}
+
+int fdp_vec_dw(const fdp_desc* d, int32_t kind, const void* dy, const void* xhat, float* grad, float* norms_sq,
+               void* ws, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  int rc = fdp_vec_workspace_bytes(d, kind, &need);
+  if (rc) return rc;
+  if (!dy || !grad || (kind != FDP_VEC_BIAS && !xhat)) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if ((rc = check_ws(ws, ws_bytes, need))) return rc;
+  const Common c = common_of(d);
+  const long long L = kind == FDP_VEC_LAYERNORM ? 2 * d->D : d->D;
+  cudaError_t e = fdp::vec_dp(kind, dy, xhat, d->in_dtype == FDP_DTYPE_F32, static_cast<int>(d->B),
+                              static_cast<int>(d->T), static_cast<int>(d->D), static_cast<float*>(ws), d->clip_c,
+                              c.inv_batch, grad, norms_sq, d->accumulate ? 1 : 0, group_noise(d, L),
+                              static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "vector-group dp");
+  return FDP_OK;
+}
+
+int fdp_bias_workspace_bytes(const fdp_desc* d, size_t* bytes) {
+  return fdp_vec_workspace_bytes(d, FDP_VEC_BIAS, bytes);
 }
 
 int fdp_bias_dw(const fdp_desc* d, const void* dy, float* grad_b, float* norms_sq, void* ws, size_t ws_bytes,
                 void* stream) {
-  size_t need = 0;
-  int rc = fdp_bias_workspace_bytes(d, &need);
+  return fdp_vec_dw(d, FDP_VEC_BIAS, dy, nullptr, grad_b, norms_sq, ws, ws_bytes, stream);
+}
+
+int fdp_embedding_workspace_bytes(const fdp_desc* d, size_t* bytes) {
+  int rc = group_validate(d);
   if (rc) return rc;
-  if (!dy || !grad_b) return fail(FDP_ERR_USAGE, "null tensor pointer");
-  if (!ws || ws_bytes < need)
-    return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
-                need);
+  if (!bytes) return fail(FDP_ERR_USAGE, "null output");
+  if (d->T > fdp::emb_max_tokens())
+    return fail(FDP_ERR_SHAPE, "embedding gradients take T <= %d positions per sample, got %lld", fdp::emb_max_tokens(),
+                (long long)d->T);
+  if (d->P >= (1ll << 31)) return fail(FDP_ERR_SHAPE, "vocabulary too large");
+  *bytes = fdp::emb_dp_work_bytes(static_cast<int>(d->B), static_cast<int>(d->T), static_cast<int>(d->D));
+  return FDP_OK;
+}
+
+int fdp_embedding_dw(const fdp_desc* d, const int64_t* tokens, const void* dy, float* grad, float* norms_sq, void* ws,
+                     size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  int rc = fdp_embedding_workspace_bytes(d, &need);
+  if (rc) return rc;
+  if (!tokens || !dy || !grad) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if ((rc = check_ws(ws, ws_bytes, need))) return rc;
   const Common c = common_of(d);
-  // the bias noise slice is [D*rank/world, D*(rank+1)/world) of its own index space
-  const long long lo = d->D * d->rank / d->world, hi = d->D * (d->rank + 1) / d->world;
-  cudaError_t e = fdp::bias_dp(dy, d->in_dtype == FDP_DTYPE_F32, static_cast<int>(d->B), static_cast<int>(d->T),
-                               static_cast<int>(d->D), static_cast<float*>(ws), d->clip_c, c.inv_batch, grad_b,
-                               norms_sq, c.add_noise, d->noise_impl, c.noise_scale, c.key_base, c.key_base_g,
-                               reinterpret_cast<const long long*>(d->device_step), static_cast<uint64_t>(d->seed),
-                               static_cast<uint64_t>(d->layer_id), lo, hi, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "bias dp");
+  cudaError_t e = fdp::emb_dp(reinterpret_cast<const long long*>(tokens), dy, d->in_dtype == FDP_DTYPE_F32,
+                              static_cast<int>(d->B), static_cast<int>(d->T), d->P, static_cast<int>(d->D), ws,
+                              d->clip_c, c.inv_batch, grad, norms_sq, d->accumulate ? 1 : 0,
+                              group_noise(d, d->P * d->D), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "embedding dp");
   return FDP_OK;
 }
 

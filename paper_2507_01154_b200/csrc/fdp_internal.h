@@ -204,12 +204,26 @@ struct F64Params {
 };
 cudaError_t f64_backward(const F64Params& p, cudaStream_t s);
 
-// ---- DP bias gradient (fdp_simt.cu): per-sample sums over t, per-sample clip, batch sum, noise
-cudaError_t bias_dp(const void* dy, int in_f32, int B, int T, int D, float* work, double clip_c, float inv_batch,
-                    float* out, float* norms_out, int add_noise, int impl, float scale, uint64_t base,
-                    uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u, long long lo,
-                    long long hi, cudaStream_t s);
-size_t bias_dp_work_bytes(int B, int D);
+// Noise of one parameter group: scale * N(key, i) for flat i in [lo, hi); the key
+// comes from step_ptr (device counter) when set.
+struct NoiseKey {
+  int add_noise, impl;
+  float scale;
+  uint64_t base, base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long lo, hi;
+};
+// fdp_params.cu: bias / RMSNorm / LayerNorm vector groups (kind = FDP_VEC_*) and embedding tables
+size_t vec_dp_work_bytes(int kind, int B, int T, int D);
+cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B, int T, int D, float* work,
+                   double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
+                   cudaStream_t s);
+size_t emb_dp_work_bytes(int B, int T, int D);
+int emb_max_tokens();
+cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, int T, long long V, int D, void* work,
+                   double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
+                   cudaStream_t s);
 
 // ---- optimizer steps (fdp_optim.cu)
 struct OptimNoise {

@@ -1,0 +1,372 @@
+// fdp_params.cu -- DP gradients of the non-linear parameter groups of a model
+// (SURVEY 8f rank 3): bias / RMSNorm / LayerNorm vectors and embedding tables,
+// each clipped per sample as its own per-layer group and finalized with the
+// reference's arithmetic (clip factor dpcore.py:41-47, sum or mean + sigma*C*N
+// dpcore.py:60-73, keyed noise rng.py:69-85 on the group's own index space).
+// The reference clips linear weights only; these are the textbook
+// per-sample gradients, pinned to oracle/dp_oracle.py's restatements.
+//
+// Vector groups (length L = D, or 2 D for LayerNorm's [gamma, beta]): per-sample
+// g_b = sum_t dY (bias, beta), sum_t dY * xhat (gamma). Three deterministic passes:
+// row-chunk partial sums (parallel over samples x T chunks x columns), a fixed-
+// order sum of the chunks with per-block norm^2 partials, and the clip / sum /
+// noise pass. All HBM-bound on reading dY (and xhat) once.
+//
+// Embedding (V x d table, tokens (B, T)): the per-sample gradient is a scatter of
+// dY rows onto the rows of the sample's tokens, so ||G_b||^2 is the token-
+// equality Gram sum_{t,s: tok_t = tok_s} <dY_t, dY_s>. Each sample's (token,
+// position) keys are sorted once in shared memory; the norm pass sums dY rows per
+// run of equal tokens (never materialising G_b), and the output pass walks all
+// samples' sorted runs per vocabulary row in fixed order -- deterministic, no
+// atomics -- writing every row (untouched rows get their noise only).
+#include "../../include/fdp.h"
+#include "fdp_internal.h"
+#include "fdp_rng.cuh"
+#include <cuda_bf16.h>
+
+namespace fdp {
+namespace {
+
+constexpr int kVCols = 256;  // columns per block
+constexpr int kVRows = 64;   // T rows per partial-sum block
+
+__device__ __forceinline__ void nk_resolve(NoiseKey& nk) {  // device step counter (graph replays)
+  if (nk.step_ptr) {
+    nk.base = absorb3(nk.seed_u, nk.layer_u, static_cast<uint64_t>(*nk.step_ptr));
+    nk.base_g = nk.base + kGamma;
+  }
+}
+__device__ __forceinline__ float nk_draw(const NoiseKey& nk, uint64_t i) {
+  return noise_draw(nk.impl, nk.base_g, nk.base, i);
+}
+
+template <typename T>
+__device__ __forceinline__ float ld(const T* p, long long i) {
+  if constexpr (sizeof(T) == 4) return __ldg(reinterpret_cast<const float*>(p) + i);
+  else return __bfloat162float(p[i]);
+}
+
+// pass 1: gpart[b][tc][l] = sum over rows [tc*kVRows, ...) of the group's per-row term
+template <typename T, int kKind>
+__global__ void __launch_bounds__(kVCols) k_vec_rows(const T* __restrict__ dy, const T* __restrict__ xh, int T_, int D,
+                                                     int n_tc, float* __restrict__ gpart) {
+  const int b = blockIdx.z, tc = blockIdx.y;
+  const int d = blockIdx.x * kVCols + threadIdx.x;
+  if (d >= D) return;
+  const int t0 = tc * kVRows, t1 = min(T_, t0 + kVRows);
+  float s = 0.0f, sx = 0.0f;
+  const long long base = static_cast<long long>(b) * T_ * D + d;
+#pragma unroll 8
+  for (int t = t0; t < t1; ++t) {
+    const long long i = base + static_cast<long long>(t) * D;
+    const float y = ld(dy, i);
+    if constexpr (kKind != FDP_VEC_RMSNORM) s += y;
+    if constexpr (kKind != FDP_VEC_BIAS) sx = fmaf(y, ld(xh, i), sx);
+  }
+  const long long L = kKind == FDP_VEC_LAYERNORM ? 2LL * D : D;
+  float* o = gpart + (static_cast<long long>(b) * n_tc + tc) * L;
+  if constexpr (kKind == FDP_VEC_BIAS) o[d] = s;
+  if constexpr (kKind == FDP_VEC_RMSNORM) o[d] = sx;
+  if constexpr (kKind == FDP_VEC_LAYERNORM) {
+    o[d] = sx;
+    o[D + d] = s;
+  }
+}
+
+// pass 2: g[b][l] = sum_tc gpart[b][tc][l] (fixed order), part[b][chunk] = sum over the block of g^2
+__global__ void __launch_bounds__(kVCols) k_vec_reduce(const float* __restrict__ gpart, int n_tc, int L,
+                                                       float* __restrict__ g, float* __restrict__ part, int n_chunks) {
+  const int b = blockIdx.y, chunk = blockIdx.x;
+  const int l = chunk * kVCols + threadIdx.x;
+  float s = 0.0f;
+  if (l < L) {
+    const float* p = gpart + static_cast<long long>(b) * n_tc * L + l;
+    for (int tc = 0; tc < n_tc; ++tc) s += p[static_cast<long long>(tc) * L];
+    g[static_cast<long long>(b) * L + l] = s;
+  }
+  __shared__ float red[kVCols / 32];
+  float sq = s * s;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < kVCols / 32; ++w) t += red[w];
+    part[static_cast<long long>(b) * n_chunks + chunk] = t;
+  }
+}
+
+// pass 3: out[l] (+)= sum_b c_b g[b][l] / batch + sigma C N(l) on [lo, hi)
+__global__ void __launch_bounds__(256) k_vec_finalize(const float* __restrict__ g, const float* __restrict__ part,
+                                                      int B, long long L, int n_chunks, double clip_c, double clip_c2,
+                                                      float inv_batch, float* out, float* norms_out, int accumulate,
+                                                      NoiseKey nk) {
+  extern __shared__ float fac[];  // [B] clip factor x mean scale
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[static_cast<long long>(b) * n_chunks + c]);
+    const double cf = (s <= clip_c2) ? 1.0 : clip_c / sqrt(s);  // dpcore.py:41-47
+    fac[b] = static_cast<float>(cf) * inv_batch;
+    if (blockIdx.x == 0 && norms_out) norms_out[b] = static_cast<float>(s);
+  }
+  __syncthreads();
+  nk_resolve(nk);
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < L;
+       l += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v = 0.0f;
+    for (int b = 0; b < B; ++b) v = fmaf(fac[b], g[static_cast<long long>(b) * L + l], v);
+    if (nk.add_noise && l >= nk.lo && l < nk.hi) v += nk.scale * nk_draw(nk, static_cast<uint64_t>(l));
+    if (accumulate) v += out[l];
+    out[l] = v;
+  }
+}
+
+// ---- embedding
+constexpr uint64_t kNoKey = ~0ull;
+constexpr int kESeg = 64;     // sorted positions per norm block
+constexpr int kEVRows = 32;   // vocabulary rows per output block
+constexpr int kECols = 1024;  // columns per output block (4 per thread)
+
+__global__ void __launch_bounds__(1024) k_emb_sort(const long long* __restrict__ tok, int T_, long long V, int n2,
+                                                   uint64_t* __restrict__ keys) {
+  extern __shared__ uint64_t sk[];  // [n2]
+  const int b = blockIdx.x;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    uint64_t k = kNoKey;
+    if (i < T_) {
+      const long long v = tok[static_cast<long long>(b) * T_ + i];
+      if (v >= 0 && v < V) k = (static_cast<uint64_t>(v) << 32) | static_cast<uint32_t>(i);
+    }
+    sk[i] = k;
+  }
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {  // bitonic sort, ascending
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = sk[lo], c = sk[hi];
+        if ((a > c) == up) {
+          sk[lo] = c;
+          sk[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < T_; i += blockDim.x) keys[static_cast<long long>(b) * T_ + i] = sk[i];
+}
+
+// norm^2 partial of sample b over the runs of equal tokens that START in sorted
+// positions [sc*kESeg, (sc+1)*kESeg), columns [dc*kVCols, ...)
+template <typename T>
+__global__ void __launch_bounds__(kVCols) k_emb_norms(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
+                                                      int T_, int D, int n_sc, int n_dc, float* __restrict__ part) {
+  const int dc = blockIdx.x, sc = blockIdx.y, b = blockIdx.z;
+  const int col = dc * kVCols + threadIdx.x;
+  const uint64_t* K = keys + static_cast<long long>(b) * T_;
+  const int k1 = min(T_, (sc + 1) * kESeg);
+  int k = sc * kESeg;
+  if (k > 0) {
+    const uint64_t prev = K[k - 1] >> 32;
+    while (k < k1 && K[k] != kNoKey && (K[k] >> 32) == prev) ++k;  // continuation of a run owned by the previous block
+  }
+  float sq = 0.0f;
+  const long long rbase = static_cast<long long>(b) * T_ * D + col;
+  while (k < k1 && K[k] != kNoKey) {
+    const uint64_t tk = K[k] >> 32;
+    float acc = 0.0f;
+    do {
+      const long long t = static_cast<long long>(K[k] & 0xffffffffull);
+      if (col < D) acc += ld(dy, rbase + t * D);
+      ++k;
+    } while (k < T_ && K[k] != kNoKey && (K[k] >> 32) == tk);
+    sq = fmaf(acc, acc, sq);
+  }
+  __shared__ float red[kVCols / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < kVCols / 32; ++w) t += red[w];
+    part[(static_cast<long long>(b) * n_sc + sc) * n_dc + dc] = t;
+  }
+}
+
+// out[v][c] (+)= sum_b c_b sum_{t: tok_bt = v} dY[b,t,c] + sigma C N(v*D + c), every row v
+template <typename T>
+__global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
+                                                 const float* __restrict__ factors, int B, int T_, long long V, int D,
+                                                 float* out, int accumulate, NoiseKey nk) {
+  extern __shared__ int sm[];  // ptr[B], beg[B], end[B]; fac[B] (float)
+  int* ptr = sm;
+  int* beg = sm + B;
+  int* end = sm + 2 * B;
+  float* fac = reinterpret_cast<float*>(sm + 3 * B);
+  const long long v0 = static_cast<long long>(blockIdx.x) * kEVRows;
+  const long long v1 = min(V, v0 + kEVRows);
+  const int c0 = blockIdx.y * kECols + 4 * threadIdx.x;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {  // first sorted position with token >= v0
+    const uint64_t* K = keys + static_cast<long long>(b) * T_;
+    const uint64_t want = static_cast<uint64_t>(v0) << 32;
+    int lo = 0, hi = T_;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (K[mid] < want) lo = mid + 1;
+      else hi = mid;
+    }
+    ptr[b] = lo;
+    fac[b] = factors[b];
+  }
+  nk_resolve(nk);
+  __syncthreads();
+  for (long long v = v0; v < v1; ++v) {
+    int touched = 0;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const uint64_t* K = keys + static_cast<long long>(b) * T_;
+      int e = ptr[b];
+      while (e < T_ && K[e] != kNoKey && static_cast<long long>(K[e] >> 32) == v) ++e;
+      beg[b] = ptr[b];
+      end[b] = e;
+      ptr[b] = e;
+      touched |= e > beg[b];
+    }
+    touched = __syncthreads_or(touched);
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (touched) {
+      for (int b = 0; b < B; ++b) {
+        const uint64_t* K = keys + static_cast<long long>(b) * T_;
+        for (int k = beg[b]; k < end[b]; ++k) {
+          const long long row = (static_cast<long long>(b) * T_ + static_cast<long long>(K[k] & 0xffffffffull)) * D;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (c0 + j < D) acc[j] = fmaf(fac[b], ld(dy, row + c0 + j), acc[j]);
+        }
+      }
+    }
+    const long long f0 = v * D + c0;
+    if (c0 < D) {
+      float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (nk.add_noise) {
+        if ((f0 & 3) == 0 && c0 + 3 < D && f0 >= nk.lo && f0 + 3 < nk.hi) {
+          const float4 q = noise_draw4(nk.impl, nk.base_g, nk.base, static_cast<uint64_t>(f0 >> 2));
+          z[0] = q.x;
+          z[1] = q.y;
+          z[2] = q.z;
+          z[3] = q.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (c0 + j < D && f0 + j >= nk.lo && f0 + j < nk.hi) z[j] = nk_draw(nk, static_cast<uint64_t>(f0 + j));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (c0 + j >= D) continue;
+        float r = acc[j] + nk.scale * z[j];
+        if (accumulate) r += out[f0 + j];
+        out[f0 + j] = r;
+      }
+    }
+    __syncthreads();  // beg / end of this row are read before the next row overwrites them
+  }
+}
+
+long long n_tchunks(int T_) { return (T_ + kVRows - 1) / kVRows; }
+int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+size_t vec_dp_work_bytes(int kind, int B, int T_, int D) {
+  const long long L = kind == FDP_VEC_LAYERNORM ? 2LL * D : D;
+  const long long n_chunks = (L + kVCols - 1) / kVCols;
+  return sizeof(float) * static_cast<size_t>(B * n_tchunks(T_) * L + B * L + B * n_chunks);
+}
+
+cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B, int T_, int D, float* work,
+                   double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
+                   cudaStream_t s) {
+  const long long L = kind == FDP_VEC_LAYERNORM ? 2LL * D : D;
+  const int n_tc = static_cast<int>(n_tchunks(T_));
+  const int n_chunks = static_cast<int>((L + kVCols - 1) / kVCols);
+  float* gpart = work;                                           // [B][n_tc][L]
+  float* g = gpart + static_cast<long long>(B) * n_tc * L;       // [B][L]
+  float* part = g + static_cast<long long>(B) * L;               // [B][n_chunks]
+  const dim3 g1((D + kVCols - 1) / kVCols, n_tc, B);
+#define FDP_VEC_ROWS(TY, K) \
+  k_vec_rows<TY, K><<<g1, kVCols, 0, s>>>(static_cast<const TY*>(dy), static_cast<const TY*>(xhat), T_, D, n_tc, gpart)
+  if (in_f32) {
+    if (kind == FDP_VEC_BIAS) FDP_VEC_ROWS(float, FDP_VEC_BIAS);
+    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(float, FDP_VEC_RMSNORM);
+    else FDP_VEC_ROWS(float, FDP_VEC_LAYERNORM);
+  } else {
+    if (kind == FDP_VEC_BIAS) FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_BIAS);
+    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_RMSNORM);
+    else FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_LAYERNORM);
+  }
+#undef FDP_VEC_ROWS
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_vec_reduce<<<dim3(n_chunks, B), kVCols, 0, s>>>(gpart, n_tc, static_cast<int>(L), g, part, n_chunks);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const long long blocks = (L + 255) / 256 < 148 ? (L + 255) / 256 : 148;
+  k_vec_finalize<<<static_cast<int>(blocks), 256, static_cast<size_t>(B) * sizeof(float), s>>>(
+      g, part, B, L, n_chunks, clip_c, clip_c * clip_c, inv_batch, out, norms_out, accumulate, nk);
+  return cudaGetLastError();
+}
+
+size_t emb_dp_work_bytes(int B, int T_, int D) {
+  const long long n_sc = (T_ + kESeg - 1) / kESeg, n_dc = (D + kVCols - 1) / kVCols;
+  return sizeof(uint64_t) * static_cast<size_t>(B) * T_ + sizeof(float) * static_cast<size_t>(B * n_sc * n_dc + B);
+}
+
+int emb_max_tokens() { return 16384; }
+
+cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, int T_, long long V, int D, void* work,
+                   double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
+                   cudaStream_t s) {
+  uint64_t* keys = static_cast<uint64_t*>(work);  // [B][T]
+  const int n_sc = (T_ + kESeg - 1) / kESeg, n_dc = (D + kVCols - 1) / kVCols;
+  float* part = reinterpret_cast<float*>(keys + static_cast<long long>(B) * T_);  // [B][n_sc][n_dc]
+  float* fac = part + static_cast<long long>(B) * n_sc * n_dc;                     // [B]
+  const int n2 = pow2_at_least(T_);
+  const size_t sort_smem = sizeof(uint64_t) * n2;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k_emb_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(uint64_t) * emb_max_tokens()));
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  k_emb_sort<<<B, 1024, sort_smem, s>>>(tokens, T_, V, n2, keys);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (in_f32)
+    k_emb_norms<float><<<dim3(n_dc, n_sc, B), kVCols, 0, s>>>(keys, static_cast<const float*>(dy), T_, D, n_sc, n_dc,
+                                                             part);
+  else
+    k_emb_norms<__nv_bfloat16><<<dim3(n_dc, n_sc, B), kVCols, 0, s>>>(
+        keys, static_cast<const __nv_bfloat16*>(dy), T_, D, n_sc, n_dc, part);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = reduce_norms_to_factors(part, B, n_sc * n_dc, clip_c, clip_c * clip_c, inv_batch, norms_out, fac, s)) !=
+      cudaSuccess)
+    return e;
+  const dim3 g3(static_cast<unsigned>((V + kEVRows - 1) / kEVRows), (D + kECols - 1) / kECols);
+  const size_t smem = static_cast<size_t>(B) * 4 * sizeof(int);
+  if (in_f32)
+    k_emb_out<float><<<g3, 256, smem, s>>>(keys, static_cast<const float*>(dy), fac, B, T_, V, D, out, accumulate, nk);
+  else
+    k_emb_out<__nv_bfloat16><<<g3, 256, smem, s>>>(keys, static_cast<const __nv_bfloat16*>(dy), fac, B, T_, V, D, out,
+                                                   accumulate, nk);
+  return cudaGetLastError();
+}
+
+}  // namespace fdp

@@ -353,96 +353,3 @@ cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int
 }
 
 }  // namespace fdp
-
-// ---------------------------------------------------------------- bias
-// DP gradient of a linear layer's bias under per-layer clipping: the per-sample
-// gradient is g_b[d] = sum_t dY[b, t, d] (B x D, tiny); clip with its own norm
-// at C, sum (or mean) over the batch, + sigma*C*noise keyed on the descriptor.
-// Two launches: per-(sample, column) sums + per-(sample, block) norm partials,
-// then one fixed-order reduce + clip + noise pass. Deterministic.
-namespace fdp {
-namespace {
-
-constexpr int kBiasCols = 256;  // columns per block of the first pass
-
-template <typename T>
-__global__ void __launch_bounds__(kBiasCols) k_bias_sums(const T* __restrict__ dy, int T_, int D, float* g,
-                                                         float* part, int n_chunks) {
-  const int b = blockIdx.y, chunk = blockIdx.x;
-  const int d = chunk * kBiasCols + threadIdx.x;
-  float s = 0.0f;
-  if (d < D) {
-    const T* p = dy + static_cast<long long>(b) * T_ * D + d;
-    for (int t = 0; t < T_; ++t) s += static_cast<float>(p[static_cast<long long>(t) * D]);
-    g[static_cast<long long>(b) * D + d] = s;
-  }
-  __shared__ float red[kBiasCols / 32];
-  float sq = s * s;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.0f;
-    for (int w = 0; w < kBiasCols / 32; ++w) t += red[w];
-    part[static_cast<long long>(b) * n_chunks + chunk] = t;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_bias_finalize(const float* g, const float* part, int B, int D, int n_chunks,
-                                                       double clip_c, double clip_c2, float inv_batch, float* out,
-                                                       float* norms_out, int add_noise, int impl, float scale,
-                                                       uint64_t base, uint64_t base_g, const long long* step_ptr,
-                                                       uint64_t seed_u, uint64_t layer_u, long long lo,
-                                                       long long hi) {
-  extern __shared__ float fac[];  // [B] clip factor x mean scale
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[static_cast<long long>(b) * n_chunks + c]);
-    const double cf = (s <= clip_c2) ? 1.0 : clip_c / sqrt(s);  // dpcore.py:41-47
-    fac[b] = static_cast<float>(cf) * inv_batch;
-    if (blockIdx.x == 0 && norms_out) norms_out[b] = static_cast<float>(s);
-  }
-  __syncthreads();
-  if (step_ptr) {
-    base = absorb3(seed_u, layer_u, static_cast<uint64_t>(*step_ptr));
-    base_g = base + kGamma;
-  }
-  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) {
-    float v = 0.0f;
-    for (int b = 0; b < B; ++b) v = fmaf(fac[b], g[static_cast<long long>(b) * D + d], v);
-    if (add_noise && d >= lo && d < hi) v += scale * noise_draw(impl, base_g, base, static_cast<uint64_t>(d));
-    out[d] = v;
-  }
-}
-
-}  // namespace
-
-cudaError_t bias_dp(const void* dy, int in_f32, int B, int T, int D, float* work, double clip_c, float inv_batch,
-                    float* out, float* norms_out, int add_noise, int impl, float scale, uint64_t base,
-                    uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u, long long lo,
-                    long long hi, cudaStream_t s) {
-  const int n_chunks = (D + kBiasCols - 1) / kBiasCols;
-  float* g = work;                                          // [B][D]
-  float* part = work + static_cast<long long>(B) * D;       // [B][n_chunks]
-  if (in_f32)
-    k_bias_sums<float><<<dim3(n_chunks, B), kBiasCols, 0, s>>>(static_cast<const float*>(dy), T, D, g, part,
-                                                               n_chunks);
-  else
-    k_bias_sums<__nv_bfloat16><<<dim3(n_chunks, B), kBiasCols, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), T, D,
-                                                                       g, part, n_chunks);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const int blocks = (D + 255) / 256 < 148 ? (D + 255) / 256 : 148;
-  k_bias_finalize<<<blocks, 256, static_cast<size_t>(B) * sizeof(float), s>>>(
-      g, part, B, D, n_chunks, clip_c, clip_c * clip_c, inv_batch, out, norms_out, add_noise, impl, scale, base, base_g,
-      step_ptr, seed_u, layer_u, lo, hi);
-  return cudaGetLastError();
-}
-
-size_t bias_dp_work_bytes(int B, int D) {
-  const int n_chunks = (D + kBiasCols - 1) / kBiasCols;
-  return sizeof(float) * (static_cast<size_t>(B) * D + static_cast<size_t>(B) * n_chunks);
-}
-
-}  // namespace fdp

@@ -132,6 +132,17 @@ class GroupedDPBackward:
         self.last_groups = 0
         for (add_noise, mean_batch, rank, world, impl), items in buckets.items():
             grads = None
+            # layers whose tiles cannot all be co-resident (e.g. a 50K-row LM head) take the
+            # per-layer two-phase kernels; the rest share the multi-layer launches
+            solo = [it for it in items if not _fits_group(it[1].shape, it[2].shape)]
+            items = [it for it in items if _fits_group(it[1].shape, it[2].shape)]
+            for m, x, dy, cfg, _, _ in solo:
+                gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,
+                          rank=rank, world=world, noise_impl=impl).grad_w.to(m.weight.dtype)
+                if m.weight.grad is None:
+                    m.weight.grad = gw
+                else:
+                    m.weight.grad += gw
             for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
                 chunk = items[lo:lo + 48]
                 try:
@@ -160,6 +171,21 @@ class GroupedDPBackward:
                         m.weight.grad = gw
                     else:
                         m.weight.grad += gw
+
+
+_FITS: dict = {}
+
+
+def _fits_group(x_shape, dy_shape) -> bool:
+    """Whether one layer's tiles fit the co-resident grid of the fused kernel (the
+    multi-layer launch's per-layer condition); cached per shape."""
+    key = (tuple(x_shape), tuple(dy_shape))
+    v = _FITS.get(key)
+    if v is None:
+        from .workflows import execution_plan
+        v = execution_plan(key[0], key[1], path="fused")["path"] == "fused"
+        _FITS[key] = v
+    return v
 
 
 class DPLinear(torch.nn.Module):

@@ -1,5 +1,10 @@
 """GPT-2 small with DP linear layers: the consumer of the hot path in a training step.
 
+``dp="full"`` makes every parameter DP: token and position
+embeddings are ``DPEmbedding``, the LayerNorms ``DPLayerNorm``, and the LM head
+an untied ``DPLinear`` over the vocabulary padded to a multiple of 64 (the
+non-DP baseline of that mode is built with ``tied=False`` and the same padding).
+
 Only the four linear layers of every block (attention c_attn / c_proj, MLP c_fc /
 c_proj) are the reference's hot path (per-layer DP weight gradients,
 workflows.py:340-421); they are ``DPLinear`` modules whose weight gradients
@@ -21,6 +26,7 @@ import torch
 import torch.nn.functional as F
 
 from .dplinear import DPLinear
+from .dpmodules import DPEmbedding, DPLayerNorm, _DPGroupModule
 
 
 @dataclass
@@ -40,11 +46,19 @@ def _linear(cin: int, cout: int, dp: bool, layer_id: int, clip_c: float, sigma: 
     return torch.nn.Linear(cin, cout, bias=True)
 
 
+def _layernorm(d: int, dp_full: bool, layer_id: int, clip_c: float, sigma: float, noise_impl: str):
+    if dp_full:
+        return DPLayerNorm(d, clip_c=clip_c, sigma=sigma, reduction="mean", layer_id=layer_id, noise_impl=noise_impl)
+    return torch.nn.LayerNorm(d)
+
+
 class Block(torch.nn.Module):
-    def __init__(self, cfg: GPT2Config, idx: int, dp: bool, clip_c: float, sigma: float, noise_impl: str):
+    def __init__(self, cfg: GPT2Config, idx: int, dp, clip_c: float, sigma: float, noise_impl: str):
         super().__init__()
-        self.ln1 = torch.nn.LayerNorm(cfg.d)
-        self.ln2 = torch.nn.LayerNorm(cfg.d)
+        full = dp == "full"
+        self.ln1 = _layernorm(cfg.d, full, 1002 + 2 * idx, clip_c, sigma, noise_impl)
+        self.ln2 = _layernorm(cfg.d, full, 1003 + 2 * idx, clip_c, sigma, noise_impl)
+        dp = bool(dp)
         base = 4 * idx
         self.c_attn = _linear(cfg.d, 3 * cfg.d, dp, base + 0, clip_c, sigma, noise_impl)
         self.attn_proj = _linear(cfg.d, cfg.d, dp, base + 1, clip_c, sigma, noise_impl)
@@ -65,14 +79,26 @@ class Block(torch.nn.Module):
 
 
 class GPT2(torch.nn.Module):
-    def __init__(self, cfg: GPT2Config, *, dp: bool = True, clip_c: float = 1.0, sigma: float = 1.0,
-                 noise_impl: str = "philox"):
+    def __init__(self, cfg: GPT2Config, *, dp=True, clip_c: float = 1.0, sigma: float = 1.0,
+                 noise_impl: str = "philox", tied: bool = True):
         super().__init__()
         self.cfg = cfg
-        self.wte = torch.nn.Embedding(cfg.vocab, cfg.d)
-        self.wpe = torch.nn.Embedding(cfg.seq, cfg.d)
+        full = dp == "full"
+        self.tied = tied and not full
+        if full:
+            self.wte = DPEmbedding(cfg.vocab, cfg.d, clip_c=clip_c, sigma=sigma, layer_id=1000, noise_impl=noise_impl)
+            self.wpe = DPEmbedding(cfg.seq, cfg.d, clip_c=clip_c, sigma=sigma, layer_id=1001, noise_impl=noise_impl)
+        else:
+            self.wte = torch.nn.Embedding(cfg.vocab, cfg.d)
+            self.wpe = torch.nn.Embedding(cfg.seq, cfg.d)
         self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl) for i in range(cfg.layers))
-        self.ln_f = torch.nn.LayerNorm(cfg.d)
+        self.ln_f = _layernorm(cfg.d, full, 1100, clip_c, sigma, noise_impl)
+        self.vocab_padded = (cfg.vocab + 63) // 64 * 64
+        self.lm_head = None
+        if not self.tied:
+            self.lm_head = (DPLinear(cfg.d, self.vocab_padded, bias=False, clip_c=clip_c, sigma=sigma,
+                                     reduction="mean", layer_id=4 * cfg.layers, noise_impl=noise_impl)
+                            if full else torch.nn.Linear(cfg.d, self.vocab_padded, bias=False))
         self.dp = dp
         for p in self.parameters():
             if p.dim() >= 2:
@@ -81,12 +107,23 @@ class GPT2(torch.nn.Module):
     def dp_layers(self):
         return [m for m in self.modules() if isinstance(m, DPLinear)]
 
+    def dp_modules(self):
+        """Every module with a per-layer DP gradient (set_step each step)."""
+        return [m for m in self.modules() if isinstance(m, (DPLinear, _DPGroupModule))]
+
     def forward(self, idx):
         B, T = idx.shape
-        x = self.wte(idx) + self.wpe(torch.arange(T, device=idx.device))[None]
+        pos = torch.arange(T, device=idx.device)
+        if self.dp == "full":  # per-sample position ids: the sample dimension stays first
+            x = self.wte(idx) + self.wpe(pos.expand(B, T))
+        else:
+            x = self.wte(idx) + self.wpe(pos)[None]
         for blk in self.blocks:
             x = blk(x)
-        return F.linear(self.ln_f(x), self.wte.weight)  # tied LM head
+        h = self.ln_f(x)
+        if self.tied:
+            return F.linear(h, self.wte.weight)  # tied LM head
+        return self.lm_head(h)[..., :self.cfg.vocab]
 
     def loss(self, idx, targets):
         with torch.autocast("cuda", dtype=torch.bfloat16):
