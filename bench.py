@@ -501,6 +501,16 @@ def main():
                      "dp_pct_of_non_dp": 100.0 * dp_t["tokens_per_s"] / nd_t["tokens_per_s"],
                      "dp_scope": "per-layer clipped + noised weight gradients of the 48 linear layers (+ their "
                                  "biases); embeddings / LayerNorm not DP (as in the reference, SPEC.md:8)"}
+            # every parameter DP: embeddings, LayerNorms, untied LM head too;
+            # the non-DP baseline of this line is the same untied model with nn modules
+            fargs = argparse.Namespace(batch=B, seq=T, steps=10, warmup=3, full=True)
+            nd_f = tg.run(False, fargs)
+            dp_f = tg.run("full", fargs)
+            train["full_dp"] = {"dp_tokens_per_s": dp_f["tokens_per_s"], "non_dp_tokens_per_s": nd_f["tokens_per_s"],
+                                "dp_pct_of_non_dp": 100.0 * dp_f["tokens_per_s"] / nd_f["tokens_per_s"],
+                                "dp_modules": dp_f["dp_modules"],
+                                "dp_scope": "every parameter: 48 linear weights + biases, 25 LayerNorms, token and "
+                                            "position embeddings, untied LM head (vocab padded to 50304)"}
         except Exception as e:  # noqa: BLE001
             train = {"error": repr(e)[:300]}
 

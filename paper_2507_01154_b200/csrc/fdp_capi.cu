@@ -1169,6 +1169,9 @@ int fdp_embedding_workspace_bytes(const fdp_desc* d, size_t* bytes) {
     return fail(FDP_ERR_SHAPE, "embedding gradients take T <= %d positions per sample, got %lld", fdp::emb_max_tokens(),
                 (long long)d->T);
   if (d->P >= (1ll << 31)) return fail(FDP_ERR_SHAPE, "vocabulary too large");
+  if (d->B > fdp::emb_max_batch())
+    return fail(FDP_ERR_SHAPE, "embedding gradients take B <= %d samples per call, got %lld", fdp::emb_max_batch(),
+                (long long)d->B);
   *bytes = fdp::emb_dp_work_bytes(static_cast<int>(d->B), static_cast<int>(d->T), static_cast<int>(d->D));
   return FDP_OK;
 }

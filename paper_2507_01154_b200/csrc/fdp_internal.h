@@ -221,6 +221,7 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
                    cudaStream_t s);
 size_t emb_dp_work_bytes(int B, int T, int D);
 int emb_max_tokens();
+int emb_max_batch();
 cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, int T, long long V, int D, void* work,
                    double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
                    cudaStream_t s);

@@ -160,32 +160,72 @@ __global__ void __launch_bounds__(1024) k_emb_sort(const long long* __restrict__
 }
 
 // norm^2 partial of sample b over the runs of equal tokens that START in sorted
-// positions [sc*kESeg, (sc+1)*kESeg), columns [dc*kVCols, ...)
+// positions [sc*kESeg, (sc+1)*kESeg), columns [dc*kVCols, ...). The block's keys
+// (plus the tail of its last run) are staged in shared memory first, so the dY
+// row loads of the run sums are independent and pipeline.
+constexpr int kEStage = 4 * kESeg;  // staged keys: own positions + the spill of the last run
 template <typename T>
 __global__ void __launch_bounds__(kVCols) k_emb_norms(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
                                                       int T_, int D, int n_sc, int n_dc, float* __restrict__ part) {
   const int dc = blockIdx.x, sc = blockIdx.y, b = blockIdx.z;
   const int col = dc * kVCols + threadIdx.x;
   const uint64_t* K = keys + static_cast<long long>(b) * T_;
-  const int k1 = min(T_, (sc + 1) * kESeg);
-  int k = sc * kESeg;
-  if (k > 0) {
-    const uint64_t prev = K[k - 1] >> 32;
-    while (k < k1 && K[k] != kNoKey && (K[k] >> 32) == prev) ++k;  // continuation of a run owned by the previous block
+  __shared__ uint64_t sk[kEStage + 1];
+  __shared__ int s_range[2];
+  __shared__ float red[kVCols / 32];
+  const int k0 = sc * kESeg, k1 = min(T_, k0 + kESeg);
+  if (threadIdx.x == 0) {
+    int k = k0;
+    if (k > 0) {  // skip the continuation of a run owned by the previous block
+      const uint64_t prev = K[k - 1] >> 32;
+      while (k < k1 && K[k] != kNoKey && (K[k] >> 32) == prev) ++k;
+    }
+    int e = k1;  // finish the last run this block starts
+    if (e > k && e < T_ && K[e - 1] != kNoKey) {
+      const uint64_t last = K[e - 1] >> 32;
+      while (e < T_ && K[e] != kNoKey && (K[e] >> 32) == last) ++e;
+    }
+    while (e > k && K[e - 1] == kNoKey) --e;  // invalid tokens sort last: never summed
+    s_range[0] = k;
+    s_range[1] = e;
   }
+  __syncthreads();
+  const int kb = s_range[0], ke = s_range[1];
   float sq = 0.0f;
   const long long rbase = static_cast<long long>(b) * T_ * D + col;
-  while (k < k1 && K[k] != kNoKey) {
-    const uint64_t tk = K[k] >> 32;
+  for (int c0 = kb; c0 < ke; c0 += kEStage) {  // usually one stage
+    const int c1 = min(ke, c0 + kEStage);
+    for (int i = threadIdx.x; i <= c1 - c0; i += blockDim.x)
+      sk[i] = (c0 + i < ke) ? K[c0 + i] : kNoKey;  // sk[c1 - c0]: sentinel closing the last run
+    __syncthreads();
+    // sk[c1 - c0] is the next key (or kNoKey at the end): a token change closes a run
+    const int n = c1 - c0;
     float acc = 0.0f;
-    do {
-      const long long t = static_cast<long long>(K[k] & 0xffffffffull);
-      if (col < D) acc += ld(dy, rbase + t * D);
-      ++k;
-    } while (k < T_ && K[k] != kNoKey && (K[k] >> 32) == tk);
-    sq = fmaf(acc, acc, sq);
+    if (col < D) {
+#pragma unroll 8
+      for (int k = 0; k < n; ++k) {
+        acc += ld(dy, rbase + static_cast<long long>(sk[k] & 0xffffffffull) * D);
+        if ((sk[k + 1] >> 32) != (sk[k] >> 32)) {
+          sq = fmaf(acc, acc, sq);
+          acc = 0.0f;
+        }
+      }
+    }
+    const bool open = c1 < ke && (sk[n] >> 32) == (sk[n - 1] >> 32);
+    if (open && col < D) {  // a run longer than the stage: finish it from global memory
+      const uint64_t tk = sk[n - 1] >> 32;
+      for (int k = c1; k < ke && (K[k] >> 32) == tk; ++k)
+        acc += ld(dy, rbase + static_cast<long long>(K[k] & 0xffffffffull) * D);
+      sq = fmaf(acc, acc, sq);
+    }
+    __syncthreads();
+    if (c1 < ke) {  // resume after the run that crossed the boundary
+      int k = c1;
+      const uint64_t tk = K[c1 - 1] >> 32;
+      while (k < ke && (K[k] >> 32) == tk) ++k;
+      c0 = k - kEStage;
+    }
   }
-  __shared__ float red[kVCols / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
@@ -197,62 +237,64 @@ __global__ void __launch_bounds__(kVCols) k_emb_norms(const uint64_t* __restrict
   }
 }
 
-// out[v][c] (+)= sum_b c_b sum_{t: tok_bt = v} dY[b,t,c] + sigma C N(v*D + c), every row v
+// out[v][c] (+)= sum_b c_b sum_{t: tok_bt = v} dY[b,t,c] + sigma C N(v*D + c), every row v.
+// One pre-pass per block finds each sample's sorted range of every row of the
+// block's kEVRows vocabulary rows (one barrier); the row loop then runs barrier-
+// free: untouched rows are a pure noise write, touched rows sum their runs.
 template <typename T>
 __global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
                                                  const float* __restrict__ factors, int B, int T_, long long V, int D,
                                                  float* out, int accumulate, NoiseKey nk) {
-  extern __shared__ int sm[];  // ptr[B], beg[B], end[B]; fac[B] (float)
-  int* ptr = sm;
-  int* beg = sm + B;
-  int* end = sm + 2 * B;
-  float* fac = reinterpret_cast<float*>(sm + 3 * B);
+  extern __shared__ int sm[];  // bound[B][kEVRows + 1]; fac[B]; touched[kEVRows]
+  int* bound = sm;
+  float* fac = reinterpret_cast<float*>(sm + B * (kEVRows + 1));
+  int* touched = reinterpret_cast<int*>(fac + B);
   const long long v0 = static_cast<long long>(blockIdx.x) * kEVRows;
-  const long long v1 = min(V, v0 + kEVRows);
-  const int c0 = blockIdx.y * kECols + 4 * threadIdx.x;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {  // first sorted position with token >= v0
+  const int nrows = static_cast<int>(min(static_cast<long long>(kEVRows), V - v0));
+  for (int r = threadIdx.x; r < kEVRows; r += blockDim.x) touched[r] = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
     const uint64_t* K = keys + static_cast<long long>(b) * T_;
     const uint64_t want = static_cast<uint64_t>(v0) << 32;
-    int lo = 0, hi = T_;
+    int lo = 0, hi = T_;  // first sorted position with token >= v0
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (K[mid] < want) lo = mid + 1;
       else hi = mid;
     }
-    ptr[b] = lo;
+    int* bd = bound + b * (kEVRows + 1);
+    int e = lo;
+    for (int r = 0; r < nrows; ++r) {  // bd[r] .. bd[r+1]: the sample's positions of row v0 + r
+      bd[r] = e;
+      while (e < T_ && K[e] != kNoKey && static_cast<long long>(K[e] >> 32) == v0 + r) ++e;
+      if (e > bd[r]) touched[r] = 1;
+    }
+    bd[nrows] = e;
     fac[b] = factors[b];
   }
   nk_resolve(nk);
   __syncthreads();
-  for (long long v = v0; v < v1; ++v) {
-    int touched = 0;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-      const uint64_t* K = keys + static_cast<long long>(b) * T_;
-      int e = ptr[b];
-      while (e < T_ && K[e] != kNoKey && static_cast<long long>(K[e] >> 32) == v) ++e;
-      beg[b] = ptr[b];
-      end[b] = e;
-      ptr[b] = e;
-      touched |= e > beg[b];
-    }
-    touched = __syncthreads_or(touched);
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (touched) {
-      for (int b = 0; b < B; ++b) {
-        const uint64_t* K = keys + static_cast<long long>(b) * T_;
-        for (int k = beg[b]; k < end[b]; ++k) {
-          const long long row = (static_cast<long long>(b) * T_ + static_cast<long long>(K[k] & 0xffffffffull)) * D;
+  const bool vec = (D & 3) == 0;
+  for (int c0 = blockIdx.y * kECols + 4 * threadIdx.x; c0 < D && c0 < (blockIdx.y + 1) * kECols; c0 += 4 * 256) {
+    for (int r = 0; r < nrows; ++r) {
+      const long long v = v0 + r;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (touched[r]) {
+        for (int b = 0; b < B; ++b) {
+          const int* bd = bound + b * (kEVRows + 1);
+          const uint64_t* K = keys + static_cast<long long>(b) * T_;
+          for (int k = bd[r]; k < bd[r + 1]; ++k) {
+            const long long row = (static_cast<long long>(b) * T_ + static_cast<long long>(K[k] & 0xffffffffull)) * D;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (c0 + j < D) acc[j] = fmaf(fac[b], ld(dy, row + c0 + j), acc[j]);
+            for (int j = 0; j < 4; ++j)
+              if (c0 + j < D) acc[j] = fmaf(fac[b], ld(dy, row + c0 + j), acc[j]);
+          }
         }
       }
-    }
-    const long long f0 = v * D + c0;
-    if (c0 < D) {
+      const long long f0 = v * D + c0;
       float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (nk.add_noise) {
-        if ((f0 & 3) == 0 && c0 + 3 < D && f0 >= nk.lo && f0 + 3 < nk.hi) {
+        if (vec && f0 >= nk.lo && f0 + 3 < nk.hi) {
           const float4 q = noise_draw4(nk.impl, nk.base_g, nk.base, static_cast<uint64_t>(f0 >> 2));
           z[0] = q.x;
           z[1] = q.y;
@@ -264,18 +306,32 @@ __global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ ke
             if (c0 + j < D && f0 + j >= nk.lo && f0 + j < nk.hi) z[j] = nk_draw(nk, static_cast<uint64_t>(f0 + j));
         }
       }
+      if (vec) {
+        float4 o = make_float4(acc[0] + nk.scale * z[0], acc[1] + nk.scale * z[1], acc[2] + nk.scale * z[2],
+                               acc[3] + nk.scale * z[3]);
+        float4* po = reinterpret_cast<float4*>(out + f0);
+        if (accumulate) {
+          const float4 p = *po;
+          o.x += p.x;
+          o.y += p.y;
+          o.z += p.z;
+          o.w += p.w;
+        }
+        __stcs(po, o);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (c0 + j >= D) continue;
-        float r = acc[j] + nk.scale * z[j];
-        if (accumulate) r += out[f0 + j];
-        out[f0 + j] = r;
+        for (int j = 0; j < 4; ++j) {
+          if (c0 + j >= D) continue;
+          float r2 = acc[j] + nk.scale * z[j];
+          if (accumulate) r2 += out[f0 + j];
+          out[f0 + j] = r2;
+        }
       }
     }
-    __syncthreads();  // beg / end of this row are read before the next row overwrites them
   }
 }
 
+size_t emb_out_smem(int B) { return sizeof(int) * (static_cast<size_t>(B) * (kEVRows + 2) + kEVRows); }
 long long n_tchunks(int T_) { return (T_ + kVRows - 1) / kVRows; }
 int pow2_at_least(int n) {
   int p = 1;
@@ -329,6 +385,7 @@ size_t emb_dp_work_bytes(int B, int T_, int D) {
 }
 
 int emb_max_tokens() { return 16384; }
+int emb_max_batch() { return 1024; }
 
 cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, int T_, long long V, int D, void* work,
                    double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
@@ -360,7 +417,16 @@ cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, i
       cudaSuccess)
     return e;
   const dim3 g3(static_cast<unsigned>((V + kEVRows - 1) / kEVRows), (D + kECols - 1) / kECols);
-  const size_t smem = static_cast<size_t>(B) * 4 * sizeof(int);
+  const size_t smem = emb_out_smem(B);
+  static bool out_attr = false;
+  if (!out_attr) {
+    if ((e = cudaFuncSetAttribute(k_emb_out<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_emb_out<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess)
+      return e;
+    out_attr = true;
+  }
   if (in_f32)
     k_emb_out<float><<<g3, 256, smem, s>>>(keys, static_cast<const float*>(dy), fac, B, T_, V, D, out, accumulate, nk);
   else

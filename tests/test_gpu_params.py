@@ -96,10 +96,11 @@ def _tokens(B, T, V, seed, bad=False):
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("B,T,V,D", [(4, 100, 37, 64), (3, 1500, 500, 70), (1, 1, 5, 8), (8, 257, 1000, 256),
-                                     (2, 64, 3, 1030)])
+                                     (2, 64, 3, 1030), (2, 2000, 2, 40)])
 def test_embedding_against_oracle(dtype, B, T, V, D):
     """Repeated tokens (small vocabularies), ragged d (per-element noise), T > 1024
-    (2048-key sort), single token, multiple column chunks."""
+    (2048-key sort), single token, multiple column chunks, runs of one token longer
+    than a norm block's key stage (V = 2, T = 2000)."""
     tok = _tokens(B, T, V, seed=T + V, bad=True)
     g = torch.Generator().manual_seed(D)
     dy = (torch.randn(B, T, D, generator=g) * 0.1).to(dtype)
