@@ -193,21 +193,46 @@ int choose_norm_phase(const fdp_desc* d) {
 struct GhostShape {
   bool pair;
   int nT, n_pairs, parts;  // parts: norm partials per sample
+  int split, split_x;      // K slices of the larger operand per tile pair
 };
 GhostShape ghost_shape(const fdp_desc* d, int sms) {
   const long long nT2 = (d->T + 255) / 256, np2 = nT2 * (nT2 + 1) / 2;
   const long long nT1 = (d->T + 127) / 128, np1 = nT1 * (nT1 + 1) / 2;
   const long long clusters = sms / 2 > 0 ? sms / 2 : 1;
-  const long long waves2 = (d->B * np2 + clusters - 1) / clusters;
-  const long long waves1 = (d->B * np1 + sms - 1) / (sms > 0 ? sms : 1);
-  int forced = env_int("FDP_GHOST_PAIR", -1);
-  // a wave of 256-row pair items takes ~1.2x a wave of 128-row single-CTA items (measured, K = P + D = 8192)
-  const bool pair = forced >= 0 ? forced != 0 : 6 * waves2 < 5 * waves1;
-  GhostShape g;
-  g.pair = pair;
-  g.nT = static_cast<int>(pair ? nT2 : nT1);
-  g.n_pairs = static_cast<int>(pair ? np2 : np1);
-  g.parts = pair ? 2 * g.n_pairs : g.n_pairs;
+  const long long ctas = sms > 0 ? sms : 1;
+  const long long nkx = (d->P + 63) / 64, nky = (d->D + 63) / 64;
+  const long long big = std::max(nkx, nky), small = std::min(nkx, nky);
+  const int forced = env_int("FDP_GHOST_PAIR", -1);
+  const int forced_split = env_int("FDP_GHOST_SPLIT", 0);
+  // Modelled time in single-CTA k-block units: waves x per-item k-blocks; a pair
+  // k-block (256x256 tile on 2 SMs) takes ~1.1-1.2x a single-CTA one (128x128 on
+  // 1 SM). Slicing the larger operand's K range S ways multiplies the items by S
+  // and recomputes the smaller Gram per slice (tools/ghost_split_sweep.py: LM head
+  // 768 -> 50304 at B=8 974 -> 924 us per layer, Llama 4096 -> 32000 at B=1 665 -> 610).
+  double best = 1e300;
+  GhostShape g{};
+  for (int pair = 1; pair >= 0; --pair) {
+    if (forced >= 0 && forced != pair) continue;
+    const long long items = d->B * (pair ? np2 : np1), slots = pair ? clusters : ctas;
+    for (long long S = 1; S <= 16 && S <= big; ++S) {
+      if (forced_split > 0 && S != forced_split) continue;
+      const long long waves = (items * S + slots - 1) / slots;
+      const double t = static_cast<double>(waves) * static_cast<double>(small + (big + S - 1) / S) * (pair ? 1.1 : 1.0);
+      if (t < best * 0.98) {
+        best = t;
+        g.pair = pair != 0;
+        g.split = static_cast<int>(S);
+      }
+    }
+  }
+  if (g.split == 0) {  // forced split larger than the K range: no slicing
+    g.pair = forced != 0;
+    g.split = 1;
+  }
+  g.split_x = nkx >= nky ? 1 : 0;
+  g.nT = static_cast<int>(g.pair ? nT2 : nT1);
+  g.n_pairs = static_cast<int>(g.pair ? np2 : np1);
+  g.parts = (g.pair ? 2 : 1) * g.n_pairs * g.split;
   return g;
 }
 
@@ -732,7 +757,9 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       g.D = p.D;
       g.nT = gs.nT;
       g.n_pairs = gs.n_pairs;
-      g.n_items = g.n_pairs * g.B;
+      g.split = gs.split;
+      g.split_x = gs.split_x;
+      g.n_items = g.n_pairs * g.B * g.split;
       g.part = p.ws_part;
       g.err = p.ws_ctrl + 1;
       g.budget_ns = p.budget_ns;

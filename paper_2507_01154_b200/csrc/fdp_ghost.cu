@@ -34,6 +34,16 @@ constexpr uint32_t kGIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<u
 // SBO = 1024 B between 8-row groups; LBO unused (one 64-element atom in K).
 __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return make_sdesc_sw128(saddr, 16, 1024); }
 
+// Work item wi = ((b * n_pairs + pair) * split + s): sample b, Gram tile pair
+// (i, j), K slice s of the split operand. The dot <Gx, Gy> is linear in each
+// Gram, so a slice of the larger operand's K range paired with the full Gram of
+// the smaller one gives a partial that sums to the sample's norm^2 (the smaller
+// Gram is recomputed per slice: cheap when P and D differ a lot, e.g. an LM head).
+struct GItem {
+  int b, i, j, pair, s;
+  int kx0, nx, ky0, ny;  // k-block ranges of the X and dY operands
+};
+
 __device__ __forceinline__ void decode_item(int wi, int n_pairs, int nT, int& b, int& i, int& j) {
   b = wi / n_pairs;
   int r = wi % n_pairs;
@@ -44,6 +54,26 @@ __device__ __forceinline__ void decode_item(int wi, int n_pairs, int nT, int& b,
     ++i;
   }
   j = i + r;
+}
+
+__device__ __forceinline__ GItem decode_split(int wi, const GhostParams& p, int nkx, int nky) {
+  GItem it;
+  it.s = wi % p.split;
+  const int wp = wi / p.split;
+  decode_item(wp, p.n_pairs, p.nT, it.b, it.i, it.j);
+  it.pair = wp % p.n_pairs;
+  it.kx0 = 0;
+  it.nx = nkx;
+  it.ky0 = 0;
+  it.ny = nky;
+  if (p.split_x) {
+    it.kx0 = it.s * nkx / p.split;
+    it.nx = (it.s + 1) * nkx / p.split - it.kx0;
+  } else {
+    it.ky0 = it.s * nky / p.split;
+    it.ny = (it.s + 1) * nky / p.split - it.ky0;
+  }
+  return it;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -86,12 +116,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
-        int b, i, j;
-        decode_item(wi, p.n_pairs, p.nT, b, i, j);
-        for (int k = 0; k < nkx + nky; ++k) {
-          const bool isx = k < nkx;
+        const GItem it = decode_split(wi, p, nkx, nky);
+        const int i = it.i, j = it.j, b = it.b;
+        for (int k = 0; k < it.nx + it.ny; ++k) {
+          const bool isx = k < it.nx;
           const CUtensorMap* m = isx ? &tm_x : &tm_dy;
-          const int kk = (isx ? k : k - nkx) * kBK;
+          const int kk = (isx ? it.kx0 + k : it.ky0 + k - it.nx) * kBK;
           mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x301);
           uint8_t* sa = smem + stage * kGStageBytes;
           mbar_arrive_expect_tx(&full[stage], i == j ? kGTileBytes : kGStageBytes);
@@ -105,12 +135,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
       for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
-        int b, i, j;
-        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        const GItem it = decode_split(wi, p, nkx, nky);
+        const int i = it.i, j = it.j;
         mbar_wait(&tempty[buf], tphase ^ 1, err, p.budget_ns, 0x302);
         tc_fence_after();
-        for (int k = 0; k < nkx + nky; ++k) {
-          const bool isx = k < nkx;
+        for (int k = 0; k < it.nx + it.ny; ++k) {
+          const bool isx = k < it.nx;
           const uint32_t dtm = tmem_base + buf * 256 + (isx ? 0 : 128);
           mbar_wait(&full[stage], phase, err, p.budget_ns, 0x303);
           tc_fence_after();
@@ -119,7 +149,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int kq = 0; kq < kBK / 16; ++kq)
             tc_mma_f16(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kGIdesc,
-                       (k == 0 || k == nkx) && kq == 0 ? 0u : 1u);
+                       (k == 0 || k == it.nx) && kq == 0 ? 0u : 1u);
           tc_commit(&empty[stage]);
           if (++stage == kGStages) { stage = 0; phase ^= 1; }
         }
@@ -132,8 +162,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
     uint32_t buf = 0, tphase = 0;
     for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
-      int b, i, j;
-      decode_item(wi, p.n_pairs, p.nT, b, i, j);
+      const GItem it = decode_split(wi, p, nkx, nky);
+      const int i = it.i, j = it.j, b = it.b;
       mbar_wait(&tfull[buf], tphase, err, p.budget_ns, 0x304);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + half * 64;
@@ -159,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float s = 0.0f;
 #pragma unroll
         for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-        p.part[static_cast<long long>(b) * p.n_pairs + (wi % p.n_pairs)] = (i == j ? 1.0f : 2.0f) * s;
+        p.part[(static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s] = (i == j ? 1.0f : 2.0f) * s;
       }
       named_bar_sync(1, 32 * kEpiWarps);
     }
@@ -232,13 +262,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (int wi = cid; wi < p.n_items; wi += n_clusters) {
-        int b, i, j;
-        decode_item(wi, p.n_pairs, p.nT, b, i, j);
+        const GItem it = decode_split(wi, p, nkx, nky);
+        const int i = it.i, j = it.j, b = it.b;
         const int ra = i * kPT + rank * kPHalf, rb = j * kPT + rank * kPHalf;
-        for (int k = 0; k < nkx + nky; ++k) {
-          const bool isx = k < nkx;
+        for (int k = 0; k < it.nx + it.ny; ++k) {
+          const bool isx = k < it.nx;
           const CUtensorMap* m = isx ? &tm_x : &tm_dy;
-          const int kk = (isx ? k : k - nkx) * kBK;
+          const int kk = (isx ? it.kx0 + k : it.ky0 + k - it.nx) * kBK;
           mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x311);
           uint8_t* sa = smem + stage * kPStageBytes;
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (i == j ? kPTileBytes : kPStageBytes));
@@ -252,11 +282,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, tph = 0;
       for (int wi = cid; wi < p.n_items; wi += n_clusters) {
-        int b, i, j;
-        decode_item(wi, p.n_pairs, p.nT, b, i, j);
-        for (int k = 0; k < nkx + nky; ++k) {
-          const bool isx = k < nkx;
-          if (k == 0 || k == nkx) {  // Gx / Gy accumulator of the previous item has been read out
+        const GItem it = decode_split(wi, p, nkx, nky);
+        const int i = it.i, j = it.j;
+        for (int k = 0; k < it.nx + it.ny; ++k) {
+          const bool isx = k < it.nx;
+          if (k == 0 || k == it.nx) {  // Gx / Gy accumulator of the previous item has been read out
             mbar_wait(&tempty[isx ? 0 : 1], tph ^ 1, err, p.budget_ns, 0x312);
             tc_fence_after();
           }
@@ -268,10 +298,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int kq = 0; kq < kBK / 16; ++kq)
             tc_mma_f16_pair(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kPIdesc,
-                            (k == 0 || k == nkx) && kq == 0 ? 0u : 1u);
+                            (k == 0 || k == it.nx) && kq == 0 ? 0u : 1u);
           tc_commit_pair(&empty[stage]);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
-          if (k == nkx - 1) tc_commit_pair(&tfull[0]);
+          if (k == it.nx - 1) tc_commit_pair(&tfull[0]);
         }
         tc_commit_pair(&tfull[1]);
         tph ^= 1;
@@ -282,8 +312,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
     uint32_t tph = 0;
     for (int wi = cid; wi < p.n_items; wi += n_clusters) {
-      int b, i, j;
-      decode_item(wi, p.n_pairs, p.nT, b, i, j);
+      const GItem it = decode_split(wi, p, nkx, nky);
+      const int i = it.i, j = it.j, b = it.b;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
       float gx[128];
       mbar_wait(&tfull[0], tph, err, p.budget_ns, 0x314);
@@ -322,7 +352,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float s = 0.0f;
 #pragma unroll
         for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-        p.part[(static_cast<long long>(b) * p.n_pairs + (wi % p.n_pairs)) * 2 + rank] = (i == j ? 1.0f : 2.0f) * s;
+        p.part[((static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s) * 2 + rank] =
+            (i == j ? 1.0f : 2.0f) * s;
       }
       named_bar_sync(1, 32 * kEpiWarps);
     }

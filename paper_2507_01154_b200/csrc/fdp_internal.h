@@ -132,8 +132,10 @@ struct GhostParams {
   int B, T, P, D;
   int nT;        // ceil(T / 128)
   int n_pairs;   // nT (nT + 1) / 2 upper-triangle Gram tile pairs per sample
-  int n_items;   // B * n_pairs
-  float* part;   // [B][n_pairs] weighted partials
+  int n_items;   // B * n_pairs * split
+  int split;     // K slices of the larger operand per tile pair (1 = none)
+  int split_x;   // 1: slice X's K (P >= D), 0: slice dY's K
+  float* part;   // [B][n_pairs][split] weighted partials (x2 for the CTA-pair kernel)
   unsigned* err;
   unsigned long long budget_ns;
 };

@@ -469,6 +469,22 @@ def test_ghost_variants_against_oracle(pair, B, T, P, D, monkeypatch):
     check(r, x, dy, cfg, BF16_TOL)
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("split", ["2", "3", "7"])
+@pytest.mark.parametrize("B,T,P,D", [(2, 300, 256, 1600), (3, 130, 1344, 192), (1, 512, 448, 448)])
+def test_ghost_k_split_against_oracle(pair, split, B, T, P, D, monkeypatch):
+    """Ghost norms with the larger operand's K range sliced (the smaller Gram
+    recomputed per slice; partials sum by linearity of <Gx, Gy>): slicing dY
+    (P < D), X (P > D), equal extents, slice counts that do not divide the K
+    blocks, single-CTA and CTA-pair kernels."""
+    monkeypatch.setenv("FDP_GHOST_PAIR", pair)
+    monkeypatch.setenv("FDP_GHOST_SPLIT", split)
+    x, dy = randn(B, T, P, D, seed=T + P + int(split))
+    cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=3, layer_id=5, step=2)
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase="ghost")
+    check(r, x, dy, cfg, BF16_TOL)
+
+
 @pytest.mark.parametrize("epi", ["0", "1"])
 @pytest.mark.parametrize("rank,world", [(0, 1), (1, 2)])
 def test_reweight_noise_placement(epi, rank, world, monkeypatch):
