@@ -182,8 +182,12 @@ def _fits_group(x_shape, dy_shape) -> bool:
     key = (tuple(x_shape), tuple(dy_shape))
     v = _FITS.get(key)
     if v is None:
+        from .errors import UsageError
         from .workflows import execution_plan
-        v = execution_plan(key[0], key[1], path="fused")["path"] == "fused"
+        try:
+            v = execution_plan(key[0], key[1], path="fused")["path"] == "fused"
+        except UsageError:  # no tensor-core path for this shape (e.g. D % 8 != 0): generic per-layer kernels
+            v = False
         _FITS[key] = v
     return v
 
