@@ -485,9 +485,10 @@ fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common&
   p.reweight = reweight ? 1 : 0;
   p.accumulate = d->accumulate;
   p.add_noise = reweight ? c.add_noise : 0;
-  // epilogue-drawn Philox noise for tiles held whole: measured faster with <= 2
-  // samples per tile (5120x13824, B=2: 496 -> 433 us), slower from 4 up
-  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", d->B <= 2 ? 1 : 0)) ? 1 : 0;
+  // epilogue-drawn Philox noise for tiles held whole (accumulator initial value, plain
+  // TMA store) instead of a noise-warp pre-fill + TMA reduce-add: 5120x13824 at B=2
+  // 496 -> 433 us; at B=4 / 8 1.6-2 % faster, neutral on 4096^2 (tools/ab_layer.py)
+  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", 1)) ? 1 : 0;
   p.noise_impl = d->noise_impl;
   p.noise_scale = c.noise_scale;
   p.key_base = c.key_base;
@@ -554,9 +555,8 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
   p.deterministic = (d->flags & FDP_FLAG_DETERMINISTIC) ? 1 : 0;
   p.poll_ns = env_int("FDP_POLL_NS", 0);
-  // epilogue-drawn noise for the reweight pass: measured faster with <= 2 samples per
-  // tile (5120x13824, B=2: 496 -> 433 us), slower from 4 up (the SFU burst per tile)
-  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", d->B <= 2 ? 1 : 0)) ? 1 : 0;
+  // epilogue-drawn noise for the reweight pass (see stream_params)
+  p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", 1)) ? 1 : 0;
   p.pub_mode = env_int("FDP_PUB_MODE", 1);
   p.poll_mode = env_int("FDP_POLL_MODE", 0);
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
