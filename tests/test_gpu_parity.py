@@ -487,12 +487,14 @@ def test_ghost_k_split_against_oracle(pair, split, B, T, P, D, monkeypatch):
 
 @pytest.mark.parametrize("epi", ["0", "1"])
 @pytest.mark.parametrize("rank,world", [(0, 1), (1, 2)])
-def test_reweight_noise_placement(epi, rank, world, monkeypatch):
+@pytest.mark.parametrize("B", [2, 5])
+def test_reweight_noise_placement(epi, rank, world, B, monkeypatch):
     """Two-phase reweight pass with Philox noise drawn in the epilogue (accumulator
     initial value, plain TMA store) or pre-filled by the noise warps (TMA
-    reduce-add): out(sigma) - out(0) is exactly the rank's slice of sigma*C*noise."""
+    reduce-add): out(sigma) - out(0) is exactly the rank's slice of sigma*C*noise
+    (B = 5: stream-K splits some tiles over clusters)."""
     monkeypatch.setenv("FDP_EPI_NOISE", epi)
-    B, T, P, D = 2, 256, 1024, 768
+    T, P, D = 256, 1024, 768
     x, dy = randn(B, T, P, D, seed=31, scale_dy=1e-2)
     cfg0 = fdp.DPConfig(1.0, 0.0, "mean", seed=5, layer_id=9, step=3)
     cfg1 = fdp.DPConfig(1.0, 1.5, "mean", seed=5, layer_id=9, step=3)
