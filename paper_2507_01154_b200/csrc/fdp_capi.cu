@@ -145,6 +145,8 @@ int validate(const fdp_desc* d, int32_t kind) {
 }
 
 struct Plan {
+  int stream_mc = 1;     // stream-K kernel cluster layout: 2 = two pairs per 4-CTA cluster (X multicast)
+  int stream_tiles = 0;  // per-CTA tile slots of the stream kernel
   int path = FDP_PATH_SIMT;
   int norm_phase = FDP_NORMS_RECOMPUTE;
   int bn = 128;
@@ -374,9 +376,21 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     else pl.launches = 3;
   }
 
+  // stream-K kernel layout (two-phase reweight, B = 1 GEMM, non-DP): two CTA pairs per
+  // 4-CTA cluster with the X operand multicast when the 256x256 pair tile is used
+  // (X boxes multicast to the pair below): measured 2.5-3 % faster on down projections
+  // (13824 -> 5120 at B = 2 / 4), 1.5-3 % slower on square / up projections
+  // (tools/ab_layer.py, profiles/r1_stream_mc_ab.jsonl), so chosen for P >= 2 D only
+  const int mc_env = env_int("FDP_STREAM_MC", -1);
+  const bool mc_want = mc_env >= 0 ? mc_env != 0 : d->P >= 2 * d->D;
+  pl.stream_mc = (pl.tc && pl.bn == 256 && pl.cg == 2 && mc_want && fdp::stream_mc_max_clusters() > 0) ? 2 : 1;
+  pl.stream_tiles = pl.tc ? fdp::stream_wtiles(pl.n_wtiles, pl.n_pt, pl.stream_mc) * pl.cg * pl.stream_mc
+                          : pl.n_tiles;
+  const long long n_slots = std::max<long long>(pl.n_tiles, pl.stream_tiles);
+
   // workspace layout
   const long long B = d->B;
-  pl.part_tiles = pl.n_tiles;
+  pl.part_tiles = static_cast<int>(n_slots);
   if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_GHOST) pl.part_tiles = ghost_shape(d, di.sms).parts;
   if (kind == FDP_KIND_EXPLICIT_DP && d->in_dtype != FDP_DTYPE_F64) {
     pl.expl_chunks = 64;
@@ -388,7 +402,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   pl.off_cnt = off;
   off = align_up(off + 4 * B, 256);
   pl.off_tile_cnt = off;
-  off = align_up(off + 4ull * pl.n_tiles, 256);
+  off = align_up(off + 4ull * n_slots, 256);
   const size_t esz = d->in_dtype == FDP_DTYPE_F64 ? 8 : 4;  // fp64 parity path keeps partials / factors in fp64
   pl.off_part = off;
   off = align_up(off + esz * B * pl.part_tiles, 256);
@@ -503,14 +517,20 @@ fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common&
   p.tile_cnt = ws_at<unsigned>(ws, pl.off_tile_cnt);
   p.ctrl = ws_at<unsigned>(ws, pl.off_ctrl);
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+  p.mc = pl.stream_mc;
   return p;
 }
 
 // Grid of the stream-K kernel: every co-resident cluster, capped by the unit count.
 int stream_grid(const fdp_desc* d, const Plan& pl, const DevInfo& di) {
+  const long long units =
+      static_cast<long long>(fdp::stream_wtiles(pl.n_wtiles, pl.n_pt, pl.stream_mc)) * d->B;
+  if (pl.stream_mc == 2) {
+    const long long clusters = fdp::stream_mc_max_clusters();
+    return static_cast<int>((units < clusters ? units : clusters) * 4);
+  }
   const int cap = fdp::tc_max_coresident_ctas(pl.bn, pl.cg);
   const long long clusters = (cap > 0 ? cap : di.sms) / pl.cg;
-  const long long units = static_cast<long long>(pl.n_wtiles) * d->B;
   return static_cast<int>((units < clusters ? units : clusters) * pl.cg);
 }
 
@@ -733,7 +753,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     q.norm_part = ws_at<float>(ws, pl.off_part);
     if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
       return cuda_fail(e, "stream-K single-sample GEMM launch");
-    if ((e = fdp::single_sample_finalize(grad_w, d->D * d->P, q.norm_part, pl.n_tiles, d->clip_c,
+    if ((e = fdp::single_sample_finalize(grad_w, d->D * d->P, q.norm_part, pl.stream_tiles, d->clip_c,
                                          d->clip_c * d->clip_c, c.inv_batch, norms, c.add_noise, d->noise_impl,
                                          c.noise_scale, c.key_base, c.key_base_g,
                                          reinterpret_cast<const long long*>(d->device_step),

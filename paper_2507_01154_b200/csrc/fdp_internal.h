@@ -92,7 +92,13 @@ struct StreamParams {
   float* norm_part;         // B == 1 single-sample path: sum of squares of each CTA tile ([n_wtiles * CG]) or null
   unsigned* ctrl;           // [0] exit counter, [1] error word
   unsigned long long budget_ns;
+  int mc;                   // 2: 4-CTA clusters (two pairs, X boxes multicast; bn 256, cg 2), else 1
 };
+// Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
+inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {
+  return mc == 2 ? ((n_wtiles / n_pt + 1) / 2) * n_pt : n_wtiles;
+}
+int stream_mc_max_clusters();
 // grid <= co-resident CTAs (split tiles wait on the cluster that initialises them)
 cudaError_t launch_stream(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
                           const StreamParams& p, int grid, cudaStream_t stream);

@@ -74,11 +74,18 @@ struct SegWalk {
   }
 };
 
-template <int BN, int CG>
+// MC = 2: a 4-CTA cluster holds two CTA pairs working on vertically adjacent pair
+// tiles (same X columns, consecutive dY row blocks) in lockstep; each X box is
+// loaded once and multicast to the CTA of both pairs that needs it, so L2 serves
+// 3/4 of the operand bytes of two independent pairs. A stage is refilled only
+// after BOTH pairs' MMAs released it (every commit arrives in all four CTAs).
+template <int BN, int CG, int MC>
 __global__ void __launch_bounds__(kTcThreads, 1)
     dpdw_stream_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
                        const __grid_constant__ CUtensorMap tm_gw, const StreamParams p) {
   using C = SCfg<BN, CG>;
+  constexpr int CL = CG * MC;  // CTAs per cluster
+  static_assert(MC == 1 || (CG == 2 && C::kBCols / 64 == MC), "multicast: one X box per pair");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + C::kStages * C::kStageBytes;
@@ -92,15 +99,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   unsigned* err = p.ctrl + 1;
-  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int rank = crank % CG;  // CTA within its pair
+  const int pi = crank / CG;    // pair within the cluster
   const bool leader = rank == 0;
-  const int cid = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+  const int cid = blockIdx.x / CL, n_clusters = gridDim.x / CL;
   const bool per_unit = p.reweight != 0;  // one TMEM accumulation per sample (scaled by c_b) vs per segment
+  // work tiles: MC pair tiles stacked along D (rows past D load zeros and are never stored)
+  const int n_wt = MC == 1 ? p.n_wtiles : ((p.n_wtiles / p.n_pt + MC - 1) / MC) * p.n_pt;
+  const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << (CG * pi));
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // MC == 2: the commits of both pairs
     }
     for (int s = 0; s < C::kNBuf; ++s) {
       mbar_init(&tfull[s], 1);
@@ -116,7 +128,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     else tmem_alloc<512>(tmem_holder);
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (CL > 1) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
@@ -132,17 +144,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ======================= TMA producer =======================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+      SegWalk w(cid, n_clusters, p.B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
-        const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+        const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
         const int p0 = (wt % p.n_pt) * BN + rank * C::kBCols;
         for (int b = bb; b < be; ++b) {
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x501);
             uint8_t* sa = smem + stage * C::kStageBytes;
             uint8_t* sb = sa + C::kABytes;
-            if constexpr (CG == 2) {
+            if constexpr (MC == 2) {  // own dY rows; X box `pi` multicast to this rank's CTA of both pairs
+              if (leader) mbar_arrive_expect_tx(&full[stage], C::kStageBytes * CG);
+              tma_load_3d_pair(sa, &tm_dy, &full[stage], d0, kb * kBK, b);
+              tma_load_3d_pair(sa + 8192, &tm_dy, &full[stage], d0 + 64, kb * kBK, b);
+              tma_load_3d_pair_mc(sb + pi * 8192, &tm_x, &full[stage], p0 + 64 * pi, kb * kBK, b,
+                                  static_cast<uint16_t>((1u << rank) | (1u << (CG + rank))));
+            } else if constexpr (CG == 2) {
               if (leader) mbar_arrive_expect_tx(&full[stage], C::kStageBytes * CG);
               tma_load_3d_pair(sa, &tm_dy, &full[stage], d0, kb * kBK, b);
               tma_load_3d_pair(sa + 8192, &tm_dy, &full[stage], d0 + 64, kb * kBK, b);
@@ -166,7 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ======================= MMA issuer (leader CTA) =======================
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
-      SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+      SegWalk w(cid, n_clusters, p.B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
         for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
@@ -189,12 +207,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 else tc_mma_f16(dtm, ad, bd, C::kIdesc, accum);
                 accum = 1;
               }
-              if constexpr (CG == 2) tc_commit_pair(&empty[stage]);
+              if constexpr (MC == 2) tc_commit_pair_mask(&empty[stage], 0xF);
+              else if constexpr (CG == 2) tc_commit_pair(&empty[stage]);
               else tc_commit(&empty[stage]);
               if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
           }
-          if constexpr (CG == 2) tc_commit_pair(&tfull[buf]);
+          if constexpr (MC == 2) tc_commit_pair_mask(&tfull[buf], pair_mask);
+          else if constexpr (CG == 2) tc_commit_pair(&tfull[buf]);
           else tc_commit(&tfull[buf]);
           if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
         }
@@ -210,18 +230,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
       kbg = kb + kGamma;
     }
-    SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+    SegWalk w(cid, n_clusters, p.B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
       const bool whole = bb == 0 && be == p.B;
       if (bb != 0 || !tile_prefilled(whole)) continue;
-      const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+      const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
       const int p0 = (wt % p.n_pt) * BN;
       prefill_rows<BN>(p.grad_w, p.D, p.P, d0, d0 + kBM, p0, p.accumulate != 0, p.add_noise != 0, p.noise_impl,
                        kbg, kb, p.noise_scale, p.noise_lo, p.noise_hi, ntid);
       __threadfence();
       named_bar_sync(3, 64);
-      if (ntid == 0) red_release_add_u32(&p.tile_cnt[wt * CG + rank], 1u);
+      if (ntid == 0) red_release_add_u32(&p.tile_cnt[wt * CL + crank], 1u);
     }
   } else if (warp >= kEpiWarp0) {
     // ======================= epilogue =======================
@@ -231,12 +251,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t nkb = p.key_base;
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     uint32_t rbuf = 0, rph = 0;
-    SegWalk w(cid, n_clusters, p.B, p.n_wtiles);
+    SegWalk w(cid, n_clusters, p.B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
       const bool whole = bb == 0 && be == p.B;
-      const int tile = wt * CG + rank;
-      const int d0 = ((wt / p.n_pt) * CG + rank) * kBM;
+      const int tile = wt * CL + crank;
+      const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
       const int p0 = (wt % p.n_pt) * BN;
       float acc[C::kCPT];
 #pragma unroll
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (CL > 1) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   if (warp == 1) {
@@ -345,14 +365,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const unsigned old = atomicAdd(&p.ctrl[0], 1u);
     if (old == gridDim.x - 1) {
       __threadfence();
-      for (int t = 0; t < p.n_wtiles * CG; ++t) p.tile_cnt[t] = 0u;
+      for (int t = 0; t < n_wt * CL; ++t) p.tile_cnt[t] = 0u;
       p.ctrl[0] = 0u;
       __threadfence();
     }
   }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int MC>
 static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
                                       const StreamParams& p, int grid, cudaStream_t stream) {
   using C = SCfg<BN, CG>;
@@ -360,8 +380,8 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(dpdw_stream_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::kSmem));
+    cudaError_t e = cudaFuncSetAttribute(dpdw_stream_kernel<BN, CG, MC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) done[dev] = true;
   }
@@ -372,9 +392,9 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   int na = 0;
-  if (CG == 2) {
+  if (CG * MC > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CG * MC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     na = 1;
@@ -383,17 +403,52 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   cfg.numAttrs = na;
   // Split tiles wait on the cluster that initialises them, which is resident:
   // the grid never exceeds the co-resident capacity (host planner).
-  return cudaLaunchKernelEx(&cfg, dpdw_stream_kernel<BN, CG>, tm_dy, tm_x, tm_gw, p);
+  return cudaLaunchKernelEx(&cfg, dpdw_stream_kernel<BN, CG, MC>, tm_dy, tm_x, tm_gw, p);
 }
 
 cudaError_t launch_stream(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
                           const StreamParams& p, int grid, cudaStream_t stream) {
   if (cg == 2) {
-    if (bn == 256) return launch_stream_impl<256, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
-    return launch_stream_impl<128, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
+    if (bn == 256) {
+      if (p.mc == 2) return launch_stream_impl<256, 2, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
+      return launch_stream_impl<256, 2, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+    }
+    return launch_stream_impl<128, 2, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
   }
-  if (bn == 256) return launch_stream_impl<256, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
-  return launch_stream_impl<128, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  if (bn == 256) return launch_stream_impl<256, 1, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  return launch_stream_impl<128, 1, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+}
+
+// Co-resident 4-CTA clusters of the multicast variant (0 if it cannot launch).
+int stream_mc_max_clusters() {
+  static int cache[64];
+  static bool have[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if (have[dev]) return cache[dev];
+  using C = SCfg<256, 2>;
+  int n = 0;
+  if (cudaFuncSetAttribute(dpdw_stream_kernel<256, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(C::kSmem)) == cudaSuccess) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4 * sms);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, dpdw_stream_kernel<256, 2, 2>, &cfg) != cudaSuccess) n = 0;
+  }
+  (void)cudaGetLastError();
+  cache[dev] = n;
+  have[dev] = true;
+  return n;
 }
 
 }  // namespace fdp

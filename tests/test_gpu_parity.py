@@ -790,3 +790,26 @@ def test_fp64_random_stream_against_oracle():
         want, wn = O.dp_backward(x, dy, ocfg(cfg), exact_noise=True)
         assert rel(host(r.grad_w), want) < F64_TOL, i
         assert rel(host(r.per_sample_norms_sq), wn) < F64_TOL, i
+
+
+@pytest.mark.parametrize("mc", ["0", "1"])
+@pytest.mark.parametrize("B,T,P,D", [(3, 300, 1536, 640), (1, 256, 2048, 640), (2, 130, 768, 1152)])
+def test_stream_multicast_layout(mc, B, T, P, D, monkeypatch):
+    """Stream-K kernel with two CTA pairs per 4-CTA cluster (X boxes multicast,
+    FDP_STREAM_MC=1) and with one pair per cluster: two-phase DP (Philox noise:
+    out(sigma) - out(0) is the noise), non-DP with accumulation, and the B = 1
+    path, on shapes with an odd number of 256-row pair blocks (the lower pair of
+    the last double tile lies past D)."""
+    monkeypatch.setenv("FDP_STREAM_MC", mc)
+    x, dy = randn(B, T, P, D, seed=P + D + B, scale_dy=1e-2)
+    cfg0 = fdp.DPConfig(0.7, 0.0, "mean", seed=2, layer_id=3, step=1)
+    r0 = fdp.backward_flashdp(x, dy, cfg0, path="two_phase", noise_impl="philox")
+    check(r0, x, dy, cfg0, BF16_TOL)
+    cfg1 = fdp.DPConfig(0.7, 1.2, "mean", seed=2, layer_id=3, step=1)
+    r1 = fdp.backward_flashdp(x, dy, cfg1, path="two_phase", noise_impl="philox")
+    n = fdp.noise_range(cfg1, 0, P * D, 0.84, noise_impl="philox").view(D, P)
+    assert rel(host(r1.grad_w - r0.grad_w), host(n)) < 1e-5
+    g0 = torch.randn(D, P, device="cuda")
+    nd = g0.clone()
+    fdp.run_backward(W.NON_DP, x, dy, None, grad_out=nd, accumulate=True)
+    assert rel(host(nd), O.nondp_backward(host(x), host(dy)) + host(g0)) < BF16_TOL
