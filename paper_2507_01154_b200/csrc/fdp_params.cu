@@ -28,7 +28,7 @@ namespace fdp {
 namespace {
 
 constexpr int kVCols = 256;  // columns per block
-constexpr int kVRows = 64;   // T rows per partial-sum block
+constexpr int kVRows = 32;   // T rows per partial-sum block
 
 __device__ __forceinline__ void nk_resolve(NoiseKey& nk) {  // device step counter (graph replays)
   if (nk.step_ptr) {
@@ -46,30 +46,71 @@ __device__ __forceinline__ float ld(const T* p, long long i) {
   else return __bfloat162float(p[i]);
 }
 
-// pass 1: gpart[b][tc][l] = sum over rows [tc*kVRows, ...) of the group's per-row term
-template <typename T, int kKind>
+// pass 1: gpart[b][tc][l] = sum over rows [tc*kVRows, ...) of the group's per-row term.
+// VW consecutive columns per thread (16-byte loads when D % VW == 0, else VW = 1),
+// all kVRows rows' loads issued before the sums: the pass is latency-bound on a
+// few tens of MB, so bytes in flight per SM decide its speed.
+template <typename T, int kKind, int VW>
 __global__ void __launch_bounds__(kVCols) k_vec_rows(const T* __restrict__ dy, const T* __restrict__ xh, int T_, int D,
                                                      int n_tc, float* __restrict__ gpart) {
   const int b = blockIdx.z, tc = blockIdx.y;
-  const int d = blockIdx.x * kVCols + threadIdx.x;
+  const int d = (blockIdx.x * kVCols + threadIdx.x) * VW;
   if (d >= D) return;
   const int t0 = tc * kVRows, t1 = min(T_, t0 + kVRows);
-  float s = 0.0f, sx = 0.0f;
+  float s[VW], sx[VW];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) s[j] = sx[j] = 0.0f;
   const long long base = static_cast<long long>(b) * T_ * D + d;
 #pragma unroll 8
   for (int t = t0; t < t1; ++t) {
     const long long i = base + static_cast<long long>(t) * D;
-    const float y = ld(dy, i);
-    if constexpr (kKind != FDP_VEC_RMSNORM) s += y;
-    if constexpr (kKind != FDP_VEC_BIAS) sx = fmaf(y, ld(xh, i), sx);
+    float y[VW], x[VW];
+    if constexpr (VW == 1) {
+      y[0] = ld(dy, i);
+      if constexpr (kKind != FDP_VEC_BIAS) x[0] = ld(xh, i);
+    } else if constexpr (sizeof(T) == 4) {  // VW = 4 floats
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(dy + i));
+      y[0] = a.x; y[1] = a.y; y[2] = a.z; y[3] = a.w;
+      if constexpr (kKind != FDP_VEC_BIAS) {
+        const float4 c = __ldcs(reinterpret_cast<const float4*>(xh + i));
+        x[0] = c.x; x[1] = c.y; x[2] = c.z; x[3] = c.w;
+      }
+    } else {  // VW = 8 bf16
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(dy + i));
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(pa[j]);
+        y[2 * j] = f.x;
+        y[2 * j + 1] = f.y;
+      }
+      if constexpr (kKind != FDP_VEC_BIAS) {
+        const uint4 c = __ldcs(reinterpret_cast<const uint4*>(xh + i));
+        const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(pc[j]);
+          x[2 * j] = f.x;
+          x[2 * j + 1] = f.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < VW; ++j) {
+      if constexpr (kKind != FDP_VEC_RMSNORM) s[j] += y[j];
+      if constexpr (kKind != FDP_VEC_BIAS) sx[j] = fmaf(y[j], x[j], sx[j]);
+    }
   }
   const long long L = kKind == FDP_VEC_LAYERNORM ? 2LL * D : D;
   float* o = gpart + (static_cast<long long>(b) * n_tc + tc) * L;
-  if constexpr (kKind == FDP_VEC_BIAS) o[d] = s;
-  if constexpr (kKind == FDP_VEC_RMSNORM) o[d] = sx;
-  if constexpr (kKind == FDP_VEC_LAYERNORM) {
-    o[d] = sx;
-    o[D + d] = s;
+#pragma unroll
+  for (int j = 0; j < VW; ++j) {
+    if constexpr (kKind == FDP_VEC_BIAS) o[d + j] = s[j];
+    if constexpr (kKind == FDP_VEC_RMSNORM) o[d + j] = sx[j];
+    if constexpr (kKind == FDP_VEC_LAYERNORM) {
+      o[d + j] = sx[j];
+      o[D + d + j] = s[j];
+    }
   }
 }
 
@@ -356,18 +397,26 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
   float* gpart = work;                                           // [B][n_tc][L]
   float* g = gpart + static_cast<long long>(B) * n_tc * L;       // [B][L]
   float* part = g + static_cast<long long>(B) * L;               // [B][n_chunks]
-  const dim3 g1((D + kVCols - 1) / kVCols, n_tc, B);
-#define FDP_VEC_ROWS(TY, K) \
-  k_vec_rows<TY, K><<<g1, kVCols, 0, s>>>(static_cast<const TY*>(dy), static_cast<const TY*>(xhat), T_, D, n_tc, gpart)
+  // 16-byte loads when every row start stays aligned (D a multiple of the vector width)
+  const bool aligned = (reinterpret_cast<uintptr_t>(dy) % 16 == 0) && (reinterpret_cast<uintptr_t>(xhat) % 16 == 0);
+  const int vw = !aligned ? 1 : in_f32 ? ((D % 4 == 0) ? 4 : 1) : ((D % 8 == 0) ? 8 : 1);
+  const dim3 g1((D / vw + kVCols - 1) / kVCols, n_tc, B);
+#define FDP_VEC_ROWS(TY, K, V) \
+  k_vec_rows<TY, K, V><<<g1, kVCols, 0, s>>>(static_cast<const TY*>(dy), static_cast<const TY*>(xhat), T_, D, n_tc, gpart)
+#define FDP_VEC_KINDS(TY, V)                                        \
+  do {                                                              \
+    if (kind == FDP_VEC_BIAS) FDP_VEC_ROWS(TY, FDP_VEC_BIAS, V);    \
+    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(TY, FDP_VEC_RMSNORM, V); \
+    else FDP_VEC_ROWS(TY, FDP_VEC_LAYERNORM, V);                    \
+  } while (0)
   if (in_f32) {
-    if (kind == FDP_VEC_BIAS) FDP_VEC_ROWS(float, FDP_VEC_BIAS);
-    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(float, FDP_VEC_RMSNORM);
-    else FDP_VEC_ROWS(float, FDP_VEC_LAYERNORM);
+    if (vw == 4) FDP_VEC_KINDS(float, 4);
+    else FDP_VEC_KINDS(float, 1);
   } else {
-    if (kind == FDP_VEC_BIAS) FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_BIAS);
-    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_RMSNORM);
-    else FDP_VEC_ROWS(__nv_bfloat16, FDP_VEC_LAYERNORM);
+    if (vw == 8) FDP_VEC_KINDS(__nv_bfloat16, 8);
+    else FDP_VEC_KINDS(__nv_bfloat16, 1);
   }
+#undef FDP_VEC_KINDS
 #undef FDP_VEC_ROWS
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

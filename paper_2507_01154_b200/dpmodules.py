@@ -47,6 +47,26 @@ def _desc(cfg: DPConfig, B, T, P, D, dtype_code, *, rank, world, mean_batch, add
 
 
 _WS: dict = {}
+_DESCS: dict = {}
+
+
+def _cached_desc(tag, cfg: DPConfig, B, T, P, D, dtype_code, *, size_fn, **kw):
+    """Descriptor + workspace size per call signature (a training loop repeats the
+    same shapes every step; only the step key changes): validated once by the C
+    library, then reused with the step patched in."""
+    key = (tag, B, T, P, D, dtype_code, cfg.clip_c, cfg.sigma, cfg.reduction, cfg.seed, cfg.layer_id,
+           tuple(sorted(kw.items())))
+    hit = _DESCS.get(key)
+    if hit is None:
+        desc = _desc(cfg, B, T, P, D, dtype_code, **kw)
+        nb = ctypes.c_size_t()
+        _lib.check(size_fn(ctypes.byref(desc), ctypes.byref(nb)))
+        if len(_DESCS) > 4096:
+            _DESCS.clear()
+        hit = _DESCS[key] = (desc, nb)
+    desc, nb = hit
+    desc.step = _lib._wrap64(cfg.step)
+    return desc, nb
 
 
 def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
@@ -82,12 +102,11 @@ def vector_dp_grad(kind: str, dy: torch.Tensor, xhat: Optional[torch.Tensor], cf
     if not dy.is_cuda:
         raise UsageError("vector_dp_grad needs CUDA tensors")
     L = 2 * D if kind == "layernorm" else D
-    desc = _desc(cfg, B, T, 8, D, _dtype_code(dy), rank=rank, world=world, mean_batch=mean_batch,
-                 add_noise=add_noise, noise_impl=noise_impl, accumulate=accumulate)
     lib = _lib.load()
     k = _lib.VEC_KIND[kind]
-    nb = ctypes.c_size_t()
-    _lib.check(lib.fdp_vec_workspace_bytes(ctypes.byref(desc), k, ctypes.byref(nb)))
+    desc, nb = _cached_desc(("vec", k), cfg, B, T, 8, D, _dtype_code(dy), rank=rank, world=world,
+                            mean_batch=mean_batch, add_noise=add_noise, noise_impl=noise_impl, accumulate=accumulate,
+                            size_fn=lambda d, out: lib.fdp_vec_workspace_bytes(d, k, out))
     if out is None:
         out = (torch.zeros if accumulate else torch.empty)(L, dtype=torch.float32, device=dy.device)
     elif out.dtype != torch.float32 or out.numel() != L or not out.is_contiguous():
@@ -115,11 +134,10 @@ def embedding_dp_grad(tokens: torch.Tensor, dy: torch.Tensor, vocab: int, cfg: D
         dy = dy.float()
     dy = dy.contiguous()
     tokens = tokens.to(torch.int64).contiguous()
-    desc = _desc(cfg, B, T, int(vocab), D, _dtype_code(dy), rank=rank, world=world, mean_batch=mean_batch,
-                 add_noise=add_noise, noise_impl=noise_impl, accumulate=accumulate)
     lib = _lib.load()
-    nb = ctypes.c_size_t()
-    _lib.check(lib.fdp_embedding_workspace_bytes(ctypes.byref(desc), ctypes.byref(nb)))
+    desc, nb = _cached_desc(("emb",), cfg, B, T, int(vocab), D, _dtype_code(dy), rank=rank, world=world,
+                            mean_batch=mean_batch, add_noise=add_noise, noise_impl=noise_impl, accumulate=accumulate,
+                            size_fn=lib.fdp_embedding_workspace_bytes)
     if out is None:
         out = (torch.zeros if accumulate else torch.empty)((vocab, D), dtype=torch.float32, device=dy.device)
     elif out.dtype != torch.float32 or tuple(out.shape) != (vocab, D) or not out.is_contiguous():

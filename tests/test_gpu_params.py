@@ -38,7 +38,7 @@ def ocfg(c: fdp.DPConfig) -> O.Cfg:
 
 @pytest.mark.parametrize("kind", ["bias", "rmsnorm", "layernorm"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("B,T,D", [(5, 70, 777), (1, 1, 64), (3, 200, 256), (16, 9, 1030)])
+@pytest.mark.parametrize("B,T,D", [(5, 70, 777), (1, 1, 64), (3, 200, 256), (16, 9, 1030), (2, 65, 8), (4, 33, 1028)])
 def test_vector_groups_against_oracle(kind, dtype, B, T, D):
     g = torch.Generator().manual_seed(B * 1000 + T + D)
     dy = (torch.randn(B, T, D, generator=g) * 0.1).to(dtype).cuda()
@@ -71,6 +71,19 @@ def test_vector_group_noise_partition_and_accumulate(rank, world):
     lo, hi = L * rank // world, L * (rank + 1) // world
     want, _ = O.dp_vector_backward(host(dy), host(xh), "layernorm", ocfg(cfg), noise_lo=lo, noise_hi=hi)
     assert rel(host(out), want + host(base)) < TOL
+
+
+def test_vector_group_unaligned_view():
+    """A dY view starting 4 bytes into its storage takes the scalar-load variant."""
+    B, T, D = 3, 40, 64
+    g = torch.Generator().manual_seed(9)
+    big = (torch.randn(B * T * D + 1, generator=g) * 0.1).cuda()
+    dy = big[1:].view(B, T, D)
+    xh = torch.randn(B, T, D, generator=g).cuda()
+    cfg = fdp.DPConfig(0.2, 0.0, "sum", seed=1, layer_id=1)
+    out = fdp.vector_dp_grad("rmsnorm", dy, xh, cfg)
+    want, _ = O.dp_vector_backward(host(dy), host(xh), "rmsnorm", ocfg(cfg))
+    assert rel(host(out), want) < TOL
 
 
 def test_bias_dw_is_the_bias_vector_group():
