@@ -24,6 +24,18 @@ def noise_partition(n: int, rank: int, world: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def set_data_parallel(modules, rank: int, world: int) -> None:
+    """Per-rank setup of every DP module of a model (DPLinear, DPLayerNorm,
+    DPRMSNorm, DPEmbedding): each adds its noise only on the rank's slice of its
+    group's index space. Pass the global batch as ``logical_batch`` to
+    ``set_step`` so ``mean`` divides by it; then ``allreduce_grads_`` over the
+    parameters' gradients gives the single-process DP gradients, noise once."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"rank {rank} out of range for world {world}")
+    for m in modules:
+        m.rank, m.world = rank, world
+
+
 def flatten_bucket(tensors: Sequence[torch.Tensor]) -> torch.Tensor:
     return torch.cat([t.reshape(-1) for t in tensors])
 

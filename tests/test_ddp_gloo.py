@@ -109,3 +109,16 @@ def test_chunked_allreduce_backward_two_ranks():
         mp.spawn(_chunk_worker, args=(2, _free_port(), x, dy, cfgs, out), nprocs=2, join=True)
         want = np.concatenate([O.dp_backward(x, dy, c, exact_noise=True)[0].reshape(-1) for c in cfgs])
         assert np.max(np.abs(out["flat"] - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+
+
+def test_set_data_parallel_sets_every_module_and_validates():
+    import pytest as _pytest
+
+    from paper_2507_01154_b200 import DPEmbedding, DPLayerNorm, DPLinear, DPRMSNorm
+    from paper_2507_01154_b200.ddp import set_data_parallel
+
+    mods = [DPLinear(8, 8), DPLayerNorm(8), DPRMSNorm(8), DPEmbedding(10, 8)]
+    set_data_parallel(mods, 1, 4)
+    assert all((m.rank, m.world) == (1, 4) for m in mods)
+    with _pytest.raises(ValueError):
+        set_data_parallel(mods, 4, 4)

@@ -140,3 +140,52 @@ def test_zero1_sharded_adam_two_ranks_equals_single_gpu():
     want = st.theta.cpu().numpy()
     start = np.linspace(-1, 1, flat.numel())
     assert np.max(np.abs((got - start) - (want - start))) / np.max(np.abs(want - start)) < 1e-4
+
+
+def _full_dp_worker(rank, world, port, out):
+    """Every-parameter DP GPT-2 (tiny) on this rank's half of the batch, gloo all-reduce of all gradients."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2507_01154_b200.ddp import allreduce_grads_, set_data_parallel
+    from paper_2507_01154_b200.dplinear import GroupedDPBackward
+    from paper_2507_01154_b200.gpt2 import GPT2, GPT2Config
+
+    torch.manual_seed(0)
+    cfg = GPT2Config(vocab=512, seq=32, d=128, heads=4, layers=1, mlp=256)
+    model = GPT2(cfg, dp="full", clip_c=0.3, sigma=0.5, noise_impl="keyed_f64", tied=False).cuda()
+    g = torch.Generator().manual_seed(5)
+    idx = torch.randint(0, cfg.vocab, (4, cfg.seq + 1), generator=g).cuda()
+    B = idx.shape[0]
+    lo, hi = B * rank // world, B * (rank + 1) // world
+    mods = model.dp_modules()
+    set_data_parallel(mods, rank, world)
+    for m in mods:
+        m.set_step(3, logical_batch=B)
+    x, y = idx[lo:hi, :-1].contiguous(), idx[lo:hi, 1:].contiguous()
+    with GroupedDPBackward():
+        # the loss is a per-token mean: rescale so this rank's share is the global mean's
+        (model.loss(x, y) * ((hi - lo) / B)).backward()
+    grads = [p.grad for p in model.parameters()]
+    if world > 1:
+        allreduce_grads_(grads)
+    torch.cuda.synchronize()
+    if rank == 0:
+        out[f"w{world}"] = [t.detach().cpu().numpy() for t in grads]
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_full_dp_gpt2_equals_single_process():
+    """SURVEY 8e for every parameter group: two ranks with rank-partitioned keyed
+    noise and the global-batch mean, all-reduced, equal one process on the whole
+    batch (noise added exactly once, per-sample clipping unchanged)."""
+    with mp.get_context("spawn").Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_full_dp_worker, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
+        mp.start_processes(_full_dp_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+        one, two = out["w1"], out["w2"]
+    assert len(one) == len(two)
+    for a, b in zip(one, two):
+        assert np.max(np.abs(a - b)) <= 2e-2 * max(float(np.max(np.abs(a))), 1e-6)
