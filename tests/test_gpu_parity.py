@@ -813,3 +813,22 @@ def test_stream_multicast_layout(mc, B, T, P, D, monkeypatch):
     nd = g0.clone()
     fdp.run_backward(W.NON_DP, x, dy, None, grad_out=nd, accumulate=True)
     assert rel(host(nd), O.nondp_backward(host(x), host(dy)) + host(g0)) < BF16_TOL
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adam"])
+def test_package_train_demo_reproduces_reference_curves(opt):
+    """fdp.train_demo (bench.train_demo on the GPU, fp64 parity path + CUDA
+    optimizer kernels) reproduces the reference's golden loss curves of every
+    workflow at every noise level to 1e-9 (criterion 9)."""
+    g = golden("train.npz")
+    train = {"dims": {"B": 4, "T": 4, "P": 8, "D": 4}, "steps": 50, "workflows": ["explicit_dp", "flashdp"],
+             "sigmas": [0.1, 0.5, 1.0], "eta": 0.05}
+    if opt == "adam":
+        train.update({"optimizer": "adam", "eta": 0.02, "beta1": 0.9, "beta2": 0.999, "eps_adam": 1e-8})
+    cfg = fdp.TrainDemoConfig.from_dict({"train": train, "mem": {"scratchpad_capacity_bytes": 8192},
+                                         "dp": {"clip_c": 1.0, "sigma": 0.0, "seed": 2024}})
+    res = fdp.train_demo(cfg)
+    for sigma, per_wf in res.items():
+        for wf, losses in per_wf.items():
+            want = g[f"{opt}_{sigma}_{wf}"]
+            assert np.max(np.abs(np.array(losses) - want)) <= 1e-9, (opt, sigma, wf)

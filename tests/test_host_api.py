@@ -179,3 +179,23 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     x = np.ones((1, 2, 8))
     with pytest.raises(Exception):
         fdp.backward_flashdp(x, x, fdp.DPConfig(1.0, 0.0))
+
+
+def test_demo_input_generator_matches_reference_golden():
+    """demo.keyed_uniform restates rng.keyed_uniform_array (rng.py:88-94): the
+    reference's own train-demo inputs (tests/golden/train.npz) bit for bit."""
+    import os
+
+    import numpy as np
+
+    from paper_2507_01154_b200.demo import TrainDemoConfig, keyed_uniform
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "train.npz"))
+    assert np.array_equal(keyed_uniform((2024, 11), 128).reshape(4, 4, 8), g["x"])
+    assert np.array_equal(keyed_uniform((2024, 12), 32, -0.5, 0.5).reshape(4, 8), g["w0"])
+    assert np.array_equal(keyed_uniform((2024, 13), 64).reshape(4, 4, 4), g["y"])
+    cfg = TrainDemoConfig.from_dict({"train": {"dims": {"B": 4, "T": 4, "P": 8, "D": 4}, "steps": 3,
+                                               "workflows": ["explicit_dp", "flashdp"], "sigmas": [0.1],
+                                               "eta": 0.05},
+                                     "mem": {"scratchpad_capacity_bytes": 8192}, "dp": {"clip_c": 1.0, "seed": 2024}})
+    assert cfg.optimizer == "sgd" and cfg.dims.P == 8
