@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ ke
   }
 }
 
-size_t emb_out_smem(int B) { return sizeof(int) * (static_cast<size_t>(B) * (kEVRows + 2) + kEVRows); }
+size_t emb_out_smem(int B) { return sizeof(int) * (static_cast<size_t>(B) * (kEVRows + 2) + kEVRows + 4); }
 long long n_tchunks(int T_) { return (T_ + kVRows - 1) / kVRows; }
 int pow2_at_least(int n) {
   int p = 1;
@@ -423,7 +423,8 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
   k_vec_reduce<<<dim3(n_chunks, B), kVCols, 0, s>>>(gpart, n_tc, static_cast<int>(L), g, part, n_chunks);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const long long blocks = (L + 255) / 256 < 148 ? (L + 255) / 256 : 148;
-  k_vec_finalize<<<static_cast<int>(blocks), 256, static_cast<size_t>(B) * sizeof(float), s>>>(
+  // factor table rounded up to whole 16-byte words: the unrolled sample loop may read fac[] in vectors
+  k_vec_finalize<<<static_cast<int>(blocks), 256, static_cast<size_t>((B + 3) / 4) * 16, s>>>(
       g, part, B, L, n_chunks, clip_c, clip_c * clip_c, inv_batch, out, norms_out, accumulate, nk);
   return cudaGetLastError();
 }

@@ -33,6 +33,26 @@ xd, dyd = inputs(2, 20, 16, 8, torch.float64)
 fdp.backward_flashdp(xd, dyd, cfg)  # fp64 parity path
 grp = fdp.PreparedGroup([(x, dy, cfg), inputs(3, 100, 512, 256) + (cfg,)], noise_impl="philox")
 grp()
+# ghost norms with K slices (single CTA and pair), multicast stream layout (down projection)
+for pair, split in (("0", "3"), ("1", "2")):
+    os.environ["FDP_GHOST_PAIR"], os.environ["FDP_GHOST_SPLIT"] = pair, split
+    fdp.backward_flashdp(*inputs(2, 300, 192, 1600), cfg, path="two_phase", norm_phase="ghost")
+os.environ.pop("FDP_GHOST_PAIR")
+os.environ.pop("FDP_GHOST_SPLIT")
+xm, dym = inputs(3, 130, 1536, 640)
+fdp.backward_flashdp(xm, dym, cfg, path="two_phase", noise_impl="philox")  # P >= 2D: 4-CTA multicast layout
+# non-linear parameter groups
+for kind in ("bias", "rmsnorm", "layernorm"):
+    for dt in (torch.bfloat16, torch.float32):
+        a, b = inputs(3, 70, 8, 777, dt)
+        fdp.vector_dp_grad(kind, b, b, cfg, noise_impl="philox")
+        a, b = inputs(2, 33, 8, 1024, dt)
+        fdp.vector_dp_grad(kind, b, b, cfg, noise_impl="keyed_f32")
+tok = torch.randint(-1, 51, (3, 300), device="cuda")
+for d in (70, 256):
+    fdp.embedding_dp_grad(tok, torch.randn(3, 300, d, device="cuda"), 50, cfg, noise_impl="philox")
+fdp.embedding_dp_grad(torch.zeros(2, 700, dtype=torch.int64, device="cuda"), torch.randn(2, 700, 40, device="cuda"),
+                      3, cfg)  # one run longer than a norm block's key stage
 st = fdp.OptimizerState.fresh(torch.zeros(1000, device="cuda"), eta=0.1)
 fdp.dp_adam_step_(st, torch.ones(1000, device="cuda"))
 torch.cuda.synchronize()
