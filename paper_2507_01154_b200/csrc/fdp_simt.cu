@@ -6,6 +6,8 @@
 // (workflows.py:246-324): pass 1 reduces per-sample norm^2 partials per 32x32
 // tile without storing G, pass 2 recomputes the tiles and sums c_b * G_b. It is
 // exact fp32 FMA arithmetic, so fp32 inputs meet the 1e-5 bar.
+#include <cstdlib>
+
 #include "fdp_internal.h"
 #include "fdp_rng.cuh"
 #include <cuda_bf16.h>
@@ -203,15 +205,15 @@ __global__ void k_noise_fill(float* out, long long lo, long long hi, float scale
 // range noised, 2 = no noise. The Philox / no-noise variants are lean enough
 // to keep 48 warps per SM streaming, which the elementwise pass needs to reach
 // HBM bandwidth with the Philox arithmetic interleaved.
-template <int kMode>
-__global__ void __launch_bounds__(256, kMode == 0 ? 1 : 6)
+template <int kMode, int kUV = 2, int kMinB = 6>
+__global__ void __launch_bounds__(256, kMode == 0 ? 1 : kMinB)
     k_single_finalize(float* __restrict__ g, long long n, const float* __restrict__ part, int n_parts, double clip_c,
                       double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl, float scale,
                       uint64_t base, uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u,
                       long long lo, long long hi) {
   float4* g4 = reinterpret_cast<float4*>(g);
   const long long n4 = n >> 2;  // n = D * P, P % 8 == 0
-  constexpr int kU = kMode == 0 ? 4 : 2;  // float4 per thread per iteration: loads in flight
+  constexpr int kU = kMode == 0 ? 4 : kUV;  // float4 per thread per iteration: loads in flight
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   float4 v[kU];
@@ -242,6 +244,11 @@ __global__ void __launch_bounds__(256, kMode == 0 ? 1 : 6)
     base_g = base + kGamma;
   }
   for (; i0 < n4; i0 += stride * kU, load()) {
+    float4 z[kU];
+    if constexpr (kMode == 1) {  // the draws do not depend on the loads in flight: compute them first
+#pragma unroll
+      for (int u = 0; u < kU; ++u) z[u] = philox_normal4(base, static_cast<uint64_t>(i0 + u * stride));
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const long long i = i0 + u * stride;
@@ -251,11 +258,10 @@ __global__ void __launch_bounds__(256, kMode == 0 ? 1 : 6)
       v[u].z *= f;
       v[u].w *= f;
       if constexpr (kMode == 1) {
-        const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
-        v[u].x += scale * z.x;
-        v[u].y += scale * z.y;
-        v[u].z += scale * z.z;
-        v[u].w += scale * z.w;
+        v[u].x += scale * z[u].x;
+        v[u].y += scale * z[u].y;
+        v[u].z += scale * z[u].z;
+        v[u].w += scale * z[u].w;
       } else if constexpr (kMode == 0) {
         const long long e = i << 2;
         if (add_noise && e + 3 >= lo && e < hi) {
@@ -298,6 +304,8 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
     const long long cap = 148LL * 6 * 4;  // 6 resident blocks per SM, a few rounds each
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    // measured (tools/ab_layer.py): 4 float4 per thread at 4 blocks/SM, or 8 blocks/SM, are slower;
+    // the pass sits at HBM speed without noise and the Philox draws add ~20 %
     auto k = mode == 1 ? k_single_finalize<1> : k_single_finalize<2>;
     k<<<static_cast<int>(blocks), threads, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch, norms_out,
                                                   add_noise, impl, noise_scale, base, base_g, step_ptr, seed_u,
