@@ -73,3 +73,31 @@ def test_llama_dp_step_with_clipping_and_noise():
         assert p.grad is not None and torch.isfinite(p.grad).all()
     norms = [mod.last_norms_sq for mod in m.dp_modules() if getattr(mod, "last_norms_sq", None) is not None]
     assert norms and all(torch.isfinite(t).all() and (t >= 0).all() for t in norms)
+
+
+def test_full_dp_gpt2_micro_batches_equal_one_batch():
+    """SURVEY 8f rank 1 with every parameter group: two micro-batches (noise only on
+    the last, mean over the logical batch, gradients accumulated by autograd) equal
+    one step on the whole batch (reference-keyed noise: exact draws)."""
+    torch.manual_seed(0)
+    cfg = GPT2Config(vocab=512, seq=32, d=128, heads=4, layers=1, mlp=256)
+    model = GPT2(cfg, dp="full", clip_c=0.3, sigma=0.5, noise_impl="keyed_f64", tied=False).cuda()
+    g = torch.Generator().manual_seed(5)
+    idx = torch.randint(0, cfg.vocab, (4, cfg.seq + 1), generator=g).cuda()
+    B = idx.shape[0]
+    mods = model.dp_modules()
+
+    def run(chunks):
+        model.zero_grad(set_to_none=True)
+        for i, (lo, hi) in enumerate(chunks):
+            for m in mods:
+                m.set_step(7, last_micro_batch=(i == len(chunks) - 1), logical_batch=B)
+            x, y = idx[lo:hi, :-1].contiguous(), idx[lo:hi, 1:].contiguous()
+            with GroupedDPBackward():
+                (model.loss(x, y) * ((hi - lo) / B)).backward()
+        return [p.grad.detach().clone() for p in model.parameters()]
+
+    whole = run([(0, 4)])
+    micro = run([(0, 2), (2, 4)])
+    for a, b in zip(whole, micro):
+        assert float((a - b).abs().max()) <= 2e-2 * max(float(a.abs().max()), 1e-6)
