@@ -105,3 +105,57 @@ def test_extreme_shapes(B, T, P, D, path):
                              O.Cfg(0.2, 1.0, "mean", 4, 1, 2), exact_noise=True)
     assert _rel(r.grad_w.double().cpu().numpy(), want) < TOL
     assert _rel(r.per_sample_norms_sq.double().cpu().numpy(), wn) < TOL
+
+
+def _group_cases():
+    rng = np.random.default_rng(20261018)
+    out = []
+    for i in range(40):
+        kind = str(rng.choice(["bias", "rmsnorm", "layernorm", "embedding"]))
+        B = int(rng.choice([1, 2, 3, 7, 16]))
+        T = int(rng.choice([1, 5, 33, 64, 130, 257]))
+        D = int(rng.choice([8, 24, 96, 130, 256, 770]))
+        V = int(rng.choice([1, 3, 40, 300]))
+        dtype = torch.bfloat16 if rng.random() < 0.5 else torch.float32
+        world = int(rng.choice([1, 1, 2, 3]))
+        rank = int(rng.integers(0, world))
+        red = str(rng.choice(["sum", "mean"]))
+        sigma = float(rng.choice([0.0, 0.7]))
+        clip_q = float(rng.choice([0.25, 0.5, 2.0]))  # C as a quantile multiple of the median norm
+        out.append((i, kind, B, T, D, V, dtype, rank, world, red, sigma, clip_q))
+    return out
+
+
+@pytest.mark.parametrize("case", _group_cases(), ids=lambda c: f"g{c[0]}-{c[1]}")
+def test_random_parameter_groups_against_oracle(case):
+    """Random bias / RMSNorm / LayerNorm / embedding groups (shapes, dtypes, rank
+    slices, reductions, clip levels) against the oracle's restatements, keyed noise."""
+    i, kind, B, T, D, V, dtype, rank, world, red, sigma, clip_q = case
+    g = torch.Generator().manual_seed(1000 + i)
+    dy = (torch.randn(B, T, D, generator=g) * 0.1).to(dtype)
+    if kind == "embedding":
+        tok = torch.randint(0, V, (B, T), generator=g)
+        G = O.embedding_per_sample_grads(tok.numpy(), dy.double().numpy(), V)
+        ns = np.einsum("bvd,bvd->b", G, G)
+    else:
+        xh = torch.randn(B, T, D, generator=g).to(dtype)
+        ns = (O.vector_per_sample_grads(dy.double().numpy(), xh.double().numpy(), kind) ** 2).sum(1)
+    C = max(float(np.median(np.sqrt(ns))) * clip_q, 1e-6)
+    cfg = fdp.DPConfig(C, sigma, red, seed=7, layer_id=i, step=3)
+    ocfg = O.Cfg(C, sigma, red, 7, i, 3)
+    norms = torch.empty(B, device="cuda")
+    if kind == "embedding":
+        n = V * D
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        got = fdp.embedding_dp_grad(tok.cuda(), dy.cuda(), V, cfg, noise_impl="keyed_f64", rank=rank, world=world,
+                                    norms_sq=norms)
+        want, wn = O.dp_embedding_backward(tok.numpy(), dy.double().numpy(), V, ocfg, noise_lo=lo, noise_hi=hi)
+    else:
+        n = 2 * D if kind == "layernorm" else D
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        got = fdp.vector_dp_grad(kind, dy.cuda(), xh.cuda(), cfg, noise_impl="keyed_f64", rank=rank, world=world,
+                                 norms_sq=norms)
+        want, wn = O.dp_vector_backward(dy.double().numpy(), xh.double().numpy(), kind, ocfg, noise_lo=lo,
+                                        noise_hi=hi)
+    assert _rel(got.double().cpu().numpy(), want) < 1e-5, case
+    assert _rel(norms.double().cpu().numpy(), wn) < 1e-5, case
