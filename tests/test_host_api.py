@@ -199,3 +199,28 @@ def test_demo_input_generator_matches_reference_golden():
                                                "eta": 0.05},
                                      "mem": {"scratchpad_capacity_bytes": 8192}, "dp": {"clip_c": 1.0, "seed": 2024}})
     assert cfg.optimizer == "sgd" and cfg.dims.P == 8
+
+
+def test_parameter_group_entry_points_validate_without_gpu():
+    """fdp_vec_* / fdp_embedding_* reject bad descriptors, kinds, dtypes and
+    extents with the reference's error codes before touching the device, and a
+    well-formed call reports a workspace size."""
+    lib = _lib.load()
+    nb = ctypes.c_size_t()
+    ok = _lib.make_desc(B=4, T=16, P=8, D=32)
+    assert lib.fdp_vec_workspace_bytes(ctypes.byref(ok), 2, ctypes.byref(nb)) == 0 and nb.value > 0
+    assert lib.fdp_vec_workspace_bytes(ctypes.byref(ok), 7, ctypes.byref(nb)) == _lib.FDP_ERR_USAGE
+    f64 = _lib.make_desc(B=4, T=16, P=8, D=32, in_dtype=_lib.DTYPE_F64)
+    assert lib.fdp_vec_workspace_bytes(ctypes.byref(f64), 0, ctypes.byref(nb)) == _lib.FDP_ERR_USAGE
+    bad = _lib.make_desc(B=0, T=16, P=8, D=32)
+    assert lib.fdp_vec_workspace_bytes(ctypes.byref(bad), 0, ctypes.byref(nb)) == _lib.FDP_ERR_SHAPE
+    assert lib.fdp_vec_dw(ctypes.byref(ok), 2, None, None, None, None, None, 0, None) == _lib.FDP_ERR_USAGE
+    emb = _lib.make_desc(B=2, T=20000, P=100, D=8)
+    assert lib.fdp_embedding_workspace_bytes(ctypes.byref(emb), ctypes.byref(nb)) == _lib.FDP_ERR_SHAPE
+    emb = _lib.make_desc(B=2000, T=16, P=100, D=8)
+    assert lib.fdp_embedding_workspace_bytes(ctypes.byref(emb), ctypes.byref(nb)) == _lib.FDP_ERR_SHAPE
+    emb = _lib.make_desc(B=2, T=16, P=100, D=8)
+    assert lib.fdp_embedding_workspace_bytes(ctypes.byref(emb), ctypes.byref(nb)) == 0 and nb.value > 0
+    small = ctypes.c_size_t(nb.value - 1)
+    assert lib.fdp_embedding_dw(ctypes.byref(emb), ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16),
+                                None, ctypes.c_void_p(16), small, None) == _lib.FDP_ERR_CAPACITY
