@@ -270,10 +270,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const bool atomic_groups = reduce_scatter && !p.deterministic;
     const bool pre_noise = ((fused || (p.mode == MODE_REWEIGHT && !p.epi_noise)) && p.add_noise) || atomic_groups;
     const bool rmw_store = pre_noise || p.accumulate;
-    // MODE_REWEIGHT with p.epi_noise (Philox, <= 2 samples per tile; host choice):
+    // MODE_REWEIGHT with p.epi_noise (Philox; host default, FDP_EPI_NOISE=0 turns it off):
     // the epilogue starts each tile's accumulator at sigma*C*N(key, d*P + p), so
-    // the tile leaves with a plain TMA store and no grad_w pre-fill. With more
-    // samples per tile the noise warps' pre-fill + TMA reduce-add is cheaper.
+    // the tile leaves with a plain TMA store and no grad_w pre-fill.
     const bool epi_noise = p.mode == MODE_REWEIGHT && p.add_noise && p.epi_noise;
     uint64_t nkb = p.key_base;
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
