@@ -65,7 +65,12 @@ def main():
                  "wait_tmem_us_med": round(float(np.median(lead[:, 0])) / 1e3, 2),
                  "wait_operands_us_med": round(float(np.median(lead[:, 1])) / 1e3, 2),
                  "issue_span_us_med": round(float(np.median(lead[:, 2])) / 1e3, 2),
-                 "units_med": float(np.median(lead[:, 3]))} if len(lead) else {}
+                 "units_med": float(np.median(lead[:, 3])),
+                 # spread over the MMA-issuing CTAs: imbalance of the packed layer ranges
+                 "issue_span_us_min": round(float(np.min(lead[:, 2])) / 1e3, 2),
+                 "issue_span_us_max": round(float(np.max(lead[:, 2])) / 1e3, 2),
+                 "wait_operands_us_max": round(float(np.max(lead[:, 1])) / 1e3, 2),
+                 "units_min": float(np.min(lead[:, 3])), "units_max": float(np.max(lead[:, 3]))} if len(lead) else {}
     print(json.dumps({"noise": noise, "sigma": sigma, "B": B, "T": T, "layers": out, "mma_issuer": mma_stats}))
 
 
