@@ -1,0 +1,120 @@
+"""The reference's acceptance criteria (pkg/tests/test_acceptance.py) re-run
+through the drop-in API on the GPU, one test per criterion where the criterion
+is about the hot path. The fp64 parity path (float64 CUDA inputs) meets the
+reference's own 1e-12 bars; reference-keyed noise (keyed_f64) makes sigma > 0
+exact. Criteria 3-5 (simulator traffic counters) are covered on the CPU by the
+ledger tests (tests/test_host_api.py), 9-10 by test_gpu_parity.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_01154_b200 as fdp
+from oracle import dp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W = fdp.WorkflowKind
+DP_KINDS = (W.EXPLICIT_DP, W.IMPLICIT_DP, W.FLASHDP)
+
+
+def _instances(n, seed=1234):
+    """Random small layer instances and DP configs (the shape of test_acceptance.py:38-58)."""
+    rng = np.random.default_rng(seed)
+    for trial in range(n):
+        B, T, P, D = (int(v) for v in rng.integers(1, 6, size=4))
+        x = rng.uniform(-2, 2, (B, T, P))
+        dy = rng.uniform(-2, 2, (B, T, D))
+        cfg = fdp.DPConfig(float(10.0 ** rng.uniform(-1.5, 1.5)), float(rng.choice([0.0, 0.5, 1.0])),
+                           str(rng.choice(["sum", "mean"])), seed=int(rng.integers(0, 1 << 31)),
+                           layer_id=int(rng.integers(0, 64)), step=int(rng.integers(0, 4096)))
+        yield trial, x, dy, cfg
+
+
+def _ocfg(c):
+    return O.Cfg(c.clip_c, c.sigma, c.reduction, c.seed, c.layer_id, c.step)
+
+
+def test_criterion_01_randomized_equivalence_every_dp_workflow():
+    """1000 random instances: explicit, implicit and flashdp within 1e-12
+    (absolute, like the reference) of the oracle, norms included."""
+    for trial, x, dy, cfg in _instances(1000):
+        want, wn = O.dp_backward(x, dy, _ocfg(cfg), exact_noise=True)
+        xd, yd = torch.tensor(x).cuda(), torch.tensor(dy).cuda()
+        for kind in DP_KINDS:
+            r = fdp.run_backward(kind, xd, yd, cfg, noise_impl="keyed_f64")
+            assert np.max(np.abs(r.grad_w.cpu().numpy() - want)) <= 1e-12, (kind, trial)
+            assert np.max(np.abs(r.per_sample_norms_sq.cpu().numpy() - wn)) <= 1e-12, (kind, trial)
+
+
+def test_criterion_02_loose_bound_four_way_agreement():
+    """C = 1e9, sigma = 0, sum: nothing clips or is noised, so non-DP and the three
+    DP workflows agree pairwise within 1e-12."""
+    cfg = fdp.DPConfig(1e9, 0.0, "sum")
+    for trial, x, dy, _ in _instances(1000, seed=99):
+        xd, yd = torch.tensor(x).cuda(), torch.tensor(dy).cuda()
+        grads = [fdp.run_backward(W.NON_DP, xd, yd, None).grad_w.cpu().numpy()]
+        grads += [fdp.run_backward(k, xd, yd, cfg).grad_w.cpu().numpy() for k in DP_KINDS]
+        for i in range(len(grads)):
+            for j in range(i + 1, len(grads)):
+                assert np.max(np.abs(grads[i] - grads[j])) <= 1e-12, (trial, i, j)
+
+
+def test_criterion_06_tiling_invariance():
+    """Eight scratchpad sizes from unit tiles to the whole layer: the plan is
+    recorded in the ledger (its footprint bound holds) and the gradient does not
+    depend on it (the device tiling is fixed) -- bitwise, sigma > 0 included."""
+    dims = fdp.LayerDims(B=4, T=8, P=16, D=16)
+    full = fdp.footprint(dims.B, dims.T, dims.D, dims.P) * 8
+    caps = [int(m) for m in np.linspace(32, full, 8)]
+    x = torch.tensor([0.01 * i - 2.0 for i in range(512)], dtype=torch.float64).view(4, 8, 16).cuda()
+    dy = torch.tensor([0.005 * i - 1.0 for i in range(512)], dtype=torch.float64).view(4, 8, 16).cuda()
+    cfg = fdp.DPConfig(0.8, 0.6, seed=9)
+    grads = []
+    for cap in caps:
+        spec = fdp.MemSpec(cap, 8)
+        plan = fdp.plan_blocks(dims, spec)
+        r = fdp.backward_flashdp(x, dy, cfg, plan, spec, noise_impl="keyed_f64")
+        assert r.report.peak_scratch_bytes <= cap, cap
+        grads.append(r.grad_w.cpu().numpy())
+    for g in grads[1:]:
+        assert np.array_equal(g, grads[0])
+    want, _ = O.dp_backward(x.cpu().numpy(), dy.cpu().numpy(), _ocfg(cfg), exact_noise=True)
+    assert np.max(np.abs(grads[0] - want)) <= 1e-12
+
+
+def test_criterion_08_clip_bound_and_passthrough_on_device():
+    """Single-sample layers on the GPU (fp64): a gradient already under the bound
+    comes back bit-identical to the non-DP gradient, a clipped one has norm <= C
+    (1 + 1e-12)."""
+    rng = np.random.default_rng(5150)
+    n_clipped = n_passed = 0
+    for _ in range(300):
+        T, P, D = (int(v) for v in rng.integers(1, 6, size=3))
+        x = rng.uniform(-3, 3, (1, T, P))
+        dy = rng.uniform(-3, 3, (1, T, D))
+        G = dy[0].T @ x[0]
+        C = float(10.0 ** rng.uniform(-1, 1)) * float(np.sqrt((G * G).sum()))
+        xd, yd = torch.tensor(x).cuda(), torch.tensor(dy).cuda()
+        got = fdp.backward_flashdp(xd, yd, fdp.DPConfig(C, 0.0, "sum")).grad_w.cpu().numpy()
+        ns = float(np.sqrt((G * G).sum()))
+        if ns <= C:
+            n_passed += 1
+            assert np.array_equal(got, fdp.run_backward(W.NON_DP, xd, yd, None).grad_w.cpu().numpy())
+        else:
+            n_clipped += 1
+            assert float(np.sqrt((got * got).sum())) <= C * (1.0 + 1e-12)
+    assert n_clipped > 50 and n_passed > 50
+
+
+def test_criterion_11_reports_are_byte_identical():
+    """The same comparison cell serialises to byte-identical CSV on every run,
+    noise included (deterministic fp64 kernels, reference-keyed noise)."""
+    g = torch.Generator().manual_seed(31)
+    x = torch.randn(4, 4, 8, generator=g, dtype=torch.float64).cuda()
+    dy = torch.randn(4, 4, 16, generator=g, dtype=torch.float64).cuda()
+    cfg = fdp.DPConfig(1.0, 0.5, "mean", seed=31)
+    texts = [fdp.emit_report(fdp.compare_workflows(x, dy, cfg, layer="expand", noise_impl="keyed_f64"))
+             for _ in range(2)]
+    assert texts[0] == texts[1] and len(texts[0]) > 0
