@@ -832,3 +832,38 @@ def test_package_train_demo_reproduces_reference_curves(opt):
         for wf, losses in per_wf.items():
             want = g[f"{opt}_{sigma}_{wf}"]
             assert np.max(np.abs(np.array(losses) - want)) <= 1e-9, (opt, sigma, wf)
+
+
+def test_bench_workload_full_size_properties():
+    """The bench's own workload at full size (GPT-2 small, 48 linear layers, B=8,
+    T=1024, sigma=1, C=1, Philox) through the one-launch group: every layer equals
+    its per-layer fused call, the noise is exactly sigma*C*N (out(sigma) - out(0)
+    == noise_range), and one layer of each shape matches the fp64 oracle on the
+    same bf16 inputs (sigma = 0)."""
+    shapes = [(768, 2304), (768, 768), (768, 3072), (3072, 768)]
+    B, T = 8, 1024
+    layers0, layers1 = [], []
+    g = torch.Generator(device="cuda").manual_seed(4)
+    for blk in range(12):
+        for j, (P, D) in enumerate(shapes):
+            x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
+            dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+            lid = 4 * blk + j
+            layers0.append((x, dy, fdp.DPConfig(1.0, 0.0, "mean", seed=1, layer_id=lid, step=3)))
+            layers1.append((x, dy, fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=lid, step=3)))
+    g0 = fdp.PreparedGroup(layers0, noise_impl="philox")
+    g1 = fdp.PreparedGroup(layers1, noise_impl="philox")
+    g0()
+    g1()
+    torch.cuda.synchronize()
+    for i, (x, dy, cfg) in enumerate(layers1):
+        n = fdp.noise_range(cfg, 0, x.shape[2] * dy.shape[2], 1.0, noise_impl="philox").view(dy.shape[2], x.shape[2])
+        assert rel(host(g1.grads[i] - g0.grads[i]), host(n)) < 1e-4, i
+        if i % 13 == 0:  # spot-check per-layer calls
+            single = fdp.backward_flashdp(x, dy, layers0[i][2], path="fused", noise_impl="philox")
+            assert rel(host(g0.grads[i]), host(single.grad_w)) < 1e-5, i
+    for i in range(4):
+        x, dy, cfg = layers0[i]
+        want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=False)
+        assert rel(host(g0.grads[i]), want) < BF16_TOL, i
+        assert rel(host(g0.norms[i]), wn) < BF16_TOL, i
