@@ -189,3 +189,40 @@ def test_two_ranks_full_dp_gpt2_equals_single_process():
     assert len(one) == len(two)
     for a, b in zip(one, two):
         assert np.max(np.abs(a - b)) <= 2e-2 * max(float(np.max(np.abs(a))), 1e-6)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_rank_partitioned_noise_sums_to_single_gpu(world):
+    """SURVEY 8e for W in {1, 2, 4, 8}: each rank runs its slice of the batch with
+    noise on its slice of [0, D*P) only and the global-batch mean; the sum over
+    ranks equals the one-process result, and the per-rank noise parts are disjoint
+    and add up to the W = 1 noise (reference-keyed: exact draws)."""
+    import paper_2507_01154_b200 as fdp
+
+    g = torch.Generator().manual_seed(17)
+    B, T, P, D = 8, 96, 256, 384
+    x = torch.randn(B, T, P, generator=g).to(torch.bfloat16).cuda()
+    dy = (torch.randn(B, T, D, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    cfg = fdp.DPConfig(0.4, 1.0, "mean", seed=8, layer_id=2, step=6)
+    cfg0 = fdp.DPConfig(0.4, 0.0, "mean", seed=8, layer_id=2, step=6)
+    one = fdp.backward_flashdp(x, dy, cfg, noise_impl="keyed_f64").grad_w
+    one0 = fdp.backward_flashdp(x, dy, cfg0, noise_impl="keyed_f64").grad_w
+    total = torch.zeros_like(one)
+    noise_parts = []
+    for r in range(world):
+        lo, hi = B * r // world, B * (r + 1) // world
+        xs, ys = x[lo:hi].contiguous(), dy[lo:hi].contiguous()
+        kw = dict(noise_impl="keyed_f64", rank=r, world=world, mean_batch=B)
+        out = fdp.backward_flashdp(xs, ys, cfg, **kw).grad_w
+        out0 = fdp.backward_flashdp(xs, ys, cfg0, **kw).grad_w
+        total += out
+        noise_parts.append((out - out0).reshape(-1))
+    scale = float(one.abs().max())
+    assert float((total - one).abs().max()) <= 1e-5 * scale
+    full_noise = (one - one0).reshape(-1)
+    n = P * D
+    for r, part in enumerate(noise_parts):
+        lo, hi = n * r // world, n * (r + 1) // world
+        assert float(part[:lo].abs().max() if lo else 0.0) <= 1e-5 * scale  # nothing outside the slice
+        assert float(part[hi:].abs().max() if hi < n else 0.0) <= 1e-5 * scale
+        assert float((part[lo:hi] - full_noise[lo:hi]).abs().max()) <= 1e-5 * scale
