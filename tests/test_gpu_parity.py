@@ -867,3 +867,30 @@ def test_bench_workload_full_size_properties():
         want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=False)
         assert rel(host(g0.grads[i]), want) < BF16_TOL, i
         assert rel(host(g0.norms[i]), wn) < BF16_TOL, i
+
+
+def test_kernel_noise_statistics_across_ranks_and_layers():
+    """SURVEY 8c for sigma > 0 with Philox: the noise the fused kernel adds
+    (out(sigma) - out(0)) has mean 0 and variance (sigma C)^2, and the parts of two
+    ranks and of two layers are uncorrelated."""
+    B, T, P, D = 4, 128, 1024, 1024
+    x, dy = randn(B, T, P, D, seed=23, scale_dy=1e-2)
+    sC = 0.5 * 1.3
+    parts = {}
+    for lid in (0, 1):
+        for r in (0, 1):
+            kw = dict(path="fused", noise_impl="philox", rank=r, world=2)
+            c1 = fdp.DPConfig(0.5, 1.3, "mean", seed=4, layer_id=lid, step=9)
+            c0 = fdp.DPConfig(0.5, 0.0, "mean", seed=4, layer_id=lid, step=9)
+            diff = (fdp.backward_flashdp(x, dy, c1, **kw).grad_w - fdp.backward_flashdp(x, dy, c0, **kw).grad_w)
+            flat = host(diff).reshape(-1)
+            half = flat.size // 2
+            parts[(lid, r)] = flat[half * r: half * (r + 1)]  # the rank's slice; the rest is 0
+            other = flat[half * (1 - r): half * (2 - r)]
+            assert np.max(np.abs(other)) < 1e-6 * sC
+    for z in parts.values():
+        z = z / sC
+        assert abs(z.mean()) < 6e-3 and abs(z.var() - 1.0) < 1.5e-2
+    n = min(len(v) for v in parts.values())
+    assert abs(np.corrcoef(parts[(0, 0)][:n], parts[(0, 1)][:n])[0, 1]) < 6e-3   # across ranks
+    assert abs(np.corrcoef(parts[(0, 0)][:n], parts[(1, 0)][:n])[0, 1]) < 6e-3   # across layers
