@@ -212,10 +212,18 @@ def main():
             dist.destroy_process_group()
         return
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # test hooks: run the N>1 code path on a one-GPU box (every rank on cuda:0, gloo);
+    # the driver's multi-GPU runs use one GPU per rank and NCCL
+    same_gpu = os.environ.get("FDP_BENCH_SAME_GPU") == "1"
+    backend = os.environ.get("FDP_BENCH_BACKEND", "nccl")
+    dev_index = 0 if same_gpu else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2507_01154_b200 as fdp
 
@@ -297,7 +305,7 @@ def main():
         graph.replay()
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     time.sleep(0.3)
     if world > 1:
