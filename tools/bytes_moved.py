@@ -3,8 +3,11 @@ movement against the naive explicit per-sample-gradient (Opacus-style) kernel).
 
 Run under ncu so every kernel's dram__bytes_{read,write}.sum is recorded:
 
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+    FDP_NO_COOP=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
         --csv --log-file gpurun_out/bytes.csv python tools/bytes_moved.py
+
+(FDP_NO_COOP=1: ncu's kernel replay cannot re-launch cooperative cluster grids; the
+grids are co-resident either way.)
     python tools/bytes_moved.py --summarize gpurun_out/bytes.csv > profiles/r1_bytes_moved.json
 
 Each workflow runs once on the same inputs, separated by marker kernels
