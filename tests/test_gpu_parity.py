@@ -894,3 +894,23 @@ def test_kernel_noise_statistics_across_ranks_and_layers():
     n = min(len(v) for v in parts.values())
     assert abs(np.corrcoef(parts[(0, 0)][:n], parts[(0, 1)][:n])[0, 1]) < 6e-3   # across ranks
     assert abs(np.corrcoef(parts[(0, 0)][:n], parts[(1, 0)][:n])[0, 1]) < 6e-3   # across layers
+
+
+@pytest.mark.parametrize("epi", ["0", "1"])
+def test_stream_multicast_keyed_noise_and_accumulate(epi, monkeypatch):
+    """4-CTA multicast layout with reference-keyed noise (noise-warp pre-fill of
+    split and whole tiles), accumulation onto grad_out and a rank slice: exact
+    against the oracle on the same bf16 inputs."""
+    monkeypatch.setenv("FDP_STREAM_MC", "1")
+    monkeypatch.setenv("FDP_EPI_NOISE", epi)
+    B, T, P, D = 3, 200, 2048, 640
+    x, dy = randn(B, T, P, D, seed=61, scale_dy=1e-2)
+    cfg = fdp.DPConfig(0.6, 0.9, "mean", seed=12, layer_id=4, step=2)
+    g0 = torch.randn(D, P, device="cuda") * 0.01
+    out = g0.clone()
+    r = fdp.backward_flashdp(x, dy, cfg, path="two_phase", noise_impl="keyed_f64", grad_out=out, accumulate=True,
+                             rank=1, world=3)
+    n = P * D
+    want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True, noise_lo=n // 3, noise_hi=2 * n // 3)
+    assert rel(host(r.grad_w), want + host(g0)) < BF16_TOL
+    assert rel(host(r.per_sample_norms_sq), wn) < BF16_TOL
