@@ -1229,6 +1229,7 @@ int fdp_embedding_dw(const fdp_desc* d, const int64_t* tokens, const void* dy, f
   int rc = fdp_embedding_workspace_bytes(d, &need);
   if (rc) return rc;
   if (!tokens || !dy || !grad) return fail(FDP_ERR_USAGE, "null tensor pointer");
+  if (reinterpret_cast<uintptr_t>(grad) % 16 != 0) return fail(FDP_ERR_USAGE, "grad must be 16-byte aligned");
   if ((rc = check_ws(ws, ws_bytes, need))) return rc;
   const Common c = common_of(d);
   cudaError_t e = fdp::emb_dp(reinterpret_cast<const long long*>(tokens), dy, d->in_dtype == FDP_DTYPE_F32,

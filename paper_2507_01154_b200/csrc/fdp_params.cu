@@ -278,14 +278,58 @@ __global__ void __launch_bounds__(kVCols) k_emb_norms(const uint64_t* __restrict
   }
 }
 
-// out[v][c] (+)= sum_b c_b sum_{t: tok_bt = v} dY[b,t,c] + sigma C N(v*D + c), every row v.
-// One pre-pass per block finds each sample's sorted range of every row of the
-// block's kEVRows vocabulary rows (one barrier); the row loop then runs barrier-
-// free: untouched rows are a pure noise write, touched rows sum their runs.
+// The table's base: out = (accumulate ? out : 0) + sigma C N(flat index) on [lo, hi),
+// a streaming pass over every row (untouched rows get their noise only). kMode 1:
+// Philox over the whole table (one draw call per float4), 0: any generator with
+// per-element range checks, 2: no noise (zero fill; nothing to do when accumulating).
+template <int kMode>
+__global__ void __launch_bounds__(256, 6) k_emb_fill(float* __restrict__ out, long long n, int accumulate,
+                                                     NoiseKey nk) {
+  nk_resolve(nk);
+  const long long n4 = n >> 2;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (kMode == 1) {
+      z = philox_normal4(nk.base, static_cast<uint64_t>(i));
+    } else if constexpr (kMode == 0) {
+      const long long e = i << 2;
+      if (e + 3 >= nk.lo && e < nk.hi) {
+        const float4 q = noise_draw4(nk.impl, nk.base_g, nk.base, static_cast<uint64_t>(i));
+        z.x = (e + 0 >= nk.lo && e + 0 < nk.hi) ? q.x : 0.f;
+        z.y = (e + 1 >= nk.lo && e + 1 < nk.hi) ? q.y : 0.f;
+        z.z = (e + 2 >= nk.lo && e + 2 < nk.hi) ? q.z : 0.f;
+        z.w = (e + 3 >= nk.lo && e + 3 < nk.hi) ? q.w : 0.f;
+      }
+    }
+    float4 v = make_float4(nk.scale * z.x, nk.scale * z.y, nk.scale * z.z, nk.scale * z.w);
+    if (kMode == 2) v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate) {
+      const float4 p = __ldcs(o4 + i);
+      v.x += p.x;
+      v.y += p.y;
+      v.z += p.z;
+      v.w += p.w;
+    }
+    __stcs(o4 + i, v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {  // tail of a table whose size is not a multiple of 4
+    const long long e = (n4 << 2) + threadIdx.x;
+    float v = (kMode != 2 && e >= nk.lo && e < nk.hi) ? nk.scale * nk_draw(nk, static_cast<uint64_t>(e)) : 0.f;
+    if (accumulate) v += out[e];
+    out[e] = v;
+  }
+}
+
+// out[v][c] += sum_b c_b sum_{t: tok_bt = v} dY[b,t,c] for the rows some sample
+// touches (after k_emb_fill). One pre-pass per block finds each sample's sorted
+// range of every row of the block's kEVRows vocabulary rows (one barrier); the
+// row loop then runs barrier-free over the touched rows, samples in fixed order.
 template <typename T>
-__global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
+__global__ void __launch_bounds__(256) k_emb_add(const uint64_t* __restrict__ keys, const T* __restrict__ dy,
                                                  const float* __restrict__ factors, int B, int T_, long long V, int D,
-                                                 float* out, int accumulate, NoiseKey nk) {
+                                                 float* out) {
   extern __shared__ int sm[];  // bound[B][kEVRows + 1]; fac[B]; touched[kEVRows]
   int* bound = sm;
   float* fac = reinterpret_cast<float*>(sm + B * (kEVRows + 1));
@@ -313,60 +357,35 @@ __global__ void __launch_bounds__(256) k_emb_out(const uint64_t* __restrict__ ke
     bd[nrows] = e;
     fac[b] = factors[b];
   }
-  nk_resolve(nk);
   __syncthreads();
   const bool vec = (D & 3) == 0;
   for (int c0 = blockIdx.y * kECols + 4 * threadIdx.x; c0 < D && c0 < (blockIdx.y + 1) * kECols; c0 += 4 * 256) {
     for (int r = 0; r < nrows; ++r) {
-      const long long v = v0 + r;
+      if (!touched[r]) continue;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (touched[r]) {
-        for (int b = 0; b < B; ++b) {
-          const int* bd = bound + b * (kEVRows + 1);
-          const uint64_t* K = keys + static_cast<long long>(b) * T_;
-          for (int k = bd[r]; k < bd[r + 1]; ++k) {
-            const long long row = (static_cast<long long>(b) * T_ + static_cast<long long>(K[k] & 0xffffffffull)) * D;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (c0 + j < D) acc[j] = fmaf(fac[b], ld(dy, row + c0 + j), acc[j]);
-          }
-        }
-      }
-      const long long f0 = v * D + c0;
-      float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (nk.add_noise) {
-        if (vec && f0 >= nk.lo && f0 + 3 < nk.hi) {
-          const float4 q = noise_draw4(nk.impl, nk.base_g, nk.base, static_cast<uint64_t>(f0 >> 2));
-          z[0] = q.x;
-          z[1] = q.y;
-          z[2] = q.z;
-          z[3] = q.w;
-        } else {
+      for (int b = 0; b < B; ++b) {
+        const int* bd = bound + b * (kEVRows + 1);
+        const uint64_t* K = keys + static_cast<long long>(b) * T_;
+        for (int k = bd[r]; k < bd[r + 1]; ++k) {
+          const long long row = (static_cast<long long>(b) * T_ + static_cast<long long>(K[k] & 0xffffffffull)) * D;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (c0 + j < D && f0 + j >= nk.lo && f0 + j < nk.hi) z[j] = nk_draw(nk, static_cast<uint64_t>(f0 + j));
+            if (c0 + j < D) acc[j] = fmaf(fac[b], ld(dy, row + c0 + j), acc[j]);
         }
       }
+      const long long f0 = (v0 + r) * D + c0;
       if (vec) {
-        float4 o = make_float4(acc[0] + nk.scale * z[0], acc[1] + nk.scale * z[1], acc[2] + nk.scale * z[2],
-                               acc[3] + nk.scale * z[3]);
         float4* po = reinterpret_cast<float4*>(out + f0);
-        if (accumulate) {
-          const float4 p = *po;
-          o.x += p.x;
-          o.y += p.y;
-          o.z += p.z;
-          o.w += p.w;
-        }
-        __stcs(po, o);
+        float4 o = *po;
+        o.x += acc[0];
+        o.y += acc[1];
+        o.z += acc[2];
+        o.w += acc[3];
+        *po = o;
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (c0 + j >= D) continue;
-          float r2 = acc[j] + nk.scale * z[j];
-          if (accumulate) r2 += out[f0 + j];
-          out[f0 + j] = r2;
-        }
+        for (int j = 0; j < 4; ++j)
+          if (c0 + j < D) out[f0 + j] += acc[j];
       }
     }
   }
@@ -466,22 +485,34 @@ cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, i
   if ((e = reduce_norms_to_factors(part, B, n_sc * n_dc, clip_c, clip_c * clip_c, inv_batch, norms_out, fac, s)) !=
       cudaSuccess)
     return e;
+  // base pass over the whole table: the noise (or zeros / the old values)
+  const long long n = V * static_cast<long long>(D);
+  const int fmode = !nk.add_noise || nk.hi <= nk.lo ? 2 : (nk.impl == 2 && nk.lo <= 0 && nk.hi >= n) ? 1 : 0;
+  if (!(fmode == 2 && accumulate)) {
+    long long blocks = (n / 4 + 255) / 256;
+    if (blocks > 148LL * 6 * 4) blocks = 148LL * 6 * 4;
+    if (blocks < 1) blocks = 1;
+    auto kf = fmode == 1 ? k_emb_fill<1> : fmode == 0 ? k_emb_fill<0> : k_emb_fill<2>;
+    kf<<<static_cast<int>(blocks), 256, 0, s>>>(out, n, accumulate, nk);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // the clipped sums onto the touched rows
   const dim3 g3(static_cast<unsigned>((V + kEVRows - 1) / kEVRows), (D + kECols - 1) / kECols);
   const size_t smem = emb_out_smem(B);
   static bool out_attr = false;
   if (!out_attr) {
-    if ((e = cudaFuncSetAttribute(k_emb_out<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(k_emb_add<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k_emb_out<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k_emb_add<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess)
       return e;
     out_attr = true;
   }
   if (in_f32)
-    k_emb_out<float><<<g3, 256, smem, s>>>(keys, static_cast<const float*>(dy), fac, B, T_, V, D, out, accumulate, nk);
+    k_emb_add<float><<<g3, 256, smem, s>>>(keys, static_cast<const float*>(dy), fac, B, T_, V, D, out);
   else
-    k_emb_out<__nv_bfloat16><<<g3, 256, smem, s>>>(keys, static_cast<const __nv_bfloat16*>(dy), fac, B, T_, V, D, out,
-                                                   accumulate, nk);
+    k_emb_add<__nv_bfloat16><<<g3, 256, smem, s>>>(keys, static_cast<const __nv_bfloat16*>(dy), fac, B, T_, V, D,
+                                                   out);
   return cudaGetLastError();
 }
 
