@@ -16,9 +16,9 @@
 // dY rows onto the rows of the sample's tokens, so ||G_b||^2 is the token-
 // equality Gram sum_{t,s: tok_t = tok_s} <dY_t, dY_s>. Each sample's (token,
 // position) keys are sorted once in shared memory; the norm pass sums dY rows per
-// run of equal tokens (never materialising G_b), and the output pass walks all
-// samples' sorted runs per vocabulary row in fixed order -- deterministic, no
-// atomics -- writing every row (untouched rows get their noise only).
+// run of equal tokens (never materialising G_b); a streaming pass writes every
+// row's noise, and the add pass walks all samples' sorted runs per vocabulary row
+// in fixed order onto the touched rows -- deterministic, no atomics.
 #include "../../include/fdp.h"
 #include "fdp_internal.h"
 #include "fdp_rng.cuh"
