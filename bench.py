@@ -270,26 +270,28 @@ def main():
     dom_events = []
 
     def step(record=False):
+        # launch on the CURRENT stream: inside torch.cuda.graph() that is the capture stream
+        st = torch.cuda.current_stream(dev)
         if group is not None:
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                group(stream)
-                e1.record(stream)
+                e0.record(st)
+                group(st)
+                e1.record(st)
                 dom_events.append((e0, e1))
             else:
-                group(stream)
+                group(st)
             device_step.add_(1)  # N>1: the chunked group already all-reduced every bucket
             return
         for name, c in calls:
             if record and name.endswith(".c_fc"):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                c(stream)
-                e1.record(stream)
+                e0.record(st)
+                c(st)
+                e1.record(st)
                 dom_events.append((e0, e1))
             else:
-                c(stream)
+                c(st)
         device_step.add_(1)
         if world > 1:
             dist.all_reduce(flat, op=dist.ReduceOp.SUM)
