@@ -914,3 +914,37 @@ def test_stream_multicast_keyed_noise_and_accumulate(epi, monkeypatch):
     want, wn = O.dp_backward(host(x), host(dy), ocfg(cfg), exact_noise=True, noise_lo=n // 3, noise_hi=2 * n // 3)
     assert rel(host(r.grad_w), want + host(g0)) < BF16_TOL
     assert rel(host(r.per_sample_norms_sq), wn) < BF16_TOL
+
+
+def test_group_launch_graph_capture_with_device_step():
+    """PreparedGroup inside a CUDA graph: replays run the persistent multi-layer
+    launch (not an empty graph), and the device step counter keys fresh noise per
+    replay exactly as direct calls with that step would."""
+    shapes = [(256, 768), (768, 256), (512, 512)]
+    B, T = 4, 128
+    layers = []
+    for i, (P, D) in enumerate(shapes):
+        x, dy = randn(B, T, P, D, seed=300 + i, scale_dy=1e-2)
+        layers.append((x, dy, fdp.DPConfig(0.3, 1.0, "mean", seed=2, layer_id=i, step=0)))
+    step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    grp = fdp.PreparedGroup(layers, noise_impl="philox", device_step=step)
+    grp()  # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g):
+            grp()
+            step.add_(1)
+    torch.cuda.current_stream().wait_stream(s)
+    for want_step in (0, 1, 2):
+        step.fill_(want_step)
+        for t in grp.grads:
+            t.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for i, (x, dy, cfg) in enumerate(layers):
+            c = fdp.DPConfig(cfg.clip_c, cfg.sigma, cfg.reduction, cfg.seed, cfg.layer_id, want_step)
+            ref = fdp.backward_flashdp(x, dy, c, path="fused", noise_impl="philox").grad_w
+            assert rel(host(grp.grads[i]), host(ref)) < 1e-5, (want_step, i)
