@@ -19,7 +19,13 @@
  *     need distinct workspaces: the workspace holds the in-kernel norm
  *     all-reduce counters (the analogue of memmodel.py:261-285).
  *   - A workspace must be zero-filled once before first use
- *     (fdp_workspace_init); every call leaves it zeroed again.
+ *     (fdp_workspace_init). Only its counter prefix has to stay zero between
+ *     calls (tile arrival / row-initialisation flags, exit counter): every call
+ *     leaves the counters of ITS layout zeroed, and a call whose layout differs
+ *     from the previous call's on the same workspace (a different shape, kind or
+ *     layer list) first zeroes the prefix on the stream (cudaMemsetAsync; always
+ *     done while the stream is being captured). Norm partials, clip factors and
+ *     explicit-path buffers are scratch: rewritten before they are read.
  *   - Return codes mirror the reference exception types (errors.py):
  *     FDP_ERR_SHAPE    -> ShapeError   (workflows.py:47-52)
  *     FDP_ERR_USAGE    -> UsageError   (dpcore.py:32-38, workflows.py:330-337)
@@ -195,6 +201,10 @@ FDP_API int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* 
 /* dpcore.noise_for_indices for flat indices [lo, hi) scaled by `scale`
  * (rng.keyed_normal_array, rng.py:69-85): out[i-lo] = scale * N(seed, layer_id, step, i). */
 FDP_API int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scale, void* stream);
+/* Same draws written as DOUBLE (the reference's own precision; with
+ * FDP_NOISE_KEYED_F64 the draw matches rng.keyed_normal_array to ~1e-15):
+ * dpcore.finalize_gradient / noise_for_indices on float64 gradients. */
+FDP_API int fdp_noise_f64(const fdp_desc* d, double* out, int64_t lo, int64_t hi, double scale, void* stream);
 
 /* Non-linear parameter groups (the reference clips linear
  * weights only). Each group is clipped per sample with its own norm at

@@ -33,7 +33,7 @@ FLAG_DETERMINISTIC = 8
 # Every symbol include/fdp.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
     "fdp_abi_version", "fdp_last_error", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes",
-    "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_partition",
+    "fdp_workspace_init", "fdp_backward", "fdp_dw", "fdp_noise", "fdp_noise_f64", "fdp_noise_partition",
     "fdp_group_workspace_bytes", "fdp_backward_group", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex",
     "fdp_sgd_step", "fdp_adam_step", "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_vec_workspace_bytes",
     "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
@@ -98,6 +98,8 @@ def load() -> ctypes.CDLL:
                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     lib.fdp_noise.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                               ctypes.c_double, ctypes.c_void_p]
+    lib.fdp_noise_f64.argtypes = [ctypes.POINTER(FdpDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_double, ctypes.c_void_p]
     lib.fdp_noise_partition.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     lib.fdp_group_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc),
@@ -125,7 +127,7 @@ def load() -> ctypes.CDLL:
     for name in ("fdp_vec_workspace_bytes", "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
                  "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",
-                 "fdp_dw", "fdp_noise", "fdp_noise_partition"):
+                 "fdp_dw", "fdp_noise", "fdp_noise_f64", "fdp_noise_partition"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -586,6 +586,57 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// ---- workspace counters (include/fdp.h "Workspace"). Every kernel that uses the
+// in-kernel counters (tile arrival / row-initialisation flags, exit counter) zeroes
+// them again when it exits, but only in ITS layout: the counter range of a call
+// lies at a shape-dependent place, so the first call with a new layout on a
+// workspace could find stale non-zero words there (norm partials, factors, another
+// layout's flags). The counters of every layout therefore live in one prefix
+// [0, prefix) of the workspace, and the prefix is zeroed on the stream before a
+// call whose layout differs from the previous call's on that workspace (and
+// always while a stream is being captured, so every CUDA graph carries its own
+// reset). Word 2 of the control block, the launch-tag generation of the tagged
+// norm partials, is never reset: tags keep increasing per workspace, so a stale
+// tagged partial can never pass for a fresh one.
+uint64_t sig_mix(uint64_t h, uint64_t v) {
+  h ^= v + kGamma + (h << 6) + (h >> 2);
+  return fdp::mix64(h);
+}
+
+std::mutex g_ws_mu;
+std::map<uintptr_t, uint64_t> g_ws_sig;
+
+int ws_prepare(void* ws, uint64_t sig, size_t prefix, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+  bool need = true;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    const uintptr_t key = reinterpret_cast<uintptr_t>(ws);
+    auto it = g_ws_sig.find(key);
+    if (st == cudaStreamCaptureStatusNone && it != g_ws_sig.end() && it->second == sig) need = false;
+    if (g_ws_sig.size() > 4096) g_ws_sig.clear();
+    g_ws_sig[key] = sig;
+  }
+  if (!need) return FDP_OK;
+  // exit counter + error word, then the counter arrays after the 256-byte control block
+  if ((e = cudaMemsetAsync(ws, 0, 8, s)) != cudaSuccess) return cuda_fail(e, "workspace counter reset");
+  if (prefix > 256 && (e = cudaMemsetAsync(static_cast<char*>(ws) + 256, 0, prefix - 256, s)) != cudaSuccess)
+    return cuda_fail(e, "workspace counter reset");
+  return FDP_OK;
+}
+
+uint64_t plan_sig(int32_t kind, const fdp_desc* d, const Plan& pl) {
+  uint64_t h = 0x5eed;
+  const long long v[] = {kind, pl.path, pl.norm_phase, pl.bn, pl.cg, pl.n_tiles, pl.n_wtiles, pl.stream_tiles,
+                         pl.stream_mc, pl.groups, static_cast<long long>(pl.off_tile_cnt),
+                         static_cast<long long>(pl.off_part), static_cast<long long>(pl.off_tag),
+                         static_cast<long long>(pl.off_acc), d->B};
+  for (long long x : v) h = sig_mix(h, static_cast<uint64_t>(x));
+  return h;
+}
+
 int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms, void* ws,
         size_t ws_bytes, cudaStream_t s) {
   int rc = validate(d, kind);
@@ -672,6 +723,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   }
 
   // ---- tensor-core paths
+  if ((rc = ws_prepare(ws, plan_sig(kind, d, pl), pl.off_part, s))) return rc;
   CUtensorMap tm_dy, tm_x;
   if ((rc = make_tmap(&tm_dy, dy, d->D, d->T, d->B))) return rc;
   if ((rc = make_tmap(&tm_x, x, d->P, d->T, d->B))) return rc;
@@ -820,6 +872,7 @@ struct GroupPlan {
   int bn = 0, cg = 1, grid = 0;
   std::vector<int> groups, c_off, n_dt2, n_pt, n_wtiles;
   std::vector<size_t> off_tagged, off_tile_cnt;
+  size_t prefix = 0;  // end of the counter prefix (ws_prepare)
   size_t total = 0;
 };
 
@@ -950,13 +1003,16 @@ int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, int
     }
   }
   if (!gpl.bn) return fail(FDP_ERR_USAGE, "a layer does not fit the co-resident fused grid; use fdp_backward per layer");
-  size_t off = 256;  // control words
+  size_t off = 256;  // control words, then every layer's tile counters (the reset prefix), then the partials
   for (int l = 0; l < n; ++l) {
-    const long long ntiles = static_cast<long long>(gpl.n_wtiles[l]) * gpl.cg;
-    gpl.off_tagged.push_back(off);
-    off = align_up(off + 8ull * descs[l].B * ntiles, 256);
     gpl.off_tile_cnt.push_back(off);
-    off = align_up(off + 4ull * ntiles, 256);
+    off += 4ull * gpl.n_wtiles[l] * gpl.cg;
+  }
+  off = align_up(off, 256);
+  gpl.prefix = off;
+  for (int l = 0; l < n; ++l) {
+    gpl.off_tagged.push_back(off);
+    off = align_up(off + 8ull * descs[l].B * gpl.n_wtiles[l] * gpl.cg, 256);
   }
   if (descs[0].flags & FDP_FLAG_TRACE) off += 2048ull * gpl.grid;  // [grid][256] u64
   gpl.total = off;
@@ -1066,6 +1122,16 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   if (!ws || ws_bytes < gpl.total)
     return fail(FDP_ERR_CAPACITY, "workspace of %zu bytes is smaller than the %zu bytes this call needs", ws_bytes,
                 gpl.total);
+  {
+    uint64_t h = sig_mix(0x9409, static_cast<uint64_t>(n));
+    h = sig_mix(h, static_cast<uint64_t>(gpl.bn * 4 + gpl.cg));
+    for (int l = 0; l < n; ++l) {
+      h = sig_mix(h, gpl.off_tile_cnt[l]);
+      h = sig_mix(h, gpl.off_tagged[l]);
+      h = sig_mix(h, static_cast<uint64_t>(gpl.n_wtiles[l]));
+    }
+    if ((rc = ws_prepare(ws, h, gpl.prefix, static_cast<cudaStream_t>(stream)))) return rc;
+  }
   static thread_local fdp::GroupParams gp;  // ~28 KB: keep it off the stack
   std::memset(&gp, 0, sizeof(gp));
   for (int l = 0; l < n; ++l) {
@@ -1135,6 +1201,19 @@ int fdp_noise(const fdp_desc* d, float* out, int64_t lo, int64_t hi, double scal
   cudaError_t e = fdp::noise_fill(out, lo, hi, scale, d->noise_impl, base, base + kGamma,
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "noise_fill");
+  return FDP_OK;
+}
+
+int fdp_noise_f64(const fdp_desc* d, double* out, int64_t lo, int64_t hi, double scale, void* stream) {
+  if (!d) return fail(FDP_ERR_USAGE, "null descriptor");
+  if (lo < 0 || hi < lo) return fail(FDP_ERR_USAGE, "bad index range [%lld, %lld)", (long long)lo, (long long)hi);
+  if (hi > lo && !out) return fail(FDP_ERR_USAGE, "null output");
+  if (d->noise_impl < FDP_NOISE_KEYED_F32 || d->noise_impl > FDP_NOISE_PHILOX)
+    return fail(FDP_ERR_USAGE, "unknown noise_impl %d", d->noise_impl);
+  const uint64_t base = absorb3(d->seed, d->layer_id, d->step);
+  cudaError_t e = fdp::noise_fill64(out, lo, hi, scale, d->noise_impl, base, base + kGamma,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "noise_fill64");
   return FDP_OK;
 }
 

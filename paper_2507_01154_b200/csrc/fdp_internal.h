@@ -248,5 +248,7 @@ cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const v
 
 cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int impl, uint64_t base,
                        uint64_t base_g, cudaStream_t s);
+cudaError_t noise_fill64(double* out, long long lo, long long hi, double scale, int impl, uint64_t base,
+                         uint64_t base_g, cudaStream_t s);
 
 }  // namespace fdp

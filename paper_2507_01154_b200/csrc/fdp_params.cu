@@ -465,12 +465,15 @@ cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, i
   float* fac = part + static_cast<long long>(B) * n_sc * n_dc;                     // [B]
   const int n2 = pow2_at_least(T_);
   const size_t sort_smem = sizeof(uint64_t) * n2;
-  static bool attr_done = false;
-  if (!attr_done) {
+  // function attributes are per device: track them per device ordinal
+  static bool attr_done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 63;
+  if (!attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_emb_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sizeof(uint64_t) * emb_max_tokens()));
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done[dev] = true;
   }
   k_emb_sort<<<B, 1024, sort_smem, s>>>(tokens, T_, V, n2, keys);
   cudaError_t e = cudaGetLastError();
@@ -499,14 +502,14 @@ cudaError_t emb_dp(const long long* tokens, const void* dy, int in_f32, int B, i
   // the clipped sums onto the touched rows
   const dim3 g3(static_cast<unsigned>((V + kEVRows - 1) / kEVRows), (D + kECols - 1) / kECols);
   const size_t smem = emb_out_smem(B);
-  static bool out_attr = false;
-  if (!out_attr) {
+  static bool out_attr[64] = {};
+  if (!out_attr[dev]) {
     if ((e = cudaFuncSetAttribute(k_emb_add<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k_emb_add<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(emb_out_smem(emb_max_batch())))) != cudaSuccess)
       return e;
-    out_attr = true;
+    out_attr[dev] = true;
   }
   if (in_f32)
     k_emb_add<float><<<g3, 256, smem, s>>>(keys, static_cast<const float*>(dy), fac, B, T_, V, D, out);

@@ -201,6 +201,17 @@ __global__ void k_noise_fill(float* out, long long lo, long long hi, float scale
   }
 }
 
+__global__ void k_noise_fill64(double* out, long long lo, long long hi, double scale, int impl, uint64_t base,
+                               uint64_t base_g) {
+  for (long long i = lo + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < hi;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (impl == 1)
+      out[i - lo] = scale * keyed_normal_f64(base_g, static_cast<uint64_t>(i));
+    else
+      out[i - lo] = scale * static_cast<double>(noise_draw(impl, base_g, base, static_cast<uint64_t>(i)));
+  }
+}
+
 // kMode: 0 = any noise impl (per-element range checks), 1 = Philox with the whole
 // range noised, 2 = no noise. The Philox / no-noise variants are lean enough
 // to keep 48 warps per SM streaming, which the elementwise pass needs to reach
@@ -357,6 +368,13 @@ cudaError_t noise_fill(float* out, long long lo, long long hi, double scale, int
                        uint64_t base_g, cudaStream_t s) {
   if (hi <= lo) return cudaSuccess;
   k_noise_fill<<<grid_for(hi - lo, 256), 256, 0, s>>>(out, lo, hi, static_cast<float>(scale), impl, base, base_g);
+  return cudaGetLastError();
+}
+
+cudaError_t noise_fill64(double* out, long long lo, long long hi, double scale, int impl, uint64_t base,
+                         uint64_t base_g, cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  k_noise_fill64<<<grid_for(hi - lo, 256), 256, 0, s>>>(out, lo, hi, scale, impl, base, base_g);
   return cudaGetLastError();
 }
 

@@ -149,12 +149,12 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     if grad_out is None:
         grad = (torch.zeros if accumulate else torch.empty)((dims.D, dims.P), dtype=out_dtype, device=device)
     else:
-        if tuple(grad_out.shape) != (dims.D, dims.P) or grad_out.dtype != out_dtype or not grad_out.is_contiguous():
-            raise ShapeError(f"grad_out must be a contiguous {out_dtype} ({dims.D}, {dims.P}) tensor")
+        _check_out(grad_out, (dims.D, dims.P), out_dtype, device, "grad_out")
         grad = grad_out
     if kind == WorkflowKind.NON_DP:
         norms = None
     elif norms_out is not None:
+        _check_out(norms_out, (dims.B,), out_dtype, device, "norms_out")
         norms = norms_out
     else:
         norms = torch.empty(dims.B, dtype=out_dtype, device=device)
@@ -194,6 +194,15 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         n_host = norms.double().cpu().numpy() if norms is not None else np.zeros(0)
         return BackwardResult(g_host, report, n_host)
     return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device))
+
+
+def _check_out(t: torch.Tensor, shape: tuple, dtype: torch.dtype, device: torch.device, name: str) -> None:
+    """Caller-supplied outputs are written by the kernels through raw pointers:
+    shape, dtype (float64 on the fp64 path), contiguity and device must match."""
+    if not isinstance(t, torch.Tensor) or tuple(t.shape) != tuple(shape) or t.dtype != dtype \
+            or not t.is_contiguous() or t.device != device:
+        got = (tuple(t.shape), t.dtype, t.device) if isinstance(t, torch.Tensor) else type(t)
+        raise ShapeError(f"{name} must be a contiguous {dtype} {tuple(shape)} tensor on {device}, got {got}")
 
 
 def _step_ptr(t: Optional[torch.Tensor]):
@@ -243,9 +252,17 @@ class PreparedBackward:
         nbytes = ctypes.c_size_t()
         _lib.check(lib.fdp_workspace_bytes(ctypes.byref(self.desc), self._k, ctypes.byref(nbytes)))
         dev = x.device
-        self.grad_w = grad_w if grad_w is not None else torch.zeros((dims.D, dims.P), dtype=torch.float32, device=dev)
-        self.norms_sq = None if kind == WorkflowKind.NON_DP else (
-            norms_sq if norms_sq is not None else torch.zeros(dims.B, dtype=torch.float32, device=dev))
+        # the fp64 parity path writes float64 outputs (include/fdp.h FDP_DTYPE_F64)
+        out_dtype = torch.float64 if x.dtype == torch.float64 else torch.float32
+        if grad_w is not None:
+            _check_out(grad_w, (dims.D, dims.P), out_dtype, dev, "grad_w")
+        self.grad_w = grad_w if grad_w is not None else torch.zeros((dims.D, dims.P), dtype=out_dtype, device=dev)
+        if kind == WorkflowKind.NON_DP:
+            self.norms_sq = None
+        else:
+            if norms_sq is not None:
+                _check_out(norms_sq, (dims.B,), out_dtype, dev, "norms_sq")
+            self.norms_sq = norms_sq if norms_sq is not None else torch.zeros(dims.B, dtype=out_dtype, device=dev)
         if workspace is None:
             workspace = torch.zeros(max(nbytes.value, 4096), dtype=torch.uint8, device=dev)
         elif workspace.numel() * workspace.element_size() < nbytes.value:
@@ -299,6 +316,10 @@ class PreparedGroup:
                                       step=cfg.step, rank=rank, world=world, mean_batch=mean_batch,
                                       accumulate=accumulate, add_noise=add_noise, noise_impl=noise_impl,
                                       device_step=_step_ptr(device_step))
+            if grads is not None:
+                _check_out(grads[i], (dims.D, dims.P), torch.float32, x.device, f"grads[{i}]")
+            if norms is not None:
+                _check_out(norms[i], (dims.B,), torch.float32, x.device, f"norms[{i}]")
             g = grads[i] if grads is not None else torch.zeros((dims.D, dims.P), dtype=torch.float32, device=x.device)
             nrm = norms[i] if norms is not None else torch.zeros(dims.B, dtype=torch.float32, device=x.device)
             self.grads.append(g)
@@ -372,6 +393,9 @@ class HostStreamedBackward:
         comp_done = [torch.cuda.Event() for _ in range(n)]
         results = []
         pending = []  # device tensors kept alive until the copy-out stream is synchronised
+        # the copy-in stream writes device slots that earlier work on the compute stream may
+        # still read (slots of a previous call, blocks the caching allocator recycled)
+        self._in.wait_stream(comp)
         for i, (x, dy, cfg) in enumerate(layers):
             dims = _dims(x, dy)
             if not (isinstance(x, torch.Tensor) and isinstance(dy, torch.Tensor)) or x.is_cuda or dy.is_cuda:

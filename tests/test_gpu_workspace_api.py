@@ -1,0 +1,124 @@
+"""Boundary hygiene on the GPU: workspace counters across
+layout changes, float64 outputs of the prepared calls, output validation, and
+the float64 dpcore drop-ins at the reference's 1e-12 tolerance."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_01154_b200 as fdp
+from oracle import dp_oracle as O
+
+pytestmark = pytest.mark.gpu
+W = fdp.WorkflowKind
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def _inputs(B, T, P, D, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
+    dy = (torch.randn(B, T, D, device="cuda", generator=g) * torch.linspace(0.5, 1.5, B, device="cuda").view(B, 1, 1)
+          ).to(torch.bfloat16)
+    return x, dy
+
+
+def test_alternating_layouts_on_one_workspace():
+    """fused, two-phase (ghost / single / recompute) and non-DP calls of different
+    shapes alternate on ONE workspace (the pool's, keyed by device and stream);
+    each result must equal the same call on a fresh zeroed workspace. A stale
+    counter from another layout would let a wait pass early (wrong sums)."""
+    cases = [((4, 256, 512, 768), "fused", "auto", W.FLASHDP), ((2, 512, 1024, 2048), "two_phase", "ghost", W.FLASHDP),
+             ((8, 128, 256, 256), "fused", "auto", W.FLASHDP), ((1, 512, 2048, 1024), "two_phase", "single", W.FLASHDP),
+             ((3, 256, 768, 512), "two_phase", "recompute", W.FLASHDP), ((4, 256, 1024, 512), "auto", "auto", W.NON_DP),
+             ((16, 128, 512, 512), "fused", "auto", W.FLASHDP)]
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    for rnd in range(3):
+        for i, ((B, T, P, D), path, phase, kind) in enumerate(cases):
+            x, dy = _inputs(B, T, P, D, 100 * rnd + i)
+            cfg = fdp.DPConfig(float(np.sqrt(T * P * D)), 0.0, "mean", seed=1, layer_id=i, step=rnd)
+            kw = dict(path=path, norm_phase=phase) if kind == W.FLASHDP else {}
+            shared = fdp.run_backward(kind, x, dy, cfg, workspace=ws, **kw)
+            fresh = fdp.run_backward(kind, x, dy, cfg, workspace=torch.zeros_like(ws), **kw)
+            torch.cuda.synchronize()
+            assert torch.equal(shared.grad_w, fresh.grad_w) or _rel(shared.grad_w.cpu(), fresh.grad_w.cpu()) < 1e-6, \
+                (rnd, i)
+            if kind == W.FLASHDP:
+                want, wn = O.dp_backward(x.double().cpu().numpy(), dy.double().cpu().numpy(),
+                                         O.Cfg(cfg.clip_c, 0.0, "mean", 1, i, rnd), exact_noise=False)
+                assert _rel(shared.grad_w.cpu(), want) < 1e-3, (rnd, i)
+
+
+def test_alternating_group_lists_on_one_workspace():
+    """Multi-layer launches with different layer lists share one workspace (as the
+    chunked data-parallel backward does)."""
+    shapes_a = [(768, 2304), (768, 768), (768, 3072), (3072, 768)]
+    shapes_b = [(512, 512), (1024, 256), (256, 1024)]
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    for rnd in range(3):
+        for shapes in (shapes_a, shapes_b, shapes_a[:2]):
+            layers = []
+            for j, (P, D) in enumerate(shapes):
+                x, dy = _inputs(4, 256, P, D, 10 * rnd + j)
+                layers.append((x, dy, fdp.DPConfig(float(np.sqrt(256 * P * D)), 0.0, "mean", layer_id=j)))
+            g1 = fdp.PreparedGroup(layers, workspace=ws)
+            g1()
+            g2 = fdp.PreparedGroup(layers)
+            g2()
+            torch.cuda.synchronize()
+            for a, b in zip(g1.grads, g2.grads):
+                assert _rel(a.cpu(), b.cpu()) < 1e-6
+
+
+def test_prepared_backward_float64_outputs():
+    """fp64 inputs take the fp64 parity path: grad_w / norms are float64 (no
+    out-of-bounds writes into float32 buffers) and match the oracle at 1e-12."""
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(3, 5, 6, generator=g, dtype=torch.float64).cuda()
+    dy = torch.randn(3, 5, 4, generator=g, dtype=torch.float64).cuda()
+    cfg = fdp.DPConfig(2.0, 0.0, "sum")
+    call = fdp.PreparedBackward(W.FLASHDP, x, dy, cfg)
+    assert call.grad_w.dtype == torch.float64 and call.norms_sq.dtype == torch.float64
+    call()
+    want, wn = O.dp_backward(x.cpu().numpy(), dy.cpu().numpy(), O.Cfg(2.0, 0.0, "sum", 0, 0, 0))
+    assert np.max(np.abs(call.grad_w.cpu().numpy() - want)) < 1e-12
+    assert np.max(np.abs(call.norms_sq.cpu().numpy() - wn)) < 1e-9
+
+
+def test_caller_outputs_are_validated():
+    x, dy = _inputs(2, 64, 128, 64, 0)
+    cfg = fdp.DPConfig(1.0, 0.0)
+    bad = [torch.empty(64, 128, dtype=torch.float64, device="cuda"), torch.empty(128, 64, device="cuda"),
+           torch.empty(64, 256, device="cuda")[:, :128]]
+    for g in bad:
+        with pytest.raises(fdp.ShapeError):
+            fdp.backward_flashdp(x, dy, cfg, grad_out=g)
+        with pytest.raises(fdp.ShapeError):
+            fdp.PreparedBackward(W.FLASHDP, x, dy, cfg, grad_w=g)
+    with pytest.raises(fdp.ShapeError):
+        fdp.backward_flashdp(x, dy, cfg, norms_out=torch.empty(3, device="cuda"))
+    with pytest.raises(fdp.ShapeError):
+        fdp.PreparedBackward(W.FLASHDP, x, dy, cfg, norms_sq=torch.empty(2, dtype=torch.float64, device="cuda"))
+
+
+def test_dpcore_float64_dropins_against_reference_golden(golden_dir):
+    """finalize_gradient / per_layer_process / accumulate_micro_batches on float64
+    gradients default to the reference's fp64 keyed draw: 1e-12 vs dpflows."""
+    g = np.load(os.path.join(golden_dir, "dpcore.npz"))
+    for tag in ("sum_s0", "sum_s07", "mean_s13"):
+        c, s, mean, seed, layer, step = g[f"cfg_{tag}"].tolist()
+        cfg = fdp.DPConfig(c, s, "mean" if mean else "sum", int(seed), int(layer), int(step))
+        gs = torch.tensor(g["g"], dtype=torch.float64, device="cuda")
+        assert np.max(np.abs(fdp.finalize_gradient(gs, 3, cfg).cpu().numpy() - g[f"finalize_{tag}"])) < 1e-12
+        ps = [torch.tensor(a, dtype=torch.float64, device="cuda") for a in g["per_sample"]]
+        assert np.max(np.abs(fdp.per_layer_process(ps, cfg).cpu().numpy() - g[f"per_layer_{tag}"])) < 1e-12
+        parts = [torch.tensor(a, dtype=torch.float64, device="cuda") for a in g["partials"]]
+        got = fdp.accumulate_micro_batches(parts, 5, cfg).cpu().numpy()
+        assert np.max(np.abs(got - g[f"micro_{tag}"])) < 1e-12
+        # host float64 tensors work too (noise drawn on the device, result on the host)
+        assert np.max(np.abs(fdp.finalize_gradient(gs.cpu(), 3, cfg).numpy() - g[f"finalize_{tag}"])) < 1e-12

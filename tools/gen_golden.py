@@ -191,8 +191,32 @@ def gen_train():
     np.savez_compressed(OUT / "train.npz", **out)
 
 
+def gen_dpcore():
+    """dpcore.finalize_gradient / per_layer_process / accumulate_micro_batches on
+    float64 inputs (dpcore.py:60-104): the drop-ins must match at 1e-12."""
+    from dpflows.dpcore import finalize_gradient, per_layer_process
+
+    out = {}
+    g = rng.keyed_uniform_array((77, 1), 6 * 10).reshape(6, 10)
+    out["g"] = g
+    cfgs = {"sum_s0": DPConfig(0.8, 0.0, "sum", 3, 4, 5), "sum_s07": DPConfig(0.8, 0.7, "sum", 3, 4, 5),
+            "mean_s13": DPConfig(2.5, 1.3, "mean", 9, 1, 2)}
+    for tag, cfg in cfgs.items():
+        out[f"cfg_{tag}"] = np.array([cfg.clip_c, cfg.sigma, cfg.reduction == "mean", cfg.seed, cfg.layer_id,
+                                      cfg.step])
+        out[f"finalize_{tag}"] = finalize_gradient(Tensor((6, 10), g.ravel()), 3, cfg).array
+        ps = [Tensor((6, 10), (rng.keyed_uniform_array((77, 2, i), 60) * (i + 1)).ravel()) for i in range(4)]
+        out["per_sample"] = np.stack([t.array for t in ps])
+        out[f"per_layer_{tag}"] = per_layer_process(ps, cfg).array
+        parts = [Tensor((6, 10), rng.keyed_uniform_array((77, 3, i), 60)) for i in range(3)]
+        out["partials"] = np.stack([t.array for t in parts])
+        out[f"micro_{tag}"] = accumulate_micro_batches(parts, 5, cfg).array
+    np.savez_compressed(OUT / "dpcore.npz", **out)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    gen_dpcore()
     gen_train()
     gen_rng()
     gen_worked()
