@@ -140,56 +140,83 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference (CPU) arm
 
-def time_cpu_layer(j: int, B: int, T: int, sigma: float, clip: float, n_seq: int = 1) -> float:
-    """Seconds the oracle port (numpy float64, BLAS threads) needs for layer type
-    j of one block at the full batch: per-sample work (G_b, norm, clip,
-    accumulate) timed on `n_seq` sequences and scaled to B (it is linear in B),
-    finalize (mean + keyed noise over D*P) timed once, as in the full step."""
+def bench_config(a, world: int, global_B: int, T: int, graph: bool) -> dict:
+    """The workload dict both arms print (identical, so the driver can pair them)."""
+    return {"workload": "gpt2-small: DP weight-gradient backward of all 48 linear layers "
+                        "(per-sample per-layer clip, mean, keyed noise)",
+            "global_batch": global_B, "seq_len": T, "parallelism": f"dp{world}",
+            "clip_c": a.clip, "sigma": a.sigma, "noise": a.noise,
+            "l2": "inputs larger than L2 (%.2f GB of X/dY per rank per step)" % (
+                sum((global_B // world) * T * (P + D) * 2 for _, _, P, D in layer_list()) / 1e9),
+            "graph": graph}
+
+
+def cpu_whole_steps(a, warmup: int, steps: int):
+    """The reference's CPU implementation of the path, WHOLE steps: every step runs
+    the flashdp arithmetic of workflows.py:340-421 (per-sample G_b = dY_b^T X_b,
+    ||G_b||^2, clip factor, clipped sum, mean + sigma*C*keyed noise over D*P) for
+    all 48 layers at the full batch, in float64 (the reference's precision), as
+    the oracle port (oracle/dp_oracle.py; the reference is pure numpy and does not
+    travel to the GPU box). The layers of a step run on a thread pool with one
+    BLAS thread per worker, one worker per host core. -> (seconds per timed step,
+    cores, sample description)."""
     import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
     from oracle import dp_oracle as O
 
-    _, P, D = GPT2_LAYERS[j]
-    rng = np.random.default_rng(j)
-    x = rng.standard_normal((n_seq, T, P)).astype(np.float32)
-    dy = (rng.standard_normal((n_seq, T, D)) * 1e-3).astype(np.float32)
-    cfg = O.Cfg(clip, sigma, "mean", 1234, j, 0)
-    t0 = time.perf_counter()
-    acc, _ = O.per_sample_accumulate(x, dy, clip)
-    t1 = time.perf_counter()
-    O.finalize(acc, B, cfg, exact_noise=False)
-    t2 = time.perf_counter()
-    return (t1 - t0) * (B / n_seq) + (t2 - t1)
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    B, T = a.batch, a.seq
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    # one (X, dY) pair per layer type, float32 storage (the math is float64), reused by the 12 blocks
+    data = [(rng.standard_normal((B, T, P)).astype(np.float32),
+             (rng.standard_normal((B, T, D)) * 1e-3).astype(np.float32)) for _, P, D in GPT2_LAYERS]
+    layers = layer_list()
 
+    def one_layer(item, step_idx):
+        lid = item[0]
+        x, dy = data[lid % len(GPT2_LAYERS)]
+        acc, norms = O.per_sample_accumulate(x, dy, a.clip)
+        out = O.finalize(acc, B, O.Cfg(a.clip, a.sigma, "mean", 1234, lid, step_idx), exact_noise=False)
+        return float(out[0, 0]) + float(norms[0])
 
-def cpu_sample_desc(B: int, n_seq: int = 1) -> str:
-    return (f"oracle/dp_oracle.py numpy float64 (reference backward_flashdp arithmetic) on the host's BLAS threads: "
-            f"each step times one of the 4 GPT-2 layer types in rotation (per-sample work on {n_seq} of {B} "
-            f"sequences x{B // n_seq}, finalize+noise once), x{4 * N_BLOCKS} to the 48-layer step")
+    per = []
+    ctx = threadpool_limits(1) if threadpool_limits else None
+    try:
+        with ThreadPoolExecutor(max_workers=cores) as pool:
+            for i in range(warmup + steps):
+                t0 = time.perf_counter()
+                sum(pool.map(lambda it: one_layer(it, i), layers))
+                if i >= warmup:
+                    per.append(time.perf_counter() - t0)
+    finally:
+        if ctx is not None:
+            ctx.unregister()
+    sample = (f"whole steps: all {len(layers)} layers x {B} sequences x T={T} per step, float64 numpy "
+              f"(oracle/dp_oracle.py restating workflows.py:340-421: per-sample G_b, norm, clip, sum, mean, "
+              f"sigma*C*noise over every D*P index with the reference's own keyed construction), "
+              f"{cores} worker threads x 1 BLAS thread; {warmup} warm-up + {steps} timed steps")
+    return sum(per) / len(per), cores, sample, sum(per)
 
 
 def run_reference_arm(a, rank: int, world: int):
+    """--impl reference: rank 0 alone times whole CPU steps (cpu_whole_steps)."""
     if rank != 0:
         return
     B, T = a.batch, a.seq
-    tokens_per_step = B * T  # one rank's workload (the metric is per-N aggregate; the CPU arm runs once)
-    per = []
-    steps = max(4, (a.steps + 3) // 4 * 4)  # whole rotations over the 4 layer types
-    for i in range(a.warmup + steps):
-        s = time_cpu_layer(i % 4, B, T, a.sigma, a.clip)
-        if i >= a.warmup:
-            per.append(s * 4 * N_BLOCKS)
-    step_s = statistics.mean(per)
-    sample = cpu_sample_desc(B)
-    value = tokens_per_step / step_s
-    cores = os.cpu_count()
+    step_s, cores, sample, timed = cpu_whole_steps(a, a.warmup, a.steps)
+    value = B * T / step_s  # one rank's workload; under torchrun only rank 0 runs this arm
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "gpt2-small 48 DP linear layers, weight-gradient backward", "global_batch": B,
-                       "seq_len": T, "parallelism": "cpu"},
+            "config": bench_config(a, world, B * world, T, False),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "timed_s": timed}
     print(json.dumps(line), flush=True)
 
 
@@ -488,10 +515,8 @@ def main():
     # ---- CPU baseline (rank 0, N=1 only): oracle port on a bounded sample
     cpu = None
     if not a.no_cpu and world == 1 and rank == 0:
-        s = sum(time_cpu_layer(j, B, T, a.sigma, a.clip) for j in range(4)) * N_BLOCKS
-        cpu = {"value": tokens_per_step / s, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": cpu_sample_desc(B).replace("each step times one of the 4 GPT-2 layer types in rotation",
-                                                    "one pass over the 4 GPT-2 layer types")}
+        s, cores, sample, _ = cpu_whole_steps(a, 1, 2)  # ~10-20 s of CPU work on the box's host cores
+        cpu = {"value": tokens_per_step / s, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
     # ---- whole training step of the same model (N=1): DP linear layers through
     # GroupedDPBackward vs plain nn.Linear, same optimizer (tools/train_gpt2.py)
@@ -529,13 +554,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "gpt2-small: DP weight-gradient backward of all 48 linear layers "
-                                   "(per-sample per-layer clip, mean, keyed noise)",
-                       "global_batch": global_B, "seq_len": T, "parallelism": f"dp{world}",
-                       "clip_c": a.clip, "sigma": a.sigma, "noise": a.noise,
-                       "l2": "inputs larger than L2 (%.2f GB of X/dY per rank per step)" % (
-                           sum(B * T * (P + D) * 2 for _, _, P, D in layers) / 1e9),
-                       "graph": bool(graph is not None)},
+            "config": bench_config(a, world, global_B, T, bool(graph is not None)),
             "tflops_per_gpu": flops_per_step_rank / (ms_per_step * 1e-3) / 1e12,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": (a.steps if group is not None else len(calls) * a.steps),
