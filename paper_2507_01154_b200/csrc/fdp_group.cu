@@ -438,10 +438,16 @@ static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
-  if (e != cudaSuccess && CG == 2) {
-    if (std::getenv("FDP_DEBUG")) std::fprintf(stderr, "fdp: cooperative cluster launch rejected (%s); plain cluster launch\n", cudaGetErrorString(e));
+  // The in-kernel norm all-reduce spin-waits on other CTAs: it needs the
+  // co-residency guarantee of the cooperative launch, especially while a
+  // collective runs concurrently on other SMs. A rejected cooperative launch is
+  // an error (no silent plain-launch retry); FDP_ALLOW_NONCOOP=1 opts into the
+  // plain cluster launch (grid <= co-resident capacity; the in-kernel watchdog
+  // turns a broken assumption into an error) for profilers that cannot replay
+  // cooperative launches.
+  if (e != cudaSuccess && CG == 2 && std::getenv("FDP_ALLOW_NONCOOP")) {
     (void)cudaGetLastError();
-    cfg.numAttrs = 1;  // cluster launch without the cooperative attribute (grid <= co-resident capacity)
+    cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
   }
   return e;

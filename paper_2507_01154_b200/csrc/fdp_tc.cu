@@ -707,11 +707,10 @@ static cudaError_t launch_tc_impl(const CUtensorMap& tm_dy, const CUtensorMap& t
   cfg.attrs = attr;
   cfg.numAttrs = na;
   e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, em, p);
-  if (e != cudaSuccess && cooperative && CG == 2) {
-    // Some drivers reject cooperative + cluster launches. The grid never exceeds
-    // the co-resident capacity (checked by the planner), so fall back to a plain
-    // cluster launch; the in-kernel watchdog turns a broken assumption into an error.
-    if (std::getenv("FDP_DEBUG")) std::fprintf(stderr, "fdp: cooperative cluster launch rejected (%s); plain cluster launch\n", cudaGetErrorString(e));
+  if (e != cudaSuccess && cooperative && CG == 2 && std::getenv("FDP_ALLOW_NONCOOP")) {
+    // A rejected cooperative launch is an error: the fused kernel's grid barrier
+    // needs co-residency (see fdp_group.cu). FDP_ALLOW_NONCOOP=1 opts into a
+    // plain cluster launch (grid <= co-resident capacity, watchdog-guarded).
     (void)cudaGetLastError();
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, dpdw_tc_kernel<BN, CG>, tm_dy, tm_x, em, p);

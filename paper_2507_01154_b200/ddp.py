@@ -11,10 +11,13 @@ ranks.
 
 from __future__ import annotations
 
+import os
 from typing import Iterable, Sequence
 
 import torch
 import torch.distributed as dist
+
+from .dpcore import DPConfig
 
 
 def noise_partition(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -210,3 +213,418 @@ class ShardedDPAdam:
         mine[:own_hi - own_lo] = theta
         dist.all_gather(pieces, mine, group=self.group)
         self.params.copy_(torch.cat(pieces)[:self.n])
+
+
+# ----------------------------------------------------------------------------- training-step data parallelism
+#
+# The pieces a multi-GPU DP training step needs beyond one layer list
+# (SURVEY 8e): gradient buckets whose collectives
+# are issued from the backward itself (reverse layer order, overlapped with the
+# dX / DP kernels of the layers still to come), NCCL held to a CTA budget so the
+# co-resident persistent DP kernels keep their SMs, and an Adam step on the
+# bucket layout -- replicated after an all-reduce (DP-Adam, config 3) or ZeRO-1
+# after a reduce-scatter (config 4), where each rank adds the DP noise of
+# exactly the shard it owns.
+
+
+def nccl_options(comm_sms: int = 4):
+    """ProcessGroupNCCL options capping NCCL at `comm_sms` CTAs per collective
+    (and NVLS at the same count), so NCCL kernels running under the backward
+    take at most that many SMs; also exported as NCCL_MAX_CTAS / NCCL_NVLS_CTAS
+    for communicators NCCL creates outside these options. None if the build has
+    no NCCL."""
+    if comm_sms < 1:
+        raise ValueError("comm_sms must be >= 1")
+    os.environ.setdefault("NCCL_MAX_CTAS", str(comm_sms))
+    os.environ.setdefault("NCCL_NVLS_CTAS", str(comm_sms))
+    try:
+        opts = dist.ProcessGroupNCCL.Options()
+    except AttributeError:  # pragma: no cover - torch built without NCCL
+        return None
+    opts.config.max_ctas = int(comm_sms)
+    opts.config.min_ctas = 1
+    try:
+        opts.config.nvls_ctas = int(comm_sms)
+    except AttributeError:  # pragma: no cover
+        pass
+    return opts
+
+
+def init_distributed(backend: str = "nccl", comm_sms: int = 4, device: "torch.device | None" = None) -> None:
+    """init_process_group with the NCCL CTA budget (nccl) or plain (gloo)."""
+    if backend == "nccl":
+        dist.init_process_group("nccl", pg_options=nccl_options(comm_sms), device_id=device)
+    else:
+        dist.init_process_group(backend)
+
+
+def group_max_ctas(device: torch.device, comm_sms: int, world: int) -> int:
+    """CTA cap of the persistent DP kernels under data parallelism: the SMs minus
+    NCCL's budget, rounded down to whole CTA pairs (0 = uncapped when world == 1)."""
+    if world <= 1 or device.type != "cuda":
+        return 0
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return max(2, (sms - comm_sms) // 2 * 2)
+
+
+class _Bucket:
+    __slots__ = ("params", "offsets", "n", "per", "flat", "pflat", "shard", "pending", "launched", "deferred",
+                 "m", "v")
+
+
+class GradBuckets:
+    """Gradient buckets of a model, filled by the backward and reduced as soon as
+    they are complete.
+
+    Parameters are taken in reverse registration order (the order the backward
+    produces their gradients for a sequential model) and packed into buckets of
+    about `bucket_bytes` fp32 bytes. Every parameter's ``.grad`` is a view of its
+    bucket's flat fp32 buffer (padded to a multiple of `world`), so autograd, the
+    DP kernels and the collective all work in place. When the last gradient of a
+    bucket has been produced -- signalled by a post-accumulate-grad hook for
+    autograd gradients and by ``mark_ready`` for the DP weight gradients that
+    GroupedDPBackward writes -- the bucket's collective is issued on a separate
+    communication stream and runs under the rest of the backward:
+
+      mode "allreduce":      all_reduce(sum) of the flat buffer (every rank gets
+                             the whole summed gradient; DP-Adam, config 3)
+      mode "reduce_scatter": reduce_scatter(sum): rank r receives the slice
+                             [r*per, (r+1)*per) of the bucket (ZeRO-1, config 4;
+                             gloo has no reduce-scatter: all-reduce + slice)
+
+    With ``flat_params`` the parameters' storage is moved into one flat buffer
+    per bucket too (same layout), so an optimizer can step a bucket or a shard of
+    it with one kernel and all-gather it in one collective.
+
+    Bucket issue order is the backward's order, identical on every rank."""
+
+    def __init__(self, params, *, bucket_bytes: int = 512 << 20, mode: str = "allreduce", group=None,
+                 rank: int = 0, world: int = 1, flat_params: bool = False, hooks: bool = True):
+        if mode not in ("allreduce", "reduce_scatter"):
+            raise ValueError(f"mode must be allreduce or reduce_scatter, got {mode!r}")
+        if world < 1 or not (0 <= rank < world):
+            raise ValueError(f"rank {rank} out of range for world {world}")
+        self.mode, self.group, self.rank, self.world = mode, group, rank, world
+        ps = [p for p in params if p.requires_grad]
+        if not ps:
+            raise ValueError("GradBuckets needs at least one trainable parameter")
+        for p in ps:
+            if p.dtype != torch.float32:
+                raise ValueError(f"GradBuckets keeps fp32 master parameters and gradients, got {p.dtype}")
+        self.device = ps[0].device
+        self.buckets: list[_Bucket] = []
+        cur, size = [], 0
+        for p in reversed(ps):
+            cur.append(p)
+            size += p.numel() * 4
+            if size >= bucket_bytes:
+                self._close(cur, flat_params)
+                cur, size = [], 0
+        if cur:
+            self._close(cur, flat_params)
+        self._where = {}
+        for i, b in enumerate(self.buckets):
+            for p in b.params:
+                self._where[id(p)] = i
+        cuda = self.device.type == "cuda"
+        self.comm = torch.cuda.Stream(self.device) if cuda and world > 1 else None
+        self._handles = []
+        if hooks:
+            from .baselines import register_inplace_grad_hook
+
+            for p in ps:
+                p.register_post_accumulate_grad_hook(self._hook)
+                register_inplace_grad_hook(p, self.mark_ready)  # gradients GEMMs write in place
+        self.issued: list[int] = []  # bucket issue order of the last backward (tests / traces)
+        self.enabled = True  # False while accumulating micro-batches (no collectives)
+
+    def _close(self, params, flat_params):
+        b = _Bucket()
+        b.params = list(params)
+        b.offsets = []
+        off = 0
+        for p in b.params:
+            b.offsets.append(off)
+            off += p.numel()
+        b.n = off
+        b.per = -(-off // self.world)
+        dev = params[0].device
+        b.flat = torch.zeros(b.per * self.world, dtype=torch.float32, device=dev)
+        b.pflat = None
+        if flat_params:
+            b.pflat = torch.zeros(b.per * self.world, dtype=torch.float32, device=dev)
+            for p, o in zip(b.params, b.offsets):
+                b.pflat[o:o + p.numel()].copy_(p.detach().reshape(-1))
+                p.data = b.pflat[o:o + p.numel()].view_as(p)
+        for p, o in zip(b.params, b.offsets):
+            p.grad = b.flat[o:o + p.numel()].view_as(p)
+        b.shard = b.flat[self.rank * b.per:(self.rank + 1) * b.per]
+        b.deferred = 0
+        b.pending = len(b.params)
+        b.launched = False
+        b.m = b.v = None
+        self.buckets.append(b)
+
+    def set_deferred(self, weights) -> None:
+        """Weights whose gradient is written outside autograd (DPLinear under
+        GroupedDPBackward): the per-bucket count GroupedDPBackward waits for
+        before it runs a bucket's DP kernels."""
+        for b in self.buckets:
+            b.deferred = 0
+        for w in weights:
+            i = self._where.get(id(w))
+            if i is not None:
+                self.buckets[i].deferred += 1
+
+    # ---- per step
+    def zero_grad(self) -> None:
+        """Zero every bucket and re-arm the readiness counters (call instead of
+        optimizer.zero_grad(); the .grad views must stay in place)."""
+        for b in self.buckets:
+            b.flat.zero_()
+            b.pending = len(b.params)
+            b.launched = False
+            for p, o in zip(b.params, b.offsets):
+                if p.grad is None or p.grad.data_ptr() != b.flat[o:].data_ptr():
+                    p.grad = b.flat[o:o + p.numel()].view_as(p)
+        self.issued = []
+
+    def bucket_of(self, p) -> int:
+        return self._where[id(p)]
+
+    def _hook(self, p):
+        self.mark_ready(p)
+
+    def mark_ready(self, p) -> None:
+        if not self.enabled:  # micro-batches before the last: gradients accumulate, no collective
+            return
+        i = self._where.get(id(p))
+        if i is None:
+            return
+        b = self.buckets[i]
+        b.pending -= 1
+        if b.pending == 0:
+            self._launch(i)
+
+    def _launch(self, i: int) -> None:
+        b = self.buckets[i]
+        if b.launched:
+            return
+        b.launched = True
+        self.issued.append(i)
+        if self.world == 1:
+            return
+        if self.comm is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self.comm.wait_event(ev)
+            with torch.cuda.stream(self.comm):
+                self._collective(b)
+        else:
+            self._collective(b)
+
+    def _collective(self, b: _Bucket) -> None:
+        if self.mode == "allreduce":
+            dist.all_reduce(b.flat, op=dist.ReduceOp.SUM, group=self.group)
+        elif dist.get_backend(self.group) == "nccl":
+            out = torch.empty_like(b.shard)
+            dist.reduce_scatter_tensor(out, b.flat, op=dist.ReduceOp.SUM, group=self.group)
+            b.shard.copy_(out)
+        else:  # gloo: all-reduce, keep this rank's slice (b.shard is a view of it)
+            dist.all_reduce(b.flat, op=dist.ReduceOp.SUM, group=self.group)
+
+    def finish(self) -> None:
+        """After backward: issue any bucket not yet issued (parameters without a
+        gradient this step), in bucket order, then order the current stream after
+        the collectives."""
+        if not self.enabled:
+            return
+        for i, b in enumerate(self.buckets):
+            if not b.launched:
+                self._launch(i)
+        if self.comm is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.comm)
+
+
+def dp_noise_keys(model) -> dict:
+    """{id(param): (DPConfig of the noise, offset in the group's index space,
+    group length, noise_impl)} for every parameter of a DP module: the key under
+    which the DP kernels would add sigma*C*N(seed, layer_id, step, i) to it
+    (DPLinear weight: layer_id, flat d*P+p; its bias: layer_id + 2**32;
+    RMSNorm gamma / LayerNorm [gamma, beta]: one group of D / 2D; embedding:
+    v*D + c). ZeRO-1 draws the same noise on the owner's shard instead."""
+    from .dplinear import DPLinear
+    from .dpmodules import DPEmbedding, DPLayerNorm, DPRMSNorm
+
+    keys = {}
+    for m in model.modules():
+        if isinstance(m, DPLinear):
+            cfg = m.dp_config()
+            keys[id(m.weight)] = (cfg, 0, m.weight.numel(), m.noise_impl)
+            if m.bias is not None:
+                bcfg = DPConfig(cfg.clip_c, cfg.sigma, cfg.reduction, cfg.seed, m.layer_id + (1 << 32), cfg.step)
+                keys[id(m.bias)] = (bcfg, 0, m.bias.numel(), m.noise_impl)
+        elif isinstance(m, (DPRMSNorm, DPLayerNorm)):
+            cfg = m.dp_config()
+            d = m.weight.numel()
+            n = d * (2 if getattr(m, "bias", None) is not None else 1)
+            keys[id(m.weight)] = (cfg, 0, n, m.noise_impl)
+            if getattr(m, "bias", None) is not None:
+                keys[id(m.bias)] = (cfg, d, n, m.noise_impl)
+        elif isinstance(m, DPEmbedding):
+            keys[id(m.weight)] = (m.dp_config(), 0, m.weight.numel(), m.noise_impl)
+    return keys
+
+
+def _torch_adam_(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel):
+    """Device-agnostic stand-in of fdp_adam_step for CPU tests (no noise)."""
+    if noise_cfg is not None and noise_cfg.sigma > 0:
+        raise RuntimeError("the torch Adam stand-in does not draw DP noise")
+    m.mul_(b1).add_(grad, alpha=1 - b1)
+    v.mul_(b2).addcmul_(grad, grad, value=1 - b2)
+    theta.sub_(eta * m / (v.sqrt() + eps))
+
+
+class BucketedAdam:
+    """Adam without bias correction and with the post-update v (the reference's
+    DP-Adam, dpcore.py:139-156) on the GradBuckets layout (flat_params=True).
+
+    mode "allreduce" (buckets were all-reduced): every rank steps every bucket
+    whole -- one fused kernel per bucket; the noise was already added once by the
+    rank partition of the DP kernels.
+    mode "reduce_scatter" (ZeRO-1): rank r steps only its shard of every bucket,
+    first adding the DP noise of exactly that shard (per parameter segment: that
+    parameter's noise key and in-group offset, `noise_keys` from dp_noise_keys),
+    then all-gathers the updated bucket; the moments exist for the shard only.
+
+    `adam_fn(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset,
+    noise_impl, layer_numel)` replaces the CUDA kernel in CPU tests."""
+
+    def __init__(self, buckets: GradBuckets, *, lr: float, beta1: float = 0.9, beta2: float = 0.999,
+                 eps: float = 1e-8, noise_keys: "dict | None" = None, adam_fn=None):
+        if any(b.pflat is None for b in buckets.buckets):
+            raise ValueError("BucketedAdam needs GradBuckets(flat_params=True)")
+        self.bk = buckets
+        self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
+        self.noise_keys = noise_keys or {}
+        self.adam_fn = adam_fn or self._kernel
+        zero1 = buckets.mode == "reduce_scatter"
+        for b in buckets.buckets:
+            n = b.per if zero1 else b.n
+            b.m = torch.zeros(n, dtype=torch.float32, device=b.flat.device)
+            b.v = torch.zeros_like(b.m)
+
+    @staticmethod
+    def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel):
+        from .dpcore import OptimizerState, dp_adam_step_
+
+        st = OptimizerState(theta=theta, m=m, v=v, eta=eta, beta1=b1, beta2=b2, eps_adam=eps)
+        dp_adam_step_(st, grad, noise=noise_cfg, noise_offset=noise_offset, noise_impl=noise_impl or "philox",
+                      layer_numel=layer_numel)
+
+    def _segments(self, b, lo: int, hi: int):
+        """(a, z, noise key or None) pieces of [lo, hi) cut at parameter bounds;
+        consecutive parameters without a noise key merge into one piece."""
+        out = []
+        for p, o in zip(b.params, b.offsets):
+            a, z = max(o, lo), min(o + p.numel(), hi)
+            if a >= z:
+                continue
+            key = self.noise_keys.get(id(p))
+            if key is not None:
+                cfg, goff, glen, impl = key
+                out.append((a, z, (cfg, goff + (a - o), glen, impl)))
+            elif out and out[-1][2] is None and out[-1][1] == a:
+                out[-1] = (out[-1][0], z, None)
+            else:
+                out.append((a, z, None))
+        return out
+
+    def step(self, dp_step: int = 0) -> None:
+        from dataclasses import replace
+
+        bk = self.bk
+        for b in bk.buckets:
+            if bk.mode == "allreduce":
+                self.adam_fn(b.pflat[:b.n], b.m, b.v, b.flat[:b.n], self.lr, self.beta1, self.beta2, self.eps,
+                             None, 0, None, 0)
+                continue
+            lo = bk.rank * b.per
+            hi = min(lo + b.per, b.n)
+            for a, z, key in self._segments(b, lo, hi):
+                th, g = b.pflat[a:z], b.shard[a - lo:z - lo]
+                mm, vv = b.m[a - lo:z - lo], b.v[a - lo:z - lo]
+                if key is None:
+                    self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0)
+                else:
+                    cfg, off, glen, impl = key
+                    self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps,
+                                 replace(cfg, step=dp_step), off, impl, glen)
+            if bk.world > 1:
+                mine = b.pflat[bk.rank * b.per:(bk.rank + 1) * b.per]
+                if dist.get_backend(bk.group) == "nccl":
+                    dist.all_gather_into_tensor(b.pflat, mine.clone(), group=bk.group)
+                else:
+                    pieces = list(b.pflat.chunk(bk.world))
+                    dist.all_gather(pieces, mine.clone(), group=bk.group)
+
+
+class DataParallelStep:
+    """One data-parallel training step of a model, DP or non-DP, on the bucket
+    layout: zero the buckets, forward + loss, backward with the buckets'
+    collectives issued from inside it, Adam (no bias correction, dpcore.py:139-156)
+    on the bucket layout.
+
+      dp=True,  mode "allreduce":      DP-Adam (config 3): the DP kernels add each
+                                       layer's noise on this rank's slice of its
+                                       index space; buckets all-reduced; replicated
+                                       Adam.
+      dp=True,  mode "reduce_scatter": ZeRO-1 (config 4): the DP kernels run without
+                                       noise, buckets reduce-scattered, each rank adds
+                                       the noise of its shard inside its Adam step and
+                                       all-gathers the parameters.
+      dp=False: the same model's non-DP step with the same buckets, collectives and
+                optimizer (the like-for-like baseline; give the model
+                FP32GradLinear projections for the DP arm's fp32 gradient path).
+
+    The loss must be the sum over samples of per-sample losses, scaled by
+    1/global_batch for dp=False (the DP modules take the mean over the logical
+    batch themselves), so the summed gradients are the global-batch ones."""
+
+    def __init__(self, model, *, dp: bool, mode: str = "allreduce", lr: float = 1e-5, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8, rank: int = 0, world: int = 1, group=None,
+                 comm_sms: int = 4, bucket_bytes: int = 512 << 20, global_batch: int = 1, adam_fn=None):
+        from .dplinear import DPLinear
+
+        self.model, self.dp, self.mode, self.world = model, dp, mode, world
+        self.global_batch = global_batch
+        self.buckets = GradBuckets(model.parameters(), bucket_bytes=bucket_bytes, mode=mode, group=group,
+                                   rank=rank, world=world, flat_params=True)
+        self.dp_mods = model.dp_modules() if dp else []
+        if dp:
+            set_data_parallel(self.dp_mods, rank, world)
+            self.buckets.set_deferred([m.weight for m in self.dp_mods if isinstance(m, DPLinear)])
+        keys = dp_noise_keys(model) if dp and mode == "reduce_scatter" else None
+        self.opt = BucketedAdam(self.buckets, lr=lr, beta1=beta1, beta2=beta2, eps=eps, noise_keys=keys,
+                                adam_fn=adam_fn)
+        dev = next(model.parameters()).device
+        self.max_ctas = group_max_ctas(dev, comm_sms, world)
+        self.last_flushes = 0
+
+    def __call__(self, step: int, loss_fn):
+        from .dplinear import GroupedDPBackward
+
+        bk = self.buckets
+        bk.zero_grad()
+        for m in self.dp_mods:
+            m.set_step(step, last_micro_batch=self.mode == "allreduce", logical_batch=self.global_batch)
+        loss = loss_fn()
+        if self.dp:
+            with GroupedDPBackward(buckets=bk, max_ctas=self.max_ctas) as g:
+                loss.backward()
+            self.last_flushes = g.flushes
+        else:
+            loss.backward()
+        bk.finish()
+        self.opt.step(dp_step=step)
+        return loss

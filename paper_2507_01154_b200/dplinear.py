@@ -82,77 +82,126 @@ _ACTIVE_GROUP: list = [None]
 class GroupedDPBackward:
     """Context manager that defers the DP weight gradients of every DPLinear whose
     backward runs inside it and computes them in ONE persistent multi-layer launch
-    (PreparedGroup / fdp_backward_group) when the context exits -- the
-    training-step form of Algorithm 1: no per-layer launch, pipelines that never
-    drain between layers, small layers packed side by side on the SMs.
+    (PreparedGroup / fdp_backward_group) -- the training-step form of Algorithm 1:
+    no per-layer launch, pipelines that never drain between layers, small layers
+    packed side by side on the SMs.
 
         with GroupedDPBackward():
             loss.backward()          # dX as usual; dW of DPLinear layers deferred
         # every DPLinear.weight.grad now holds its DP gradient (accumulated into an
         # existing .grad, as autograd would for micro-batches)
 
-    Each layer keeps its own DPConfig (C, sigma, layer_id noise key, step). The
-    (X, dY) pairs of the layers are held until the context exits. Layers the
-    fused multi-layer launch cannot take (fp32 compute dtype, shapes over the
-    co-resident grid) run through the per-layer kernels instead."""
+    Each layer keeps its own DPConfig (C, sigma, layer_id noise key, step). Layers
+    the fused multi-layer launch cannot take (fp32 compute dtype, shapes over the
+    co-resident grid) run through the per-layer kernels instead.
 
-    def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0):
+    Data parallel training (``buckets``: a ddp.GradBuckets over the model): the
+    deferred layers are flushed bucket by bucket DURING the backward -- as soon as
+    every DPLinear weight of a gradient bucket has recorded its (X, dY), that
+    bucket's DP kernels run and the bucket is marked ready, so its collective
+    starts on the communication stream while the backward continues with the
+    earlier layers (reverse layer order). (X, dY) of a layer are released when its
+    bucket flushes, not at the end of the backward. ``max_ctas`` caps the
+    persistent launches so NCCL keeps its SMs."""
+
+    def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0, buckets=None):
         self.noise_impl = noise_impl
         self.max_ctas = max_ctas
+        self.buckets = buckets
         self._pending: list = []
         self.last_groups = 0
+        self.flushes = 0
         self._ws = None
+        self._waiting: dict = {}
 
     def __enter__(self):
         if _ACTIVE_GROUP[0] is not None:
             raise RuntimeError("GroupedDPBackward contexts do not nest")
         _ACTIVE_GROUP[0] = self
         self._pending = []
+        self._waiting = {}
+        self.flushes = 0
         return self
 
     def __exit__(self, exc_type, exc, tb):
         _ACTIVE_GROUP[0] = None
         if exc_type is None:
+            for items in self._waiting.values():  # buckets whose other DP weights never ran
+                self._flush_items(items)
+            self._waiting = {}
             self.flush()
         self._pending = []
         return False
 
     def _record(self, module, x3, dy3, cfg, add_noise, mean_batch):
-        self._pending.append((module, x3, dy3, cfg, add_noise, mean_batch))
+        item = (module, x3, dy3, cfg, add_noise, mean_batch)
+        bk = self.buckets
+        if bk is None or id(module.weight) not in bk._where:
+            self._pending.append(item)
+            return
+        i = bk.bucket_of(module.weight)
+        waiting = self._waiting.setdefault(i, [])
+        waiting.append(item)
+        if len(waiting) == bk.buckets[i].deferred:  # every DP weight of the bucket is here: run it now
+            del self._waiting[i]
+            self._flush_items(waiting)
 
     def flush(self) -> None:
+        self._flush_items(self._pending)
+        self._pending = []
+
+    def _flush_items(self, pending) -> None:
         from .workflows import PreparedGroup, WorkflowKind, _run
         from .errors import CapacityError, UsageError
 
+        if not pending:
+            return
+        self.flushes += 1
+
+        def out_for(m):  # write straight into an fp32 .grad (bucket view / micro-batch sum)
+            g = m.weight.grad
+            if g is not None and g.dtype == torch.float32 and g.is_contiguous() and g.shape == m.weight.shape:
+                return g
+            return None
+
+        def deliver(m, gw, direct):
+            if not direct:
+                gw = gw.to(m.weight.dtype)
+                if m.weight.grad is None:
+                    m.weight.grad = gw
+                else:
+                    m.weight.grad += gw
+            if self.buckets is not None:
+                self.buckets.mark_ready(m.weight)
+
         buckets: dict = {}
-        for item in self._pending:  # one launch per (noise on/off, mean divisor, partition, noise generator)
+        for item in pending:  # one launch per (noise on/off, mean divisor, partition, noise generator)
             m, _, _, _, add_noise, mean_batch = item
             key = (add_noise, mean_batch, m.rank, m.world, self.noise_impl or m.noise_impl)
             buckets.setdefault(key, []).append(item)
         self.last_groups = 0
         for (add_noise, mean_batch, rank, world, impl), items in buckets.items():
-            grads = None
             # layers whose tiles cannot all be co-resident (e.g. a 50K-row LM head) take the
             # per-layer two-phase kernels; the rest share the multi-layer launches
             solo = [it for it in items if not _fits_group(it[1].shape, it[2].shape)]
             items = [it for it in items if _fits_group(it[1].shape, it[2].shape)]
             for m, x, dy, cfg, _, _ in solo:
+                g = out_for(m)
                 gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,
-                          rank=rank, world=world, noise_impl=impl).grad_w.to(m.weight.dtype)
-                if m.weight.grad is None:
-                    m.weight.grad = gw
-                else:
-                    m.weight.grad += gw
+                          rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None).grad_w
+                deliver(m, gw, g is not None)
             for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
                 chunk = items[lo:lo + 48]
+                direct = all(out_for(m) is not None for m, *_ in chunk)
                 try:
-                    # every element of a fresh (non-accumulating) group output is written by the
-                    # kernel: no zero-fill; the workspace is kept (the kernel leaves it zeroed)
-                    grads_out = [torch.empty(dy.shape[2], x.shape[2], dtype=torch.float32, device=x.device)
-                                 for _, x, dy, _, _, _ in chunk]
+                    # a fresh (non-accumulating) group output is written whole by the kernel: no
+                    # zero-fill; existing fp32 .grad tensors are accumulated into in place
+                    grads_out = ([out_for(m) for m, *_ in chunk] if direct else
+                                 [torch.empty(dy.shape[2], x.shape[2], dtype=torch.float32, device=x.device)
+                                  for _, x, dy, _, _, _ in chunk])
                     glayers = [(x, dy, cfg) for _, x, dy, cfg, _, _ in chunk]
                     kw = dict(grads=grads_out, noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
-                              mean_batch=mean_batch, max_ctas=self.max_ctas)
+                              mean_batch=mean_batch, max_ctas=self.max_ctas, accumulate=direct)
                     try:
                         grp = PreparedGroup(glayers, workspace=self._ws, **kw)
                     except CapacityError:  # cached workspace too small for this layer list: grow it
@@ -162,15 +211,14 @@ class GroupedDPBackward:
                     grads = grp.grads
                     self.last_groups += 1
                 except UsageError:  # per-layer kernels (two-phase for layers over the co-resident grid)
-                    grads = [_run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise,
-                                  mean_batch=mean_batch, rank=rank, world=world, noise_impl=impl).grad_w
-                             for _, x, dy, cfg, _, _ in chunk]
+                    grads = []
+                    for m, x, dy, cfg, _, _ in chunk:
+                        g = out_for(m) if direct else None
+                        grads.append(_run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise,
+                                          mean_batch=mean_batch, rank=rank, world=world, noise_impl=impl,
+                                          grad_out=g, accumulate=g is not None).grad_w)
                 for (m, _, _, _, _, _), gw in zip(chunk, grads):
-                    gw = gw.to(m.weight.dtype)
-                    if m.weight.grad is None:
-                        m.weight.grad = gw
-                    else:
-                        m.weight.grad += gw
+                    deliver(m, gw, direct)
 
 
 _FITS: dict = {}

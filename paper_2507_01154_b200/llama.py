@@ -58,7 +58,8 @@ def _rope(q, k, cos, sin):
 
 
 class Block(torch.nn.Module):
-    def __init__(self, cfg: LlamaConfig, idx: int, dp: bool, clip_c: float, sigma: float, noise_impl: str):
+    def __init__(self, cfg: LlamaConfig, idx: int, dp: bool, clip_c: float, sigma: float, noise_impl: str,
+                 linear_cls=torch.nn.Linear):
         super().__init__()
         self.heads = cfg.heads
 
@@ -66,7 +67,7 @@ class Block(torch.nn.Module):
             if dp:
                 return DPLinear(cin, cout, bias=False, clip_c=clip_c, sigma=sigma, reduction="mean",
                                 layer_id=7 * idx + j, noise_impl=noise_impl)
-            return torch.nn.Linear(cin, cout, bias=False)
+            return linear_cls(cin, cout, bias=False)
 
         def norm(j):
             if dp:
@@ -94,11 +95,22 @@ class Block(torch.nn.Module):
 
 
 class Llama(torch.nn.Module):
+    """``nondp_linear``: the non-DP model's projection class -- "torch" (nn.Linear:
+    bf16 dW GEMM cast into the fp32 .grad by autograd) or "fp32grad"
+    (baselines.FP32GradLinear: cuBLAS writes the fp32 weight gradient directly,
+    the DP kernels' precision; the like-for-like baseline)."""
+
     def __init__(self, cfg: LlamaConfig, *, dp: bool = True, clip_c: float = 1.0, sigma: float = 1.0,
-                 noise_impl: str = "philox"):
+                 noise_impl: str = "philox", nondp_linear: str = "torch"):
         super().__init__()
         self.cfg = cfg
         self.dp = dp
+        if nondp_linear == "fp32grad":
+            from .baselines import FP32GradLinear as linear_cls
+        elif nondp_linear == "torch":
+            linear_cls = torch.nn.Linear
+        else:
+            raise ValueError(f"nondp_linear must be torch or fp32grad, got {nondp_linear!r}")
         if dp:
             self.embed = DPEmbedding(cfg.vocab, cfg.d, clip_c=clip_c, sigma=sigma, layer_id=200000,
                                      noise_impl=noise_impl)
@@ -108,8 +120,9 @@ class Llama(torch.nn.Module):
         else:
             self.embed = torch.nn.Embedding(cfg.vocab, cfg.d)
             self.norm = _RMSNorm(cfg.d, cfg.eps)
-            self.lm_head = torch.nn.Linear(cfg.d, cfg.vocab, bias=False)
-        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl) for i in range(cfg.layers))
+            self.lm_head = linear_cls(cfg.d, cfg.vocab, bias=False)
+        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl, linear_cls)
+                                          for i in range(cfg.layers))
         for p in self.parameters():
             if p.dim() >= 2:
                 torch.nn.init.normal_(p, std=0.02)
@@ -131,7 +144,16 @@ class Llama(torch.nn.Module):
             x = blk(x, cos, sin)
         return self.lm_head(self.norm(x))
 
-    def loss(self, idx, targets):
+    def loss(self, idx, targets, reduction: str = "mean"):
+        """reduction "mean": over every token of the batch. "sample_sum": sum over
+        samples of each sample's mean token loss -- the per-sample loss whose
+        gradient is the sample's own, independent of how the batch is split over
+        ranks (the DP modules then take the mean over the logical batch)."""
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = self(idx)
-        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))
+        if reduction == "mean":
+            return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))
+        if reduction == "sample_sum":
+            tok = F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1), reduction="none")
+            return tok.view(idx.shape[0], -1).mean(1).sum()
+        raise ValueError(f"unknown reduction {reduction!r}")

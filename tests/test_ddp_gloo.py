@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -122,3 +123,90 @@ def test_set_data_parallel_sets_every_module_and_validates():
     assert all((m.rank, m.world) == (1, 4) for m in mods)
     with _pytest.raises(ValueError):
         set_data_parallel(mods, 4, 4)
+
+
+# ---------------------------------------------------------------- bucketed training step (GradBuckets)
+
+
+def _bucket_model():
+    torch.manual_seed(0)
+    return torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.Tanh(), torch.nn.Linear(32, 24), torch.nn.Tanh(),
+                               torch.nn.Linear(24, 8))
+
+
+def _bucket_worker(rank, world, port, mode, out):
+    from paper_2507_01154_b200.ddp import DataParallelStep, _torch_adam_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    model = _bucket_model()
+    g = torch.Generator().manual_seed(3)
+    x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+    lo, hi = 8 * rank // world, 8 * (rank + 1) // world
+    step = DataParallelStep(model, dp=False, mode=mode, lr=1e-2, rank=rank, world=world, global_batch=8,
+                            adam_fn=_torch_adam_, bucket_bytes=600)  # several buckets
+    seen = []
+    model[0].weight.register_post_accumulate_grad_hook(lambda p: seen.append(len(step.buckets.issued)))
+    for i in range(3):
+        step(i, lambda: ((model(x[lo:hi]) - y[lo:hi]) ** 2).sum(1).sum() / 8)
+    out[(mode, world, rank)] = ([p.detach().clone() for p in model.parameters()], list(step.buckets.issued),
+                                len(step.buckets.buckets), seen)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_bucketed_step_two_ranks_equals_single_process():
+    """DataParallelStep on a 5-layer model, world 2 over gloo, both bucket modes
+    (all-reduce + replicated Adam; reduce-scatter + ZeRO-1 Adam + all-gather):
+    the parameters after 3 steps equal the single-process run on the global
+    batch; buckets are issued in the same order on both ranks, and the first
+    buckets are issued while the backward is still running (before the first
+    layer's gradient exists)."""
+    for mode in ("allreduce", "reduce_scatter"):
+        with mp.Manager() as mgr:
+            out = mgr.dict()
+            _bucket_worker(0, 1, _free_port(), mode, out)
+            mp.spawn(_bucket_worker, args=(2, _free_port(), mode, out), nprocs=2, join=True)
+            ref, _, nb, _ = out[(mode, 1, 0)]
+            assert nb >= 3
+            for r in range(2):
+                got, issued, _, seen = out[(mode, 2, r)]
+                for a, b in zip(got, ref):
+                    assert torch.allclose(a, b, rtol=1e-5, atol=1e-6), mode
+                assert issued == out[(mode, 2, 0)][1]
+                assert all(s >= 1 for s in seen)  # overlap: earlier buckets already on the wire
+
+
+def test_grad_buckets_layout_and_validation():
+    from paper_2507_01154_b200.ddp import GradBuckets
+
+    model = _bucket_model()
+    bk = GradBuckets(model.parameters(), bucket_bytes=1200, mode="reduce_scatter", rank=1, world=3,
+                     flat_params=True, hooks=False)
+    ps = list(model.parameters())
+    # reverse registration order, every grad / param a view of its bucket, shards padded to world
+    assert bk.buckets[0].params[0] is ps[-1]
+    for b in bk.buckets:
+        assert b.flat.numel() == 3 * b.per >= b.n
+        assert b.shard.data_ptr() == b.flat[b.per:].data_ptr()
+        for p, o in zip(b.params, b.offsets):
+            assert p.grad.data_ptr() == b.flat[o:].data_ptr() and p.data_ptr() == b.pflat[o:].data_ptr()
+    with pytest.raises(ValueError):
+        GradBuckets(model.parameters(), mode="ring")
+    with pytest.raises(ValueError):
+        GradBuckets([torch.nn.Parameter(torch.zeros(3, dtype=torch.float64))])
+
+
+def test_nccl_options_cap_ctas(monkeypatch):
+    from paper_2507_01154_b200.ddp import nccl_options
+
+    monkeypatch.delenv("NCCL_MAX_CTAS", raising=False)
+    opts = nccl_options(4)
+    assert os.environ["NCCL_MAX_CTAS"] == "4"
+    if opts is not None:
+        assert opts.config.max_ctas == 4
+    with pytest.raises(ValueError):
+        nccl_options(0)

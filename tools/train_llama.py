@@ -1,14 +1,31 @@
-"""Llama-2 training step on one GPU, every parameter DP vs non-DP (BASELINE
-configs 3/4 shapes, SURVEY 8d E2E inputs, N=1).
+"""Llama-2 DP pre-training step vs the same model's non-DP step, on 1..N GPUs
+(BASELINE configs 3 and 4; PAPER.md:6, :37, :247 -- FlashDP at 90 % of non-DP on
+Llama-13B; setup PAPER.md:535-537).
 
-    python tools/train_llama.py --model llama-7b [--layers 32] [--batch 1] [--seq 2048]
+    python tools/train_llama.py --model llama-7b [--layers L] [--batch B] [--seq 2048]
+    torchrun --nnodes 1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29511 \
+        tools/train_llama.py --model llama-7b                       # config 3: DP-Adam, all-reduce
+    torchrun --nnodes 1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29511 \
+        tools/train_llama.py --model llama-13b --zero1              # config 4: ZeRO-1
 
-Same model twice: torch modules (non-DP) and DPLinear / DPRMSNorm / DPEmbedding
-with GroupedDPBackward (DP: per-layer clip C=1, sigma=1, Philox noise), fused
-AdamW on fp32 master weights, bf16 autocast, random init, synthetic token ids.
-Prints one JSON line. --layers below the model's depth measures a shallower
-stack of the same blocks (stated in the line): the per-block ratio is what the
-depth does not change.
+One process per GPU (NCCL capped at --comm-sms CTAs). Both arms run the SAME
+data-parallel machinery (ddp.DataParallelStep): fp32 master weights in flat
+per-bucket buffers, gradient buckets reduced from inside the backward on a
+communication stream, Adam without bias correction on the bucket layout
+(replicated after an all-reduce, or ZeRO-1 after a reduce-scatter with the DP
+noise added on the owner's shard). They differ only in the gradients:
+
+  DP:     every parameter DP -- DPLinear (7 projections per block + LM head),
+          DPRMSNorm, DPEmbedding -- per-layer clip C, sigma, Philox noise added
+          once per element; the DP linear weight gradients run bucket by bucket
+          inside the backward (GroupedDPBackward(buckets=...)).
+  non-DP: nn.Linear replaced by FP32GradLinear (cuBLAS writes the fp32 weight
+          gradient, the DP kernels' precision), torch RMSNorm / Embedding.
+
+Random-init weights (same seed on every rank), synthetic token ids (different
+per rank), bf16 autocast. Timing: CUDA events over --steps steps after
+--warmup, barrier + synchronize on both sides, max over ranks. Rank 0 prints
+one JSON line with global tokens/s of both arms and DP as % of non-DP.
 """
 import argparse
 import gc
@@ -19,51 +36,55 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
 
-from paper_2507_01154_b200.dplinear import GroupedDPBackward  # noqa: E402
+from paper_2507_01154_b200.ddp import DataParallelStep, init_distributed  # noqa: E402
 from paper_2507_01154_b200.llama import Llama, LlamaConfig  # noqa: E402
 
 
-def run(dp: bool, a) -> dict:
-    torch.manual_seed(0)
+def run(dp: bool, a, rank: int, world: int, dev: torch.device) -> dict:
+    torch.manual_seed(0)  # identical initial weights on every rank
     cfg = LlamaConfig.named(a.model, seq=a.seq, **({"layers": a.layers} if a.layers else {}))
-    with torch.device("cuda"):
-        model = Llama(cfg, dp=dp, clip_c=1.0, sigma=1.0)
-    opt = torch.optim.AdamW(model.parameters(), lr=1e-5, fused=True)
-    g = torch.Generator(device="cuda").manual_seed(1)
-    idx = torch.randint(0, cfg.vocab, (a.batch, a.seq + 1), device="cuda", generator=g)
+    with torch.device(dev):
+        model = Llama(cfg, dp=dp, clip_c=a.clip, sigma=a.sigma, noise_impl="philox", nondp_linear=a.nondp_linear)
+    gB = a.batch * world
+    step = DataParallelStep(model, dp=dp, mode="reduce_scatter" if a.zero1 else "allreduce", lr=1e-5,
+                            rank=rank, world=world, comm_sms=a.comm_sms, bucket_bytes=a.bucket_mb << 20,
+                            global_batch=gB)
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    idx = torch.randint(0, cfg.vocab, (a.batch, a.seq + 1), device=dev, generator=g)
     x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
-    mods = model.dp_modules() if dp else []
+    scale = 1.0 if dp else 1.0 / gB  # DP modules take the mean over the logical batch themselves
 
-    def step(i):
-        for m in mods:
-            m.set_step(i)
-        opt.zero_grad(set_to_none=True)
-        loss = model.loss(x, y)
-        if dp:
-            with GroupedDPBackward():
-                loss.backward()
-        else:
-            loss.backward()
-        opt.step()
-        return loss
+    def one(i):
+        return step(i, lambda: model.loss(x, y, reduction="sample_sum") * scale)
 
-    torch.cuda.reset_peak_memory_stats()
+    torch.cuda.reset_peak_memory_stats(dev)
     for i in range(a.warmup):
-        step(i)
-    torch.cuda.synchronize()
+        one(i)
+    torch.cuda.synchronize(dev)
     time.sleep(1.0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(a.steps):
-        loss = step(a.warmup + i)
+        loss = one(a.warmup + i)
     e1.record()
-    torch.cuda.synchronize()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
-    out = {"ms_per_step": ms, "tokens_per_s": a.batch * a.seq / (ms * 1e-3), "loss": float(loss.detach()),
-           "dp_modules": len(mods), "params": sum(p.numel() for p in model.parameters()),
-           "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
-    del model, opt, mods
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = {"ms_per_step": ms, "tokens_per_s": gB * a.seq / (ms * 1e-3), "loss": float(loss.detach()) / (
+        a.batch if dp else a.batch / gB), "dp_modules": len(step.dp_mods),
+           "params": sum(p.numel() for p in model.parameters()), "buckets": len(step.buckets.buckets),
+           "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+    del model, step
     gc.collect()
     torch.cuda.empty_cache()
     return out
@@ -73,19 +94,44 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama-7b", choices=["llama-7b", "llama-13b"])
     ap.add_argument("--layers", type=int, default=0, help="0 = the model's depth")
-    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=1, help="sequences per rank")
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--zero1", action="store_true", help="reduce-scatter + ZeRO-1 Adam (config 4)")
+    ap.add_argument("--comm-sms", type=int, default=4)
+    ap.add_argument("--bucket-mb", type=int, default=512)
+    ap.add_argument("--clip", type=float, default=1.0)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--nondp-linear", default="fp32grad", choices=["fp32grad", "torch"])
+    ap.add_argument("--arms", default="nondp,dp")
     a = ap.parse_args()
-    nd = run(False, a)
-    dp = run(True, a)
-    print(json.dumps({"model": a.model, "layers": a.layers or LlamaConfig.named(a.model).layers, "batch": a.batch,
-                      "seq": a.seq, "dp": dp, "non_dp": nd,
-                      "dp_pct_of_non_dp": 100.0 * dp["tokens_per_s"] / nd["tokens_per_s"],
-                      "note": "one GPU; every parameter DP (7 projections per block + LM head: DPLinear; RMSNorms; "
-                              "token embedding), per-layer clip C=1, sigma=1, Philox; fused AdamW; random init, "
-                              "synthetic tokens"}))
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        init_distributed("nccl", comm_sms=a.comm_sms, device=dev)
+    res = {}
+    for arm in a.arms.split(","):
+        res[arm] = run(arm == "dp", a, rank, world, dev)
+    if rank == 0:
+        line = {"model": a.model, "layers": a.layers or LlamaConfig.named(a.model).layers, "gpus": world,
+                "batch_per_gpu": a.batch, "global_batch": a.batch * world, "seq": a.seq,
+                "parallelism": ("zero1" if a.zero1 else "allreduce") + f"-dp{world}",
+                "comm_sms": a.comm_sms, "bucket_mb": a.bucket_mb, "nondp_linear": a.nondp_linear}
+        line.update(res)
+        if "dp" in res and "nondp" in res:
+            line["dp_pct_of_non_dp"] = 100.0 * res["dp"]["tokens_per_s"] / res["nondp"]["tokens_per_s"]
+        line["note"] = ("every parameter DP (7 projections per block + LM head: DPLinear; RMSNorms; token "
+                        "embedding), per-layer clip C, sigma, Philox; non-DP: FP32GradLinear projections (fp32 "
+                        "weight gradients from cuBLAS); both arms: same buckets, collectives and Adam; random init, "
+                        "synthetic tokens")
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
