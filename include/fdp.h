@@ -177,6 +177,33 @@ FDP_API int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const v
 FDP_API int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
            void* ws, size_t ws_bytes, void* stream);
 
+/* Deferred finalize chain. On the single-sample path (B == 1: the sample's
+ * gradient is the layer's GEMM), the clip factor needs the norm of the whole
+ * GEMM result, so the clip + noise pass over grad_w (an HBM-bound elementwise
+ * pass, ~0.3-0.5 of the GEMM time at Llama shapes) cannot start before the GEMM
+ * ends. A chained call leaves that pass PENDING in the chain instead; the next
+ * chained call carries it inside its own stream-K GEMM, whose idle noise and
+ * epilogue warps stream it while the tensor cores run (single-sample, two-phase
+ * reweight or non-DP calls carry; any other call runs it standalone first), and
+ * fdp_chain_flush runs the last one. Until then the pending layer's grad_w holds
+ * the unclipped G and its norms_sq is unwritten. A chain is single-stream and
+ * host-side state (one per backward stream); results are identical to
+ * unchained calls. Reference semantics unchanged: workflows.py:340-421 /
+ * dpcore.py:60-73, the pass is only moved in time.
+ *   fdp_chain_create / fdp_chain_destroy: the chain object (destroy after a flush).
+ *   fdp_dw_chained / fdp_backward_chained: fdp_dw / fdp_backward with a chain.
+ *   fdp_chain_flush: run the pending finalize (if any) on `stream`.
+ *   fdp_chain_stats: jobs carried by a later GEMM / run standalone, pending flag. */
+typedef struct fdp_chain fdp_chain;
+FDP_API int fdp_chain_create(fdp_chain** out);
+FDP_API int fdp_chain_destroy(fdp_chain* chain);
+FDP_API int fdp_chain_flush(fdp_chain* chain, void* stream);
+FDP_API int fdp_chain_stats(const fdp_chain* chain, int64_t* carried, int64_t* flushed, int32_t* pending);
+FDP_API int fdp_dw_chained(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
+                           void* ws, size_t ws_bytes, fdp_chain* chain, void* stream);
+FDP_API int fdp_backward_chained(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w,
+                                 float* norms_sq, void* ws, size_t ws_bytes, fdp_chain* chain, void* stream);
+
 /* The fused DP backward of n layers (n <= 48) in ONE persistent cooperative
  * launch: the training-step batching of Algorithm 1 (every layer keeps its own
  * DPConfig, noise key, per-sample norms and outputs; the producer/MMA/epilogue

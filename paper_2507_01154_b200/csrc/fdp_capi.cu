@@ -12,9 +12,24 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <string>
 #include <map>
 #include <vector>
+
+// Host-side state of a deferred-finalize chain (include/fdp.h, fdp_dw_chained):
+// at most one pending single-sample finalize, and two device slots (ping-pong)
+// for the norm partials of the pending layer, so the call carrying the pending
+// job can write its own partials meanwhile.
+struct fdp_chain {
+  bool pending = false;
+  fdp::FinJob job{};
+  float* part[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  int slot = 0;  // slot the next pending job's partials go to
+  int dev = -1;
+  long long carried = 0, flushed = 0;  // statistics: jobs carried by a GEMM / run standalone
+};
 
 namespace {
 
@@ -637,8 +652,38 @@ uint64_t plan_sig(int32_t kind, const fdp_desc* d, const Plan& pl) {
   return h;
 }
 
+int chain_flush(fdp_chain* c, cudaStream_t s) {
+  if (!c || !c->pending) return FDP_OK;
+  c->pending = false;
+  ++c->flushed;
+  cudaError_t e = fdp::single_sample_finalize(c->job, s);
+  if (e != cudaSuccess) return cuda_fail(e, "deferred single-sample finalize");
+  return FDP_OK;
+}
+
+// device slot for `n` partials of the next pending job (grown outside graph capture only)
+float* chain_slot(fdp_chain* c, size_t n, cudaStream_t s) {
+  const int k = c->slot;
+  if (c->cap[k] >= n && c->part[k]) return c->part[k];
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return nullptr;
+  if (c->part[k]) {
+    cudaStreamSynchronize(s);
+    cudaFree(c->part[k]);
+    c->part[k] = nullptr;
+    c->cap[k] = 0;
+  }
+  const size_t want = n < 4096 ? 4096 : n;
+  if (cudaMalloc(reinterpret_cast<void**>(&c->part[k]), want * sizeof(float)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  c->cap[k] = want;
+  return c->part[k];
+}
+
 int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms, void* ws,
-        size_t ws_bytes, cudaStream_t s) {
+        size_t ws_bytes, cudaStream_t s, fdp_chain* chain = nullptr) {
   int rc = validate(d, kind);
   if (rc) return rc;
   if (!x || !dy || !grad_w) return fail(FDP_ERR_USAGE, "null tensor pointer");
@@ -654,6 +699,28 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     return fail(FDP_ERR_USAGE, "x and dy must be 16-byte aligned for the tensor-core path");
   const Common c = common_of(d);
   cudaError_t e;
+
+  // Deferred-finalize chain: a pending job is carried by this call's first stream-K
+  // launch (single-sample GEMM, two-phase reweight, non-DP), else run standalone
+  // first; it must not touch this call's buffers.
+  const bool stream_k = env_int("FDP_STREAMK", 1) != 0;
+  const bool has_stream_launch =
+      pl.tc && d->in_dtype != FDP_DTYPE_F64 &&
+      ((kind == FDP_KIND_NON_DP && stream_k) ||
+       ((kind == FDP_KIND_FLASHDP || kind == FDP_KIND_IMPLICIT_DP) && pl.path == FDP_PATH_TWO_PHASE &&
+        (pl.norm_phase == FDP_NORMS_SINGLE || stream_k)));
+  fdp::FinJob carry{};
+  if (chain && chain->pending) {
+    const void* g = chain->job.g;
+    const bool alias = g == grad_w || g == x || g == dy || g == norms;
+    if (has_stream_launch && !alias && env_int("FDP_NO_CARRY", 0) == 0) {
+      carry = chain->job;
+      chain->pending = false;
+      ++chain->carried;
+    } else if ((rc = chain_flush(chain, s))) {
+      return rc;
+    }
+  }
 
   if (d->in_dtype == FDP_DTYPE_F64) {  // fp64 parity path: every workflow kind computes the same quantity
     fdp::F64Params q{};
@@ -762,6 +829,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   if (kind == FDP_KIND_NON_DP) {
     if (use_stream) {
       fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, false);
+      q.fin = carry;
       if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
         return cuda_fail(e, "stream-K nondp launch");
       return FDP_OK;
@@ -802,16 +870,39 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   // the GEMM epilogue and one elementwise pass applies the clip factor and the noise
   if (pl.norm_phase == FDP_NORMS_SINGLE) {
     fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, false);
-    q.norm_part = ws_at<float>(ws, pl.off_part);
+    q.fin = carry;
+    // with a chain, the partials go to a chain slot and this layer's finalize becomes
+    // the chain's pending job (carried by the next call's GEMM, or fdp_chain_flush)
+    float* slot = chain ? chain_slot(chain, static_cast<size_t>(pl.stream_tiles), s) : nullptr;
+    q.norm_part = slot ? slot : ws_at<float>(ws, pl.off_part);
     if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
       return cuda_fail(e, "stream-K single-sample GEMM launch");
-    if ((e = fdp::single_sample_finalize(grad_w, d->D * d->P, q.norm_part, pl.stream_tiles, d->clip_c,
-                                         d->clip_c * d->clip_c, c.inv_batch, norms, c.add_noise, d->noise_impl,
-                                         c.noise_scale, c.key_base, c.key_base_g,
-                                         reinterpret_cast<const long long*>(d->device_step),
-                                         static_cast<uint64_t>(d->seed), static_cast<uint64_t>(d->layer_id),
-                                         c.noise_lo, c.noise_hi, s)) != cudaSuccess)
-      return cuda_fail(e, "single-sample finalize");
+    fdp::FinJob j{};
+    j.g = grad_w;
+    j.n = d->D * d->P;
+    j.part = q.norm_part;
+    j.n_parts = pl.stream_tiles;
+    j.clip_c = d->clip_c;
+    j.clip_c2 = d->clip_c * d->clip_c;
+    j.inv_batch = c.inv_batch;
+    j.norms_out = norms;
+    j.add_noise = c.add_noise;
+    j.impl = d->noise_impl;
+    j.scale = c.noise_scale;
+    j.base = c.key_base;
+    j.base_g = c.key_base_g;
+    j.step_ptr = reinterpret_cast<const long long*>(d->device_step);
+    j.seed_u = static_cast<uint64_t>(d->seed);
+    j.layer_u = static_cast<uint64_t>(d->layer_id);
+    j.lo = c.noise_lo;
+    j.hi = c.noise_hi;
+    if (slot) {
+      chain->job = j;
+      chain->pending = true;
+      chain->slot ^= 1;
+      return FDP_OK;
+    }
+    if ((e = fdp::single_sample_finalize(j, s)) != cudaSuccess) return cuda_fail(e, "single-sample finalize");
     return FDP_OK;
   }
   // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass
@@ -855,6 +946,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     }
     if (use_stream) {  // stream-K over (tile, sample) units: no partial last wave
       fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, true);
+      q.fin = carry;
       if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
         return cuda_fail(e, "stream-K reweight launch");
     } else {
@@ -1088,6 +1180,46 @@ int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, floa
 }
 
 
+int fdp_chain_create(fdp_chain** out) {
+  if (!out) return fail(FDP_ERR_USAGE, "null output");
+  *out = new (std::nothrow) fdp_chain();
+  if (!*out) return fail(FDP_ERR_CAPACITY, "out of host memory");
+  return FDP_OK;
+}
+
+int fdp_chain_destroy(fdp_chain* c) {
+  if (!c) return FDP_OK;
+  if (c->pending) return fail(FDP_ERR_USAGE, "fdp_chain_destroy: a finalize is still pending (fdp_chain_flush first)");
+  for (int k = 0; k < 2; ++k)
+    if (c->part[k]) cudaFree(c->part[k]);
+  delete c;
+  return FDP_OK;
+}
+
+int fdp_chain_flush(fdp_chain* c, void* stream) {
+  if (!c) return fail(FDP_ERR_USAGE, "null chain");
+  return chain_flush(c, static_cast<cudaStream_t>(stream));
+}
+
+int fdp_chain_stats(const fdp_chain* c, int64_t* carried, int64_t* flushed, int32_t* pending) {
+  if (!c) return fail(FDP_ERR_USAGE, "null chain");
+  if (carried) *carried = c->carried;
+  if (flushed) *flushed = c->flushed;
+  if (pending) *pending = c->pending ? 1 : 0;
+  return FDP_OK;
+}
+
+int fdp_backward_chained(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w,
+                         float* norms_sq, void* ws, size_t ws_bytes, fdp_chain* chain, void* stream) {
+  if (!chain) return fail(FDP_ERR_USAGE, "null chain");
+  return run(kind, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream), chain);
+}
+
+int fdp_dw_chained(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq, void* ws,
+                   size_t ws_bytes, fdp_chain* chain, void* stream) {
+  return fdp_backward_chained(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, chain, stream);
+}
+
 int fdp_group_workspace_bytes_ex(int32_t n, const fdp_desc* descs, int32_t max_ctas, size_t* bytes) {
   if (!descs || !bytes) return fail(FDP_ERR_USAGE, "null argument");
   if (max_ctas < 0) return fail(FDP_ERR_USAGE, "max_ctas must be >= 0, got %d", max_ctas);
@@ -1186,6 +1318,7 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   gp.poll_ns = env_int("FDP_POLL_NS", 0);
   gp.pub_mode = env_int("FDP_PUB_MODE", 1);
   gp.poll_mode = env_int("FDP_POLL_MODE", 0);
+  gp.pf_ahead = env_int("FDP_PF_AHEAD", 0);
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
   float* red = reinterpret_cast<float*>(tmem_holder + 4);
   float* bcast = red + kEpiWarps;
   volatile unsigned* pf_done = reinterpret_cast<volatile unsigned*>(bcast + 1);  // layers pre-filled so far
+  volatile int* ep_layer = reinterpret_cast<volatile int*>(bcast + 2);          // layer the epilogue is on
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
     *pf_done = 0u;
+    *ep_layer = 0;
     fence_mbar_init();
     fence_proxy_async_smem();
   }
@@ -195,12 +197,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     // ======================= noise warps: pre-fill this CTA's grad_w rows =======================
     // (accumulate ? old : 0) + sigma*C*noise, or zeros when only sample groups need
     // initialised rows for their reduce-adds. Runs ahead across layers.
+    // Bounded run-ahead: a pre-filled row must still be in L2 when the epilogue's
+    // reduce-add of the same row arrives. Unbounded, the two noise warps finish
+    // every layer's pre-fill early in the launch and the rows are evicted and
+    // re-read (grad_w crosses DRAM three times: 1.245x the algorithmic bytes on
+    // the 48-layer GPT-2 step); started with the layer's own epilogue, a row lives
+    // in L2 for about one layer's sample units.
     const int ntid = (warp - 2) * 32 + lane;
     for (int l = 0; l < gp.n_layers; ++l) {
       const GLayer& L = gp.L[l];
       const int lc = lcid(L);
       const bool draw = L.add_noise != 0 && gp.dbg_noise != 1;
       if (lc < L.n_wtiles * L.groups && (L.add_noise != 0 || L.groups > 1)) {
+        if (gp.pf_ahead >= 0) {
+          const uint64_t t0 = globaltimer_ns();
+          while (*ep_layer < l - gp.pf_ahead) {
+            if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x408);
+            __nanosleep(256);
+          }
+        }
         uint64_t kb = L.key_base, kbg = L.key_base_g;
         if (L.step_ptr) {
           kb = absorb3(L.seed_u, L.layer_u, static_cast<uint64_t>(*L.step_ptr));
@@ -255,6 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     for (int l = 0; l < gp.n_layers; ++l) {
       const GLayer& L = gp.L[l];
       const int lc = lcid(L);
+      if (etid == 0) *ep_layer = l;  // releases the noise warps' pre-fill of layers <= l + pf_ahead
       if (lc >= L.n_wtiles * L.groups) continue;
       const int wt = lc % L.n_wtiles, group = lc / L.n_wtiles;
       const int tile = wt * CG + rank;

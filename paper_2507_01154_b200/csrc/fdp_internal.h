@@ -76,6 +76,26 @@ cudaError_t launch_tc(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMa
 // Upper bound on co-resident CTAs of the (bn, cg) kernel on this device (0: cannot run).
 int tc_max_coresident_ctas(int bn, int cg);
 
+// Deferred finalize of a single-sample layer (B == 1): grad_w <- c * G + sigma*C*noise
+// with c from the layer's norm partials (dpcore.py:41-47, 60-73). Run standalone
+// (single_sample_finalize) or carried by the NEXT stream-K launch, whose idle noise
+// and epilogue warps stream it while the tensor cores run that launch's GEMM.
+struct FinJob {
+  float* g;               // (D, P) fp32 gradient holding the unclipped G (nullptr: no job)
+  long long n;            // D * P (P % 8 == 0)
+  const float* part;      // per-tile sums of squares of G
+  int n_parts;
+  double clip_c, clip_c2;
+  float inv_batch;
+  float* norms_out;       // (1,) ||G||^2 or nullptr
+  int add_noise, impl;
+  float scale;
+  uint64_t base, base_g;
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+  long long lo, hi;       // the rank's noise slice of [0, n)
+};
+
 // ---- stream-K persistent kernel (fdp_stream.cu): two-phase reweight pass and non-DP dW
 struct StreamParams {
   int B, P, D, n_pt, n_wtiles, n_kb;
@@ -93,6 +113,7 @@ struct StreamParams {
   unsigned* ctrl;           // [0] exit counter, [1] error word
   unsigned long long budget_ns;
   int mc;                   // 2: 4-CTA clusters (two pairs, X boxes multicast; bn 256, cg 2), else 1
+  FinJob fin;               // carried deferred finalize of the previous single-sample layer (fin.g == nullptr: none)
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {
@@ -130,6 +151,9 @@ struct GroupParams {
   int dbg_noise;  // debug (FDP_DEBUG_NOISE): 1 = no draws (zero pre-fill), 2 = draws scaled by 0
   int pub_mode, poll_mode, poll_ns;  // experiments (FDP_PUB_MODE, FDP_POLL_MODE, FDP_POLL_NS)
   int nosync;  // debug (FDP_DEBUG_NOSYNC): clip factors from whatever partials are present, no wait
+  // noise / row pre-fill run-ahead bound: the noise warps start layer l once the
+  // epilogue has started layer l - pf_ahead (FDP_PF_AHEAD; < 0 = unbounded)
+  int pf_ahead;
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
 
@@ -189,6 +213,7 @@ cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int P, c
 
 // B == 1 second pass: ||G||^2 from the per-tile partials (fixed order), then
 // grad_w = grad_w * min(1, C/||G||) * inv_batch (+ sigma*C*noise on [lo, hi)).
+cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s);
 cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part, int n_parts, double clip_c,
                                    double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl,
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,

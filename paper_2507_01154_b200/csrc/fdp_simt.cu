@@ -325,6 +325,12 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
   return cudaGetLastError();
 }
 
+cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s) {
+  return single_sample_finalize(j.g, j.n, j.part, j.n_parts, j.clip_c, j.clip_c2, j.inv_batch, j.norms_out,
+                                j.add_noise, j.impl, j.scale, j.base, j.base_g, j.step_ptr, j.seed_u, j.layer_u, j.lo,
+                                j.hi, s);
+}
+
 cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s) {
   k_partial_norms<<<dim3(p.n_pt, p.n_dt, p.B), 256, 0, s>>>(p);
   return cudaGetLastError();

@@ -74,6 +74,90 @@ struct SegWalk {
   }
 };
 
+// Carried deferred finalize (FinJob): this CTA's contiguous slice of the float4
+// index space, handed out in warp-sized chunks of 32 x kFinU float4 through a
+// shared-memory counter to whichever worker warp is idle (the noise warps all
+// the time, the epilogue warps while they wait for a TMEM buffer). Streaming
+// loads / stores (evict-first) keep the GEMM operands in L2.
+constexpr int kFinU = 4;
+struct FinWorker {
+  const FinJob* j;
+  unsigned* ctr;
+  long long lo, hi;  // float4 range of this CTA
+  float f;           // clip factor (per warp, lazily)
+  bool have_f;
+  uint64_t base, base_g;
+  int mode;          // 1: Philox over the whole range, 2: no noise, 0: generic
+
+  __device__ __forceinline__ void init(const FinJob* job, unsigned* counter) {
+    j = job;
+    ctr = counter;
+    const long long n4 = j->n >> 2;
+    lo = n4 * blockIdx.x / gridDim.x;
+    hi = n4 * (blockIdx.x + 1) / gridDim.x;
+    have_f = false;
+    base = j->base;
+    base_g = j->base_g;
+    if (j->add_noise && j->step_ptr) {
+      base = absorb3(j->seed_u, j->layer_u, static_cast<uint64_t>(*j->step_ptr));
+      base_g = base + kGamma;
+    }
+    mode = (!j->add_noise || j->hi <= j->lo) ? 2 : (j->impl == 2 && j->lo <= 0 && j->hi >= j->n) ? 1 : 0;
+  }
+  // fixed-order fp64 sum of the partials: the same factor in every warp of every CTA
+  __device__ __forceinline__ void factor(int lane) {
+    double t = 0.0;
+    for (int i = lane; i < j->n_parts; i += 32) t += static_cast<double>(j->part[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    const double cf = (t <= j->clip_c2) ? 1.0 : j->clip_c / sqrt(t);  // dpcore.py:41-47
+    f = static_cast<float>(cf) * j->inv_batch;
+    have_f = true;
+    if (lane == 0 && blockIdx.x == 0 && j->norms_out && threadIdx.x == 64) j->norms_out[0] = static_cast<float>(t);
+  }
+  // one chunk for the calling warp; false when this CTA's slice is exhausted
+  __device__ __forceinline__ bool chunk(int lane) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(ctr, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    const long long s0 = lo + static_cast<long long>(k) * (32 * kFinU);
+    if (s0 >= hi) return false;
+    if (!have_f) factor(lane);
+    float4* g4 = reinterpret_cast<float4*>(j->g);
+    float4 v[kFinU];
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u) {
+      const long long i = s0 + u * 32 + lane;
+      if (i < hi) v[u] = __ldcs(g4 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kFinU; ++u) {
+      const long long i = s0 + u * 32 + lane;
+      if (i >= hi) continue;
+      float4 r = make_float4(v[u].x * f, v[u].y * f, v[u].z * f, v[u].w * f);
+      if (mode == 1) {
+        const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
+        r.x += j->scale * z.x;
+        r.y += j->scale * z.y;
+        r.z += j->scale * z.z;
+        r.w += j->scale * z.w;
+      } else if (mode == 0) {
+        const long long e = i << 2;
+        if (e + 3 >= j->lo && e < j->hi) {
+          const float4 z = j->impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
+                                        : noise_draw4(j->impl, base_g, base, static_cast<uint64_t>(i));
+          if (e + 0 >= j->lo && e + 0 < j->hi) r.x += j->scale * z.x;
+          if (e + 1 >= j->lo && e + 1 < j->hi) r.y += j->scale * z.y;
+          if (e + 2 >= j->lo && e + 2 < j->hi) r.z += j->scale * z.z;
+          if (e + 3 >= j->lo && e + 3 < j->hi) r.w += j->scale * z.w;
+        }
+      }
+      __stcs(g4 + i, r);
+    }
+    return true;
+  }
+};
+
 // MC = 2: a 4-CTA cluster holds two CTA pairs working on vertically adjacent pair
 // tiles (same X columns, consecutive dY row blocks) in lockstep; each X box is
 // loaded once and multicast to the CTA of both pairs that needs it, so L2 serves
@@ -95,6 +179,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tempty = tfull + C::kNBuf;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps] tile sum-of-squares partials
+  unsigned* fin_ctr = reinterpret_cast<unsigned*>(red + kEpiWarps);  // carried finalize: next chunk
+  const bool fin_on = p.fin.g != nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -118,6 +204,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
+    *fin_ctr = 0u;
     fence_mbar_init();
     fence_proxy_async_smem();
     prefetch_tmap(&tm_dy);
@@ -243,6 +330,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       named_bar_sync(3, 64);
       if (ntid == 0) red_release_add_u32(&p.tile_cnt[wt * CL + crank], 1u);
     }
+    if (fin_on) {  // the carried finalize of the previous layer, for as long as work is left
+      FinWorker fw;
+      fw.init(&p.fin, fin_ctr);
+      if (blockIdx.x == 0 && warp == 2) fw.factor(lane);  // also writes the layer's ||G||^2
+      while (fw.chunk(lane)) {
+      }
+    }
   } else if (warp >= kEpiWarp0) {
     // ======================= epilogue =======================
     const int ew = warp - kEpiWarp0;
@@ -251,9 +345,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t nkb = p.key_base;
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     uint32_t rbuf = 0, rph = 0;
+    FinWorker fw;
+    if (fin_on) fw.init(&p.fin, fin_ctr);
+    bool fin_left = fin_on;
     SegWalk w(cid, n_clusters, p.B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
+      if (fin_left) {  // idle until this segment's first accumulator is complete: stream the carried finalize
+        const uint32_t a = smem_u32(&tfull[rbuf]);
+        while (!mbar_try_wait(a, rph)) {
+          if (!fw.chunk(lane)) {
+            fin_left = false;
+            break;
+          }
+        }
+      }
       const bool whole = bb == 0 && be == p.B;
       const int tile = wt * CL + crank;
       const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
@@ -348,6 +454,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           bulk_commit();
         }
       }
+    }
+    while (fin_left && fw.chunk(lane)) {
     }
     if (etid == 0) bulk_wait_all();
   }

@@ -337,6 +337,7 @@ class GradBuckets:
                 register_inplace_grad_hook(p, self.mark_ready)  # gradients GEMMs write in place
         self.issued: list[int] = []  # bucket issue order of the last backward (tests / traces)
         self.enabled = True  # False while accumulating micro-batches (no collectives)
+        self.trace = [] if os.environ.get("FDP_DDP_TRACE") == "1" else None  # (bucket, param, pending) per ready
 
     def _close(self, params, flat_params):
         b = _Bucket()
@@ -402,6 +403,8 @@ class GradBuckets:
         if i is None:
             return
         b = self.buckets[i]
+        if self.trace is not None:
+            self.trace.append((i, b.params.index(p), b.pending))
         b.pending -= 1
         if b.pending == 0:
             self._launch(i)
@@ -412,9 +415,11 @@ class GradBuckets:
             return
         b.launched = True
         self.issued.append(i)
-        if self.world == 1:
+        if self.world == 1 or os.environ.get("FDP_DDP_NOCOMM") == "1":  # debug: local gradients only
             return
         if self.comm is not None:
+            if os.environ.get("FDP_DDP_SYNC") == "1":  # debug: full device sync before the collective
+                torch.cuda.synchronize(self.device)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.device))
             self.comm.wait_event(ev)

@@ -104,7 +104,8 @@ class GroupedDPBackward:
     bucket flushes, not at the end of the backward. ``max_ctas`` caps the
     persistent launches so NCCL keeps its SMs."""
 
-    def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0, buckets=None):
+    def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0, buckets=None,
+                 defer_finalize: bool = True):
         self.noise_impl = noise_impl
         self.max_ctas = max_ctas
         self.buckets = buckets
@@ -113,6 +114,8 @@ class GroupedDPBackward:
         self.flushes = 0
         self._ws = None
         self._waiting: dict = {}
+        self.chain = None  # DeferredChain of the per-layer (solo) kernels; None: built on first use
+        self.defer_finalize = defer_finalize
 
     def __enter__(self):
         if _ACTIVE_GROUP[0] is not None:
@@ -150,6 +153,13 @@ class GroupedDPBackward:
         self._flush_items(self._pending)
         self._pending = []
 
+    def _chain(self):
+        if self.chain is None:
+            from .workflows import DeferredChain
+
+            self.chain = DeferredChain()
+        return self.chain
+
     def _flush_items(self, pending) -> None:
         from .workflows import PreparedGroup, WorkflowKind, _run
         from .errors import CapacityError, UsageError
@@ -185,11 +195,20 @@ class GroupedDPBackward:
             # per-layer two-phase kernels; the rest share the multi-layer launches
             solo = [it for it in items if not _fits_group(it[1].shape, it[2].shape)]
             items = [it for it in items if _fits_group(it[1].shape, it[2].shape)]
+            # per-layer kernels in sequence through a deferred-finalize chain: a
+            # single-sample layer's clip + noise pass runs inside the next layer's
+            # GEMM (include/fdp.h fdp_dw_chained); the last one is flushed here
+            done = []
             for m, x, dy, cfg, _, _ in solo:
                 g = out_for(m)
                 gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,
-                          rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None).grad_w
-                deliver(m, gw, g is not None)
+                          rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None,
+                          chain=self._chain() if self.defer_finalize else None).grad_w
+                done.append((m, gw, g is not None))
+            if done and self.defer_finalize:
+                self._chain().flush()
+            for m, gw, direct in done:
+                deliver(m, gw, direct)
             for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
                 chunk = items[lo:lo + 48]
                 direct = all(out_for(m) is not None for m, *_ in chunk)

@@ -121,3 +121,61 @@ def ledger(kind: str, B: int, T: int, P: int, D: int, width: int, plan=None, dp:
                              peak_scratch_bytes=(plan.b * plan.t * (plan.p + plan.d) + plan.b * plan.d * plan.p
                                                  + plan.b) * width)
     raise UsageError(f"unknown workflow kind {kind!r}")
+
+
+def device_ledger(kind: str, path: str, norm_phase: str, launches: int, B: int, T: int, P: int, D: int,
+                  in_width: int, out_width: int, *, n_tiles: int = 1, groups: int = 1, accumulate: bool = False,
+                  add_noise: bool = True) -> TrafficReport:
+    """Ledger of the path the device actually executed (the report
+    describes the path taken), in BYTES of the real element types: X / dY of
+    `in_width` bytes, grad_w and norms of `out_width` bytes.
+
+      fused      one launch: X, dY read once; per (sample, CTA tile) one norm
+                 partial (8-byte tagged slot) published and polled (barriers: one
+                 block-wise all-reduce per sample); grad_w written once, plus one
+                 pre-fill write and one reduce-add read+write per extra sample group
+      two_phase  ghost:     X, dY read by the Gram norm pass AND the reweight pass
+                            (inputs twice), Gram flops T^2 (P+D) per sample redundant
+                 recompute: inputs twice, the per-sample contraction computed twice
+                 single:    B == 1, the GEMM writes G, one pass reads it and writes
+                            c * G + noise (grad_w written twice, read once)
+      simt       partial-norm pass + weighted pass: inputs twice, contraction twice
+      explicit   G and G' materialised (2 B D P out_width bytes), 5 launches
+      non_dp     inputs once, grad_w once
+    Peak scratch is the device workspace's per-sample state (norm slots), not a
+    simulated scratchpad."""
+    inputs = B * T * (P + D) * in_width
+    gw = D * P * out_width
+    grad_flops = 2 * B * T * D * P
+    clip_flops = 4 * B * D * P
+    emit = D * P if add_noise else 0
+    acc_read = gw if accumulate else 0
+    if kind == "non_dp":
+        return TrafficReport(bytes_loaded=inputs + acc_read, bytes_stored=gw, flops=grad_flops,
+                             kernel_launches=launches)
+    if kind == "explicit_dp":
+        g = B * D * P * out_width
+        return TrafficReport(bytes_loaded=inputs + 3 * g + B * out_width + acc_read,
+                             bytes_stored=2 * g + B * out_width + gw, flops=grad_flops + clip_flops + emit,
+                             kernel_launches=launches, barriers=launches - 1, per_sample_grad_bytes_stored=2 * g,
+                             peak_scratch_bytes=2 * g)
+    norm_slots = B * n_tiles * 8
+    if kind == "flashdp" and path == "fused":
+        extra = (groups - 1) * gw  # sample groups: rows pre-filled once, every group reduce-adds onto them
+        return TrafficReport(bytes_loaded=inputs + norm_slots + extra + acc_read,
+                             bytes_stored=gw + norm_slots + extra + B * out_width,
+                             flops=grad_flops + clip_flops + emit, barriers=B, kernel_launches=launches,
+                             peak_scratch_bytes=norm_slots)
+    if kind == "flashdp" and path == "two_phase" and norm_phase == "single":
+        return TrafficReport(bytes_loaded=inputs + gw + acc_read, bytes_stored=2 * gw + B * out_width,
+                             flops=grad_flops + 2 * D * P + emit, barriers=launches - 1, kernel_launches=launches,
+                             peak_scratch_bytes=n_tiles * 4)
+    if kind == "flashdp" and path == "two_phase" and norm_phase == "ghost":
+        ghost = B * T * T * (P + D)
+        return TrafficReport(bytes_loaded=2 * inputs + acc_read, bytes_stored=gw + B * out_width,
+                             flops=grad_flops + ghost + B * D * P + emit, redundant_flops=ghost,
+                             barriers=launches - 1, kernel_launches=launches, peak_scratch_bytes=norm_slots)
+    # recompute norm phase (flashdp two-phase / implicit) and the generic SIMT path
+    return TrafficReport(bytes_loaded=2 * inputs + acc_read, bytes_stored=gw + B * out_width,
+                         flops=2 * grad_flops + clip_flops + emit, redundant_flops=grad_flops,
+                         barriers=launches - 1, kernel_launches=launches, peak_scratch_bytes=norm_slots)

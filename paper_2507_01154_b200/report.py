@@ -81,7 +81,7 @@ def _run_cell(kind: WorkflowKind, x, dy, cfg: DPConfig, micro_batch: Optional[tu
     if size * steps != x.shape[0]:
         raise UsageError(f"micro_batch {size}x{steps} does not cover B={x.shape[0]}")
     from .memmodel import merge_reports
-    parts, reports, norms = [], [], []
+    parts, reports, refs, norms = [], [], [], []
     micro_cfg = DPConfig(clip_c=cfg.clip_c, sigma=0.0, reduction="sum", seed=cfg.seed, layer_id=cfg.layer_id,
                          step=cfg.step)
     for i in range(steps):
@@ -90,12 +90,13 @@ def _run_cell(kind: WorkflowKind, x, dy, cfg: DPConfig, micro_batch: Optional[tu
                                                                                                **opts)
         parts.append(res.grad_w)
         reports.append(res.report)
+        refs.append(res.reference_report)
         norms.append(res.per_sample_norms_sq)
-    report = merge_reports(reports)
+    report, ref = merge_reports(reports), merge_reports(refs)
     if kind == WorkflowKind.NON_DP:
-        return BackwardResult(sum(parts[1:], parts[0].clone()), report, torch.zeros(0, device=x.device))
+        return BackwardResult(sum(parts[1:], parts[0].clone()), report, torch.zeros(0, device=x.device), ref)
     grad = accumulate_micro_batches(parts, x.shape[0], cfg, noise_impl=opts.get("noise_impl", "keyed_f32"))
-    return BackwardResult(grad, report, torch.cat(norms))
+    return BackwardResult(grad, report, torch.cat(norms), ref)
 
 
 def compare_workflows(x: torch.Tensor, dy: torch.Tensor, cfg: DPConfig, *, layer: str = "layer",
@@ -117,12 +118,14 @@ def compare_workflows(x: torch.Tensor, dy: torch.Tensor, cfg: DPConfig, *, layer
             results[kind], times[kind] = _timed(fn, time_reps)
         else:
             results[kind] = fn()
-    base = results[WorkflowKind.NON_DP].report
+    # the rows are the reference's schema and ledgers (what dpflows would print);
+    # the executed-path ledgers stay on each BackwardResult.report
+    base = results[WorkflowKind.NON_DP].reference_report
     base_traffic = base.bytes_loaded + base.bytes_stored
     rows = []
     for kind in workflows:
         res = results[kind]
-        rep = res.report
+        rep = res.reference_report
         rows.append(ComparisonRow(
             workflow=kind.value, layer=layer, B=int(x.shape[0]),
             bytes_loaded=rep.bytes_loaded, bytes_stored=rep.bytes_stored,

@@ -32,7 +32,7 @@ import torch
 from . import _lib
 from .dpcore import DPConfig
 from .errors import OrderingFault, ShapeError, UsageError
-from .memmodel import B200_SPEC, MemSpec, TrafficReport, ledger
+from .memmodel import B200_SPEC, MemSpec, TrafficReport, device_ledger, ledger
 from .tensor import Tensor
 from .tiling import BlockPlan, LayerDims, check_plan, plan_blocks
 
@@ -47,8 +47,11 @@ class WorkflowKind(Enum):
 @dataclass
 class BackwardResult:
     grad_w: object             # torch (D,P) fp32 on the GPU, or Tensor for host callers
-    report: TrafficReport      # closed-form ledger of the workflow (memmodel.ledger)
+    report: TrafficReport      # ledger of the path the device executed (memmodel.device_ledger)
     per_sample_norms_sq: object  # torch (B,) fp32, or np.ndarray for host callers
+    # the reference simulator's ledger of the same call and block plan
+    # (memmodel.ledger, workflows.py:340-440 semantics; what dpflows itself returns)
+    reference_report: Optional[TrafficReport] = None
 
 
 # ---------------------------------------------------------------- workspaces
@@ -119,7 +122,7 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
          accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
          skip_barrier: bool = False, short_timeout: bool = False, workspace: Optional[torch.Tensor] = None,
          device_step: Optional[torch.Tensor] = None, norm_phase: str = "auto",
-         deterministic: bool = False) -> BackwardResult:
+         deterministic: bool = False, chain: Optional[DeferredChain] = None) -> BackwardResult:
     dims = _dims(x, dy)
     if kind != WorkflowKind.NON_DP and cfg is None:
         raise UsageError("DP workflows need a DPConfig")
@@ -166,10 +169,20 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         ws = workspace.view(torch.uint8) if workspace.dtype != torch.uint8 else workspace
     else:
         ws = _POOL.get(ws_bytes.value, device, stream)
-    rc = lib.fdp_backward(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
-                          norms.data_ptr() if norms is not None else None, ws.data_ptr(), ws.numel(),
-                          stream.cuda_stream)
-    _lib.check(rc)
+    if chain is not None:
+        if host:
+            raise UsageError("chain= needs device inputs (the pending finalize writes device memory later)")
+        rc = lib.fdp_backward_chained(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                                      norms.data_ptr() if norms is not None else None, ws.data_ptr(), ws.numel(),
+                                      chain.handle, stream.cuda_stream)
+        _lib.check(rc)
+        if chain.stats()["pending"]:
+            chain.hold(grad, norms)  # this call's finalize is pending: keep its outputs alive
+    else:
+        rc = lib.fdp_backward(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                              norms.data_ptr() if norms is not None else None, ws.data_ptr(), ws.numel(),
+                              stream.cuda_stream)
+        _lib.check(rc)
 
     if skip_barrier:
         # The kernel records whether a clip read the norm accumulator before every
@@ -185,15 +198,38 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
     if wplan is None:  # the reference plans every kind from the spec (workflows.py:437-438)
         wplan = plan_blocks(dims, spec or B200_SPEC)
     width = (spec or B200_SPEC).dtype_width_bytes
-    report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)
+    ref_report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)
+    report = _executed_ledger(kind, desc, dims, xd.element_size(), out_dtype, accumulate, add_noise and c.sigma > 0)
 
     if host_torch:
-        return BackwardResult(grad.cpu(), report, norms.cpu() if norms is not None else torch.zeros(0))
+        return BackwardResult(grad.cpu(), report, norms.cpu() if norms is not None else torch.zeros(0), ref_report)
     if host:
         g_host = Tensor((dims.D, dims.P), grad.double().cpu().numpy())
         n_host = norms.double().cpu().numpy() if norms is not None else np.zeros(0)
-        return BackwardResult(g_host, report, n_host)
-    return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device))
+        return BackwardResult(g_host, report, n_host, ref_report)
+    return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device), ref_report)
+
+
+_PLAN_CACHE: dict = {}
+
+
+def _executed_ledger(kind: WorkflowKind, desc, dims: LayerDims, in_width: int, out_dtype, accumulate: bool,
+                     add_noise: bool) -> TrafficReport:
+    """device_ledger of the plan the C library resolved for this descriptor."""
+    key = (kind.value, dims.B, dims.T, dims.P, dims.D, desc.in_dtype, desc.path, desc.norm_phase, desc.flags,
+           torch.cuda.current_device())
+    info = _PLAN_CACHE.get(key)
+    if info is None:
+        info = _lib.plan(desc, kind.value)
+        if len(_PLAN_CACHE) > 4096:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = info
+    path = _lib.PATH_NAMES[info.path]
+    phase = _lib.NORM_PHASE_NAMES.get(info.norm_phase, "auto")
+    out_w = 8 if out_dtype == torch.float64 else 4
+    n_tiles = max(1, info.n_d * info.n_p)
+    return device_ledger(kind.value, path, phase, info.launches, dims.B, dims.T, dims.P, dims.D, in_width, out_w,
+                         n_tiles=n_tiles, groups=info.groups, accumulate=accumulate, add_noise=add_noise)
 
 
 def _check_out(t: torch.Tensor, shape: tuple, dtype: torch.dtype, device: torch.device, name: str) -> None:
@@ -203,6 +239,50 @@ def _check_out(t: torch.Tensor, shape: tuple, dtype: torch.dtype, device: torch.
             or not t.is_contiguous() or t.device != device:
         got = (tuple(t.shape), t.dtype, t.device) if isinstance(t, torch.Tensor) else type(t)
         raise ShapeError(f"{name} must be a contiguous {dtype} {tuple(shape)} tensor on {device}, got {got}")
+
+
+class DeferredChain:
+    """A deferred-finalize chain (include/fdp.h fdp_chain): pass it as ``chain=``
+    to consecutive DP backward calls on one stream. A single-sample layer's
+    clip + noise pass (B == 1) is then carried by the next call's GEMM kernel,
+    whose idle warps stream it under the tensor-core work, instead of running as
+    its own HBM-bound pass; ``flush()`` runs the last pending one. Until a later
+    call or ``flush()``, the pending layer's grad_w holds the unclipped G and its
+    norms are unwritten. Results equal the unchained calls."""
+
+    def __init__(self):
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.fdp_chain_create(ctypes.byref(h)))
+        self._h = h
+        self._keep = []  # tensors the pending job writes (kept alive until it ran)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def hold(self, *tensors) -> None:
+        self._keep = [t for t in tensors if t is not None]
+
+    def flush(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(self._lib.fdp_chain_flush(self._h, s.cuda_stream))
+        self._keep = []
+
+    def stats(self) -> dict:
+        c, f, p = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        _lib.check(self._lib.fdp_chain_stats(self._h, ctypes.byref(c), ctypes.byref(f), ctypes.byref(p)))
+        return {"carried": c.value, "standalone": f.value, "pending": bool(p.value)}
+
+    def __del__(self):
+        try:
+            if self._h:
+                if self.stats()["pending"]:
+                    self.flush()
+                self._lib.fdp_chain_destroy(self._h)
+                self._h = None
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 def _step_ptr(t: Optional[torch.Tensor]):
@@ -232,10 +312,11 @@ class PreparedBackward:
                  path: str = "auto", noise_impl: str = "keyed_f32", accumulate: bool = False,
                  add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
                  device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
-                 norm_phase: str = "auto", deterministic: bool = False):
+                 norm_phase: str = "auto", deterministic: bool = False, chain: Optional["DeferredChain"] = None):
         dims = _dims(x, dy)
         if not (x.is_cuda and dy.is_cuda and x.is_contiguous() and dy.is_contiguous() and x.dtype == dy.dtype):
             raise UsageError("PreparedBackward needs contiguous CUDA inputs of one dtype")
+        self.chain = chain
         c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
         self.kind = kind
         self.x, self.dy = x, dy
@@ -279,7 +360,10 @@ class PreparedBackward:
 
     def __call__(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
-        _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
+        if self.chain is not None:  # single-sample finalize deferred into the next chained call
+            _lib.check(self._lib.fdp_backward_chained(*self._args, self.chain.handle, s.cuda_stream))
+        else:
+            _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
 
 
 class PreparedGroup:
@@ -436,8 +520,11 @@ class HostStreamedBackward:
                     n_host.copy_(norms, non_blocking=True)
             pending.append((grad, norms))
             width = (spec or B200_SPEC).dtype_width_bytes
-            report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=plan_blocks(dims, spec or B200_SPEC))
-            results.append(BackwardResult(g_host, report, n_host if kind != WorkflowKind.NON_DP else torch.zeros(0)))
+            ref = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=plan_blocks(dims, spec or B200_SPEC))
+            report = _executed_ledger(kind, desc, dims, xd.element_size(), torch.float32, False,
+                                      c.sigma > 0)
+            results.append(BackwardResult(g_host, report, n_host if kind != WorkflowKind.NON_DP else torch.zeros(0),
+                                          ref))
         self._out.synchronize()
         comp.wait_stream(self._out)  # later device work on these buffers (caching allocator reuse) orders after
         del pending

@@ -120,7 +120,7 @@ def test_random_small_instances_against_reference_golden():
         r = fdp.backward_flashdp(x, dy, cfg, plan, noise_impl="keyed_f64")
         assert rel(host(r.grad_w), g[f"grad{i}"]) < F32_TOL, i
         assert rel(host(r.per_sample_norms_sq), g[f"norms{i}"]) < F32_TOL, i
-        assert r.report.kernel_launches == nb and r.report.barriers == nb + 1
+        assert r.reference_report.kernel_launches == nb and r.reference_report.barriers == nb + 1
 
 
 def test_micro_batches_against_reference_golden():

@@ -122,3 +122,26 @@ def test_dpcore_float64_dropins_against_reference_golden(golden_dir):
         assert np.max(np.abs(got - g[f"micro_{tag}"])) < 1e-12
         # host float64 tensors work too (noise drawn on the device, result on the host)
         assert np.max(np.abs(fdp.finalize_gradient(gs.cpu(), 3, cfg).numpy() - g[f"finalize_{tag}"])) < 1e-12
+
+
+def test_report_describes_the_executed_path():
+    """BackwardResult.report is the ledger of what the device ran (SURVEY 8b);
+    reference_report keeps the reference simulator's ledger of the plan."""
+    B, T, P, D = 4, 256, 512, 768
+    x, dy = _inputs(B, T, P, D, 1)
+    cfg = fdp.DPConfig(1.0, 1.0, "mean")
+    inputs = B * T * (P + D) * 2
+    fused = fdp.backward_flashdp(x, dy, cfg, path="fused")
+    assert fused.report.kernel_launches == 1 and fused.report.redundant_flops == 0
+    assert inputs <= fused.report.bytes_loaded < inputs + 8 * D * P  # inputs read once
+    assert fused.report.per_sample_grad_bytes_stored == 0 and fused.report.barriers == B
+    ghost = fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase="ghost")
+    assert ghost.report.bytes_loaded >= 2 * inputs and ghost.report.redundant_flops == B * T * T * (P + D)
+    assert ghost.report.kernel_launches == 3
+    x1, dy1 = _inputs(1, T, P, D, 2)
+    single = fdp.backward_flashdp(x1, dy1, cfg, path="two_phase", norm_phase="single")
+    assert single.report.kernel_launches == 2 and single.report.bytes_stored >= 2 * 4 * D * P
+    expl = fdp.backward_explicit(x, dy, cfg)
+    assert expl.report.per_sample_grad_bytes_stored == 2 * B * D * P * 4
+    for r in (fused, ghost, single, expl):
+        assert r.reference_report is not None and r.reference_report.kernel_launches >= 1

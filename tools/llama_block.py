@@ -1,13 +1,23 @@
 """Llama-7B / Llama-13B transformer-block DP weight gradients on one B200 (BASELINE
 configs 3/4, per GPU): the 7 linear layers of a block (q, k, v, o, gate, up,
-down) through the auto-selected path vs cuBLAS non-DP dW, B in {1, 2, 4}, T=2048.
+down) vs cuBLAS non-DP dW with fp32 output (the like-for-like baseline: the DP
+kernels write fp32 gradients too), B in {1, 2, 4}, T=2048.
 
-Also the implied training-step ratio if dW is one third of the step's flops
-(forward 2, dX 2, dW 2 flops per parameter per token): (1 + 1 + 1) / (1 + 1 + r)
-with r = DP dW time / non-DP dW time.
+Each block is timed as the SEQUENCE the backward runs (down, up, gate, o, v, k,
+q), back to back on one stream:
+  dp_chained  per-layer DP kernels through a DeferredChain: a single-sample
+              layer's clip + noise pass is carried by the next layer's GEMM kernel
+              (B = 1), the last one flushed at the end of the block
+  dp          the same calls unchained (every layer's pass standalone)
+  nondp       cuBLAS torch.mm(dY^T, X, out_dtype=fp32) per layer
+and each layer alone (dp_us / nondp_us per layer).
 
-    python tools/llama_block.py > profiles/r1_llama_blocks.jsonl
+Implied training-step ratio if dW is one third of the step's flops (forward 2,
+dX 2, dW 2 flops per parameter per token): 3 / (2 + r), r = DP dW / non-DP dW.
+
+    python tools/llama_block.py [--models llama-7b,llama-13b] [--batches 1,2,4] > profiles/rNN_llama_blocks.jsonl
 """
+import argparse
 import json
 import os
 import sys
@@ -33,40 +43,74 @@ def timed(fn, n=5):
 
 
 def main():
-    T = 2048
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--models", default="llama-7b,llama-13b")
+    ap.add_argument("--batches", default="1,2,4")
+    ap.add_argument("--T", type=int, default=2048)
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    T = a.T
     g = torch.Generator(device="cuda").manual_seed(0)
-    variants = {"separate": lambda d, ff: [("q", d, d), ("k", d, d), ("v", d, d), ("o", d, d), ("gate", d, ff),
-                                           ("up", d, ff), ("down", ff, d)],
-                # fused projections (one clip group each, like GPT-2's c_attn): qkv and gate_up
-                "fused_qkv_gateup": lambda d, ff: [("qkv", d, 3 * d), ("o", d, d), ("gate_up", d, 2 * ff),
-                                                   ("down", ff, d)]}
-    for (name, (d, ff)), (vname, vshapes) in [(m, v) for m in MODELS.items() for v in variants.items()]:
-        shapes = vshapes(d, ff)
-        for B in (1, 2, 4):
-            row = {"model": name, "projections": vname, "B": B, "T": T, "layers": {}}
-            dp_total = nd_total = 0.0
+    for name in a.models.split(","):
+        d, ff = MODELS[name]
+        # backward order of a block
+        shapes = [("down", ff, d), ("up", d, ff), ("gate", d, ff), ("o", d, d), ("v", d, d), ("k", d, d),
+                  ("q", d, d)]
+        for B in (int(b) for b in a.batches.split(",")):
+            row = {"model": name, "B": B, "T": T, "layers": {}}
+            ins, chained, plain, nd = [], [], [], []
+            chain = fdp.DeferredChain()
+            ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
             flops = 0.0
-            for lname, P, D in shapes:
+            for j, (lname, P, D) in enumerate(shapes):
                 x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
                 dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
-                cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=0)
-                c = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox")
-                dp_us = timed(c)
+                cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=j)
+                gw = torch.zeros(D, P, device="cuda")
+                nrm = torch.zeros(B, device="cuda")
+                plain.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
+                                                  grad_w=gw, norms_sq=nrm, workspace=ws))
+                chained.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
+                                                    grad_w=gw, norms_sq=nrm, workspace=ws, chain=chain))
                 x2, y2 = x.view(-1, P), dy.view(-1, D)
-                nd_us = timed(lambda: torch.mm(y2.t(), x2, out_dtype=torch.float32))
-                plan = fdp._lib.PATH_NAMES[c.plan.path] + (
-                    "/" + fdp._lib.NORM_PHASE_NAMES.get(c.plan.norm_phase, "") if c.plan.path == 2 else "")
-                row["layers"][lname] = {"dp_us": round(dp_us, 1), "nondp_us": round(nd_us, 1), "path": plan}
-                dp_total += dp_us
-                nd_total += nd_us
+                nd.append((x2, y2))
+                ins.append((x, dy))
                 flops += 2.0 * B * T * P * D
-                del x, dy, c
-                torch.cuda.empty_cache()
-            r = dp_total / nd_total
-            row.update({"dp_us": round(dp_total, 1), "nondp_us": round(nd_total, 1),
-                        "dp_tflops": round(flops / dp_total / 1e6, 1), "dw_ratio": round(r, 3),
-                        "implied_step_pct_of_nondp": round(100.0 * 3.0 / (2.0 + r), 1)})
+                c = plain[-1]
+                path = fdp._lib.PATH_NAMES[c.plan.path] + (
+                    "/" + fdp._lib.NORM_PHASE_NAMES.get(c.plan.norm_phase, "") if c.plan.path == 2 else "")
+                row["layers"][lname] = {"dp_us": round(timed(c, a.reps), 1),
+                                        "nondp_us": round(timed(lambda: torch.mm(y2.t(), x2, out_dtype=torch.float32),
+                                                                a.reps), 1),
+                                        "path": path}
+
+            def dp_chained():
+                for c in chained:
+                    c()
+                chain.flush()
+
+            def dp_plain():
+                for c in plain:
+                    c()
+
+            def nondp():
+                for x2, y2 in nd:
+                    torch.mm(y2.t(), x2, out_dtype=torch.float32)
+
+            res = {}
+            for _ in range(2):  # alternate, keep the best
+                for k, fn in (("dp_chained", dp_chained), ("dp", dp_plain), ("nondp", nondp)):
+                    t = timed(fn, a.reps)
+                    res[k] = min(res.get(k, 1e30), t)
+            st = chain.stats()
+            r = res["dp_chained"] / res["nondp"]
+            row.update({"dp_chained_us": round(res["dp_chained"], 1), "dp_us": round(res["dp"], 1),
+                        "nondp_us": round(res["nondp"], 1), "dp_tflops": round(flops / res["dp_chained"] / 1e6, 1),
+                        "dw_ratio": round(r, 3), "dw_ratio_unchained": round(res["dp"] / res["nondp"], 3),
+                        "implied_step_pct_of_nondp": round(100.0 * 3.0 / (2.0 + r), 1), "chain": st})
             print(json.dumps(row), flush=True)
+            del ins, chained, plain, nd, chain, ws
+            torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
