@@ -114,6 +114,7 @@ struct StreamParams {
   unsigned long long budget_ns;
   int mc;                   // 2: 4-CTA clusters (two pairs, X boxes multicast; bn 256, cg 2), else 1
   FinJob fin;               // carried deferred finalize of the previous single-sample layer (fin.g == nullptr: none)
+  int fin_epi;              // epilogue warps also stream the carried finalize while idle (FDP_FIN_EPI)
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {

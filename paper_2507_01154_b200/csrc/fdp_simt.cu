@@ -264,24 +264,26 @@ __global__ void __launch_bounds__(256, kMode == 0 ? 1 : kMinB)
     for (int u = 0; u < kU; ++u) {
       const long long i = i0 + u * stride;
       if (i >= n4) continue;
-      v[u].x *= f;
-      v[u].y *= f;
-      v[u].z *= f;
-      v[u].w *= f;
+      // explicit roundings (c * G, then one fma with the noise): the same bits as the
+      // finalize a stream-K GEMM carries for a deferred chain (fdp_stream.cu fin_chunk)
+      v[u].x = __fmul_rn(v[u].x, f);
+      v[u].y = __fmul_rn(v[u].y, f);
+      v[u].z = __fmul_rn(v[u].z, f);
+      v[u].w = __fmul_rn(v[u].w, f);
       if constexpr (kMode == 1) {
-        v[u].x += scale * z[u].x;
-        v[u].y += scale * z[u].y;
-        v[u].z += scale * z[u].z;
-        v[u].w += scale * z[u].w;
+        v[u].x = __fmaf_rn(scale, z[u].x, v[u].x);
+        v[u].y = __fmaf_rn(scale, z[u].y, v[u].y);
+        v[u].z = __fmaf_rn(scale, z[u].z, v[u].z);
+        v[u].w = __fmaf_rn(scale, z[u].w, v[u].w);
       } else if constexpr (kMode == 0) {
         const long long e = i << 2;
         if (add_noise && e + 3 >= lo && e < hi) {
           const float4 z = impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
                                      : noise_draw4(impl, base_g, base, static_cast<uint64_t>(i));
-          if (e + 0 >= lo && e + 0 < hi) v[u].x += scale * z.x;
-          if (e + 1 >= lo && e + 1 < hi) v[u].y += scale * z.y;
-          if (e + 2 >= lo && e + 2 < hi) v[u].z += scale * z.z;
-          if (e + 3 >= lo && e + 3 < hi) v[u].w += scale * z.w;
+          if (e + 0 >= lo && e + 0 < hi) v[u].x = __fmaf_rn(scale, z.x, v[u].x);
+          if (e + 1 >= lo && e + 1 < hi) v[u].y = __fmaf_rn(scale, z.y, v[u].y);
+          if (e + 2 >= lo && e + 2 < hi) v[u].z = __fmaf_rn(scale, z.z, v[u].z);
+          if (e + 3 >= lo && e + 3 < hi) v[u].w = __fmaf_rn(scale, z.w, v[u].w);
         }
       }
       __stcs(g4 + i, v[u]);

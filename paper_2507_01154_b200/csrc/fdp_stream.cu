@@ -78,85 +78,99 @@ struct SegWalk {
 // index space, handed out in warp-sized chunks of 32 x kFinU float4 through a
 // shared-memory counter to whichever worker warp is idle (the noise warps all
 // the time, the epilogue warps while they wait for a TMEM buffer). Streaming
-// loads / stores (evict-first) keep the GEMM operands in L2.
+// loads / stores (evict-first) keep the GEMM operands in L2. No per-warp state
+// lives across the epilogue's tile work (the job is read from the kernel
+// parameters, the clip factor and the noise key from shared memory), so the
+// accumulator registers are untouched.
 constexpr int kFinU = 4;
-struct FinWorker {
-  const FinJob* j;
-  unsigned* ctr;
-  long long lo, hi;  // float4 range of this CTA
-  float f;           // clip factor (per warp, lazily)
-  bool have_f;
+constexpr int kFinPf = 24;  // chunks prefetched ahead into L2 (48 KB per CTA in flight)
+struct FinShared {
+  unsigned ctr;       // next chunk
+  unsigned ready;     // factor + key published
+  float f;            // clip factor x mean scale
+  unsigned pad;
   uint64_t base, base_g;
-  int mode;          // 1: Philox over the whole range, 2: no noise, 0: generic
+};
 
-  __device__ __forceinline__ void init(const FinJob* job, unsigned* counter) {
-    j = job;
-    ctr = counter;
-    const long long n4 = j->n >> 2;
-    lo = n4 * blockIdx.x / gridDim.x;
-    hi = n4 * (blockIdx.x + 1) / gridDim.x;
-    have_f = false;
-    base = j->base;
-    base_g = j->base_g;
-    if (j->add_noise && j->step_ptr) {
-      base = absorb3(j->seed_u, j->layer_u, static_cast<uint64_t>(*j->step_ptr));
+// fixed-order fp64 sum of the partials (the same factor in every CTA); the key of a
+// device step counter is absorbed once. Every warp may call it: identical results.
+__device__ __forceinline__ void fin_setup(const FinJob& j, FinShared* fs, int lane) {
+  double t = 0.0;
+  for (int i = lane; i < j.n_parts; i += 32) t += static_cast<double>(j.part[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) {
+    const double cf = (t <= j.clip_c2) ? 1.0 : j.clip_c / sqrt(t);  // dpcore.py:41-47
+    uint64_t base = j.base, base_g = j.base_g;
+    if (j.add_noise && j.step_ptr) {
+      base = absorb3(j.seed_u, j.layer_u, static_cast<uint64_t>(*j.step_ptr));
       base_g = base + kGamma;
     }
-    mode = (!j->add_noise || j->hi <= j->lo) ? 2 : (j->impl == 2 && j->lo <= 0 && j->hi >= j->n) ? 1 : 0;
+    fs->f = static_cast<float>(cf) * j.inv_batch;
+    fs->base = base;
+    fs->base_g = base_g;
+    __threadfence_block();
+    atomicExch(&fs->ready, 1u);
+    if (blockIdx.x == 0 && threadIdx.x == 64 && j.norms_out) j.norms_out[0] = static_cast<float>(t);
   }
-  // fixed-order fp64 sum of the partials: the same factor in every warp of every CTA
-  __device__ __forceinline__ void factor(int lane) {
-    double t = 0.0;
-    for (int i = lane; i < j->n_parts; i += 32) t += static_cast<double>(j->part[i]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    const double cf = (t <= j->clip_c2) ? 1.0 : j->clip_c / sqrt(t);  // dpcore.py:41-47
-    f = static_cast<float>(cf) * j->inv_batch;
-    have_f = true;
-    if (lane == 0 && blockIdx.x == 0 && j->norms_out && threadIdx.x == 64) j->norms_out[0] = static_cast<float>(t);
-  }
-  // one chunk for the calling warp; false when this CTA's slice is exhausted
-  __device__ __forceinline__ bool chunk(int lane) {
-    unsigned k = 0;
-    if (lane == 0) k = atomicAdd(ctr, 1u);
-    k = __shfl_sync(0xffffffffu, k, 0);
-    const long long s0 = lo + static_cast<long long>(k) * (32 * kFinU);
-    if (s0 >= hi) return false;
-    if (!have_f) factor(lane);
-    float4* g4 = reinterpret_cast<float4*>(j->g);
-    float4 v[kFinU];
-#pragma unroll
-    for (int u = 0; u < kFinU; ++u) {
-      const long long i = s0 + u * 32 + lane;
-      if (i < hi) v[u] = __ldcs(g4 + i);
+  __syncwarp();
+}
+
+// one chunk for the calling warp; false when this CTA's slice is exhausted
+__device__ __forceinline__ bool fin_chunk(const FinJob& j, FinShared* fs, int lane) {
+  unsigned k = 0;
+  if (lane == 0) k = atomicAdd(&fs->ctr, 1u);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  const long long n4 = j.n >> 2;
+  const long long lo = n4 * blockIdx.x / gridDim.x, hi = n4 * (blockIdx.x + 1) / gridDim.x;
+  const long long s0 = lo + static_cast<long long>(k) * (32 * kFinU);
+  if (s0 >= hi) return false;
+  if (lane == 0) {  // keep DRAM busy ahead of the workers: the chunk kFinPf claims from now into L2
+    const long long pf = s0 + static_cast<long long>(kFinPf) * (32 * kFinU);
+    if (pf < hi) {
+      const long long e = pf + 32 * kFinU < hi ? pf + 32 * kFinU : hi;
+      prefetch_l2_bulk_evict_first(reinterpret_cast<const float4*>(j.g) + pf, static_cast<uint32_t>((e - pf) * 16));
     }
+  }
+  if (!*reinterpret_cast<volatile unsigned*>(&fs->ready)) fin_setup(j, fs, lane);
+  const float f = fs->f;
+  const uint64_t base = fs->base, base_g = fs->base_g;
+  const int mode = (!j.add_noise || j.hi <= j.lo) ? 2 : (j.impl == 2 && j.lo <= 0 && j.hi >= j.n) ? 1 : 0;
+  float4* g4 = reinterpret_cast<float4*>(j.g);
+  float4 v[kFinU];
 #pragma unroll
-    for (int u = 0; u < kFinU; ++u) {
-      const long long i = s0 + u * 32 + lane;
-      if (i >= hi) continue;
-      float4 r = make_float4(v[u].x * f, v[u].y * f, v[u].z * f, v[u].w * f);
-      if (mode == 1) {
-        const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
-        r.x += j->scale * z.x;
-        r.y += j->scale * z.y;
-        r.z += j->scale * z.z;
-        r.w += j->scale * z.w;
-      } else if (mode == 0) {
-        const long long e = i << 2;
-        if (e + 3 >= j->lo && e < j->hi) {
-          const float4 z = j->impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
-                                        : noise_draw4(j->impl, base_g, base, static_cast<uint64_t>(i));
-          if (e + 0 >= j->lo && e + 0 < j->hi) r.x += j->scale * z.x;
-          if (e + 1 >= j->lo && e + 1 < j->hi) r.y += j->scale * z.y;
-          if (e + 2 >= j->lo && e + 2 < j->hi) r.z += j->scale * z.z;
-          if (e + 3 >= j->lo && e + 3 < j->hi) r.w += j->scale * z.w;
-        }
+  for (int u = 0; u < kFinU; ++u) {
+    const long long i = s0 + u * 32 + lane;
+    if (i < hi) v[u] = __ldcs(g4 + i);
+  }
+#pragma unroll
+  for (int u = 0; u < kFinU; ++u) {
+    const long long i = s0 + u * 32 + lane;
+    if (i >= hi) continue;
+    // explicit roundings (c * G, then one fma with the noise): bitwise the standalone pass
+    float4 r = make_float4(__fmul_rn(v[u].x, f), __fmul_rn(v[u].y, f), __fmul_rn(v[u].z, f),
+                           __fmul_rn(v[u].w, f));
+    if (mode == 1) {
+      const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
+      r.x = __fmaf_rn(j.scale, z.x, r.x);
+      r.y = __fmaf_rn(j.scale, z.y, r.y);
+      r.z = __fmaf_rn(j.scale, z.z, r.z);
+      r.w = __fmaf_rn(j.scale, z.w, r.w);
+    } else if (mode == 0) {
+      const long long e = i << 2;
+      if (e + 3 >= j.lo && e < j.hi) {
+        const float4 z = j.impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
+                                     : noise_draw4(j.impl, base_g, base, static_cast<uint64_t>(i));
+        if (e + 0 >= j.lo && e + 0 < j.hi) r.x = __fmaf_rn(j.scale, z.x, r.x);
+        if (e + 1 >= j.lo && e + 1 < j.hi) r.y = __fmaf_rn(j.scale, z.y, r.y);
+        if (e + 2 >= j.lo && e + 2 < j.hi) r.z = __fmaf_rn(j.scale, z.z, r.z);
+        if (e + 3 >= j.lo && e + 3 < j.hi) r.w = __fmaf_rn(j.scale, z.w, r.w);
       }
-      __stcs(g4 + i, r);
     }
-    return true;
+    __stcs(g4 + i, r);
   }
-};
+  return true;
+}
 
 // MC = 2: a 4-CTA cluster holds two CTA pairs working on vertically adjacent pair
 // tiles (same X columns, consecutive dY row blocks) in lockstep; each X box is
@@ -179,7 +193,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tempty = tfull + C::kNBuf;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps] tile sum-of-squares partials
-  unsigned* fin_ctr = reinterpret_cast<unsigned*>(red + kEpiWarps);  // carried finalize: next chunk
+  FinShared* fin_sh = reinterpret_cast<FinShared*>(
+      (reinterpret_cast<uintptr_t>(red + kEpiWarps) + 15) & ~uintptr_t(15));  // carried finalize state
   const bool fin_on = p.fin.g != nullptr;
 
   const int warp = threadIdx.x >> 5;
@@ -204,7 +219,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
-    *fin_ctr = 0u;
+    fin_sh->ctr = 0u;
+    fin_sh->ready = 0u;
     fence_mbar_init();
     fence_proxy_async_smem();
     prefetch_tmap(&tm_dy);
@@ -331,10 +347,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (ntid == 0) red_release_add_u32(&p.tile_cnt[wt * CL + crank], 1u);
     }
     if (fin_on) {  // the carried finalize of the previous layer, for as long as work is left
-      FinWorker fw;
-      fw.init(&p.fin, fin_ctr);
-      if (blockIdx.x == 0 && warp == 2) fw.factor(lane);  // also writes the layer's ||G||^2
-      while (fw.chunk(lane)) {
+      if (warp == 2) {
+        if (lane == 0) {  // the first kFinPf chunks of this CTA's slice into L2
+          const long long n4 = p.fin.n >> 2;
+          const long long lo = n4 * blockIdx.x / gridDim.x, hi = n4 * (blockIdx.x + 1) / gridDim.x;
+          const long long e = lo + static_cast<long long>(kFinPf) * 32 * kFinU < hi
+                                  ? lo + static_cast<long long>(kFinPf) * 32 * kFinU : hi;
+          for (long long a = lo; a < e; a += 32 * kFinU) {
+            const long long b = a + 32 * kFinU < e ? a + 32 * kFinU : e;
+            prefetch_l2_bulk_evict_first(reinterpret_cast<const float4*>(p.fin.g) + a, static_cast<uint32_t>((b - a) * 16));
+          }
+        }
+        fin_setup(p.fin, fin_sh, lane);  // CTA 0's also writes the layer's ||G||^2
+      }
+      while (fin_chunk(p.fin, fin_sh, lane)) {
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -345,16 +371,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t nkb = p.key_base;
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     uint32_t rbuf = 0, rph = 0;
-    FinWorker fw;
-    if (fin_on) fw.init(&p.fin, fin_ctr);
-    bool fin_left = fin_on;
+    bool fin_left = fin_on && p.fin_epi;
     SegWalk w(cid, n_clusters, p.B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
       if (fin_left) {  // idle until this segment's first accumulator is complete: stream the carried finalize
         const uint32_t a = smem_u32(&tfull[rbuf]);
-        while (!mbar_try_wait(a, rph)) {
-          if (!fw.chunk(lane)) {
+        while (!__any_sync(0xffffffffu, mbar_try_wait(a, rph))) {  // warp-uniform exit
+          if (!fin_chunk(p.fin, fin_sh, lane)) {
             fin_left = false;
             break;
           }
@@ -455,7 +479,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
-    while (fin_left && fw.chunk(lane)) {
+    while (fin_left && fin_chunk(p.fin, fin_sh, lane)) {
     }
     if (etid == 0) bulk_wait_all();
   }

@@ -269,7 +269,7 @@ def group_max_ctas(device: torch.device, comm_sms: int, world: int) -> int:
 
 class _Bucket:
     __slots__ = ("params", "offsets", "n", "per", "flat", "pflat", "shard", "pending", "launched", "deferred",
-                 "m", "v")
+                 "m", "v", "marked")
 
 
 class GradBuckets:
@@ -322,6 +322,7 @@ class GradBuckets:
                 cur, size = [], 0
         if cur:
             self._close(cur, flat_params)
+        self._external: set = set()  # ids of parameters whose readiness is signalled explicitly
         self._where = {}
         for i, b in enumerate(self.buckets):
             for p in b.params:
@@ -334,7 +335,7 @@ class GradBuckets:
 
             for p in ps:
                 p.register_post_accumulate_grad_hook(self._hook)
-                register_inplace_grad_hook(p, self.mark_ready)  # gradients GEMMs write in place
+                register_inplace_grad_hook(p, self._inplace)  # gradients GEMMs write in place
         self.issued: list[int] = []  # bucket issue order of the last backward (tests / traces)
         self.enabled = True  # False while accumulating micro-batches (no collectives)
         self.trace = [] if os.environ.get("FDP_DDP_TRACE") == "1" else None  # (bucket, param, pending) per ready
@@ -363,6 +364,7 @@ class GradBuckets:
         b.deferred = 0
         b.pending = len(b.params)
         b.launched = False
+        b.marked = set()
         b.m = b.v = None
         self.buckets.append(b)
 
@@ -376,6 +378,7 @@ class GradBuckets:
             i = self._where.get(id(w))
             if i is not None:
                 self.buckets[i].deferred += 1
+                self._external.add(id(w))
 
     # ---- per step
     def zero_grad(self) -> None:
@@ -385,6 +388,7 @@ class GradBuckets:
             b.flat.zero_()
             b.pending = len(b.params)
             b.launched = False
+            b.marked = set()
             for p, o in zip(b.params, b.offsets):
                 if p.grad is None or p.grad.data_ptr() != b.flat[o:].data_ptr():
                     p.grad = b.flat[o:o + p.numel()].view_as(p)
@@ -394,6 +398,14 @@ class GradBuckets:
         return self._where[id(p)]
 
     def _hook(self, p):
+        # autograd runs post-accumulate hooks even when a Function returned no
+        # gradient for the parameter (a gradient written in place or deferred):
+        # those parameters are signalled explicitly, never by this hook
+        if id(p) not in self._external:
+            self.mark_ready(p)
+
+    def _inplace(self, p):
+        self._external.add(id(p))
         self.mark_ready(p)
 
     def mark_ready(self, p) -> None:
@@ -403,8 +415,11 @@ class GradBuckets:
         if i is None:
             return
         b = self.buckets[i]
+        if id(p) in b.marked:  # one readiness signal per parameter and step
+            return
+        b.marked.add(id(p))
         if self.trace is not None:
-            self.trace.append((i, b.params.index(p), b.pending))
+            self.trace.append((i, next(k for k, q in enumerate(b.params) if q is p), b.pending))
         b.pending -= 1
         if b.pending == 0:
             self._launch(i)

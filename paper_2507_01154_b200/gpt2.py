@@ -39,11 +39,24 @@ class GPT2Config:
     mlp: int = 3072
 
 
-def _linear(cin: int, cout: int, dp: bool, layer_id: int, clip_c: float, sigma: float, noise_impl: str):
+def _linear(cin: int, cout: int, dp: bool, layer_id: int, clip_c: float, sigma: float, noise_impl: str,
+            nondp_cls=torch.nn.Linear):
     if dp:
         return DPLinear(cin, cout, bias=True, clip_c=clip_c, sigma=sigma, reduction="mean", layer_id=layer_id,
                         noise_impl=noise_impl)
-    return torch.nn.Linear(cin, cout, bias=True)
+    return nondp_cls(cin, cout, bias=True)
+
+
+def _nondp_cls(name: str):
+    """non-DP projections: "torch" (nn.Linear: autocast bf16 dW cast into the fp32
+    .grad) or "fp32grad" (baselines.FP32GradLinear: cuBLAS writes the fp32 weight
+    gradient, the DP kernels' output precision -- the like-for-like baseline)."""
+    if name == "torch":
+        return torch.nn.Linear
+    if name == "fp32grad":
+        from .baselines import FP32GradLinear
+        return FP32GradLinear
+    raise ValueError(f"nondp_linear must be torch or fp32grad, got {name!r}")
 
 
 def _layernorm(d: int, dp_full: bool, layer_id: int, clip_c: float, sigma: float, noise_impl: str):
@@ -53,17 +66,18 @@ def _layernorm(d: int, dp_full: bool, layer_id: int, clip_c: float, sigma: float
 
 
 class Block(torch.nn.Module):
-    def __init__(self, cfg: GPT2Config, idx: int, dp, clip_c: float, sigma: float, noise_impl: str):
+    def __init__(self, cfg: GPT2Config, idx: int, dp, clip_c: float, sigma: float, noise_impl: str,
+                 nondp_cls=torch.nn.Linear):
         super().__init__()
         full = dp == "full"
         self.ln1 = _layernorm(cfg.d, full, 1002 + 2 * idx, clip_c, sigma, noise_impl)
         self.ln2 = _layernorm(cfg.d, full, 1003 + 2 * idx, clip_c, sigma, noise_impl)
         dp = bool(dp)
         base = 4 * idx
-        self.c_attn = _linear(cfg.d, 3 * cfg.d, dp, base + 0, clip_c, sigma, noise_impl)
-        self.attn_proj = _linear(cfg.d, cfg.d, dp, base + 1, clip_c, sigma, noise_impl)
-        self.c_fc = _linear(cfg.d, cfg.mlp, dp, base + 2, clip_c, sigma, noise_impl)
-        self.mlp_proj = _linear(cfg.mlp, cfg.d, dp, base + 3, clip_c, sigma, noise_impl)
+        self.c_attn = _linear(cfg.d, 3 * cfg.d, dp, base + 0, clip_c, sigma, noise_impl, nondp_cls)
+        self.attn_proj = _linear(cfg.d, cfg.d, dp, base + 1, clip_c, sigma, noise_impl, nondp_cls)
+        self.c_fc = _linear(cfg.d, cfg.mlp, dp, base + 2, clip_c, sigma, noise_impl, nondp_cls)
+        self.mlp_proj = _linear(cfg.mlp, cfg.d, dp, base + 3, clip_c, sigma, noise_impl, nondp_cls)
         self.heads = cfg.heads
 
     def forward(self, x):
@@ -80,9 +94,10 @@ class Block(torch.nn.Module):
 
 class GPT2(torch.nn.Module):
     def __init__(self, cfg: GPT2Config, *, dp=True, clip_c: float = 1.0, sigma: float = 1.0,
-                 noise_impl: str = "philox", tied: bool = True):
+                 noise_impl: str = "philox", tied: bool = True, nondp_linear: str = "torch"):
         super().__init__()
         self.cfg = cfg
+        nondp_cls = _nondp_cls(nondp_linear)
         full = dp == "full"
         self.tied = tied and not full
         if full:
@@ -91,14 +106,15 @@ class GPT2(torch.nn.Module):
         else:
             self.wte = torch.nn.Embedding(cfg.vocab, cfg.d)
             self.wpe = torch.nn.Embedding(cfg.seq, cfg.d)
-        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl) for i in range(cfg.layers))
+        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl, nondp_cls)
+                                          for i in range(cfg.layers))
         self.ln_f = _layernorm(cfg.d, full, 1100, clip_c, sigma, noise_impl)
         self.vocab_padded = (cfg.vocab + 63) // 64 * 64
         self.lm_head = None
         if not self.tied:
             self.lm_head = (DPLinear(cfg.d, self.vocab_padded, bias=False, clip_c=clip_c, sigma=sigma,
                                      reduction="mean", layer_id=4 * cfg.layers, noise_impl=noise_impl)
-                            if full else torch.nn.Linear(cfg.d, self.vocab_padded, bias=False))
+                            if full else nondp_cls(cfg.d, self.vocab_padded, bias=False))
         self.dp = dp
         for p in self.parameters():
             if p.dim() >= 2:

@@ -111,18 +111,23 @@ class Llama(torch.nn.Module):
             linear_cls = torch.nn.Linear
         else:
             raise ValueError(f"nondp_linear must be torch or fp32grad, got {nondp_linear!r}")
+        # registration order = forward order (embedding, blocks, final norm, LM head), so
+        # reversed(parameters()) is the order the backward produces the gradients
+        # (ddp.GradBuckets fills and reduces its buckets in that order)
         if dp:
             self.embed = DPEmbedding(cfg.vocab, cfg.d, clip_c=clip_c, sigma=sigma, layer_id=200000,
                                      noise_impl=noise_impl)
+        else:
+            self.embed = torch.nn.Embedding(cfg.vocab, cfg.d)
+        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl, linear_cls)
+                                          for i in range(cfg.layers))
+        if dp:
             self.norm = DPRMSNorm(cfg.d, cfg.eps, clip_c=clip_c, sigma=sigma, layer_id=200001, noise_impl=noise_impl)
             self.lm_head = DPLinear(cfg.d, cfg.vocab, bias=False, clip_c=clip_c, sigma=sigma, reduction="mean",
                                     layer_id=200002, noise_impl=noise_impl)
         else:
-            self.embed = torch.nn.Embedding(cfg.vocab, cfg.d)
             self.norm = _RMSNorm(cfg.d, cfg.eps)
             self.lm_head = linear_cls(cfg.d, cfg.vocab, bias=False)
-        self.blocks = torch.nn.ModuleList(Block(cfg, i, dp, clip_c, sigma, noise_impl, linear_cls)
-                                          for i in range(cfg.layers))
         for p in self.parameters():
             if p.dim() >= 2:
                 torch.nn.init.normal_(p, std=0.02)

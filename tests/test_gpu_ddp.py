@@ -258,11 +258,18 @@ def _llama_step_worker(rank, world, port, mode, dp, out):
     step = DataParallelStep(model, dp=dp, mode=mode, lr=1e-3, rank=rank, world=world, global_batch=B,
                             bucket_bytes=1 << 20)
     scale = 1.0 if dp else 1.0 / B
+    grads = None
     for i in range(2):
         step(i, lambda: model.loss(x, y, reduction="sample_sum") * scale)
+        if i == 0:  # the reduced gradients of step 0 (this rank's shard under reduce-scatter)
+            torch.cuda.synchronize()
+            bk = step.buckets
+            grads = [(b.flat if mode == "allreduce" else b.shard).detach().cpu().clone() for b in bk.buckets]
+            pers = [b.per for b in bk.buckets]
     torch.cuda.synchronize()
     out[(mode, dp, world, rank)] = ([p.detach().cpu().clone() for p in model.parameters()],
-                                    list(step.buckets.issued), len(step.buckets.buckets), step.last_flushes)
+                                    list(step.buckets.issued), len(step.buckets.buckets), step.last_flushes,
+                                    grads, pers)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -285,12 +292,19 @@ def test_bucketed_llama_step_two_ranks_equals_single_process(mode, dp):
                            start_method="spawn")
         mp.start_processes(_llama_step_worker, args=(2, _free_port(), mode, dp, out), nprocs=2, join=True,
                            start_method="spawn")
-        ref, _, nb, flushes = out[(mode, dp, 1, 0)]
+        ref, _, nb, flushes, ref_g, _ = out[(mode, dp, 1, 0)]
         assert nb >= 3
         if dp:
             assert flushes >= 2  # DP kernels ran bucket by bucket inside the backward
         for r in range(2):
-            got, issued, _, _ = out[(mode, dp, 2, r)]
+            got, issued, _, _, g2, pers = out[(mode, dp, 2, r)]
             assert issued == out[(mode, dp, 2, 0)][1]
-            for a, b in zip(got, ref):
-                assert torch.allclose(a, b, rtol=1e-4, atol=2e-6), (mode, dp, float((a - b).abs().max()))
+            # step-0 gradients: summed over the ranks == the single-process gradients
+            for k, (a, full) in enumerate(zip(g2, ref_g)):
+                b = full if mode == "allreduce" else torch.cat([full, torch.zeros(2 * pers[k])])[
+                    r * pers[k]:(r + 1) * pers[k]]
+                n = min(a.numel(), b.numel())
+                assert torch.allclose(a[:n], b[:n], rtol=1e-4, atol=1e-6 * float(b.abs().max())), (mode, dp, k)
+            if dp:  # parameters after two DP-Adam steps (noise keeps every gradient away from 0)
+                for a, b in zip(got, ref):
+                    assert torch.allclose(a, b, rtol=1e-4, atol=2e-6), (mode, dp, float((a - b).abs().max()))

@@ -22,7 +22,8 @@ from paper_2507_01154_b200.gpt2 import GPT2, GPT2Config  # noqa: E402
 def run(dp, a) -> dict:
     torch.manual_seed(0)
     cfg = GPT2Config(seq=a.seq)
-    model = GPT2(cfg, dp=dp, clip_c=1.0, sigma=1.0, tied=not a.full).cuda()
+    model = GPT2(cfg, dp=dp, clip_c=1.0, sigma=1.0, tied=not a.full,
+                 nondp_linear=getattr(a, "nondp_linear", "fp32grad")).cuda()
     opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
     g = torch.Generator(device="cuda").manual_seed(1)
     idx = torch.randint(0, cfg.vocab, (a.batch, a.seq + 1), device="cuda", generator=g)
@@ -63,12 +64,16 @@ def main():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--nondp-linear", default="fp32grad", choices=["fp32grad", "torch"],
+                    help="non-DP projections: fp32grad = cuBLAS writes fp32 weight gradients (like-for-like with the "
+                         "DP kernels); torch = nn.Linear under autocast (bf16 dW cast into fp32 .grad)")
     ap.add_argument("--full", action="store_true", help="every parameter DP (embeddings, LayerNorms, untied LM "
                     "head); the non-DP baseline is then untied too")
     a = ap.parse_args()
     nd = run(False, a)
     dp = run("full" if a.full else True, a)
     print(json.dumps({"model": "gpt2-small (124M), random init, synthetic tokens", "batch": a.batch, "seq": a.seq,
+                      "nondp_linear": a.nondp_linear,
                       "dp_scope": "every parameter (untied LM head)" if a.full else "the 48 linear layers",
                       "dp": dp, "non_dp": nd, "dp_pct_of_non_dp": 100.0 * dp["tokens_per_s"] / nd["tokens_per_s"],
                       "note": ("DP = per-layer clipped + noised gradients of every parameter: the 48 linear layers "
