@@ -11,6 +11,8 @@ from cuBLAS with fp32 output, accumulated in place into an fp32 ``.grad``
 
 from __future__ import annotations
 
+import weakref
+
 import torch
 
 
@@ -54,19 +56,28 @@ class _FP32GradLinearFn(torch.autograd.Function):
         return dx, gw, gb
 
 
+# id(weight) -> (weakref to the weight, weakref to the bound hook): weak on both ends, so
+# a registry entry never keeps a model or its gradient buckets alive
 _READY_HOOKS: dict = {}
 
 
 def _notify(weight: torch.Tensor) -> None:
     """A gradient written in place bypasses AccumulateGrad (no post-accumulate
     hook): tell the gradient bucket (ddp.GradBuckets) directly."""
-    fn = _READY_HOOKS.get(id(weight))
+    entry = _READY_HOOKS.get(id(weight))
+    if entry is None or entry[0]() is not weight:
+        return
+    fn = entry[1]()
     if fn is not None:
         fn(weight)
 
 
 def register_inplace_grad_hook(weight: torch.Tensor, fn) -> None:
-    _READY_HOOKS[id(weight)] = fn
+    if len(_READY_HOOKS) > 4096:  # drop entries whose weight or hook owner is gone
+        for k in [k for k, (w, f) in _READY_HOOKS.items() if w() is None or f() is None]:
+            del _READY_HOOKS[k]
+    ref = weakref.WeakMethod(fn) if hasattr(fn, "__self__") else (lambda f=fn: f)
+    _READY_HOOKS[id(weight)] = (weakref.ref(weight), ref)
 
 
 class FP32GradLinear(torch.nn.Linear):

@@ -1320,6 +1320,7 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   gp.pub_mode = env_int("FDP_PUB_MODE", 1);
   gp.poll_mode = env_int("FDP_POLL_MODE", 0);
   gp.pf_ahead = env_int("FDP_PF_AHEAD", 0);
+  gp.pair_dsmem = env_int("FDP_PAIR_DSMEM", 0);
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

@@ -60,11 +60,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kNBuf;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::kNBuf);
+  uint64_t* pair_bar = tempty + C::kNBuf;  // CG == 2: the follower's norm partial has landed (leader)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pair_bar + 1);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);
   float* bcast = red + kEpiWarps;
   volatile unsigned* pf_done = reinterpret_cast<volatile unsigned*>(bcast + 1);  // layers pre-filled so far
   volatile int* ep_layer = reinterpret_cast<volatile int*>(bcast + 2);          // layer the epilogue is on
+  float* pair_sx = bcast + 4;  // [2] (leader) the follower CTA's tile partial, by unit parity
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
+    mbar_init(pair_bar, 1);
     *pf_done = 0u;
     *ep_layer = 0;
     fence_mbar_init();
@@ -242,6 +245,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
     const int row = q * 32 + lane, col0 = half * C::kCPT;
     uint32_t rbuf = 0, rph = 0;
+    // FDP_PAIR_DSMEM=1 (gp.pair_dsmem): CTA pairs (CG == 2) combine their two tile
+    // partials on chip: the follower CTA writes its partial into the leader's shared
+    // memory (DSMEM) and release-arrives on the leader's barrier; the leader adds the
+    // two in a fixed order and publishes ONE tagged slot per pair tile, so the
+    // block-wise all-reduce polls n_wtiles slots per sample instead of n_tiles
+    // (north_star (2): warp shuffles -> named barrier -> cluster DSMEM -> grid-level
+    // all-reduce in L2). Off by default: the leader's publish now waits for the
+    // follower's, an extra on-chip hop on every sample's critical path -- measured
+    // 1432 vs 1275 us on the 48-layer GPT-2 step (profiles/r2_pair_dsmem_ab.jsonl);
+    // each CTA publishing its own 8-byte slot and every poller summing both is cheaper.
+    uint32_t pair_phase = 0;
+    const uint32_t pair_bar_leader = CG == 2 ? dsmem_map(pair_bar, 0) : 0u;
+    const uint32_t pair_sx_leader = CG == 2 ? dsmem_map(pair_sx, 0) : 0u;
     // pass 1 of sample b's unit in TMEM buffer `buf`: intra-block reduce of
     // ||G_b||^2 over this CTA tile, published as one tagged 8-byte atomic
     auto pass1_publish = [&](const GLayer& Lx, int bx, int tilex, uint32_t bufx) {
@@ -263,8 +279,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         float sx = 0.0f;
 #pragma unroll
         for (int w = 0; w < kEpiWarps; ++w) sx += red[w];
-        publish_u64(Lx.tagged + static_cast<long long>(bx) * Lx.n_tiles + tilex,
-                    (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(sx), gp.pub_mode);
+        if (CG == 2 && gp.pair_dsmem) {
+          const uint32_t par = pair_phase & 1u;
+          if (rank != 0) {
+            dsmem_st_f32(pair_sx_leader + 4u * par, sx);
+            mbar_arrive_remote_release(pair_bar_leader);
+          } else {
+            const uint32_t a = smem_u32(pair_bar);
+            const uint64_t t0 = globaltimer_ns();
+            while (!mbar_try_wait_cluster(a, par)) {
+              if (globaltimer_ns() - t0 > gp.budget_ns) watchdog_trap(err, 0x409);
+            }
+            const float sp = reinterpret_cast<volatile float*>(pair_sx)[par];
+            publish_u64(Lx.tagged + static_cast<long long>(bx) * Lx.n_tiles + tilex / 2,
+                        (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(sx + sp), gp.pub_mode);
+          }
+          ++pair_phase;
+        } else {
+          publish_u64(Lx.tagged + static_cast<long long>(bx) * Lx.n_tiles + tilex,
+                      (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(sx), gp.pub_mode);
+        }
       }
     };
     for (int l = 0; l < gp.n_layers; ++l) {
@@ -295,12 +329,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         // block-wise all-reduce: fixed-order fp64 sum of the tagged partials
         if (ew == 0) {
           const unsigned long long* slots = L.tagged + static_cast<long long>(b) * L.n_tiles;
+          const int n_slots = gp.pair_dsmem ? L.n_tiles / CG : L.n_tiles;  // per pair tile (DSMEM) or CTA tile
           constexpr int kMaxPer = 5;
           unsigned long long v[kMaxPer];
 #pragma unroll
           for (int k = 0; k < kMaxPer; ++k) {
             const int i = lane + 32 * k;
-            v[k] = i < L.n_tiles ? poll_u64(slots + i, gp.poll_mode) : (static_cast<unsigned long long>(tag) << 32);
+            v[k] = i < n_slots ? poll_u64(slots + i, gp.poll_mode) : (static_cast<unsigned long long>(tag) << 32);
           }
           const uint64_t t0 = globaltimer_ns();
           while (true) {  // re-poll every stale slot at once: one L2 round trip per iteration
@@ -317,7 +352,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
           double s = 0.0;
 #pragma unroll
           for (int k = 0; k < kMaxPer; ++k)
-            if (lane + 32 * k < L.n_tiles) s += static_cast<double>(__uint_as_float(static_cast<unsigned>(v[k])));
+            if (lane + 32 * k < n_slots) s += static_cast<double>(__uint_as_float(static_cast<unsigned>(v[k])));
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
           if (lane == 0) {

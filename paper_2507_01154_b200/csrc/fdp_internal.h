@@ -115,6 +115,10 @@ struct StreamParams {
   int mc;                   // 2: 4-CTA clusters (two pairs, X boxes multicast; bn 256, cg 2), else 1
   FinJob fin;               // carried deferred finalize of the previous single-sample layer (fin.g == nullptr: none)
   int fin_epi;              // epilogue warps also stream the carried finalize while idle (FDP_FIN_EPI)
+  // spill norm phase: every (tile, sample) unit is its own whole tile, stored unscaled to
+  // the per-sample buffer G[b] (tm_gw is then a 3-D (P, D, B) map) with its sum of
+  // squares in norm_part[(b * n_wtiles + wt) * CG * MC + crank]; p.B is the real batch
+  int spill;
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {
@@ -155,6 +159,7 @@ struct GroupParams {
   // noise / row pre-fill run-ahead bound: the noise warps start layer l once the
   // epilogue has started layer l - pf_ahead (FDP_PF_AHEAD; < 0 = unbounded)
   int pf_ahead;
+  int pair_dsmem;  // CTA-pair norm partials combined in DSMEM before publishing (FDP_PAIR_DSMEM; default off)
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
 
@@ -215,6 +220,11 @@ cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int P, c
 // B == 1 second pass: ||G||^2 from the per-tile partials (fixed order), then
 // grad_w = grad_w * min(1, C/||G||) * inv_batch (+ sigma*C*noise on [lo, hi)).
 cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s);
+// spill combine: out = (accumulate ? out : 0) + sum_b fac[b] * G[b] + scale * noise (rank slice)
+cudaError_t spill_combine(float* out, const float* G, int B, long long n, const float* fac, int accumulate,
+                          int add_noise, int impl, float scale, uint64_t base, uint64_t base_g,
+                          const long long* step_ptr, uint64_t seed_u, uint64_t layer_u, long long lo, long long hi,
+                          cudaStream_t s);
 cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part, int n_parts, double clip_c,
                                    double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl,
                                    float noise_scale, uint64_t base, uint64_t base_g, const long long* step_ptr,

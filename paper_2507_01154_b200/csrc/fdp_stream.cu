@@ -177,7 +177,7 @@ __device__ __forceinline__ bool fin_chunk(const FinJob& j, FinShared* fs, int la
 // loaded once and multicast to the CTA of both pairs that needs it, so L2 serves
 // 3/4 of the operand bytes of two independent pairs. A stage is refilled only
 // after BOTH pairs' MMAs released it (every commit arrives in all four CTAs).
-template <int BN, int CG, int MC>
+template <int BN, int CG, int MC, bool FIN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     dpdw_stream_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
                        const __grid_constant__ CUtensorMap tm_gw, const StreamParams p) {
@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps] tile sum-of-squares partials
   FinShared* fin_sh = reinterpret_cast<FinShared*>(
       (reinterpret_cast<uintptr_t>(red + kEpiWarps) + 15) & ~uintptr_t(15));  // carried finalize state
-  const bool fin_on = p.fin.g != nullptr;
+  // carried finalize: a separate instantiation, so the plain kernels keep their register allocation
+  const bool fin_on = FIN && p.fin.g != nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -207,7 +208,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int cid = blockIdx.x / CL, n_clusters = gridDim.x / CL;
   const bool per_unit = p.reweight != 0;  // one TMEM accumulation per sample (scaled by c_b) vs per segment
   // work tiles: MC pair tiles stacked along D (rows past D load zeros and are never stored)
-  const int n_wt = MC == 1 ? p.n_wtiles : ((p.n_wtiles / p.n_pt + MC - 1) / MC) * p.n_pt;
+  const int n_wt_real = MC == 1 ? p.n_wtiles : ((p.n_wtiles / p.n_pt + MC - 1) / MC) * p.n_pt;
+  // spill: virtual work tiles (sample-major) of one unit each: wt' = b * n_wt_real + wt
+  const bool spill = MC == 1 && p.spill != 0;
+  const int n_wt = spill ? n_wt_real * p.B : n_wt_real;
+  const int walk_B = spill ? 1 : p.B;
   const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << (CG * pi));
 
   if (warp == 0 && lane == 0) {
@@ -247,9 +252,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ======================= TMA producer =======================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      SegWalk w(cid, n_clusters, p.B, n_wt);
+      SegWalk w(cid, n_clusters, walk_B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
+        const int sb = spill ? wt / n_wt_real : 0;  // spill: the unit's sample
+        if (spill) {
+          wt -= sb * n_wt_real;
+          bb = sb;
+          be = sb + 1;
+        }
         const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
         const int p0 = (wt % p.n_pt) * BN + rank * C::kBCols;
         for (int b = bb; b < be; ++b) {
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ======================= MMA issuer (leader CTA) =======================
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
-      SegWalk w(cid, n_clusters, p.B, n_wt);
+      SegWalk w(cid, n_clusters, walk_B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
         for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
@@ -333,7 +344,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       kb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
       kbg = kb + kGamma;
     }
-    SegWalk w(cid, n_clusters, p.B, n_wt);
+    SegWalk w(cid, n_clusters, walk_B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
       const bool whole = bb == 0 && be == p.B;
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     uint32_t rbuf = 0, rph = 0;
     bool fin_left = fin_on && p.fin_epi;
-    SegWalk w(cid, n_clusters, p.B, n_wt);
+    SegWalk w(cid, n_clusters, walk_B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
       if (fin_left) {  // idle until this segment's first accumulator is complete: stream the carried finalize
@@ -384,8 +395,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
-      const bool whole = bb == 0 && be == p.B;
-      const int tile = wt * CL + crank;
+      const bool whole = bb == 0 && be == walk_B;
+      const int tile = wt * CL + crank;  // spill: (b * n_wtiles + wt) * CL + crank, the unit's partial slot
+      const int sb = spill ? wt / n_wt_real : 0;
+      if (spill) wt -= sb * n_wt_real;
       const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
       const int p0 = (wt % p.n_pt) * BN;
       float acc[C::kCPT];
@@ -472,7 +485,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int col = p0 + h * C::kCPT + c * 32;
-            if (rmw) tma_reduce_add_2d(&tm_gw, sbuf + h * (kBM * 128), col, d0);
+            if (spill) tma_store_3d(&tm_gw, sbuf + h * (kBM * 128), col, d0, sb);  // G[b], unscaled
+            else if (rmw) tma_reduce_add_2d(&tm_gw, sbuf + h * (kBM * 128), col, d0);
             else tma_store_2d(&tm_gw, sbuf + h * (kBM * 128), col, d0);
           }
           bulk_commit();
@@ -497,14 +511,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const unsigned old = atomicAdd(&p.ctrl[0], 1u);
     if (old == gridDim.x - 1) {
       __threadfence();
-      for (int t = 0; t < n_wt * CL; ++t) p.tile_cnt[t] = 0u;
+      if (!spill)  // spill units are whole tiles: their counters are never touched
+        for (int t = 0; t < n_wt * CL; ++t) p.tile_cnt[t] = 0u;
       p.ctrl[0] = 0u;
       __threadfence();
     }
   }
 }
 
-template <int BN, int CG, int MC>
+template <int BN, int CG, int MC, bool FIN>
 static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
                                       const StreamParams& p, int grid, cudaStream_t stream) {
   using C = SCfg<BN, CG>;
@@ -512,7 +527,7 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(dpdw_stream_kernel<BN, CG, MC>,
+    cudaError_t e = cudaFuncSetAttribute(dpdw_stream_kernel<BN, CG, MC, FIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) done[dev] = true;
@@ -535,20 +550,27 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   cfg.numAttrs = na;
   // Split tiles wait on the cluster that initialises them, which is resident:
   // the grid never exceeds the co-resident capacity (host planner).
-  return cudaLaunchKernelEx(&cfg, dpdw_stream_kernel<BN, CG, MC>, tm_dy, tm_x, tm_gw, p);
+  return cudaLaunchKernelEx(&cfg, dpdw_stream_kernel<BN, CG, MC, FIN>, tm_dy, tm_x, tm_gw, p);
+}
+
+template <bool FIN>
+static cudaError_t launch_stream_fin(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x,
+                                     const CUtensorMap& tm_gw, const StreamParams& p, int grid, cudaStream_t stream) {
+  if (cg == 2) {
+    if (bn == 256) {
+      if (p.mc == 2) return launch_stream_impl<256, 2, 2, FIN>(tm_dy, tm_x, tm_gw, p, grid, stream);
+      return launch_stream_impl<256, 2, 1, FIN>(tm_dy, tm_x, tm_gw, p, grid, stream);
+    }
+    return launch_stream_impl<128, 2, 1, FIN>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  }
+  if (bn == 256) return launch_stream_impl<256, 1, 1, FIN>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  return launch_stream_impl<128, 1, 1, FIN>(tm_dy, tm_x, tm_gw, p, grid, stream);
 }
 
 cudaError_t launch_stream(int bn, int cg, const CUtensorMap& tm_dy, const CUtensorMap& tm_x, const CUtensorMap& tm_gw,
                           const StreamParams& p, int grid, cudaStream_t stream) {
-  if (cg == 2) {
-    if (bn == 256) {
-      if (p.mc == 2) return launch_stream_impl<256, 2, 2>(tm_dy, tm_x, tm_gw, p, grid, stream);
-      return launch_stream_impl<256, 2, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
-    }
-    return launch_stream_impl<128, 2, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
-  }
-  if (bn == 256) return launch_stream_impl<256, 1, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
-  return launch_stream_impl<128, 1, 1>(tm_dy, tm_x, tm_gw, p, grid, stream);
+  if (p.fin.g) return launch_stream_fin<true>(bn, cg, tm_dy, tm_x, tm_gw, p, grid, stream);
+  return launch_stream_fin<false>(bn, cg, tm_dy, tm_x, tm_gw, p, grid, stream);
 }
 
 // Co-resident 4-CTA clusters of the multicast variant (0 if it cannot launch).
@@ -560,7 +582,7 @@ int stream_mc_max_clusters() {
   if (have[dev]) return cache[dev];
   using C = SCfg<256, 2>;
   int n = 0;
-  if (cudaFuncSetAttribute(dpdw_stream_kernel<256, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(dpdw_stream_kernel<256, 2, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(C::kSmem)) == cudaSuccess) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -575,7 +597,7 @@ int stream_mc_max_clusters() {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&n, dpdw_stream_kernel<256, 2, 2>, &cfg) != cudaSuccess) n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, dpdw_stream_kernel<256, 2, 2, false>, &cfg) != cudaSuccess) n = 0;
   }
   (void)cudaGetLastError();
   cache[dev] = n;

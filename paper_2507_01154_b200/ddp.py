@@ -331,10 +331,21 @@ class GradBuckets:
         self.comm = torch.cuda.Stream(self.device) if cuda and world > 1 else None
         self._handles = []
         if hooks:
+            import weakref
+
             from .baselines import register_inplace_grad_hook
 
+            # the hooks live on the parameters (C++ side, invisible to the cycle collector):
+            # they hold this object weakly, so dropping the buckets frees their buffers
+            wself = weakref.ref(self)
+
+            def _post_acc(p, wself=wself):
+                me = wself()
+                if me is not None:
+                    me._hook(p)
+
             for p in ps:
-                p.register_post_accumulate_grad_hook(self._hook)
+                p.register_post_accumulate_grad_hook(_post_acc)
                 register_inplace_grad_hook(p, self._inplace)  # gradients GEMMs write in place
         self.issued: list[int] = []  # bucket issue order of the last backward (tests / traces)
         self.enabled = True  # False while accumulating micro-batches (no collectives)

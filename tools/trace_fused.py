@@ -1,6 +1,6 @@
 """Phase trace of the fused kernel (FDP_FLAG_TRACE): where does each CTA spend time?
 
-    python tools/trace_fused.py [layer] [bn] [noise] [B] [T]
+    python tools/trace_fused.py [layer|PxD] [bn] [noise] [B] [T]
 """
 import ctypes
 import json
@@ -23,7 +23,7 @@ def main():
     B = int(sys.argv[4]) if len(sys.argv) > 4 else 8
     T = int(sys.argv[5]) if len(sys.argv) > 5 else 1024
     os.environ["FDP_FORCE_BN"] = bn
-    P, D = SHAPES[name]
+    P, D = SHAPES[name] if name in SHAPES else (int(v) for v in name.split("x"))  # "PxD" for any shape
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
     dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)

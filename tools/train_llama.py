@@ -34,6 +34,9 @@ import os
 import sys
 import time
 
+# full-depth models: parameters move into per-bucket flat buffers after construction;
+# expandable segments let the freed per-parameter blocks serve the bucket-sized optimizer state
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
@@ -80,12 +83,16 @@ def run(dp: bool, a, rank: int, world: int, dev: torch.device) -> dict:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    out = {"ms_per_step": ms, "tokens_per_s": gB * a.seq / (ms * 1e-3), "loss": float(loss.detach()) / (
-        a.batch if dp else a.batch / gB), "dp_modules": len(step.dp_mods),
-           "params": sum(p.numel() for p in model.parameters()), "buckets": len(step.buckets.buckets),
-           "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
-    del model, step
-    gc.collect()
+    out = {"ms_per_step": ms, "tokens_per_s": gB * a.seq / (ms * 1e-3),
+           "loss_per_sample": float(loss.detach()) / (a.batch if dp else a.batch / gB),
+           "dp_modules": len(step.dp_mods), "params": sum(p.numel() for p in model.parameters()),
+           "buckets": len(step.buckets.buckets), "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+    return out
+
+
+def run_arm(dp: bool, a, rank: int, world: int, dev: torch.device) -> dict:
+    out = run(dp, a, rank, world, dev)
+    gc.collect()  # the arm's model, buckets and optimizer state are unreachable now
     torch.cuda.empty_cache()
     return out
 
@@ -115,7 +122,7 @@ def main():
         init_distributed("nccl", comm_sms=a.comm_sms, device=dev)
     res = {}
     for arm in a.arms.split(","):
-        res[arm] = run(arm == "dp", a, rank, world, dev)
+        res[arm] = run_arm(arm == "dp", a, rank, world, dev)
     if rank == 0:
         line = {"model": a.model, "layers": a.layers or LlamaConfig.named(a.model).layers, "gpus": world,
                 "batch_per_gpu": a.batch, "global_batch": a.batch * world, "seq": a.seq,
