@@ -356,8 +356,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
           if (lane == 0) {
-            const double cf = (s <= L.clip_c2) ? 1.0 : L.clip_c / sqrt(s);  // dpcore.py:41-47
-            *bcast = static_cast<float>(cf) * L.inv_batch;
+            *bcast = clip_factor_f(s, L.clip_c, L.clip_c2) * L.inv_batch;  // dpcore.py:41-47
             if (tile == 0) L.norms_out[b] = static_cast<float>(s);
           }
         }

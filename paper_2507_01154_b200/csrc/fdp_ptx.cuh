@@ -261,6 +261,18 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask) : "memory");
 }
 
+// clip_factor (dpcore.py:41-47) on the epilogue's critical path: the passthrough test
+// (||g||^2 <= C^2, zero norm included) stays in fp64 -- under-bound gradients pass
+// through bit-exactly -- and C / sqrt(s) is one correctly rounded fp32 rsqrt and
+// multiply (~1 ulp of the float factor the kernels use anyway) instead of the fp64
+// sqrt + division sequence, which took 0.5-1.4 us per sample unit on the single
+// thread forming it (phase traces at T = 128 / 512). Sums beyond fp32 range keep fp64.
+__device__ __forceinline__ float clip_factor_f(double s, double clip_c, double clip_c2) {
+  if (s <= clip_c2) return 1.0f;
+  if (s < 1.0e37) return __fmul_rn(static_cast<float>(clip_c), __frsqrt_rn(static_cast<float>(s)));
+  return static_cast<float>(clip_c / sqrt(s));
+}
+
 // ---------------------------------------------------------------- distributed shared memory (cluster)
 // Address of `p`'s copy in CTA `rank` of the cluster (shared::cluster window).
 __device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {

@@ -413,8 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
           if (lane == 0) {
             // clip_factor (dpcore.py:41-47): zero norm and ||g|| <= C pass through unscaled
-            const double cf = (s <= p.clip_c2) ? 1.0 : p.clip_c / sqrt(s);
-            *bcast = static_cast<float>(cf) * p.inv_batch;
+            *bcast = clip_factor_f(s, p.clip_c, p.clip_c2) * p.inv_batch;
             if (tile == 0) p.norms_out[ub] = static_cast<float>(s);
           }
         }

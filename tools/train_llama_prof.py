@@ -12,10 +12,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
-from paper_2507_01154_b200.dplinear import GroupedDPBackward  # noqa: E402
+from paper_2507_01154_b200.ddp import DataParallelStep  # noqa: E402
 from paper_2507_01154_b200.llama import Llama, LlamaConfig  # noqa: E402
 
 GROUPS = [("fdp_dp_dW", ("dpdw_", "ghost_norm", "k_single_finalize", "k_reduce_norms")),
+          ("fdp_optimizer", ("k_adam", "k_sgd")),
           ("fdp_param_groups", ("k_vec_", "k_emb_")),
           ("gemm (cuBLAS)", ("nvjet", "gemm", "cutlass", "sm90_", "sm100_")),
           ("attention", ("flash", "fmha", "attention")),
@@ -39,25 +40,22 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--zero1", action="store_true")
     a = ap.parse_args()
     for dp in (False, True):
         torch.manual_seed(0)
         cfg = LlamaConfig.named(a.model, seq=a.seq, layers=a.layers)
         with torch.device("cuda"):
-            model = Llama(cfg, dp=dp)
-        opt = torch.optim.AdamW(model.parameters(), lr=1e-5, fused=True)
+            model = Llama(cfg, dp=dp, nondp_linear="fp32grad")
+        dstep = DataParallelStep(model, dp=dp, mode="reduce_scatter" if a.zero1 else "allreduce", lr=1e-5,
+                                 global_batch=a.batch)
         idx = torch.randint(0, cfg.vocab, (a.batch, a.seq + 1), device="cuda")
         x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
+        it = [0]
 
         def step():
-            opt.zero_grad(set_to_none=True)
-            loss = model.loss(x, y)
-            if dp:
-                with GroupedDPBackward():
-                    loss.backward()
-            else:
-                loss.backward()
-            opt.step()
+            it[0] += 1
+            dstep(it[0], lambda: model.loss(x, y, reduction="sample_sum") * (1.0 if dp else 1.0 / a.batch))
 
         for _ in range(3):
             step()
@@ -79,7 +77,9 @@ def main():
                           {k: round(v, 3) for k, v in sorted(tot.items(), key=lambda kv: -kv[1])},
                           "top_kernels_ms": {k: round(v, 3) for k, v in
                                              sorted(top.items(), key=lambda kv: -kv[1])[:14]}}), flush=True)
-        del model, opt
+        del model, dstep, step
+        import gc
+        gc.collect()
         torch.cuda.empty_cache()
 
 
