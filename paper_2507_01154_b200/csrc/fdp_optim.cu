@@ -56,6 +56,75 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ theta, T* __restri
   }
 }
 
+// fp32 Adam without noise (all-reduce DP-Adam, the non-DP baseline): float4 streams,
+// two quads in flight per thread, evict-first loads; the same per-element arithmetic
+// as k_adam<float> (bitwise: identical operation order). Element i4 covers [4 i4, 4 i4 + 4).
+__device__ __forceinline__ void adam_quad(float4& t, float4& mm, float4& vv, const float4 gg, float eta, float b1,
+                                          float b2, float eps) {
+  const float c1 = 1.0f - b1, c2 = 1.0f - b2;
+#define FDP_ADAM1(c)                                      \
+  {                                                       \
+    const float mi = b1 * mm.c + c1 * gg.c;               \
+    const float vi = b2 * vv.c + c2 * (gg.c * gg.c);      \
+    const float eta_hat = eta / (sqrtf(vi) + eps);        \
+    t.c = t.c - eta_hat * mi;                             \
+    mm.c = mi;                                            \
+    vv.c = vi;                                            \
+  }
+  FDP_ADAM1(x) FDP_ADAM1(y) FDP_ADAM1(z) FDP_ADAM1(w)
+#undef FDP_ADAM1
+}
+
+// kNoise: add the shard's Philox noise first, one quad draw per float4 (the noise
+// index offset is a multiple of 4, so quad i4 of this segment is Philox block
+// offset / 4 + i4 -- the same draws as the scalar kernel's per-element calls)
+template <bool kNoise>
+__global__ void __launch_bounds__(256) k_adam_f32x4(float4* __restrict__ theta, float4* __restrict__ m,
+                                                    float4* __restrict__ v, const float4* __restrict__ g,
+                                                    long long n4, float eta, float b1, float b2, float eps,
+                                                    NoiseArgs na) {
+  uint64_t base = na.base;
+  if (kNoise && na.step_ptr) base = absorb3(na.seed_u, na.layer_u, static_cast<uint64_t>(*na.step_ptr));
+  const uint64_t q0 = static_cast<uint64_t>(na.offset) >> 2;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += 2 * stride) {
+    const long long j = i + stride;
+    const bool two = j < n4;
+    float4 g0 = __ldcs(g + i), m0 = __ldcs(m + i), v0 = __ldcs(v + i), t0 = __ldcs(theta + i);
+    float4 g1 = g0, m1 = m0, v1 = v0, t1 = t0;
+    if (two) {
+      g1 = __ldcs(g + j);
+      m1 = __ldcs(m + j);
+      v1 = __ldcs(v + j);
+      t1 = __ldcs(theta + j);
+    }
+    if constexpr (kNoise) {
+      const float4 z0 = philox_normal4(base, q0 + static_cast<uint64_t>(i));
+      g0.x += na.scale * z0.x;
+      g0.y += na.scale * z0.y;
+      g0.z += na.scale * z0.z;
+      g0.w += na.scale * z0.w;
+      if (two) {
+        const float4 z1 = philox_normal4(base, q0 + static_cast<uint64_t>(j));
+        g1.x += na.scale * z1.x;
+        g1.y += na.scale * z1.y;
+        g1.z += na.scale * z1.z;
+        g1.w += na.scale * z1.w;
+      }
+    }
+    adam_quad(t0, m0, v0, g0, eta, b1, b2, eps);
+    __stcs(theta + i, t0);
+    __stcs(m + i, m0);
+    __stcs(v + i, v0);
+    if (two) {
+      adam_quad(t1, m1, v1, g1, eta, b1, b2, eps);
+      __stcs(theta + j, t1);
+      __stcs(m + j, m1);
+      __stcs(v + j, v1);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_sgd(T* __restrict__ theta, const T* __restrict__ g, long long n, T eta,
                                              NoiseArgs na) {
@@ -89,11 +158,35 @@ cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const v
       k_adam<double><<<blocks_for(n), 256, 0, s>>>(static_cast<double*>(theta), static_cast<double*>(m),
                                                    static_cast<double*>(v), static_cast<const double*>(g), n, eta, b1,
                                                    b2, eps, na);
-    else
+    else if ((!na.on || (na.impl == 2 && (na.offset & 3) == 0)) &&
+             ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(m) |
+               reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g)) & 15u) == 0) {
+      // quads over the aligned body (Philox noise: one draw per quad), the scalar kernel for the tail
+      const long long n4 = n >> 2;
+      if (n4 > 0) {
+        long long blocks = (n4 + 511) / 512;
+        if (blocks > 148LL * 8) blocks = 148LL * 8;
+        auto k = na.on ? k_adam_f32x4<true> : k_adam_f32x4<false>;
+        k<<<static_cast<int>(blocks), 256, 0, s>>>(
+            static_cast<float4*>(theta), static_cast<float4*>(m), static_cast<float4*>(v),
+            static_cast<const float4*>(g), n4, static_cast<float>(eta), static_cast<float>(b1),
+            static_cast<float>(b2), static_cast<float>(eps), na);
+      }
+      const long long done = n4 << 2;
+      if (done < n) {
+        NoiseArgs tail = na;
+        tail.offset += done;
+        k_adam<float><<<1, 256, 0, s>>>(static_cast<float*>(theta) + done, static_cast<float*>(m) + done,
+                                        static_cast<float*>(v) + done, static_cast<const float*>(g) + done, n - done,
+                                        static_cast<float>(eta), static_cast<float>(b1), static_cast<float>(b2),
+                                        static_cast<float>(eps), tail);
+      }
+    } else {
       k_adam<float><<<blocks_for(n), 256, 0, s>>>(static_cast<float*>(theta), static_cast<float*>(m),
                                                   static_cast<float*>(v), static_cast<const float*>(g), n,
                                                   static_cast<float>(eta), static_cast<float>(b1),
                                                   static_cast<float>(b2), static_cast<float>(eps), na);
+    }
   } else {
     if (f64)
       k_sgd<double><<<blocks_for(n), 256, 0, s>>>(static_cast<double*>(theta), static_cast<const double*>(g), n, eta,

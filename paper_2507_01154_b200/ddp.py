@@ -356,11 +356,11 @@ class GradBuckets:
         b.params = list(params)
         b.offsets = []
         off = 0
-        for p in b.params:
+        for p in b.params:  # 16-byte aligned segments (vectorised optimizer kernels, quad-aligned noise)
             b.offsets.append(off)
-            off += p.numel()
+            off += -(-p.numel() // 4) * 4
         b.n = off
-        b.per = -(-off // self.world)
+        b.per = -(-off // (4 * self.world)) * 4
         dev = params[0].device
         b.flat = torch.zeros(b.per * self.world, dtype=torch.float32, device=dev)
         b.pflat = None

@@ -147,3 +147,58 @@ def test_report_describes_the_executed_path():
     assert expl.report.per_sample_grad_bytes_stored == 2 * B * D * P * 4
     for r in (fused, ghost, single, expl):
         assert r.reference_report is not None and r.reference_report.kernel_launches >= 1
+
+
+@pytest.mark.parametrize("n", [4096 * 1024 + 3, 17, 1 << 20])
+def test_vectorized_adam_matches_the_scalar_formula(n):
+    """fp32 Adam without noise takes the float4 kernel on aligned buffers (plus a
+    scalar tail): same per-element arithmetic as dpcore.py:139-156 (no bias
+    correction, post-update v), checked against a float64 evaluation."""
+    from paper_2507_01154_b200.dpcore import OptimizerState, dp_adam_step_
+
+    g = torch.Generator(device="cuda").manual_seed(n % 97)
+    theta = torch.randn(n, device="cuda", generator=g)
+    grad = torch.randn(n, device="cuda", generator=g)
+    m = torch.randn(n, device="cuda", generator=g) * 0.1
+    v = torch.rand(n, device="cuda", generator=g) * 0.01
+    t64, m64, v64, g64 = theta.double(), m.double(), v.double(), grad.double()
+    st = OptimizerState(theta=theta, m=m, v=v, eta=1e-3, beta1=0.9, beta2=0.999, eps_adam=1e-8)
+    dp_adam_step_(st, grad)
+    # the kernel's constants are fp32 (1 - beta2 = 0.00099998713 in fp32): reference with the same constants
+    f32 = lambda c: float(torch.tensor(c, dtype=torch.float32))  # noqa: E731
+    b1, b2 = f32(0.9), f32(0.999)
+    c1, c2 = f32(1.0 - b1), f32(1.0 - b2)
+    m_ref = b1 * m64 + c1 * g64
+    v_ref = b2 * v64 + c2 * g64 * g64
+    t_ref = t64 - f32(1e-3) / (v_ref.sqrt() + f32(1e-8)) * m_ref
+    torch.cuda.synchronize()
+    assert torch.allclose(m.double(), m_ref, rtol=1e-6, atol=1e-7)
+    assert torch.allclose(v.double(), v_ref, rtol=1e-6, atol=1e-9)
+    assert torch.allclose(theta.double(), t_ref, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("offset,n", [(0, 1 << 20), (4096, 1000003), (3, 4099)])
+def test_adam_with_shard_noise_vector_and_scalar_paths(offset, n):
+    """ZeRO-1 owner-shard noise inside the fp32 Adam step: the quad-aligned float4
+    kernel (offset % 4 == 0, Philox: one draw per quad) and the scalar kernel
+    (other offsets) both add exactly sigma*C*N(seed, layer_id, step, offset + i)."""
+    from paper_2507_01154_b200.dpcore import OptimizerState, dp_adam_step_
+
+    g = torch.Generator(device="cuda").manual_seed(n % 89)
+    theta = torch.randn(n, device="cuda", generator=g)
+    grad = torch.randn(n, device="cuda", generator=g) * 1e-2
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    cfg = fdp.DPConfig(0.5, 0.8, "mean", seed=7, layer_id=3, step=11)
+    noise = fdp.noise_range(cfg, offset, offset + n, cfg.sigma * cfg.clip_c, noise_impl="philox")
+    g_eff = (grad + noise).double()
+    t0 = theta.double()
+    st = OptimizerState(theta=theta, m=m, v=v, eta=1e-3, beta1=0.9, beta2=0.999, eps_adam=1e-8)
+    dp_adam_step_(st, grad, noise=cfg, noise_offset=offset, noise_impl="philox", layer_numel=offset + n + 8)
+    torch.cuda.synchronize()
+    f32 = lambda c: float(torch.tensor(c, dtype=torch.float32))  # noqa: E731
+    m_ref = f32(1.0 - f32(0.9)) * g_eff
+    assert torch.allclose(m.double(), m_ref, rtol=1e-5, atol=1e-8)
+    v_ref = f32(1.0 - f32(0.999)) * g_eff * g_eff
+    t_ref = t0 - f32(1e-3) / (v_ref.sqrt() + f32(1e-8)) * m_ref
+    assert torch.allclose(theta.double(), t_ref, rtol=1e-5, atol=1e-6)
