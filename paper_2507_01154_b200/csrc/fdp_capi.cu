@@ -534,6 +534,7 @@ fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common&
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
   p.mc = pl.stream_mc;
   p.fin_epi = env_int("FDP_FIN_EPI", 1);
+  p.swizzle = env_int("FDP_STREAM_SWIZZLE", 0);
   return p;
 }
 

@@ -119,6 +119,7 @@ struct StreamParams {
   // the per-sample buffer G[b] (tm_gw is then a 3-D (P, D, B) map) with its sum of
   // squares in norm_part[(b * n_wtiles + wt) * CG * MC + crank]; p.B is the real batch
   int spill;
+  int swizzle;  // tile raster: 0/1 row-major, G > 1 grouped by G row blocks (FDP_STREAM_SWIZZLE)
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {

@@ -172,6 +172,26 @@ __device__ __forceinline__ bool fin_chunk(const FinJob& j, FinShared* fs, int la
   return true;
 }
 
+// Tile raster: work tile wt -> (row block r, column tile c). swz <= 1: row-major (a
+// wave of K consecutive tiles spans ~K/n_pt row blocks and EVERY column tile, so the
+// whole X operand streams through L2 once per wave). swz = G > 1: grouped raster --
+// G row blocks walked column by column, so a wave covers a compact G x (K/G) block
+// of tiles and its operand rows / columns are re-read from L2 instead of DRAM.
+__device__ __forceinline__ void tile_rc(int wt, int n_rows, int n_pt, int swz, int& r, int& c) {
+  if (swz <= 1) {
+    r = wt / n_pt;
+    c = wt - r * n_pt;
+    return;
+  }
+  const int per_group = swz * n_pt;
+  const int grp = wt / per_group;
+  const int first = grp * swz;
+  const int rows_in = n_rows - first < swz ? n_rows - first : swz;
+  const int local = wt - grp * per_group;
+  c = local / rows_in;
+  r = first + (local - c * rows_in);
+}
+
 // MC = 2: a 4-CTA cluster holds two CTA pairs working on vertically adjacent pair
 // tiles (same X columns, consecutive dY row blocks) in lockstep; each X box is
 // loaded once and multicast to the CTA of both pairs that needs it, so L2 serves
@@ -261,8 +281,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           bb = sb;
           be = sb + 1;
         }
-        const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
-        const int p0 = (wt % p.n_pt) * BN + rank * C::kBCols;
+        int tr, tc;
+        tile_rc(wt, n_wt_real / p.n_pt, p.n_pt, p.swizzle, tr, tc);
+        const int d0 = (tr * CL + crank) * kBM;
+        const int p0 = tc * BN + rank * C::kBCols;
         for (int b = bb; b < be; ++b) {
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x501);
@@ -349,8 +371,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     while (w.next(wt, bb, be)) {
       const bool whole = bb == 0 && be == p.B;
       if (bb != 0 || !tile_prefilled(whole)) continue;
-      const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
-      const int p0 = (wt % p.n_pt) * BN;
+      int tr, tc;
+      tile_rc(wt, n_wt_real / p.n_pt, p.n_pt, p.swizzle, tr, tc);
+      const int d0 = (tr * CL + crank) * kBM;
+      const int p0 = tc * BN;
       prefill_rows<BN>(p.grad_w, p.D, p.P, d0, d0 + kBM, p0, p.accumulate != 0, p.add_noise != 0, p.noise_impl,
                        kbg, kb, p.noise_scale, p.noise_lo, p.noise_hi, ntid);
       __threadfence();
@@ -399,8 +423,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int tile = wt * CL + crank;  // spill: (b * n_wtiles + wt) * CL + crank, the unit's partial slot
       const int sb = spill ? wt / n_wt_real : 0;
       if (spill) wt -= sb * n_wt_real;
-      const int d0 = ((wt / p.n_pt) * CL + crank) * kBM;
-      const int p0 = (wt % p.n_pt) * BN;
+      int tr, tc;
+      tile_rc(wt, n_wt_real / p.n_pt, p.n_pt, p.swizzle, tr, tc);
+      const int d0 = (tr * CL + crank) * kBM;
+      const int p0 = tc * BN;
       float acc[C::kCPT];
 #pragma unroll
       for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
