@@ -396,8 +396,12 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   // (X boxes multicast to the pair below): measured 2.5-3 % faster on down projections
   // (13824 -> 5120 at B = 2 / 4), 1.5-3 % slower on square / up projections
   // (tools/ab_layer.py, profiles/r1_stream_mc_ab.jsonl), so chosen for P >= 2 D only
+  // round 2: on the same down projections a grouped tile raster on 2-CTA clusters beats the
+  // multicast layout (13824 -> 5120, T=2048: B=1 358 -> 332 us, B=2 612 -> 572 us, A/B in
+  // profiles/r2_stream_swizzle_ab.jsonl; the 4-CTA layout only fits 33 clusters = 132 SMs), so
+  // multicast is opt-in (FDP_STREAM_MC=1) and the raster is grouped by 8 row blocks there
   const int mc_env = env_int("FDP_STREAM_MC", -1);
-  const bool mc_want = mc_env >= 0 ? mc_env != 0 : d->P >= 2 * d->D;
+  const bool mc_want = mc_env >= 0 ? mc_env != 0 : false;
   pl.stream_mc = (pl.tc && pl.bn == 256 && pl.cg == 2 && mc_want && fdp::stream_mc_max_clusters() > 0) ? 2 : 1;
   pl.stream_tiles = pl.tc ? fdp::stream_wtiles(pl.n_wtiles, pl.n_pt, pl.stream_mc) * pl.cg * pl.stream_mc
                           : pl.n_tiles;
@@ -534,7 +538,7 @@ fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common&
   p.budget_ns = (d->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
   p.mc = pl.stream_mc;
   p.fin_epi = env_int("FDP_FIN_EPI", 1);
-  p.swizzle = env_int("FDP_STREAM_SWIZZLE", 0);
+  p.swizzle = env_int("FDP_STREAM_SWIZZLE", d->P >= 2 * d->D ? 8 : 0);
   return p;
 }
 

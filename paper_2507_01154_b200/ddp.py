@@ -576,14 +576,18 @@ class BucketedAdam:
 
         bk = self.bk
         for b in bk.buckets:
-            if bk.mode == "allreduce":
+            if bk.mode == "allreduce" and not self.noise_keys:
                 self.adam_fn(b.pflat[:b.n], b.m, b.v, b.flat[:b.n], self.lr, self.beta1, self.beta2, self.eps,
                              None, 0, None, 0)
                 continue
-            lo = bk.rank * b.per
-            hi = min(lo + b.per, b.n)
+            # ZeRO-1: this rank's shard; all-reduce with noise keys: the whole bucket on every
+            # rank, each element's noise drawn once per rank from the same keys (counter-based,
+            # so every replica adds the same noise and the parameters stay identical)
+            lo = bk.rank * b.per if bk.mode == "reduce_scatter" else 0
+            hi = min(lo + b.per, b.n) if bk.mode == "reduce_scatter" else b.n
+            src = b.shard if bk.mode == "reduce_scatter" else b.flat
             for a, z, key in self._segments(b, lo, hi):
-                th, g = b.pflat[a:z], b.shard[a - lo:z - lo]
+                th, g = b.pflat[a:z], src[a - lo:z - lo]
                 mm, vv = b.m[a - lo:z - lo], b.v[a - lo:z - lo]
                 if key is None:
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0)
@@ -591,7 +595,7 @@ class BucketedAdam:
                     cfg, off, glen, impl = key
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps,
                                  replace(cfg, step=dp_step), off, impl, glen)
-            if bk.world > 1:
+            if bk.world > 1 and bk.mode == "reduce_scatter":
                 mine = b.pflat[bk.rank * b.per:(bk.rank + 1) * b.per]
                 if dist.get_backend(bk.group) == "nccl":
                     dist.all_gather_into_tensor(b.pflat, mine.clone(), group=bk.group)
@@ -606,10 +610,11 @@ class DataParallelStep:
     collectives issued from inside it, Adam (no bias correction, dpcore.py:139-156)
     on the bucket layout.
 
-      dp=True,  mode "allreduce":      DP-Adam (config 3): the DP kernels add each
-                                       layer's noise on this rank's slice of its
-                                       index space; buckets all-reduced; replicated
-                                       Adam.
+      dp=True,  mode "allreduce":      DP-Adam (config 3): buckets all-reduced,
+                                       replicated Adam; the noise is added inside the
+                                       Adam step on every replica from the same keyed
+                                       draws (noise_in_optimizer, default), or by the
+                                       DP kernels on each rank's slice of every layer.
       dp=True,  mode "reduce_scatter": ZeRO-1 (config 4): the DP kernels run without
                                        noise, buckets reduce-scattered, each rank adds
                                        the noise of its shard inside its Adam step and
@@ -624,10 +629,15 @@ class DataParallelStep:
 
     def __init__(self, model, *, dp: bool, mode: str = "allreduce", lr: float = 1e-5, beta1: float = 0.9,
                  beta2: float = 0.999, eps: float = 1e-8, rank: int = 0, world: int = 1, group=None,
-                 comm_sms: int = 4, bucket_bytes: int = 512 << 20, global_batch: int = 1, adam_fn=None):
+                 comm_sms: int = 4, bucket_bytes: int = 512 << 20, global_batch: int = 1, adam_fn=None,
+                 noise_in_optimizer: bool = True):
         from .dplinear import DPLinear
 
         self.model, self.dp, self.mode, self.world = model, dp, mode, world
+        # where the DP noise is added: in the optimizer step (the finalize fused into Adam:
+        # ZeRO-1 on the owner's shard, all-reduce on every replica with the same keyed draws)
+        # or, all-reduce only, by the DP kernels on each rank's slice of every layer
+        self.noise_in_optimizer = bool(noise_in_optimizer) or mode == "reduce_scatter"
         self.global_batch = global_batch
         self.buckets = GradBuckets(model.parameters(), bucket_bytes=bucket_bytes, mode=mode, group=group,
                                    rank=rank, world=world, flat_params=True)
@@ -635,7 +645,7 @@ class DataParallelStep:
         if dp:
             set_data_parallel(self.dp_mods, rank, world)
             self.buckets.set_deferred([m.weight for m in self.dp_mods if isinstance(m, DPLinear)])
-        keys = dp_noise_keys(model) if dp and mode == "reduce_scatter" else None
+        keys = dp_noise_keys(model) if dp and self.noise_in_optimizer else None
         self.opt = BucketedAdam(self.buckets, lr=lr, beta1=beta1, beta2=beta2, eps=eps, noise_keys=keys,
                                 adam_fn=adam_fn)
         dev = next(model.parameters()).device
@@ -647,8 +657,8 @@ class DataParallelStep:
 
         bk = self.buckets
         bk.zero_grad()
-        for m in self.dp_mods:
-            m.set_step(step, last_micro_batch=self.mode == "allreduce", logical_batch=self.global_batch)
+        for m in self.dp_mods:  # kernel noise only when the optimizer does not add it
+            m.set_step(step, last_micro_batch=not self.noise_in_optimizer, logical_batch=self.global_batch)
         loss = loss_fn()
         if self.dp:
             with GroupedDPBackward(buckets=bk, max_ctas=self.max_ctas) as g:

@@ -237,7 +237,7 @@ def _tiny_llama_cfg():
     return LlamaConfig(vocab=512, d=256, heads=4, layers=2, mlp=512, seq=128)
 
 
-def _llama_step_worker(rank, world, port, mode, dp, out):
+def _llama_step_worker(rank, world, port, mode, dp, out, opt_noise=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -256,7 +256,7 @@ def _llama_step_worker(rank, world, port, mode, dp, out):
     lo, hi = B * rank // world, B * (rank + 1) // world
     x, y = idx[lo:hi, :-1].contiguous(), idx[lo:hi, 1:].contiguous()
     step = DataParallelStep(model, dp=dp, mode=mode, lr=1e-3, rank=rank, world=world, global_batch=B,
-                            bucket_bytes=1 << 20)
+                            bucket_bytes=1 << 20, noise_in_optimizer=opt_noise)
     scale = 1.0 if dp else 1.0 / B
     grads = None
     for i in range(2):
@@ -267,7 +267,7 @@ def _llama_step_worker(rank, world, port, mode, dp, out):
             grads = [(b.flat if mode == "allreduce" else b.shard).detach().cpu().clone() for b in bk.buckets]
             pers = [b.per for b in bk.buckets]
     torch.cuda.synchronize()
-    out[(mode, dp, world, rank)] = ([p.detach().cpu().clone() for p in model.parameters()],
+    out[(mode, dp, world, rank, opt_noise)] = ([p.detach().cpu().clone() for p in model.parameters()],
                                     list(step.buckets.issued), len(step.buckets.buckets), step.last_flushes,
                                     grads, pers)
     if world > 1:
@@ -275,30 +275,32 @@ def _llama_step_worker(rank, world, port, mode, dp, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["allreduce", "reduce_scatter"])
+@pytest.mark.parametrize("mode,opt_noise", [("allreduce", True), ("allreduce", False), ("reduce_scatter", True)])
 @pytest.mark.parametrize("dp", [True, False])
-def test_bucketed_llama_step_two_ranks_equals_single_process(mode, dp):
+def test_bucketed_llama_step_two_ranks_equals_single_process(mode, opt_noise, dp):
     """Two ranks (processes) sharing cuda:0 over gloo run the tiny-Llama training
     step through DataParallelStep: every parameter DP (DPLinear / DPRMSNorm /
     DPEmbedding, Philox noise), gradient buckets flushed from inside the backward
     (GroupedDPBackward(buckets=...)), then all-reduce + replicated DP-Adam or
-    reduce-scatter + ZeRO-1 Adam with the noise added on the owner's shard.
+    reduce-scatter + ZeRO-1 Adam with the noise added on the owner's shard
+    (all-reduce: the noise either inside every replica's Adam step from the same
+    keyed draws, or by the DP kernels on each rank's slice).
     After two steps the parameters equal the single-process run on the global
     batch (noise once per element either way). dp=False: the non-DP baseline
     (FP32GradLinear projections) through the same buckets and optimizer."""
     with mp.get_context("spawn").Manager() as mgr:
         out = mgr.dict()
-        mp.start_processes(_llama_step_worker, args=(1, _free_port(), mode, dp, out), nprocs=1, join=True,
-                           start_method="spawn")
-        mp.start_processes(_llama_step_worker, args=(2, _free_port(), mode, dp, out), nprocs=2, join=True,
-                           start_method="spawn")
-        ref, _, nb, flushes, ref_g, _ = out[(mode, dp, 1, 0)]
+        mp.start_processes(_llama_step_worker, args=(1, _free_port(), mode, dp, out, opt_noise), nprocs=1,
+                           join=True, start_method="spawn")
+        mp.start_processes(_llama_step_worker, args=(2, _free_port(), mode, dp, out, opt_noise), nprocs=2,
+                           join=True, start_method="spawn")
+        ref, _, nb, flushes, ref_g, _ = out[(mode, dp, 1, 0, opt_noise)]
         assert nb >= 3
         if dp:
             assert flushes >= 2  # DP kernels ran bucket by bucket inside the backward
         for r in range(2):
-            got, issued, _, _, g2, pers = out[(mode, dp, 2, r)]
-            assert issued == out[(mode, dp, 2, 0)][1]
+            got, issued, _, _, g2, pers = out[(mode, dp, 2, r, opt_noise)]
+            assert issued == out[(mode, dp, 2, 0, opt_noise)][1]
             # step-0 gradients: summed over the ranks == the single-process gradients
             for k, (a, full) in enumerate(zip(g2, ref_g)):
                 b = full if mode == "allreduce" else torch.cat([full, torch.zeros(2 * pers[k])])[
