@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-train", action="store_true",
                     help="skip the GPT-2 training-step comparison (DP linear layers vs nn.Linear)")
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
+    ap.add_argument("--no-llama", action="store_true", help="skip the Llama-13B-shape training-step comparison")
+    ap.add_argument("--llama-layers", type=int, default=8)
     ap.add_argument("--per-layer", action="store_true",
                     help="one fused launch per layer instead of one multi-layer launch per step")
     ap.add_argument("--chunks", type=int, default=4,
@@ -552,6 +554,35 @@ def main():
         except Exception as e:  # noqa: BLE001
             train = {"error": repr(e)[:300]}
 
+    # ---- BASELINE config 4 (the paper's headline): Llama-13B-shape DP pre-training step vs
+    # the same model's non-DP step, every parameter DP, ZeRO-1 DP-Adam, one GPU, a reduced
+    # depth (stated); tools/train_llama.py is the full driver (torchrun for N GPUs)
+    llama = None
+    if not a.no_train and not a.no_llama and world == 1:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import gc
+
+            import train_llama as tl
+
+            largs = argparse.Namespace(model="llama-13b", layers=a.llama_layers, batch=1, seq=2048, steps=3,
+                                       warmup=2, zero1=True, comm_sms=4, bucket_mb=512, clip=1.0, sigma=1.0,
+                                       nondp_linear="fp32grad")
+            gc.collect()
+            torch.cuda.empty_cache()
+            nd_l = tl.run_arm(False, largs, 0, 1, dev)
+            dp_l = tl.run_arm(True, largs, 0, 1, dev)
+            llama = {"model": f"llama-13b shapes (d=5120, 40 heads, MLP 13824, vocab 32000), {a.llama_layers} of 40 "
+                              f"blocks, B=1, T=2048, every parameter DP, ZeRO-1 DP-Adam (noise on the owner's shard), "
+                              f"random init, synthetic tokens; non-DP = the same model with FP32GradLinear projections, "
+                              f"same buckets / optimizer",
+                     "dp_tokens_per_s": dp_l["tokens_per_s"], "non_dp_tokens_per_s": nd_l["tokens_per_s"],
+                     "dp_ms_per_step": dp_l["ms_per_step"], "non_dp_ms_per_step": nd_l["ms_per_step"],
+                     "dp_pct_of_non_dp": 100.0 * dp_l["tokens_per_s"] / nd_l["tokens_per_s"],
+                     "params": dp_l["params"]}
+        except Exception as e:  # noqa: BLE001
+            llama = {"error": repr(e)[:300]}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -567,6 +598,8 @@ def main():
         line.update(extra)
         if train is not None:
             line["train_step"] = train
+        if llama is not None:
+            line["llama13b_train_step"] = llama
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
