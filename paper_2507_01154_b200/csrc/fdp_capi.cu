@@ -189,6 +189,16 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
+// SMs a per-layer call leaves free (FDP_RESERVE_SMS, default 0): under data
+// parallelism (ddp.DataParallelStep sets it to its NCCL CTA budget) every grid is
+// capped so the collective's CTAs stay resident next to ours and the grids that
+// rely on co-residency (split tiles waiting on the cluster that initialises them,
+// the fused per-sample all-reduce) never wait on a CTA that cannot be scheduled.
+int reserved_sms() {
+  const int r = env_int("FDP_RESERVE_SMS", 0);
+  return r > 0 ? r : 0;
+}
+
 // Ghost norms cost ~T^2 (P + D) (1 + 1/nT) flops per sample, recomputing the
 // per-sample gradient 2 T P D: take the cheaper one unless the caller forces it.
 bool single_ok(const fdp_desc* d) { return d->B == 1 && !d->accumulate; }
@@ -311,7 +321,8 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
         if (!allowed(bn, cg)) continue;
         int ndt2, npt;
         const long long nwt = tiles_for(bn, cg, ndt2, npt);
-        const long long cap = fdp::tc_max_coresident_ctas(bn, cg);
+        long long cap = fdp::tc_max_coresident_ctas(bn, cg);
+        if (cap > 0) cap = std::max<long long>(0, cap - ((reserved_sms() + cg - 1) / cg) * cg);
         const long long need = nwt * cg;
         if (cap <= 0 || need > cap) continue;
         long long g = cap / need;
@@ -378,7 +389,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     pl.launches = 1;
   } else if (pl.tc) {
     const int cap = fdp::tc_max_coresident_ctas(pl.bn, pl.cg);
-    const int max_clusters = (cap > 0 ? cap : di.sms) / pl.cg;
+    const int max_clusters = std::max(1, ((cap > 0 ? cap : di.sms) - reserved_sms()) / pl.cg);
     pl.grid = (pl.n_wtiles < max_clusters ? pl.n_wtiles : max_clusters) * pl.cg;
     if (kind == FDP_KIND_NON_DP) pl.launches = 1;
     else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;  // G, norms, reduce, clip, sum
@@ -547,11 +558,11 @@ int stream_grid(const fdp_desc* d, const Plan& pl, const DevInfo& di) {
   const long long units =
       static_cast<long long>(fdp::stream_wtiles(pl.n_wtiles, pl.n_pt, pl.stream_mc)) * d->B;
   if (pl.stream_mc == 2) {
-    const long long clusters = fdp::stream_mc_max_clusters();
+    const long long clusters = std::max(1, fdp::stream_mc_max_clusters() - (reserved_sms() + 3) / 4);
     return static_cast<int>((units < clusters ? units : clusters) * 4);
   }
   const int cap = fdp::tc_max_coresident_ctas(pl.bn, pl.cg);
-  const long long clusters = (cap > 0 ? cap : di.sms) / pl.cg;
+  const long long clusters = std::max(1, ((cap > 0 ? cap : di.sms) - reserved_sms()) / pl.cg);
   return static_cast<int>((units < clusters ? units : clusters) * pl.cg);
 }
 
@@ -933,11 +944,12 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       g.err = p.ws_ctrl + 1;
       g.budget_ns = p.budget_ns;
       if (gs.pair) {
-        const int clusters = di.sms / 2;
+        const int clusters = std::max(1, (di.sms - reserved_sms()) / 2);
         const int grid = 2 * (g.n_items < clusters ? g.n_items : clusters);
         if ((e = fdp::launch_ghost_pair(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
       } else {
-        const int grid = g.n_items < di.sms ? g.n_items : di.sms;
+        const int slots = std::max(1, di.sms - reserved_sms());
+        const int grid = g.n_items < slots ? g.n_items : slots;
         if ((e = fdp::launch_ghost(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
       }
       if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, gs.parts, d->clip_c, p.clip_c2, c.inv_batch, norms,

@@ -650,6 +650,8 @@ class DataParallelStep:
                                 adam_fn=adam_fn)
         dev = next(model.parameters()).device
         self.max_ctas = group_max_ctas(dev, comm_sms, world)
+        if world > 1:  # per-layer DP kernels leave NCCL's SMs free too (fdp_capi.cu reserved_sms)
+            os.environ["FDP_RESERVE_SMS"] = str(int(comm_sms))
         self.last_flushes = 0
 
     def __call__(self, step: int, loss_fn):

@@ -202,3 +202,22 @@ def test_adam_with_shard_noise_vector_and_scalar_paths(offset, n):
     v_ref = f32(1.0 - f32(0.999)) * g_eff * g_eff
     t_ref = t0 - f32(1e-3) / (v_ref.sqrt() + f32(1e-8)) * m_ref
     assert torch.allclose(theta.double(), t_ref, rtol=1e-5, atol=1e-6)
+
+
+def test_reserved_sms_caps_every_per_layer_grid(monkeypatch):
+    """FDP_RESERVE_SMS (set by ddp.DataParallelStep under data parallelism): the
+    per-layer grids leave that many SMs to NCCL, with unchanged results."""
+    cases = [((2, 512, 2048, 2048), "two_phase", "ghost"), ((1, 512, 2048, 2048), "two_phase", "single"),
+             ((4, 256, 512, 768), "fused", "auto")]
+    for (B, T, P, D), path, phase in cases:
+        x, dy = _inputs(B, T, P, D, 3)
+        cfg = fdp.DPConfig(float(np.sqrt(T * P * D)), 0.0, "mean")
+        ref = fdp.backward_flashdp(x, dy, cfg, path=path, norm_phase=phase).grad_w.clone()
+        full = fdp.execution_plan((B, T, P), (B, T, D), path=path)["grid"]
+        monkeypatch.setenv("FDP_RESERVE_SMS", "20")
+        capped = fdp.execution_plan((B, T, P), (B, T, D), path=path)["grid"]
+        got = fdp.backward_flashdp(x, dy, cfg, path=path, norm_phase=phase).grad_w
+        monkeypatch.delenv("FDP_RESERVE_SMS")
+        torch.cuda.synchronize()
+        assert capped <= max(full, 148 - 20), (path, full, capped)
+        assert _rel(got.cpu(), ref.cpu()) < 1e-5, path
