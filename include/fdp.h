@@ -117,7 +117,14 @@ enum fdp_flags { FDP_FLAG_SKIP_BARRIER = 1, FDP_FLAG_TIMEOUT_SHORT = 2,
  * sample's gradient IS the layer's GEMM, so it is computed once (stream-K
  * tcgen05, per-tile sums of squares in the epilogue) and one elementwise pass
  * applies the clip factor and the noise. */
-enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2, FDP_NORMS_SINGLE = 3 };
+/* SPILL (opt-in, never chosen by AUTO): every sample's gradient G_b is one GEMM
+ * (K = T) written unscaled to the workspace (B * D * P fp32) with its norm from
+ * the epilogue, then one elementwise pass forms sum_b c_b G_b + noise. It DOES
+ * materialise per-sample gradients in HBM -- the thing FlashDP avoids -- trading
+ * B * D * P * 8 bytes of traffic for the ghost phase's T^2 (P + D) flops; see
+ * DESIGN.md for where that trade wins on B200. */
+enum fdp_norm_phase { FDP_NORMS_AUTO = 0, FDP_NORMS_GHOST = 1, FDP_NORMS_RECOMPUTE = 2, FDP_NORMS_SINGLE = 3,
+                      FDP_NORMS_SPILL = 4 };
 
 typedef struct fdp_desc {
   int64_t B, T, P, D;       /* X (B,T,P), dY (B,T,D)                          */

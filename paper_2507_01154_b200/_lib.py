@@ -23,7 +23,7 @@ NOISE = {"keyed_f32": 0, "keyed_f64": 1, "philox": 2}
 PATH = {"auto": 0, "fused": 1, "two_phase": 2, "simt": 3}
 PATH_NAMES = {v: k for k, v in PATH.items()}
 KIND = {"non_dp": 0, "explicit_dp": 1, "implicit_dp": 2, "flashdp": 3}
-NORM_PHASE = {"auto": 0, "ghost": 1, "recompute": 2, "single": 3}
+NORM_PHASE = {"auto": 0, "ghost": 1, "recompute": 2, "single": 3, "spill": 4}
 NORM_PHASE_NAMES = {v: k for k, v in NORM_PHASE.items()}
 FLAG_SKIP_BARRIER = 1
 FLAG_TIMEOUT_SHORT = 2

@@ -152,7 +152,7 @@ int validate(const fdp_desc* d, int32_t kind) {
   if (d->noise_impl < FDP_NOISE_KEYED_F32 || d->noise_impl > FDP_NOISE_PHILOX)
     return fail(FDP_ERR_USAGE, "unknown noise_impl %d", d->noise_impl);
   if (d->path < FDP_PATH_AUTO || d->path > FDP_PATH_SIMT) return fail(FDP_ERR_USAGE, "unknown path %d", d->path);
-  if (d->norm_phase < FDP_NORMS_AUTO || d->norm_phase > FDP_NORMS_SINGLE)
+  if (d->norm_phase < FDP_NORMS_AUTO || d->norm_phase > FDP_NORMS_SPILL)
     return fail(FDP_ERR_USAGE, "unknown norm_phase %d", d->norm_phase);
   if (d->norm_phase == FDP_NORMS_SINGLE && (d->B != 1 || d->accumulate))
     return fail(FDP_ERR_USAGE, "norm_phase single needs B == 1 and accumulate == 0");
@@ -206,6 +206,9 @@ bool single_ok(const fdp_desc* d) { return d->B == 1 && !d->accumulate; }
 int choose_norm_phase(const fdp_desc* d) {
   if (d->norm_phase != FDP_NORMS_AUTO) return d->norm_phase;
   if (single_ok(d)) return FDP_NORMS_SINGLE;
+  // FDP_NORM_PHASE=spill: opt into the per-sample-spill phase for every auto two-phase layer
+  if (const char* v = std::getenv("FDP_NORM_PHASE"))
+    if (std::strcmp(v, "spill") == 0 && d->B <= 64) return FDP_NORMS_SPILL;
   const double nT = static_cast<double>((d->T + 127) / 128);
   const double ghost = static_cast<double>(d->T) * d->T * (d->P + d->D) * (1.0 + 1.0 / nT);
   const double recompute = 2.0 * d->T * d->P * d->D;
@@ -394,6 +397,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     if (kind == FDP_KIND_NON_DP) pl.launches = 1;
     else if (kind == FDP_KIND_EXPLICIT_DP) pl.launches = 5;  // G, norms, reduce, clip, sum
     else if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_SINGLE) pl.launches = 2;  // GEMM, finalize
+    else if (pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_SPILL) pl.launches = 3;  // GEMMs, factors, combine
     else pl.launches = 3;                                     // norms, reduce, reweight
   } else {
     pl.grid = pl.n_tiles;
@@ -413,7 +417,9 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
   // multicast is opt-in (FDP_STREAM_MC=1) and the raster is grouped by 8 row blocks there
   const int mc_env = env_int("FDP_STREAM_MC", -1);
   const bool mc_want = mc_env >= 0 ? mc_env != 0 : false;
-  pl.stream_mc = (pl.tc && pl.bn == 256 && pl.cg == 2 && mc_want && fdp::stream_mc_max_clusters() > 0) ? 2 : 1;
+  const bool spill = pl.path == FDP_PATH_TWO_PHASE && pl.norm_phase == FDP_NORMS_SPILL;
+  pl.stream_mc = (pl.tc && pl.bn == 256 && pl.cg == 2 && mc_want && !spill && fdp::stream_mc_max_clusters() > 0)
+                     ? 2 : 1;
   pl.stream_tiles = pl.tc ? fdp::stream_wtiles(pl.n_wtiles, pl.n_pt, pl.stream_mc) * pl.cg * pl.stream_mc
                           : pl.n_tiles;
   const long long n_slots = std::max<long long>(pl.n_tiles, pl.stream_tiles);
@@ -445,6 +451,10 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
     off = align_up(off + 4ull * pl.groups * pl.n_tiles * fdp::kBM * pl.bn, 256);
   pl.off_g = off;
   pl.off_gp = off;
+  if (spill) {  // the per-sample gradients G[b] (B, D, P) fp32
+    off = align_up(off + 4ull * B * d->D * d->P, 256);
+    pl.off_gp = off;
+  }
   if (kind == FDP_KIND_EXPLICIT_DP && d->in_dtype != FDP_DTYPE_F64) {
     const size_t gbytes = 4ull * B * d->D * d->P;
     pl.off_gp = align_up(off + gbytes, 256);
@@ -920,6 +930,35 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       return FDP_OK;
     }
     if ((e = fdp::single_sample_finalize(j, s)) != cudaSuccess) return cuda_fail(e, "single-sample finalize");
+    return FDP_OK;
+  }
+  // TWO_PHASE, spill (opt-in): per-sample GEMMs to G[b] with their norms, factors, one combine pass
+  if (pl.norm_phase == FDP_NORMS_SPILL) {
+    float* G = ws_at<float>(ws, pl.off_g);
+    CUtensorMap tm_g;
+    const cuuint64_t gdims[3] = {static_cast<cuuint64_t>(d->P), static_cast<cuuint64_t>(d->D),
+                                 static_cast<cuuint64_t>(d->B)};
+    const cuuint64_t gstr[2] = {static_cast<cuuint64_t>(d->P * 4), static_cast<cuuint64_t>(d->P * d->D * 4)};
+    const cuuint32_t gbox[3] = {32, static_cast<cuuint32_t>(fdp::kBM), 1};
+    if ((rc = make_tmap_f32(&tm_g, G, 3, gdims, gstr, gbox))) return rc;
+    fdp::StreamParams q = stream_params(d, pl, c, G, ws, false);
+    q.spill = 1;
+    q.accumulate = 0;
+    q.add_noise = 0;
+    q.epi_noise = 0;
+    q.norm_part = ws_at<float>(ws, pl.off_part);
+    q.fin = carry;
+    if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, tm_g, q, stream_grid(d, pl, di), s)) != cudaSuccess)
+      return cuda_fail(e, "stream-K per-sample (spill) GEMM launch");
+    float* fac = ws_at<float>(ws, pl.off_factor);
+    if ((e = fdp::reduce_norms_to_factors(q.norm_part, static_cast<int>(d->B), pl.stream_tiles, d->clip_c,
+                                          d->clip_c * d->clip_c, c.inv_batch, norms, fac, s)) != cudaSuccess)
+      return cuda_fail(e, "factor reduce");
+    if ((e = fdp::spill_combine(grad_w, G, static_cast<int>(d->B), d->D * d->P, fac, d->accumulate, c.add_noise,
+                                d->noise_impl, c.noise_scale, c.key_base, c.key_base_g,
+                                reinterpret_cast<const long long*>(d->device_step), static_cast<uint64_t>(d->seed),
+                                static_cast<uint64_t>(d->layer_id), c.noise_lo, c.noise_hi, s)) != cudaSuccess)
+      return cuda_fail(e, "spill combine");
     return FDP_OK;
   }
   // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass

@@ -327,6 +327,70 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
   return cudaGetLastError();
 }
 
+// spill combine: out = (accumulate ? out : 0) + sum_b fac[b] * G[b] (+ noise), b in order
+// (fixed fp32 order), float4 streams; kMode as in k_single_finalize.
+template <int kMode>
+__global__ void __launch_bounds__(256) k_spill_combine(float* __restrict__ out, const float* __restrict__ G, int B,
+                                                       long long n, const float* __restrict__ fac, int accumulate,
+                                                       int impl, float scale, uint64_t base, uint64_t base_g,
+                                                       const long long* step_ptr, uint64_t seed_u, uint64_t layer_u,
+                                                       long long lo, long long hi) {
+  __shared__ float s_fac[64];
+  for (int b = threadIdx.x; b < B && b < 64; b += blockDim.x) s_fac[b] = fac[b];
+  __syncthreads();
+  if (kMode != 2 && step_ptr) {
+    base = absorb3(seed_u, layer_u, static_cast<uint64_t>(*step_ptr));
+    base_g = base + kGamma;
+  }
+  float4* o4 = reinterpret_cast<float4*>(out);
+  const float4* g4 = reinterpret_cast<const float4*>(G);
+  const long long n4 = n >> 2;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 a = accumulate ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int b = 0; b < B; ++b) {
+      const float f = b < 64 ? s_fac[b] : fac[b];
+      const float4 g = __ldcs(g4 + static_cast<long long>(b) * n4 + i);
+      a.x = __fmaf_rn(f, g.x, a.x);
+      a.y = __fmaf_rn(f, g.y, a.y);
+      a.z = __fmaf_rn(f, g.z, a.z);
+      a.w = __fmaf_rn(f, g.w, a.w);
+    }
+    if constexpr (kMode == 1) {
+      const float4 z = philox_normal4(base, static_cast<uint64_t>(i));
+      a.x = __fmaf_rn(scale, z.x, a.x);
+      a.y = __fmaf_rn(scale, z.y, a.y);
+      a.z = __fmaf_rn(scale, z.z, a.z);
+      a.w = __fmaf_rn(scale, z.w, a.w);
+    } else if constexpr (kMode == 0) {
+      const long long e = i << 2;
+      if (e + 3 >= lo && e < hi) {
+        const float4 z = impl == 2 ? philox_normal4(base, static_cast<uint64_t>(i))
+                                   : noise_draw4(impl, base_g, base, static_cast<uint64_t>(i));
+        if (e + 0 >= lo && e + 0 < hi) a.x = __fmaf_rn(scale, z.x, a.x);
+        if (e + 1 >= lo && e + 1 < hi) a.y = __fmaf_rn(scale, z.y, a.y);
+        if (e + 2 >= lo && e + 2 < hi) a.z = __fmaf_rn(scale, z.z, a.z);
+        if (e + 3 >= lo && e + 3 < hi) a.w = __fmaf_rn(scale, z.w, a.w);
+      }
+    }
+    __stcs(o4 + i, a);
+  }
+}
+
+cudaError_t spill_combine(float* out, const float* G, int B, long long n, const float* fac, int accumulate,
+                          int add_noise, int impl, float scale, uint64_t base, uint64_t base_g,
+                          const long long* step_ptr, uint64_t seed_u, uint64_t layer_u, long long lo, long long hi,
+                          cudaStream_t s) {
+  const int mode = !add_noise || hi <= lo ? 2 : (impl == 2 && lo <= 0 && hi >= n) ? 1 : 0;
+  long long blocks = (n / 4 + 255) / 256;
+  if (blocks > 148LL * 8) blocks = 148LL * 8;
+  if (blocks < 1) blocks = 1;
+  auto k = mode == 1 ? k_spill_combine<1> : mode == 0 ? k_spill_combine<0> : k_spill_combine<2>;
+  k<<<static_cast<int>(blocks), 256, 0, s>>>(out, G, B, n, fac, accumulate, impl, scale, base, base_g, step_ptr, seed_u,
+                                             layer_u, lo, hi);
+  return cudaGetLastError();
+}
+
 cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s) {
   return single_sample_finalize(j.g, j.n, j.part, j.n_parts, j.clip_c, j.clip_c2, j.inv_batch, j.norms_out,
                                 j.add_noise, j.impl, j.scale, j.base, j.base_g, j.step_ptr, j.seed_u, j.layer_u, j.lo,

@@ -170,6 +170,11 @@ def device_ledger(kind: str, path: str, norm_phase: str, launches: int, B: int, 
         return TrafficReport(bytes_loaded=inputs + gw + acc_read, bytes_stored=2 * gw + B * out_width,
                              flops=grad_flops + 2 * D * P + emit, barriers=launches - 1, kernel_launches=launches,
                              peak_scratch_bytes=n_tiles * 4)
+    if kind == "flashdp" and path == "two_phase" and norm_phase == "spill":
+        g = B * D * P * out_width  # per-sample gradients written once, read once by the combine pass
+        return TrafficReport(bytes_loaded=inputs + g + acc_read, bytes_stored=g + gw + B * out_width,
+                             flops=grad_flops + 2 * B * D * P + emit, barriers=launches - 1,
+                             kernel_launches=launches, per_sample_grad_bytes_stored=g, peak_scratch_bytes=g)
     if kind == "flashdp" and path == "two_phase" and norm_phase == "ghost":
         ghost = B * T * T * (P + D)
         return TrafficReport(bytes_loaded=2 * inputs + acc_read, bytes_stored=gw + B * out_width,

@@ -214,3 +214,29 @@ def test_bench_workload_every_layer_against_oracle():
             per_sample_norms_sq = grp.norms[i]
 
         _check(R, want, wn)
+
+
+# ---------------------------------------------------------------- opt-in spill norm phase
+
+
+@pytest.mark.parametrize("B,P,D", [(2, 4096, 4096), (4, 5120, 13824), (2, 13824, 5120)])
+def test_llama_spill_norm_phase(B, P, D):
+    """norm_phase="spill" (opt-in): per-sample GEMMs to G[b] + one combine pass."""
+    _run_case(B, 2048, P, D, seed=60 + B, path="two_phase", norm_phase="spill")
+
+
+@pytest.mark.parametrize("noise_impl,rank,world", [("keyed_f32", 0, 1), ("keyed_f32", 1, 3), ("keyed_f64", 0, 2)])
+def test_spill_noise_partition_and_accumulate(noise_impl, rank, world):
+    B, T, P, D = 3, 512, 1024, 768
+    x, dy = _inputs(B, T, P, D, 70, [0.6, 1.0, 1.5])
+    C = float(np.sqrt(T * P * D))
+    cfg = fdp.DPConfig(C, 1e-3, "mean", seed=3, layer_id=4, step=1)
+    base = torch.randn(D, P, device="cuda")
+    got = base.clone()
+    fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase="spill", noise_impl=noise_impl, rank=rank,
+                         world=world, grad_out=got, accumulate=True)
+    ref = base.clone()
+    fdp.backward_flashdp(x, dy, cfg, path="two_phase", norm_phase="ghost", noise_impl=noise_impl, rank=rank,
+                         world=world, grad_out=ref, accumulate=True)
+    torch.cuda.synchronize()
+    assert float((got - ref).abs().max() / ref.abs().max()) < 1e-5
