@@ -369,8 +369,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     SegWalk w(cid, n_clusters, walk_B, n_wt);
     int wt, bb, be;
     while (w.next(wt, bb, be)) {
-      const bool whole = bb == 0 && be == p.B;
-      if (bb != 0 || !tile_prefilled(whole)) continue;
+      const bool whole = bb == 0 && be == walk_B;
+      if (spill || bb != 0 || !tile_prefilled(whole)) continue;  // spill units are whole, stored unscaled
       int tr, tc;
       tile_rc(wt, n_wt_real / p.n_pt, p.n_pt, p.swizzle, tr, tc);
       const int d0 = (tr * CL + crank) * kBM;
