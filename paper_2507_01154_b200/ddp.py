@@ -444,8 +444,6 @@ class GradBuckets:
         if self.world == 1 or os.environ.get("FDP_DDP_NOCOMM") == "1":  # debug: local gradients only
             return
         if self.comm is not None:
-            if os.environ.get("FDP_DDP_SYNC") == "1":  # debug: full device sync before the collective
-                torch.cuda.synchronize(self.device)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.device))
             self.comm.wait_event(ev)

@@ -210,3 +210,48 @@ def test_nccl_options_cap_ctas(monkeypatch):
         assert opts.config.max_ctas == 4
     with pytest.raises(ValueError):
         nccl_options(0)
+
+
+def _micro_worker(rank, world, port, out):
+    """Two micro-batches per step: buckets disabled on the first (gradients accumulate
+    into the bucket views, no collective), enabled on the last (one collective per
+    bucket for the sum of both micro-batches)."""
+    from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets, _torch_adam_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    model = _bucket_model()
+    g = torch.Generator().manual_seed(9)
+    x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+    bk = GradBuckets(model.parameters(), bucket_bytes=600, rank=rank, world=world, flat_params=True)
+    opt = BucketedAdam(bk, lr=1e-2, adam_fn=_torch_adam_)
+    per = 8 // world
+    for step in range(2):
+        bk.zero_grad()
+        for mb in range(2):  # micro-batches of this rank's samples
+            bk.enabled = mb == 1
+            lo = rank * per + mb * per // 2
+            hi = lo + per // 2
+            (((model(x[lo:hi]) - y[lo:hi]) ** 2).sum(1).sum() / 8).backward()
+        bk.finish()
+        opt.step(step)
+    out[(world, rank)] = ([p.detach().clone() for p in model.parameters()], list(bk.issued))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_grad_buckets_micro_batches_reduce_once():
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        _micro_worker(0, 1, _free_port(), out)
+        mp.spawn(_micro_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+        ref, issued1 = out[(1, 0)]
+        assert len(issued1) == len(set(issued1))  # each bucket issued once per step
+        for r in range(2):
+            got, issued = out[(2, r)]
+            assert issued == issued1
+            for a, b in zip(got, ref):
+                assert torch.allclose(a, b, rtol=1e-5, atol=1e-6)
