@@ -1,6 +1,6 @@
 """Interleaved A/B timing of native-layer variants on single layers (any path).
 
-    python tools/ab_layer.py "B,T,P,D[;B,T,P,D...]" VAR1 VAR2 ...   (VAR as in tools/ab.py)
+    [AB_PATH=fused|two_phase] python tools/ab_layer.py "B,T,P,D[;B,T,P,D...]" VAR1 VAR2 ...   (VAR as in tools/ab.py)
 
 Round-robin over variants with an idle gap before each measurement (same thermal
 start); prints min / median per (shape, variant) as JSON lines.
@@ -51,7 +51,8 @@ def main():
             os.environ.clear()
             os.environ.update(base_env)
             os.environ.update(parse(v))
-            calls[v] = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox")
+            calls[v] = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
+                                            path=os.environ.get("AB_PATH", "auto"))
         res = {v: [] for v in variants}
         for _ in range(ROUNDS):
             for v in variants:
