@@ -617,7 +617,6 @@ fdp::TcParams tc_params(const fdp_desc* d, const Plan& pl, const Common& c, floa
   p.skip_barrier = (d->flags & FDP_FLAG_SKIP_BARRIER) ? 1 : 0;
   p.deterministic = (d->flags & FDP_FLAG_DETERMINISTIC) ? 1 : 0;
   p.poll_ns = env_int("FDP_POLL_NS", 0);
-  p.pipe = env_int("FDP_FUSED_PIPE", 1);
   // epilogue-drawn noise for the reweight pass (see stream_params)
   p.epi_noise = (d->noise_impl == FDP_NOISE_PHILOX && env_int("FDP_EPI_NOISE", 1)) ? 1 : 0;
   p.pub_mode = env_int("FDP_PUB_MODE", 1);
@@ -1378,7 +1377,6 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   gp.poll_mode = env_int("FDP_POLL_MODE", 0);
   gp.pf_ahead = env_int("FDP_PF_AHEAD", 0);
   gp.pair_dsmem = env_int("FDP_PAIR_DSMEM", 0);
-  gp.pipe = env_int("FDP_GROUP_PIPE", 0);
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

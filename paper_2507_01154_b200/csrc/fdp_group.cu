@@ -317,15 +317,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
 
       bool first = true;
-      auto next_ready = [&]() -> uint32_t {
+      for (int b = group; b < L.B; b += L.groups) {
         mbar_wait(&tfull[rbuf], rph, err, gp.budget_ns, 0x404);
         tc_fence_after();
-        const uint32_t bx = rbuf;
+        const uint32_t buf = rbuf;
         if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
-        return bx;
-      };
-      // block-wise all-reduce of sample b: fixed-order fp64 sum of the tagged partials
-      auto wait_factor_g = [&](int b) -> float {
+        pass1_publish(L, b, tile, buf);
+        if (first && l < 16) GTRACE(8 * l);  // layer l: first sample published
+        first = false;
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
+        // block-wise all-reduce: fixed-order fp64 sum of the tagged partials
         if (ew == 0) {
           const unsigned long long* slots = L.tagged + static_cast<long long>(b) * L.n_tiles;
           const int n_slots = gp.pair_dsmem ? L.n_tiles / CG : L.n_tiles;  // per pair tile (DSMEM) or CTA tile
@@ -360,11 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
           }
         }
         named_bar_sync(1, 32 * kEpiWarps);
-        return *bcast;
-      };
-      // clip + accumulate sample b's tile from TMEM buffer bx, then free the buffer
-      auto accumulate_release = [&](uint32_t bx, float f) {
-        const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bx * BN + col0;
+        const float f = *bcast;
 #pragma unroll
         for (int c = 0; c < C::kCPT / 16; ++c) {
           float v[16];
@@ -376,34 +373,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_leader(&tempty[bx]);
-          else mbar_arrive(&tempty[bx]);
-        }
-      };
-      if (gp.pipe && group + L.groups < L.B) {
-        // depth-2 pipeline (see fdp_tc.cu MODE_FUSED): sample b+groups is read and
-        // published while sample b's all-reduce is in flight
-        uint32_t b_cur = next_ready();
-        pass1_publish(L, group, tile, b_cur);
-        if (l < 16) GTRACE(8 * l);  // layer l: first sample published
-        for (int b = group; b < L.B; b += L.groups) {
-          uint32_t b_next = 0;
-          if (b + L.groups < L.B) {
-            b_next = next_ready();
-            pass1_publish(L, b + L.groups, tile, b_next);
-          }
-          const float f = wait_factor_g(b);
-          accumulate_release(b_cur, f);
-          b_cur = b_next;
-        }
-      } else {
-        for (int b = group; b < L.B; b += L.groups) {
-          const uint32_t buf = next_ready();
-          pass1_publish(L, b, tile, buf);
-          if (first && l < 16) GTRACE(8 * l);  // layer l: first sample published
-          first = false;
-          const float f = wait_factor_g(b);
-          accumulate_release(buf, f);
+          if constexpr (CG == 2) mbar_arrive_leader(&tempty[buf]);
+          else mbar_arrive(&tempty[buf]);
         }
       }
 

@@ -59,7 +59,6 @@ struct TcParams {
   // 0 = st.relaxed, 2 = st.release) and poll with ld.relaxed (0) / volatile (1) / acquire (2)
   int pub_mode, poll_mode;
   int poll_ns;  // back-off between polls of the norm partials (FDP_POLL_NS, default 0: spin)
-  int pipe;     // MODE_FUSED: depth-2 pipelined epilogue over the TMEM buffers (FDP_FUSED_PIPE, default 1)
   unsigned long long budget_ns;
   unsigned long long* trace;  // [grid][128] phase timestamps or nullptr
 };
@@ -162,7 +161,6 @@ struct GroupParams {
   // epilogue has started layer l - pf_ahead (FDP_PF_AHEAD; < 0 = unbounded)
   int pf_ahead;
   int pair_dsmem;  // CTA-pair norm partials combined in DSMEM before publishing (FDP_PAIR_DSMEM; default off)
-  int pipe;        // depth-2 pipelined epilogue over the TMEM buffers (FDP_GROUP_PIPE)
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
 

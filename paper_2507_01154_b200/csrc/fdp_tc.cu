@@ -434,40 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       };
 
       FDP_TRACE(0);
-      if (p.mode == MODE_FUSED && p.pipe && n_units > 1) {
-        // Depth-2 pipeline over the NBUF >= 2 TMEM buffers: unit u+1's pass 1 and
-        // publish run while unit u's block-wise all-reduce is in flight, then u is
-        // clipped, accumulated and its buffer released. The per-unit chain (TMEM
-        // pass 1 -> block reduce -> publish -> poll of every CTA's partial -> factor
-        // -> pass 2) is ~2.4 us at T = 128 against ~0.55 us of MMA (phase traces);
-        // overlapping two units' chains hides the all-reduce latency behind the
-        // next unit's TMEM reads. Same arithmetic and order per unit: bitwise
-        // equal to the unpipelined loop.
-        uint32_t b_cur = wait_ready();
-        FDP_TRACE(9);
-        trace_u = 0;
-        publish(b0, b_cur);
-        FDP_TRACE(8);
-        for (int u = 0; u < n_units; ++u) {
-          const int ub = b0 + u * b_step;
-          uint32_t b_next = 0;
-          if (u + 1 < n_units) {
-            b_next = wait_ready();
-            if (u + 1 < 16) FDP_TRACE(9 + 4 * (u + 1));
-            trace_u = u + 1 < 16 ? u + 1 : -1;
-            publish(ub + b_step, b_next);
-            if (u + 1 < 16) FDP_TRACE(8 + 4 * (u + 1));
-          }
-          trace_u = u < 16 ? u : -1;
-          const float f = wait_factor(ub);
-          FDP_TRACE(10 + 4 * u);
-          accumulate_scaled(b_cur, f);
-          if (trace_u >= 0) FDP_TRACE(66 + 4 * trace_u);  // pass 2 done
-          trace_u = -1;
-          release(b_cur);
-          b_cur = b_next;
-        }
-      } else if (p.mode == MODE_FUSED) {
+      if (p.mode == MODE_FUSED) {
         // per sample: publish the norm partial, draw a noise chunk while the
         // block-wise all-reduce is in flight, clip + accumulate, free the TMEM
         // buffer (the MMA of the next samples proceeds meanwhile)
