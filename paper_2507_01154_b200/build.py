@@ -26,7 +26,7 @@ HEADERS = ["fdp_internal.h", "fdp_ptx.cuh", "fdp_rng.cuh", "fdp_prefill.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
+         "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"] + os.environ.get("FDP_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:

@@ -560,7 +560,48 @@ fdp::StreamParams stream_params(const fdp_desc* d, const Plan& pl, const Common&
   p.mc = pl.stream_mc;
   p.fin_epi = env_int("FDP_FIN_EPI", 1);
   p.swizzle = env_int("FDP_STREAM_SWIZZLE", d->P >= 2 * d->D ? 8 : 0);
+  p.dbg = env_int("FDP_DEBUG_STREAM", 0);
+  if (env_int("FDP_STREAM_TRACE", 0)) {  // timing experiments: per-CTA wait totals (synchronous report)
+    static unsigned long long* buf[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!buf[dev & 63] && cudaMalloc(&buf[dev & 63], 1024 * 8 * sizeof(unsigned long long)) != cudaSuccess)
+      buf[dev & 63] = nullptr;
+    p.trace = buf[dev & 63];
+  }
   return p;
+}
+
+// FDP_STREAM_TRACE: mean / max over CTAs of each wait total, one JSON line on stderr
+void stream_trace_report(const fdp::StreamParams& q, const char* what, int grid, cudaStream_t s) {
+  if (!q.trace || grid > 1024) return;
+  std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
+  cudaStreamSynchronize(s);
+  cudaMemcpy(h.data(), q.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  static const char* names[8] = {"prod_wait_empty", "mma_wait_tempty", "mma_wait_full", "epi_wait_tfull",
+                                 "epi_wait_prefill", "epi_store", "epi_end", "cta_end"};
+  std::fprintf(stderr, "{\"stream_trace\": \"%s\", \"grid\": %d", what, grid);
+  for (int k = 0; k < 8; ++k) {
+    double sum = 0.0, mx = 0.0;
+    for (int b = 0; b < grid; ++b) {
+      const double v = static_cast<double>(h[static_cast<size_t>(b) * 8 + k]) * 1e-3;
+      sum += v;
+      mx = v > mx ? v : mx;
+    }
+    std::fprintf(stderr, ", \"%s_us\": [%.2f, %.2f]", names[k], sum / grid, mx);
+  }
+  if (env_int("FDP_STREAM_TRACE", 0) > 1) {  // every CTA's row
+    std::fprintf(stderr, ", \"ctas\": [");
+    for (int b = 0; b < grid; ++b) {
+      std::fprintf(stderr, "%s[", b ? ", " : "");
+      for (int k = 0; k < 8; ++k)
+        std::fprintf(stderr, "%s%.1f", k ? ", " : "", static_cast<double>(h[static_cast<size_t>(b) * 8 + k]) * 1e-3);
+      std::fprintf(stderr, "]");
+    }
+    std::fprintf(stderr, "]");
+  }
+  std::fprintf(stderr, "}\n");
+  cudaMemset(q.trace, 0, h.size() * sizeof(unsigned long long));
 }
 
 // Grid of the stream-K kernel: every co-resident cluster, capped by the unit count.
@@ -859,6 +900,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       q.fin = carry;
       if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
         return cuda_fail(e, "stream-K nondp launch");
+      stream_trace_report(q, "nondp", stream_grid(d, pl, di), s);
       return FDP_OK;
     }
     fdp::TcParams p = tc_params(d, pl, c, grad_w, nullptr, ws, fdp::MODE_NONDP);
@@ -1006,6 +1048,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       q.fin = carry;
       if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
         return cuda_fail(e, "stream-K reweight launch");
+      stream_trace_report(q, "reweight", stream_grid(d, pl, di), s);
     } else {
       fdp::TcParams q = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_REWEIGHT);
       if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, q, pl.grid, false, s)) != cudaSuccess)

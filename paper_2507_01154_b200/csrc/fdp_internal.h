@@ -120,6 +120,8 @@ struct StreamParams {
   // squares in norm_part[(b * n_wtiles + wt) * CG * MC + crank]; p.B is the real batch
   int spill;
   int swizzle;  // tile raster: 0/1 row-major, G > 1 grouped by G row blocks (FDP_STREAM_SWIZZLE)
+  int dbg;      // timing experiments only (FDP_DEBUG_STREAM): 1 skip the TMEM readout, 2 skip the MMAs
+  unsigned long long* trace;  // FDP_STREAM_TRACE: per-CTA wait-time totals [gridDim.x][8] (ns), or null
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {

@@ -45,18 +45,39 @@ struct SCfg {
 // tiles in wave order (tile w*K + c), so the clusters of a wave work on
 // neighbouring tiles whose operand rows share L2; the units of the remaining
 // R = n_wtiles mod K tiles (tile-major, R*B of them) are split evenly, cluster c
-// taking [R B c / K, R B (c+1) / K).
+// taking [R B c / K, R B (c+1) / K). The tail range is walked from its END, and
+// its last segment -- the tile the cluster opens (samples from 0) -- goes before
+// the waves: a split tile's opening segment is finished (its rows initialised)
+// long before the clusters continuing it reach their stores, which come last.
 struct SegWalk {
   int cid, K, B, waves, w;
+  int phase;  // 0: the tail's opening segment (if any), 1: the waves, 2: the rest of the tail
   long long u, hi, tail0;
-  __device__ __forceinline__ SegWalk(int cid_, int K_, int B_, int n_wtiles) : cid(cid_), K(K_), B(B_), w(0) {
+  __device__ __forceinline__ SegWalk(int cid_, int K_, int B_, int n_wtiles)
+      : cid(cid_), K(K_), B(B_), w(0), phase(0) {
     waves = n_wtiles / K_;
     tail0 = static_cast<long long>(waves) * K_;
     const long long tail_units = (static_cast<long long>(n_wtiles) - tail0) * B_;
     u = tail_units * cid_ / K_;
     hi = tail_units * (cid_ + 1) / K_;
   }
+  // the last segment of the remaining tail range [u, hi)
+  __device__ __forceinline__ void tail_seg(int& wt, int& bb, int& be) {
+    const long long t0 = ((hi - 1) / B) * B;  // first unit of the tile holding the range's last unit
+    const long long s0 = t0 > u ? t0 : u;
+    wt = static_cast<int>(tail0 + (hi - 1) / B);
+    bb = static_cast<int>(s0 - t0);
+    be = static_cast<int>(hi - t0);
+    hi = s0;
+  }
   __device__ __forceinline__ bool next(int& wt, int& bb, int& be) {
+    if (phase == 0) {  // the tile this cluster opens goes first: its rows are published early
+      phase = 1;
+      if (u < hi && ((hi - 1) / B) * B >= u) {
+        tail_seg(wt, bb, be);
+        return true;
+      }
+    }
     if (w < waves) {
       wt = w * K + cid;
       bb = 0;
@@ -65,11 +86,7 @@ struct SegWalk {
       return true;
     }
     if (u >= hi) return false;
-    wt = static_cast<int>(tail0 + u / B);
-    bb = static_cast<int>(u % B);
-    const long long left = hi - u;
-    be = left < static_cast<long long>(B - bb) ? bb + static_cast<int>(left) : B;
-    u += be - bb;
+    tail_seg(wt, bb, be);
     return true;
   }
 };
@@ -197,6 +214,20 @@ __device__ __forceinline__ void tile_rc(int wt, int n_rows, int n_pt, int swz, i
 // loaded once and multicast to the CTA of both pairs that needs it, so L2 serves
 // 3/4 of the operand bytes of two independent pairs. A stage is refilled only
 // after BOTH pairs' MMAs released it (every commit arrives in all four CTAs).
+// wait-time accounting of one role's thread (FDP_STREAM_TRACE; timing experiments only)
+struct WaitClock {
+  unsigned long long* slot;
+  unsigned long long acc = 0;
+  __device__ __forceinline__ explicit WaitClock(unsigned long long* s) : slot(s) {}
+  __device__ __forceinline__ uint64_t start() const { return slot ? globaltimer_ns() : 0; }
+  __device__ __forceinline__ void stop(uint64_t t0) {
+    if (slot) acc += globaltimer_ns() - t0;
+  }
+  __device__ __forceinline__ void flush() const {
+    if (slot) *slot = acc;
+  }
+};
+
 template <int BN, int CG, int MC, bool FIN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     dpdw_stream_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_x,
@@ -234,6 +265,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int n_wt = spill ? n_wt_real * p.B : n_wt_real;
   const int walk_B = spill ? 1 : p.B;
   const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << (CG * pi));
+#ifdef FDP_STREAM_TRACE_ON  // timing experiments (build with -DFDP_STREAM_TRACE_ON, run with FDP_STREAM_TRACE=1)
+  unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+#else
+  constexpr unsigned long long* trace = nullptr;
+#endif
+  const uint64_t t_start = trace ? globaltimer_ns() : 0;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -261,17 +298,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  // noise of a whole tile drawn into the accumulator (Philox) instead of pre-filled
+  // Philox noise drawn into the accumulator of a tile's first segment (the whole tile,
+  // or the split tile's first samples) by the 256 epilogue threads, instead of a
+  // pre-fill by the two noise warps that every later segment of the tile waits for
   const bool epi_noise = p.add_noise && p.epi_noise && p.noise_impl == 2;
-  // does tile (split or whole) get its rows initialised by a pre-fill?
+  // epi_init: the noise, if any, is drawn by the epilogue. A split tile then needs no
+  // pre-fill: when accumulating every segment reduce-adds; otherwise the tile's
+  // opening segment (samples from 0) stores plainly and publishes the rows through
+  // the tile counter, and the continuing segments reduce-add after it.
+  const bool epi_init = !p.add_noise || epi_noise;
+  // does tile (split or whole) get its rows initialised by a noise-warp pre-fill?
   auto tile_prefilled = [&](bool whole) {
-    return whole ? (p.add_noise && !epi_noise) : (!p.accumulate || p.add_noise);
+    return whole ? (p.add_noise && !epi_noise) : (!epi_init && (!p.accumulate || p.add_noise));
   };
 
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      WaitClock wc(trace ? trace + 0 : nullptr);
       SegWalk w(cid, n_clusters, walk_B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
@@ -287,7 +332,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int p0 = tc * BN + rank * C::kBCols;
         for (int b = bb; b < be; ++b) {
           for (int kb = 0; kb < p.n_kb; ++kb) {
+            const uint64_t tw = wc.start();
             mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x501);
+            wc.stop(tw);
             uint8_t* sa = smem + stage * C::kStageBytes;
             uint8_t* sb = sa + C::kABytes;
             if constexpr (MC == 2) {  // own dY rows; X box `pi` multicast to this rank's CTA of both pairs
@@ -315,23 +362,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
+      wc.flush();
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (leader CTA) =======================
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      WaitClock wt_e(trace ? trace + 1 : nullptr), wt_f(trace ? trace + 2 : nullptr);
       SegWalk w(cid, n_clusters, walk_B, n_wt);
       int wt, bb, be;
       while (w.next(wt, bb, be)) {
         for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
           const int ue = per_unit ? ub + 1 : be;
+          const uint64_t t0 = wt_e.start();
           mbar_wait(&tempty[buf], tphase ^ 1, err, p.budget_ns, 0x502);
+          wt_e.stop(t0);
           tc_fence_after();
           const uint32_t dtm = tmem_base + buf * BN;
           uint32_t accum = 0;
           for (int b = ub; b < ue; ++b) {
             for (int kb = 0; kb < p.n_kb; ++kb) {
+              const uint64_t t1 = wt_f.start();
               mbar_wait(&full[stage], phase, err, p.budget_ns, 0x503);
+              wt_f.stop(t1);
               tc_fence_after();
               const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
               const uint32_t b_base = a_base + C::kABytes;
@@ -339,6 +392,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               for (int k = 0; k < kBK / 16; ++k) {
                 const uint64_t ad = make_sdesc_sw128(a_base + k * 2048, 8192, 1024);
                 const uint64_t bd = make_sdesc_sw128(b_base + k * 2048, 8192, 1024);
+                if (p.dbg & 2) continue;
                 if constexpr (CG == 2) tc_mma_f16_pair(dtm, ad, bd, C::kIdesc, accum);
                 else tc_mma_f16(dtm, ad, bd, C::kIdesc, accum);
                 accum = 1;
@@ -355,6 +409,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (++buf == C::kNBuf) { buf = 0; tphase ^= 1; }
         }
       }
+      wt_e.flush();
+      wt_f.flush();
     }
   } else if (warp == 2 || warp == 3) {
     // ======================= noise warps: initialise the rows of tiles this cluster opens =======================
@@ -375,7 +431,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tile_rc(wt, n_wt_real / p.n_pt, p.n_pt, p.swizzle, tr, tc);
       const int d0 = (tr * CL + crank) * kBM;
       const int p0 = tc * BN;
-      prefill_rows<BN>(p.grad_w, p.D, p.P, d0, d0 + kBM, p0, p.accumulate != 0, p.add_noise != 0, p.noise_impl,
+      prefill_rows<BN>(p.grad_w, p.D, p.P, d0, d0 + kBM, p0, p.accumulate != 0, p.add_noise && !epi_noise, p.noise_impl,
                        kbg, kb, p.noise_scale, p.noise_lo, p.noise_hi, ntid);
       __threadfence();
       named_bar_sync(3, 64);
@@ -406,6 +462,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t nkb = p.key_base;
     if (epi_noise && p.step_ptr) nkb = absorb3(p.seed_u, p.layer_u, static_cast<uint64_t>(*p.step_ptr));
     uint32_t rbuf = 0, rph = 0;
+    WaitClock wc_t(trace && etid == 0 ? trace + 3 : nullptr), wc_c(trace && etid == 0 ? trace + 4 : nullptr),
+        wc_s(trace && etid == 0 ? trace + 5 : nullptr);
     bool fin_left = fin_on && p.fin_epi;
     SegWalk w(cid, n_clusters, walk_B, n_wt);
     int wt, bb, be;
@@ -430,14 +488,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float acc[C::kCPT];
 #pragma unroll
       for (int i = 0; i < C::kCPT; ++i) acc[i] = 0.0f;
-      if (epi_noise && whole) {  // the tile's Philox noise starts the accumulator (rank slice only)
+      if (epi_noise) {
+        // the tile's Philox noise starts the accumulators (rank slice only), split over the
+        // tile's segments by column quads in proportion to their samples: every quad is
+        // drawn once, and the drawing is spread like the units (a split tile's first
+        // cluster no longer draws the whole tile while the others wait)
+        const int q_lo = (C::kCPT / 4) * bb / walk_B, q_hi = (C::kCPT / 4) * be / walk_B;
         const long long frow = static_cast<long long>(d0 + row) * p.P;
         const bool row_ok = d0 + row < p.D;
 #pragma unroll
         for (int q4 = 0; q4 < C::kCPT / 4; ++q4) {
           const int col = p0 + col0 + 4 * q4;
           const long long f = frow + col;
-          if (row_ok && col < p.P && f + 3 >= p.noise_lo && f < p.noise_hi) {  // P % 8 == 0: quads stay in a row
+          if (q4 >= q_lo && q4 < q_hi && row_ok && col < p.P && f + 3 >= p.noise_lo &&
+              f < p.noise_hi) {  // P % 8 == 0: quads stay in a row
             const float4 n = philox_normal4(nkb, static_cast<uint64_t>(f >> 2));
             acc[4 * q4 + 0] = (f + 0 >= p.noise_lo && f + 0 < p.noise_hi) ? p.noise_scale * n.x : 0.0f;
             acc[4 * q4 + 1] = (f + 1 >= p.noise_lo && f + 1 < p.noise_hi) ? p.noise_scale * n.y : 0.0f;
@@ -446,20 +510,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
+      // the next unit's clip factor is loaded one unit ahead: its L2 latency overlaps
+      // this unit's TMEM readout instead of sitting between the buffer wait and the FMAs
+      float f_next = per_unit ? __ldg(p.factors_in + bb) : 1.0f;
       for (int ub = bb; ub < be; ub += per_unit ? 1 : (be - bb)) {
+        const float f = f_next;
+        if (per_unit && ub + 1 < be) f_next = __ldg(p.factors_in + ub + 1);
+        const uint64_t tw = wc_t.start();
         mbar_wait(&tfull[rbuf], rph, err, p.budget_ns, 0x504);
+        wc_t.stop(tw);
         tc_fence_after();
         const uint32_t buf = rbuf;
         if (++rbuf == C::kNBuf) { rbuf = 0; rph ^= 1; }
-        const float f = per_unit ? p.factors_in[ub] : 1.0f;
         const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + col0;
+        if (p.dbg & 1) {
+        } else if constexpr (C::kCPT <= 64) {  // 128-column tiles: registers allow 32 columns per TMEM round trip
 #pragma unroll
-        for (int c = 0; c < C::kCPT / 16; ++c) {
-          float v[16];
-          tmem_ld16(tb + c * 16, v);
-          tmem_wait_ld();
+          for (int c = 0; c < C::kCPT / 32; ++c) {
+            float v[32];
+            tmem_ld32(tb + c * 32, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+            for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fmaf(f, v[i], acc[c * 32 + i]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < C::kCPT / 16; ++c) {
+            float v[16];
+            tmem_ld16(tb + c * 16, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -485,14 +567,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       // ---- finalize: reduce-add onto initialised rows (split tiles, accumulation,
       // pre-filled noise) or plain store; 32-column boxes, double-buffered
-      const bool rmw = !whole || p.accumulate || (p.add_noise && !epi_noise);
-      if (tile_prefilled(whole) && etid == 0) {
+      const bool split_init = epi_init && !whole && !p.accumulate && !spill;  // opening store / continuations
+      const bool opening = split_init && bb == 0;
+      const bool rmw = !opening && (!whole || p.accumulate || (p.add_noise && !epi_noise));
+      if ((tile_prefilled(whole) || (split_init && bb != 0)) && etid == 0) {
         const uint64_t t0 = globaltimer_ns();
         while (ld_acquire_u32(&p.tile_cnt[tile]) < 1u) {
           if (globaltimer_ns() - t0 > p.budget_ns) watchdog_trap(err, 0x505);
           __nanosleep(64);
         }
+        if (trace) wc_c.acc += globaltimer_ns() - t0;
       }
+      const uint64_t ts = wc_s.start();
 #pragma unroll
       for (int c = 0; c < C::kCPT / 32; ++c) {
         uint8_t* sbuf = stg + (c & 1) * (2 * kBM * 128);
@@ -518,10 +604,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           bulk_commit();
         }
       }
+      if (opening && etid == 0) {  // the rows are initialised once this segment's stores have landed
+        bulk_wait_all();
+        fence_proxy_async_global();
+        __threadfence();
+        red_release_add_u32(&p.tile_cnt[tile], 1u);
+      }
+      wc_s.stop(ts);
     }
     while (fin_left && fin_chunk(p.fin, fin_sh, lane)) {
     }
     if (etid == 0) bulk_wait_all();
+    wc_t.flush();
+    wc_c.flush();
+    wc_s.flush();
+    if (trace && etid == 0) trace[6] = globaltimer_ns() - t_start;  // the epilogue's last store drained
   }
 
   tc_fence_before();
@@ -532,6 +629,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if constexpr (CG == 2) tmem_dealloc_pair<512>(tmem_base);
     else tmem_dealloc<512>(tmem_base);
   }
+  if (trace && threadIdx.x == 0) trace[7] = globaltimer_ns() - t_start;
   if (threadIdx.x == 0) {  // last CTA out re-arms the tile counters
     __threadfence();
     const unsigned old = atomicAdd(&p.ctrl[0], 1u);

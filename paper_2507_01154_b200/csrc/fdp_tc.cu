@@ -453,10 +453,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           release(b);
         }
       } else if (p.mode == MODE_REWEIGHT) {
-        int u = 0;
-        for (int ub = b0; ub < p.B; ub += b_step, ++u) {
+        float f_next = b0 < p.B ? __ldg(p.factors_in + b0) : 0.0f;  // one unit ahead (L2 latency off the path)
+        for (int ub = b0; ub < p.B; ub += b_step) {
+          const float f = f_next;
+          if (ub + b_step < p.B) f_next = __ldg(p.factors_in + ub + b_step);
           const uint32_t b = wait_ready();
-          accumulate_scaled(b, p.factors_in[ub]);
+          accumulate_scaled(b, f);
           release(b);
         }
       } else if (p.mode == MODE_NORMS) {
