@@ -334,8 +334,12 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
         while (g & (g - 1)) --g;  // 1, 2, 4 or 8: slices of 128 rows stay whole 8-row swizzle atoms
         const double units = static_cast<double>((d->B + g - 1) / g);
         const double unit_flops = 2.0 * fdp::kBM * bn * static_cast<double>(d->T);
-        // a sample is never faster than one block-wise all-reduce round (~2.5 us)
-        const double unit_t = std::max(unit_flops / sm_rate(bn, cg), 2.5e-6);
+        // a sample unit: its MMA or the two TMEM passes over its accumulator (norm, clip;
+        // ~160 GB/s per SM), whichever is longer, plus one block-wise all-reduce round
+        // (calibrated on B200: 1024^2 / 2048^2 at B=64, T=128; 2048^2 at B=32, T=256;
+        // GPT-2 c_fc at B=8, T=1024 -- tools/nondp_cmp.py)
+        const double read_t = 2.0 * fdp::kBM * bn * 4.0 / 160e9;
+        const double unit_t = std::max(unit_flops / sm_rate(bn, cg), read_t) + 1.2e-6;
         const double est = units * unit_t + (g > 1 ? 4e-6 : 0.0) + 8e-6;
         if (est < best * 0.97) {
           best = est;
@@ -353,7 +357,7 @@ int make_plan(const fdp_desc* d, int32_t kind, const DevInfo& di, Plan& pl) {
                                     ? 0.0
                                     : std::min(ghost_flops, dw_flops);
       const double two_phase_est = (norm_flops / 0.55e15) + dw_flops / 1.1e15 + 25e-6;
-      if (best_bn && want == FDP_PATH_AUTO && two_phase_est < 0.8 * best) best_bn = 0;
+      if (best_bn && want == FDP_PATH_AUTO && two_phase_est < best) best_bn = 0;
       if (best_bn && want != FDP_PATH_TWO_PHASE) {
         pl.path = FDP_PATH_FUSED;
         pl.bn = best_bn;

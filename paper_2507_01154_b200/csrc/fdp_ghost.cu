@@ -118,15 +118,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int wi = blockIdx.x; wi < p.n_items; wi += gridDim.x) {
         const GItem it = decode_split(wi, p, nkx, nky);
         const int i = it.i, j = it.j, b = it.b;
-        for (int k = 0; k < it.nx + it.ny; ++k) {
+        // diagonal tiles (A == B) carry two k-blocks per stage: twice the bytes in flight
+        for (int k = 0; k < it.nx + it.ny;) {
           const bool isx = k < it.nx;
           const CUtensorMap* m = isx ? &tm_x : &tm_dy;
+          const int end = isx ? it.nx : it.nx + it.ny;
+          const int cnt = (i == j && k + 1 < end) ? 2 : 1;
           const int kk = (isx ? it.kx0 + k : it.ky0 + k - it.nx) * kBK;
           mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x301);
           uint8_t* sa = smem + stage * kGStageBytes;
-          mbar_arrive_expect_tx(&full[stage], i == j ? kGTileBytes : kGStageBytes);
+          mbar_arrive_expect_tx(&full[stage], (i == j ? cnt : 2) * kGTileBytes);
           tma_load_3d(sa, m, &full[stage], kk, i * kGT, b);
           if (i != j) tma_load_3d(sa + kGTileBytes, m, &full[stage], kk, j * kGT, b);
+          else if (cnt == 2) tma_load_3d(sa + kGTileBytes, m, &full[stage], kk + kBK, i * kGT, b);
+          k += cnt;
           if (++stage == kGStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -139,18 +144,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int i = it.i, j = it.j;
         mbar_wait(&tempty[buf], tphase ^ 1, err, p.budget_ns, 0x302);
         tc_fence_after();
-        for (int k = 0; k < it.nx + it.ny; ++k) {
+        for (int k = 0; k < it.nx + it.ny;) {
           const bool isx = k < it.nx;
+          const int end = isx ? it.nx : it.nx + it.ny;
+          const int cnt = (i == j && k + 1 < end) ? 2 : 1;
           const uint32_t dtm = tmem_base + buf * 256 + (isx ? 0 : 128);
           mbar_wait(&full[stage], phase, err, p.budget_ns, 0x303);
           tc_fence_after();
-          const uint32_t a = smem_u32(smem + stage * kGStageBytes);
-          const uint32_t bb = (i == j) ? a : a + kGTileBytes;
+          const uint32_t base = smem_u32(smem + stage * kGStageBytes);
+          for (int h = 0; h < cnt; ++h) {
+            const uint32_t a = base + h * kGTileBytes;
+            const uint32_t bb = (i == j) ? a : a + kGTileBytes;
 #pragma unroll
-          for (int kq = 0; kq < kBK / 16; ++kq)
-            tc_mma_f16(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kGIdesc,
-                       (k == 0 || k == it.nx) && kq == 0 ? 0u : 1u);
+            for (int kq = 0; kq < kBK / 16; ++kq)
+              tc_mma_f16(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kGIdesc,
+                         (k == 0 || k == it.nx) && h == 0 && kq == 0 ? 0u : 1u);
+          }
           tc_commit(&empty[stage]);
+          k += cnt;
           if (++stage == kGStages) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[buf]);
