@@ -211,6 +211,19 @@ FDP_API int fdp_dw_chained(const fdp_desc* d, const void* x, const void* dy, flo
 FDP_API int fdp_backward_chained(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w,
                                  float* norms_sq, void* ws, size_t ws_bytes, fdp_chain* chain, void* stream);
 
+/* DP backward of n (1..3) layers that read the SAME input X (B, T, P) -- the q/k/v
+ * projections of an attention block, gate/up of a SwiGLU MLP -- each with its own
+ * dY_l (B, T, D_l), DPConfig, clip C_l and outputs. Per-layer clipping is unchanged
+ * (||G_l||^2 = <X X^T, dY_l dY_l^T>); when every layer takes the two-phase path with
+ * ghost norms, ONE Gram launch computes each X X^T tile once for all layers and the
+ * dY Grams of each, then every layer runs its factor reduce and reweighted pass.
+ * Otherwise the layers run one by one (fdp_backward; same results). Each layer has
+ * its own workspace (fdp_workspace_bytes of its desc). Extends workflows.py:340-421
+ * (per layer); the shared Gram is a scheduling of the ghost norms, not a new rule. */
+FDP_API int fdp_backward_shared_x(int32_t n, const fdp_desc* descs, const void* x, const void* const* dy,
+                                  float* const* grad_w, float* const* norms_sq, void* const* ws,
+                                  const size_t* ws_bytes, void* stream);
+
 /* The fused DP backward of n layers (n <= 48) in ONE persistent cooperative
  * launch: the training-step batching of Algorithm 1 (every layer keeps its own
  * DPConfig, noise key, per-sample norms and outputs; the producer/MMA/epilogue

@@ -754,8 +754,10 @@ float* chain_slot(fdp_chain* c, size_t n, cudaStream_t s) {
   return c->part[k];
 }
 
+// pre_parts > 0: the two-phase ghost norm partials of this layer (pre_parts per sample)
+// are already in the workspace (fdp_backward_shared_x); the norm phase is skipped.
 int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms, void* ws,
-        size_t ws_bytes, cudaStream_t s, fdp_chain* chain = nullptr) {
+        size_t ws_bytes, cudaStream_t s, fdp_chain* chain = nullptr, int pre_parts = 0) {
   int rc = validate(d, kind);
   if (rc) return rc;
   if (!x || !dy || !grad_w) return fail(FDP_ERR_USAGE, "null tensor pointer");
@@ -1010,7 +1012,11 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass
   {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_NORMS);
-    if (pl.norm_phase == FDP_NORMS_GHOST) {
+    if (pl.norm_phase == FDP_NORMS_GHOST && pre_parts > 0) {
+      if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pre_parts, d->clip_c, p.clip_c2, c.inv_batch, norms,
+                                            ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+        return cuda_fail(e, "factor reduce");
+    } else if (pl.norm_phase == FDP_NORMS_GHOST) {
       CUtensorMap gx, gy;
       if ((rc = make_tmap(&gx, x, d->P, d->T, d->B, 128))) return rc;
       if ((rc = make_tmap(&gy, dy, d->D, d->T, d->B, 128))) return rc;
@@ -1283,6 +1289,72 @@ int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, floa
   return run(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
+int fdp_backward_shared_x(int32_t n, const fdp_desc* descs, const void* x, const void* const* dy,
+                          float* const* grad_w, float* const* norms_sq, void* const* ws, const size_t* ws_bytes,
+                          void* stream) {
+  if (n < 1 || n > 3) return fail(FDP_ERR_USAGE, "fdp_backward_shared_x takes 1..3 layers, got %d", n);
+  if (!descs || !x || !dy || !grad_w || !norms_sq || !ws || !ws_bytes) return fail(FDP_ERR_USAGE, "null argument");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc;
+  for (int l = 0; l < n; ++l)
+    if ((rc = validate(&descs[l], FDP_KIND_FLASHDP))) return rc;
+  DevInfo di;
+  if ((rc = get_dev(di))) return rc;
+  // the shared X Gram applies when every layer runs the two-phase path with ghost norms on
+  // the same (B, T, P) bf16 input; otherwise each layer runs on its own (same results)
+  bool shared = n > 1 && env_int("FDP_SHARED_X", 1) != 0;
+  Plan pls[3];
+  const fdp_desc* d0 = &descs[0];
+  for (int l = 0; l < n; ++l) {
+    const fdp_desc* d = &descs[l];
+    if ((rc = make_plan(d, FDP_KIND_FLASHDP, di, pls[l]))) return rc;
+    if (d->B != d0->B || d->T != d0->T || d->P != d0->P || d->in_dtype != FDP_DTYPE_BF16 ||
+        pls[l].path != FDP_PATH_TWO_PHASE || pls[l].norm_phase != FDP_NORMS_GHOST || !dy[l] || !aligned16(dy[l]))
+      shared = false;
+  }
+  const long long nT2 = (d0->T + 255) / 256, np2 = nT2 * (nT2 + 1) / 2;
+  const int parts = static_cast<int>(2 * np2);  // CTA-pair Gram tiles, no K split
+  if (shared) {
+    for (int l = 0; l < n; ++l) {
+      const size_t need = static_cast<size_t>(d0->B) * parts * sizeof(float);
+      if (!ws[l] || ws_bytes[l] < pls[l].total || pls[l].off_factor - pls[l].off_part < need || !aligned16(x))
+        shared = false;
+    }
+  }
+  if (shared) {
+    CUtensorMap gx, gy[3];
+    if ((rc = make_tmap(&gx, x, d0->P, d0->T, d0->B, 128))) return rc;
+    for (int l = 0; l < n; ++l)
+      if ((rc = make_tmap(&gy[l], dy[l], descs[l].D, descs[l].T, descs[l].B, 128))) return rc;
+    fdp::GhostParams g{};
+    g.B = static_cast<int>(d0->B);
+    g.T = static_cast<int>(d0->T);
+    g.P = static_cast<int>(d0->P);
+    g.D = static_cast<int>(descs[0].D);
+    g.nT = static_cast<int>(nT2);
+    g.n_pairs = static_cast<int>(np2);
+    g.split = 1;
+    g.split_x = 1;
+    g.n_items = g.n_pairs * g.B;
+    g.part = ws_at<float>(ws[0], pls[0].off_part);
+    g.err = ws_at<unsigned>(ws[0], pls[0].off_ctrl) + 1;
+    g.budget_ns = (d0->flags & FDP_FLAG_TIMEOUT_SHORT) ? 200000000ull : 4000000000ull;
+    g.n_dy = n;
+    g.D1 = n > 1 ? static_cast<int>(descs[1].D) : 0;
+    g.D2 = n > 2 ? static_cast<int>(descs[2].D) : 0;
+    g.part1 = n > 1 ? ws_at<float>(ws[1], pls[1].off_part) : nullptr;
+    g.part2 = n > 2 ? ws_at<float>(ws[2], pls[2].off_part) : nullptr;
+    const int clusters = std::max(1, (di.sms - reserved_sms()) / 2);
+    const int grid = 2 * (g.n_items < clusters ? g.n_items : clusters);
+    cudaError_t e = fdp::launch_ghost_pair(gx, gy[0], g, grid, s, n > 1 ? &gy[1] : nullptr, n > 2 ? &gy[2] : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "shared-X ghost-norm launch");
+  }
+  for (int l = 0; l < n; ++l)
+    if ((rc = run(FDP_KIND_FLASHDP, &descs[l], x, dy[l], grad_w[l], norms_sq[l], ws[l], ws_bytes[l], s, nullptr,
+                  shared ? parts : 0)))
+      return rc;
+  return FDP_OK;
+}
 
 int fdp_chain_create(fdp_chain** out) {
   if (!out) return fail(FDP_ERR_USAGE, "null output");

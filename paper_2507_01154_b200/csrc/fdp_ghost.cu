@@ -232,6 +232,7 @@ constexpr uint32_t kPIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<u
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     ghost_norm_pair_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
+                           const __grid_constant__ CUtensorMap tm_dy1, const __grid_constant__ CUtensorMap tm_dy2,
                            const GhostParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -248,6 +249,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int rank = static_cast<int>(cluster_ctarank());
   const bool leader = rank == 0;
   const int cid = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+  // layers sharing X (n_dy > 1, split == 1): one Gx per item, then one Gy per layer
+  const int n_dy = p.n_dy > 1 ? p.n_dy : 1;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full[s], 1);
@@ -261,6 +264,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     fence_proxy_async_smem();
     prefetch_tmap(&tm_x);
     prefetch_tmap(&tm_dy);
+    if (n_dy > 1) prefetch_tmap(&tm_dy1);
+    if (n_dy > 2) prefetch_tmap(&tm_dy2);
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_holder);
   tc_fence_before();
@@ -268,6 +273,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int nkx = (p.P + kBK - 1) / kBK, nky = (p.D + kBK - 1) / kBK;
+  // k-block range of layer l's dY operand for an item (layer 0 carries the K split)
+  auto y_range = [&](const GItem& it, int l, int& ky0, int& ny) {
+    ky0 = l == 0 ? it.ky0 : 0;
+    ny = l == 0 ? it.ny : ((l == 1 ? p.D1 : p.D2) + kBK - 1) / kBK;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -276,58 +286,67 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const GItem it = decode_split(wi, p, nkx, nky);
         const int i = it.i, j = it.j, b = it.b;
         const int ra = i * kPT + rank * kPHalf, rb = j * kPT + rank * kPHalf;
-        for (int k = 0; k < it.nx + it.ny; ++k) {
-          const bool isx = k < it.nx;
-          const CUtensorMap* m = isx ? &tm_x : &tm_dy;
-          const int kk = (isx ? it.kx0 + k : it.ky0 + k - it.nx) * kBK;
+        auto load = [&](const CUtensorMap* m, int kk) {
           mbar_wait(&empty[stage], phase ^ 1, err, p.budget_ns, 0x311);
           uint8_t* sa = smem + stage * kPStageBytes;
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (i == j ? kPTileBytes : kPStageBytes));
           tma_load_3d_pair(sa, m, &full[stage], kk, ra, b);
           if (i != j) tma_load_3d_pair(sa + kPTileBytes, m, &full[stage], kk, rb, b);
           if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        };
+        for (int k = 0; k < it.nx; ++k) load(&tm_x, (it.kx0 + k) * kBK);
+        for (int l = 0; l < n_dy; ++l) {
+          const CUtensorMap* m = l == 0 ? &tm_dy : (l == 1 ? &tm_dy1 : &tm_dy2);
+          int ky0, ny;
+          y_range(it, l, ky0, ny);
+          for (int k = 0; k < ny; ++k) load(m, (ky0 + k) * kBK);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      uint32_t stage = 0, phase = 0, tph = 0;
+      uint32_t stage = 0, phase = 0, ph0 = 0, ph1 = 0;
       for (int wi = cid; wi < p.n_items; wi += n_clusters) {
         const GItem it = decode_split(wi, p, nkx, nky);
         const int i = it.i, j = it.j;
-        for (int k = 0; k < it.nx + it.ny; ++k) {
-          const bool isx = k < it.nx;
-          if (k == 0 || k == it.nx) {  // Gx / Gy accumulator of the previous item has been read out
-            mbar_wait(&tempty[isx ? 0 : 1], tph ^ 1, err, p.budget_ns, 0x312);
-            tc_fence_after();
-          }
-          const uint32_t dtm = tmem_base + (isx ? 0u : static_cast<uint32_t>(kPT));
-          mbar_wait(&full[stage], phase, err, p.budget_ns, 0x313);
+        // n k-blocks into the accumulator at column offset col (the previous use has been read out)
+        auto gram = [&](int n, uint32_t col, uint64_t* free_bar, uint32_t free_ph, uint64_t* done_bar) {
+          mbar_wait(free_bar, free_ph ^ 1, err, p.budget_ns, 0x312);
           tc_fence_after();
-          const uint32_t a = smem_u32(smem + stage * kPStageBytes);
-          const uint32_t bb = (i == j) ? a : a + kPTileBytes;
+          for (int k = 0; k < n; ++k) {
+            mbar_wait(&full[stage], phase, err, p.budget_ns, 0x313);
+            tc_fence_after();
+            const uint32_t a = smem_u32(smem + stage * kPStageBytes);
+            const uint32_t bb = (i == j) ? a : a + kPTileBytes;
 #pragma unroll
-          for (int kq = 0; kq < kBK / 16; ++kq)
-            tc_mma_f16_pair(dtm, kdesc(a + kq * 32), kdesc(bb + kq * 32), kPIdesc,
-                            (k == 0 || k == it.nx) && kq == 0 ? 0u : 1u);
-          tc_commit_pair(&empty[stage]);
-          if (++stage == kPStages) { stage = 0; phase ^= 1; }
-          if (k == it.nx - 1) tc_commit_pair(&tfull[0]);
+            for (int kq = 0; kq < kBK / 16; ++kq)
+              tc_mma_f16_pair(tmem_base + col, kdesc(a + kq * 32), kdesc(bb + kq * 32), kPIdesc,
+                              k == 0 && kq == 0 ? 0u : 1u);
+            tc_commit_pair(&empty[stage]);
+            if (++stage == kPStages) { stage = 0; phase ^= 1; }
+          }
+          tc_commit_pair(done_bar);
+        };
+        gram(it.nx, 0u, &tempty[0], ph0, &tfull[0]);
+        ph0 ^= 1;
+        for (int l = 0; l < n_dy; ++l) {
+          int ky0, ny;
+          y_range(it, l, ky0, ny);
+          gram(ny, static_cast<uint32_t>(kPT), &tempty[1], ph1, &tfull[1]);
+          ph1 ^= 1;
         }
-        tc_commit_pair(&tfull[1]);
-        tph ^= 1;
       }
     }
   } else if (warp >= kEpiWarp0) {
     const int ew = warp - kEpiWarp0;
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
-    uint32_t tph = 0;
+    uint32_t ph0 = 0, ph1 = 0;
     for (int wi = cid; wi < p.n_items; wi += n_clusters) {
       const GItem it = decode_split(wi, p, nkx, nky);
       const int i = it.i, j = it.j, b = it.b;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
       float gx[128];
-      mbar_wait(&tfull[0], tph, err, p.budget_ns, 0x314);
+      mbar_wait(&tfull[0], ph0, err, p.budget_ns, 0x314);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -340,33 +359,37 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty[0]);
-      mbar_wait(&tfull[1], tph, err, p.budget_ns, 0x315);
-      tc_fence_after();
-      float part = 0.0f;
+      ph0 ^= 1;
+      for (int l = 0; l < n_dy; ++l) {
+        mbar_wait(&tfull[1], ph1, err, p.budget_ns, 0x315);
+        tc_fence_after();
+        float part = 0.0f;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        float v[16];
-        tmem_ld16(tb + kPT + c * 16, v);
-        tmem_wait_ld();
+        for (int c = 0; c < 8; ++c) {
+          float v[16];
+          tmem_ld16(tb + kPT + c * 16, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) part = fmaf(gx[c * 16 + e], v[e], part);
+          for (int e = 0; e < 16; ++e) part = fmaf(gx[c * 16 + e], v[e], part);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[1]);
+        ph1 ^= 1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) red[ew] = part;
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (etid == 0) {
+          float s = 0.0f;
+#pragma unroll
+          for (int w = 0; w < kEpiWarps; ++w) s += red[w];
+          float* out = l == 0 ? p.part : (l == 1 ? p.part1 : p.part2);
+          out[((static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s) * 2 + rank] =
+              (i == j ? 1.0f : 2.0f) * s;
+        }
+        named_bar_sync(1, 32 * kEpiWarps);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty[1]);
-      tph ^= 1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) red[ew] = part;
-      named_bar_sync(1, 32 * kEpiWarps);
-      if (etid == 0) {
-        float s = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-        p.part[((static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s) * 2 + rank] =
-            (i == j ? 1.0f : 2.0f) * s;
-      }
-      named_bar_sync(1, 32 * kEpiWarps);
     }
   }
   tc_fence_before();
@@ -378,7 +401,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }  // namespace
 
 cudaError_t launch_ghost_pair(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, const CUtensorMap* tm_dy1, const CUtensorMap* tm_dy2) {
   static bool done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -400,7 +423,8 @@ cudaError_t launch_ghost_pair(const CUtensorMap& tm_x, const CUtensorMap& tm_dy,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, ghost_norm_pair_kernel, tm_x, tm_dy, p);
+  return cudaLaunchKernelEx(&cfg, ghost_norm_pair_kernel, tm_x, tm_dy, tm_dy1 ? *tm_dy1 : tm_dy,
+                            tm_dy2 ? *tm_dy2 : tm_dy, p);
 }
 
 cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,

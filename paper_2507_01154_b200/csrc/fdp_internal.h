@@ -177,12 +177,18 @@ struct GhostParams {
   float* part;   // [B][n_pairs][split] weighted partials (x2 for the CTA-pair kernel)
   unsigned* err;
   unsigned long long budget_ns;
+  // CTA-pair kernel only: n_dy (2 or 3) layers sharing X -- one X Gram per item, one dY
+  // Gram per layer (split must be 1); layer l in {1, 2} has D_l and its partials in part_l
+  int n_dy;
+  int D1, D2;
+  float *part1, *part2;
 };
 cudaError_t launch_ghost(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
                          cudaStream_t stream);
 // CTA-pair variant: 256x256 Gram tiles (nT = ceil(T/256)), partials [B][n_pairs][2], grid = 2 x clusters.
 cudaError_t launch_ghost_pair(const CUtensorMap& tm_x, const CUtensorMap& tm_dy, const GhostParams& p, int grid,
-                              cudaStream_t stream);
+                              cudaStream_t stream, const CUtensorMap* tm_dy1 = nullptr,
+                              const CUtensorMap* tm_dy2 = nullptr);
 
 // ---- SIMT (CUDA-core) kernels: generic shapes, fp32 inputs, explicit baseline
 struct SimtParams {

@@ -22,12 +22,33 @@ from __future__ import annotations
 from typing import Optional
 
 import ctypes
+import weakref
 
 import torch
 
 from . import _lib
 from .dpcore import DPConfig
 from .workflows import WorkflowKind, _run
+
+
+_CAST: list = [None]  # (source tensor, its version, dtype, the cast, its version) -- weak references
+
+
+def _cast_shared(x: torch.Tensor, dtype) -> torch.Tensor:
+    """x.to(dtype), reusing the previous call's cast when the same (unmodified) input
+    comes again: projections fed by one activation (q/k/v, gate/up) then save ONE
+    compute-dtype copy, which is also what lets their backward share the X Gram
+    (fdp_backward_shared_x recognises the common input by its address)."""
+    if x.dtype == dtype:
+        return x
+    c = _CAST[0]
+    if c is not None and c[0]() is x and c[1] == x._version and c[2] == dtype:
+        xc = c[3]()
+        if xc is not None and xc._version == c[4]:
+            return xc
+    xc = x.to(dtype)
+    _CAST[0] = (weakref.ref(x), x._version, dtype, weakref.ref(xc), xc._version)  # no reference kept alive
+    return xc
 
 
 class _DPLinearFn(torch.autograd.Function):
@@ -40,7 +61,7 @@ class _DPLinearFn(torch.autograd.Function):
         # the DP kernel consumes, no second cast in backward), else the input's
         cdt = torch.get_autocast_dtype("cuda") if torch.is_autocast_enabled("cuda") else x.dtype
         with torch.autocast("cuda", enabled=False):
-            xc = x.to(cdt)
+            xc = _cast_shared(x, cdt)
             wc = weight.to(cdt)
             y = torch.nn.functional.linear(xc, wc, None if bias is None else bias.to(cdt))
         ctx.save_for_backward(xc, wc)
@@ -117,6 +138,7 @@ class GroupedDPBackward:
         self._pending: list = []
         self.last_groups = 0
         self.flushes = 0
+        self.shared_x_calls = 0  # fdp_backward_shared_x calls (layers reading one X) in the last backward
         self._ws = None
         self._waiting: dict = {}
         self.chain = None  # DeferredChain of the per-layer (solo) kernels; None: built on first use
@@ -129,6 +151,7 @@ class GroupedDPBackward:
         self._pending = []
         self._waiting = {}
         self.flushes = 0
+        self.shared_x_calls = 0
         return self
 
     def __exit__(self, exc_type, exc, tb):
@@ -166,7 +189,7 @@ class GroupedDPBackward:
         return self.chain
 
     def _flush_items(self, pending) -> None:
-        from .workflows import PreparedGroup, WorkflowKind, _run
+        from .workflows import PreparedGroup, WorkflowKind, _run, _run_shared_x
         from .errors import CapacityError, UsageError
 
         if not pending:
@@ -204,7 +227,25 @@ class GroupedDPBackward:
             # single-sample layer's clip + noise pass runs inside the next layer's
             # GEMM (include/fdp.h fdp_dw_chained); the last one is flushed here
             done = []
-            for m, x, dy, cfg, _, _ in solo:
+            # layers reading the same X (q/k/v, gate/up) share the ghost phase's X Gram:
+            # one fdp_backward_shared_x call per run of up to 3 of them
+            runs: list = []
+            for it in solo:
+                x = it[1]
+                if (not self.defer_finalize and runs and len(runs[-1]) < 3 and x.dtype == torch.bfloat16
+                        and runs[-1][0][1].data_ptr() == x.data_ptr() and runs[-1][0][1].shape == x.shape):
+                    runs[-1].append(it)
+                else:
+                    runs.append([it])
+            for run in runs:
+                if len(run) > 1:
+                    self.shared_x_calls += 1
+                    gws = _run_shared_x(run[0][1], [(dy, cfg, out_for(m)) for m, _, dy, cfg, _, _ in run],
+                                        noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
+                                        mean_batch=mean_batch)
+                    done.extend((m, gw, out_for(m) is not None) for (m, *_), gw in zip(run, gws))
+                    continue
+                m, x, dy, cfg, _, _ = run[0]
                 g = out_for(m)
                 gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,
                           rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None,

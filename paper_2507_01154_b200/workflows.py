@@ -66,8 +66,11 @@ class _WorkspacePool:
         self._lock = threading.Lock()
         self._bufs: dict = {}
 
-    def get(self, nbytes: int, device: torch.device, stream: torch.cuda.Stream) -> torch.Tensor:
-        key = (device.index, stream.cuda_stream)
+    def get(self, nbytes: int, device: torch.device, stream: torch.cuda.Stream, slot=None) -> torch.Tensor:
+        # `slot`: a separate buffer for callers that need several workspaces at once
+        # (each buffer is always used from its start, so the C library's per-address
+        # layout signature keeps its counters valid)
+        key = (device.index, stream.cuda_stream, slot)
         with self._lock:
             buf = self._bufs.get(key)
             if buf is None or buf.numel() < nbytes:
@@ -208,6 +211,45 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         n_host = norms.double().cpu().numpy() if norms is not None else np.zeros(0)
         return BackwardResult(g_host, report, n_host, ref_report)
     return BackwardResult(grad, report, norms if norms is not None else torch.zeros(0, device=device), ref_report)
+
+
+def _run_shared_x(x: torch.Tensor, layers: list, *, noise_impl: str = "keyed_f32", add_noise: bool = True,
+                  rank: int = 0, world: int = 1, mean_batch: int = 0) -> list:
+    """FLASHDP backward of 1..3 layers that read the same device input X through ONE
+    fdp_backward_shared_x call (include/fdp.h: the ghost phase computes X X^T once for
+    all of them). `layers`: (dy, cfg, grad_out or None) per layer; returns the grads
+    (grad_out, accumulated into, when given)."""
+    n = len(layers)
+    if not 1 <= n <= 3:
+        raise UsageError(f"_run_shared_x takes 1..3 layers, got {n}")
+    lib = _lib.load()
+    device = x.device
+    descs = (_lib.FdpDesc * n)()
+    grads, norms, sizes = [], [], []
+    for k, (dy, cfg, g) in enumerate(layers):
+        dims = _dims(x, dy)
+        descs[k] = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=_input_dtype_code(x),
+                                  reduction=cfg.reduction, clip_c=cfg.clip_c, sigma=cfg.sigma, seed=cfg.seed,
+                                  layer_id=cfg.layer_id, step=cfg.step, rank=rank, world=world,
+                                  mean_batch=mean_batch, accumulate=g is not None, add_noise=add_noise,
+                                  noise_impl=noise_impl)
+        nb = ctypes.c_size_t()
+        _lib.check(lib.fdp_workspace_bytes(ctypes.byref(descs[k]), _lib.KIND["flashdp"], ctypes.byref(nb)))
+        sizes.append(nb.value)
+        if g is not None:
+            _check_out(g, (dims.D, dims.P), torch.float32, device, "grad_out")
+        grads.append(g if g is not None else torch.empty((dims.D, dims.P), dtype=torch.float32, device=device))
+        norms.append(torch.empty(dims.B, dtype=torch.float32, device=device))
+    stream = torch.cuda.current_stream(device)
+    # one workspace per layer (the ghost phase fills every layer's partials before any reweight)
+    wss = [_POOL.get(sizes[k], device, stream, slot=("shared_x", k)) for k in range(n)]
+    ptrs = ctypes.c_void_p * n
+    rc = lib.fdp_backward_shared_x(n, descs, x.data_ptr(), ptrs(*[dy.data_ptr() for dy, _, _ in layers]),
+                                   ptrs(*[g.data_ptr() for g in grads]), ptrs(*[t.data_ptr() for t in norms]),
+                                   ptrs(*[w.data_ptr() for w in wss]),
+                                   (ctypes.c_size_t * n)(*[w.numel() for w in wss]), stream.cuda_stream)
+    _lib.check(rc)
+    return grads
 
 
 _PLAN_CACHE: dict = {}
@@ -364,6 +406,45 @@ class PreparedBackward:
             _lib.check(self._lib.fdp_backward_chained(*self._args, self.chain.handle, s.cuda_stream))
         else:
             _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
+
+
+class PreparedSharedX:
+    """Two or three prepared FLASHDP layers that read the same input X (q/k/v of an
+    attention block, gate/up of a SwiGLU MLP) run through ONE C-ABI call
+    (`fdp_backward_shared_x`): when each takes the two-phase ghost path, the X Gram
+    of every tile pair is computed once for all of them; per-layer clipping, noise
+    and outputs are those of the individual calls (include/fdp.h)."""
+
+    def __init__(self, layers: list):
+        if not 1 <= len(layers) <= 3:
+            raise UsageError(f"PreparedSharedX takes 1..3 layers, got {len(layers)}")
+        x0 = layers[0].x
+        for pb in layers:
+            if pb.kind != WorkflowKind.FLASHDP or pb.chain is not None:
+                raise UsageError("PreparedSharedX layers must be unchained FLASHDP PreparedBackward calls")
+            if pb.x.data_ptr() != x0.data_ptr() or pb.x.shape != x0.shape:
+                raise UsageError("PreparedSharedX layers must share one X tensor")
+        self.layers = layers
+        self.x = x0
+        n = len(layers)
+        self._descs = (_lib.FdpDesc * n)(*[pb.desc for pb in layers])
+        ptrs = ctypes.c_void_p * n
+        self._dy = ptrs(*[pb.dy.data_ptr() for pb in layers])
+        self._gw = ptrs(*[pb.grad_w.data_ptr() for pb in layers])
+        self._ns = ptrs(*[pb.norms_sq.data_ptr() for pb in layers])
+        self._ws = ptrs(*[pb.workspace.data_ptr() for pb in layers])
+        self._wsb = (ctypes.c_size_t * n)(*[pb.workspace.numel() * pb.workspace.element_size() for pb in layers])
+        self._lib = _lib.load()
+
+    def set_step(self, step: int) -> None:
+        for k, pb in enumerate(self.layers):
+            pb.set_step(step)
+            self._descs[k].step = pb.desc.step
+
+    def __call__(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
+        _lib.check(self._lib.fdp_backward_shared_x(len(self.layers), self._descs, self.x.data_ptr(), self._dy,
+                                                   self._gw, self._ns, self._ws, self._wsb, s.cuda_stream))
 
 
 class PreparedGroup:

@@ -9,6 +9,9 @@ q), back to back on one stream:
               layer's clip + noise pass is carried by the next layer's GEMM kernel
               (B = 1), the last one flushed at the end of the block
   dp          the same calls unchained (every layer's pass standalone)
+  dp_shared_x the unchained calls with q/k/v and gate/up each through ONE
+              fdp_backward_shared_x call (they read the same X: one X Gram per tile
+              pair in the ghost phase)
   nondp       cuBLAS torch.mm(dY^T, X, out_dtype=fp32) per layer
 and each layer alone (dp_us / nondp_us per layer).
 
@@ -58,12 +61,21 @@ def main():
                   ("q", d, d)]
         for B in (int(b) for b in a.batches.split(",")):
             row = {"model": name, "B": B, "T": T, "layers": {}}
-            ins, chained, plain, nd = [], [], [], []
+            ins, chained, plain, nd, own = [], [], [], [], []
+            shared_x = {}
             chain = fdp.DeferredChain()
             ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
             flops = 0.0
             for j, (lname, P, D) in enumerate(shapes):
-                x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
+                # up/gate read the MLP norm's output, v/k/q the attention norm's: one X each
+                if lname in ("up", "v"):
+                    shared_x[lname] = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
+                if lname in ("up", "gate"):
+                    x = shared_x["up"]
+                elif lname in ("v", "k", "q"):
+                    x = shared_x["v"]
+                else:
+                    x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
                 dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
                 cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=j)
                 gw = torch.zeros(D, P, device="cuda")
@@ -72,6 +84,8 @@ def main():
                                                   grad_w=gw, norms_sq=nrm, workspace=ws))
                 chained.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
                                                     grad_w=gw, norms_sq=nrm, workspace=ws, chain=chain))
+                own.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
+                                                grad_w=gw, norms_sq=nrm))  # own workspace (shared-X arm)
                 x2, y2 = x.view(-1, P), dy.view(-1, D)
                 nd.append((x2, y2))
                 ins.append((x, dy))
@@ -93,13 +107,23 @@ def main():
                 for c in plain:
                     c()
 
+            names = [sn[0] for sn in shapes]
+            sx_calls = [own[names.index("down")], fdp.PreparedSharedX([own[names.index("up")], own[names.index("gate")]]),
+                        own[names.index("o")],
+                        fdp.PreparedSharedX([own[names.index("v")], own[names.index("k")], own[names.index("q")]])]
+
+            def dp_shared_x():
+                for c in sx_calls:
+                    c()
+
             def nondp():
                 for x2, y2 in nd:
                     torch.mm(y2.t(), x2, out_dtype=torch.float32)
 
             res = {}
             for _ in range(2):  # alternate, keep the best
-                for k, fn in (("dp_chained", dp_chained), ("dp", dp_plain), ("nondp", nondp)):
+                for k, fn in (("dp_chained", dp_chained), ("dp", dp_plain), ("dp_shared_x", dp_shared_x),
+                              ("nondp", nondp)):
                     t = timed(fn, a.reps)
                     res[k] = min(res.get(k, 1e30), t)
             st = chain.stats()
@@ -107,9 +131,11 @@ def main():
             row.update({"dp_chained_us": round(res["dp_chained"], 1), "dp_us": round(res["dp"], 1),
                         "nondp_us": round(res["nondp"], 1), "dp_tflops": round(flops / res["dp_chained"] / 1e6, 1),
                         "dw_ratio": round(r, 3), "dw_ratio_unchained": round(res["dp"] / res["nondp"], 3),
+                        "dp_shared_x_us": round(res["dp_shared_x"], 1),
+                        "dw_ratio_shared_x": round(res["dp_shared_x"] / res["nondp"], 3),
                         "implied_step_pct_of_nondp": round(100.0 * 3.0 / (2.0 + r), 1), "chain": st})
             print(json.dumps(row), flush=True)
-            del ins, chained, plain, nd, chain, ws
+            del ins, chained, plain, nd, chain, ws, own, sx_calls, shared_x
             torch.cuda.empty_cache()
 
 
