@@ -53,6 +53,23 @@ for d in (70, 256):
     fdp.embedding_dp_grad(tok, torch.randn(3, 300, d, device="cuda"), 50, cfg, noise_impl="philox")
 fdp.embedding_dp_grad(torch.zeros(2, 700, dtype=torch.int64, device="cuda"), torch.randn(2, 700, 40, device="cuda"),
                       3, cfg)  # one run longer than a norm block's key stage
+# round 2: shared-X ghost (3 layers, partial 256-row Gram tiles), spill norm phase, deferred chain,
+# stream-K reweight with split tiles (opening-segment stores, continuation reduce-adds), accumulate
+xs = inputs(2, 300, 384, 8)[0]
+pbs = [fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, xs, inputs(2, 300, 8, D)[1], cfg, path="two_phase",
+                            norm_phase="ghost", noise_impl="philox") for D in (256, 512, 384)]
+fdp.PreparedSharedX(pbs)()
+fdp.backward_flashdp(*inputs(3, 200, 512, 256), cfg, path="two_phase", norm_phase="spill", noise_impl="philox")
+chain = fdp.DeferredChain()
+for D in (256, 384):
+    fdp.workflows._run(fdp.WorkflowKind.FLASHDP, *inputs(1, 256, 512, D), cfg, None, None, path="two_phase",
+                       noise_impl="philox", chain=chain)
+chain.flush()
+xk, dyk = inputs(40, 64, 512, 512)
+for acc in (False, True):
+    gout = torch.zeros(512, 512, device="cuda")
+    fdp.workflows._run(fdp.WorkflowKind.FLASHDP, xk, dyk, cfg, None, None, path="two_phase", noise_impl="philox",
+                       grad_out=gout, accumulate=acc)
 st = fdp.OptimizerState.fresh(torch.zeros(1000, device="cuda"), eta=0.1)
 fdp.dp_adam_step_(st, torch.ones(1000, device="cuda"))
 torch.cuda.synchronize()
