@@ -567,7 +567,7 @@ def main():
 
             largs = argparse.Namespace(model="llama-13b", layers=a.llama_layers, batch=1, seq=2048, steps=3,
                                        warmup=2, zero1=True, comm_sms=4, bucket_mb=512, clip=1.0, sigma=1.0,
-                                       nondp_linear="fp32grad")
+                                       nondp_linear="fp32grad", defer_clip="auto")
             gc.collect()
             torch.cuda.empty_cache()
             nd_l = tl.run_arm(False, largs, 0, 1, dev)
@@ -575,7 +575,9 @@ def main():
             llama = {"model": f"llama-13b shapes (d=5120, 40 heads, MLP 13824, vocab 32000), {a.llama_layers} of 40 "
                               f"blocks, B=1, T=2048, every parameter DP, ZeRO-1 DP-Adam (noise on the owner's shard), "
                               f"random init, synthetic tokens; non-DP = the same model with FP32GradLinear projections, "
-                              f"same buckets / optimizer",
+                              f"same buckets / optimizer; B=1: the projections' clip factors applied in the "
+                              f"Adam step (deferred clip, fdp_dw_deferred)",
+                     "deferred_clips": dp_l.get("deferred_clips"),
                      "dp_tokens_per_s": dp_l["tokens_per_s"], "non_dp_tokens_per_s": nd_l["tokens_per_s"],
                      "dp_ms_per_step": dp_l["ms_per_step"], "non_dp_ms_per_step": nd_l["ms_per_step"],
                      "dp_pct_of_non_dp": 100.0 * dp_l["tokens_per_s"] / nd_l["tokens_per_s"],

@@ -184,6 +184,21 @@ FDP_API int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const v
 FDP_API int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
            void* ws, size_t ws_bytes, void* stream);
 
+/* fdp_dw with the clip factor handed to the consumer (deferred clip).
+ * On the single-sample path (B == 1, accumulate == 0) without noise in this call
+ * (add_noise == 0 or sigma == 0), grad_w receives the sample's UNCLIPPED gradient
+ * G, norms_sq[0] its ||G||^2, and grad_scale[0] (a device float) the factor
+ * min(1, C/||G||) / mean_batch (x 1 for reduction sum) -- the elementwise clip
+ * pass over grad_w is not run. The DP gradient is grad_scale[0] * grad_w, formed
+ * by whoever reads grad_w next: the optimizer step (fdp_adam_step_scaled /
+ * fdp_sgd_step_scaled, rounding identical to the pass) or the data-parallel
+ * collective (NCCL PreMulSum with grad_scale as the device scalar: every rank
+ * scales its own contribution inside the reduction). On every other path the
+ * call is fdp_dw and grad_scale[0] = 1. Replaces dpcore.clip_and_accumulate's
+ * scaling step (dpcore.py:50-57, 60-73) in time only: same factor, same product. */
+FDP_API int fdp_dw_deferred(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
+                            float* grad_scale, void* ws, size_t ws_bytes, void* stream);
+
 /* Deferred finalize chain. On the single-sample path (B == 1: the sample's
  * gradient is the layer's GEMM), the clip factor needs the norm of the whole
  * GEMM result, so the clip + noise pass over grad_w (an HBM-bound elementwise
@@ -293,6 +308,15 @@ FDP_API int fdp_sgd_step(int32_t dtype, void* theta, const void* grad, int64_t n
 FDP_API int fdp_adam_step(int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n, double eta,
                           double beta1, double beta2, double eps, const fdp_desc* noise, int64_t noise_offset,
                           void* stream);
+
+/* The same steps on grad_scale[0] * grad (device scalar from fdp_dw_deferred;
+ * fp32 state only): g = grad * grad_scale[0] rounded, then the noise, then the
+ * update -- bitwise what fdp_dw's finalize followed by fdp_adam_step computes. */
+FDP_API int fdp_sgd_step_scaled(int32_t dtype, void* theta, const void* grad, const float* grad_scale, int64_t n,
+                                double eta, const fdp_desc* noise, int64_t noise_offset, void* stream);
+FDP_API int fdp_adam_step_scaled(int32_t dtype, void* theta, void* m, void* v, const void* grad,
+                                 const float* grad_scale, int64_t n, double eta, double beta1, double beta2,
+                                 double eps, const fdp_desc* noise, int64_t noise_offset, void* stream);
 
 /* Noise slice [lo, hi) of [0, n) owned by `rank` of `world` (data-parallel
  * noise-once partition). Pure host arithmetic. */

@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = (
     "fdp_sgd_step", "fdp_adam_step", "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_vec_workspace_bytes",
     "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
     "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
-    "fdp_backward_chained", "fdp_backward_shared_x",
+    "fdp_backward_chained", "fdp_backward_shared_x", "fdp_dw_deferred", "fdp_sgd_step_scaled",
+    "fdp_adam_step_scaled",
 )
 VEC_KIND = {"bias": 0, "rmsnorm": 1, "layernorm": 2}
 
@@ -139,7 +140,15 @@ def load() -> ctypes.CDLL:
     lib.fdp_backward_shared_x.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpDesc), ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p]
-    for name in ("fdp_backward_shared_x", "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
+    lib.fdp_dw_deferred.argtypes = [ctypes.POINTER(FdpDesc)] + [ctypes.c_void_p] * 6 + [ctypes.c_size_t,
+                                                                                       ctypes.c_void_p]
+    lib.fdp_sgd_step_scaled.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_void_p]
+    lib.fdp_adam_step_scaled.argtypes = [ctypes.c_int32] + [ctypes.c_void_p] * 5 + [
+        ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p,
+        ctypes.c_int64, ctypes.c_void_p]
+    for name in ("fdp_dw_deferred", "fdp_sgd_step_scaled", "fdp_adam_step_scaled", "fdp_backward_shared_x", "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
                  "fdp_backward_chained", "fdp_vec_workspace_bytes", "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
                  "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",

@@ -756,8 +756,12 @@ float* chain_slot(fdp_chain* c, size_t n, cudaStream_t s) {
 
 // pre_parts > 0: the two-phase ghost norm partials of this layer (pre_parts per sample)
 // are already in the workspace (fdp_backward_shared_x); the norm phase is skipped.
+// scale_out (fdp_dw_deferred): on the single-sample path without noise, leave the
+// unclipped G in grad_w and write its clip factor x 1/mean_batch to scale_out[0]
+// instead of running the elementwise pass (*deferred = true); the caller applies it.
 int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms, void* ws,
-        size_t ws_bytes, cudaStream_t s, fdp_chain* chain = nullptr, int pre_parts = 0) {
+        size_t ws_bytes, cudaStream_t s, fdp_chain* chain = nullptr, int pre_parts = 0, float* scale_out = nullptr,
+        bool* deferred = nullptr) {
   int rc = validate(d, kind);
   if (rc) return rc;
   if (!x || !dy || !grad_w) return fail(FDP_ERR_USAGE, "null tensor pointer");
@@ -975,6 +979,12 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       chain->job = j;
       chain->pending = true;
       chain->slot ^= 1;
+      return FDP_OK;
+    }
+    if (scale_out && !c.add_noise) {  // deferred clip: the consumer forms scale * G
+      if ((e = fdp::single_sample_factor(j, scale_out, s)) != cudaSuccess)
+        return cuda_fail(e, "single-sample clip factor");
+      if (deferred) *deferred = true;
       return FDP_OK;
     }
     if ((e = fdp::single_sample_finalize(j, s)) != cudaSuccess) return cuda_fail(e, "single-sample finalize");
@@ -1287,6 +1297,20 @@ int fdp_backward(int32_t kind, const fdp_desc* d, const void* x, const void* dy,
 int fdp_dw(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq, void* ws,
            size_t ws_bytes, void* stream) {
   return run(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int fdp_dw_deferred(const fdp_desc* d, const void* x, const void* dy, float* grad_w, float* norms_sq,
+                    float* grad_scale, void* ws, size_t ws_bytes, void* stream) {
+  if (!grad_scale) return fail(FDP_ERR_USAGE, "grad_scale must not be null");
+  if (reinterpret_cast<uintptr_t>(grad_scale) & 3u) return fail(FDP_ERR_USAGE, "grad_scale must be 4-byte aligned");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  bool deferred = false;
+  int rc = run(FDP_KIND_FLASHDP, d, x, dy, grad_w, norms_sq, ws, ws_bytes, s, nullptr, 0, grad_scale, &deferred);
+  if (rc || deferred) return rc;
+  fdp::FinJob none{};  // finalised in place: the consumer's scale is 1
+  cudaError_t e = fdp::single_sample_factor(none, grad_scale, s);
+  if (e != cudaSuccess) return cuda_fail(e, "grad_scale fill");
+  return FDP_OK;
 }
 
 int fdp_backward_shared_x(int32_t n, const fdp_desc* descs, const void* x, const void* const* dy,
@@ -1631,7 +1655,10 @@ int fdp_embedding_dw(const fdp_desc* d, const int64_t* tokens, const void* dy, f
 
 static int optim_common(int adam, int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n,
                         double eta, double b1, double b2, double eps, const fdp_desc* noise, int64_t noise_offset,
-                        void* stream) {
+                        void* stream, const float* grad_scale = nullptr) {
+  if (grad_scale && dtype != FDP_DTYPE_F32) return fail(FDP_ERR_USAGE, "grad_scale needs fp32 state");
+  if (grad_scale && (reinterpret_cast<uintptr_t>(grad_scale) & 3u))
+    return fail(FDP_ERR_USAGE, "grad_scale must be 4-byte aligned");
   if (dtype != FDP_DTYPE_F32 && dtype != FDP_DTYPE_F64)
     return fail(FDP_ERR_USAGE, "optimizer state must be fp32 (1) or fp64 (2), got dtype %d", dtype);
   if (n < 0) return fail(FDP_ERR_SHAPE, "negative element count %lld", (long long)n);
@@ -1655,6 +1682,7 @@ static int optim_common(int adam, int32_t dtype, void* theta, void* m, void* v, 
     nz.layer_u = static_cast<uint64_t>(noise->layer_id);
     nz.offset = noise_offset;
   }
+  nz.grad_scale = grad_scale;
   cudaError_t e = fdp::optim_step(adam, dtype == FDP_DTYPE_F64, theta, m, v, grad, n, eta, b1, b2, eps, nz,
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, adam ? "adam step" : "sgd step");
@@ -1669,6 +1697,21 @@ int fdp_sgd_step(int32_t dtype, void* theta, const void* grad, int64_t n, double
 int fdp_adam_step(int32_t dtype, void* theta, void* m, void* v, const void* grad, int64_t n, double eta,
                   double beta1, double beta2, double eps, const fdp_desc* noise, int64_t noise_offset, void* stream) {
   return optim_common(1, dtype, theta, m, v, grad, n, eta, beta1, beta2, eps, noise, noise_offset, stream);
+}
+
+int fdp_sgd_step_scaled(int32_t dtype, void* theta, const void* grad, const float* grad_scale, int64_t n, double eta,
+                        const fdp_desc* noise, int64_t noise_offset, void* stream) {
+  if (!grad_scale) return fail(FDP_ERR_USAGE, "grad_scale must not be null");
+  return optim_common(0, dtype, theta, nullptr, nullptr, grad, n, eta, 0.0, 0.0, 0.0, noise, noise_offset, stream,
+                      grad_scale);
+}
+
+int fdp_adam_step_scaled(int32_t dtype, void* theta, void* m, void* v, const void* grad, const float* grad_scale,
+                         int64_t n, double eta, double beta1, double beta2, double eps, const fdp_desc* noise,
+                         int64_t noise_offset, void* stream) {
+  if (!grad_scale) return fail(FDP_ERR_USAGE, "grad_scale must not be null");
+  return optim_common(1, dtype, theta, m, v, grad, n, eta, beta1, beta2, eps, noise, noise_offset, stream,
+                      grad_scale);
 }
 
 int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi) {

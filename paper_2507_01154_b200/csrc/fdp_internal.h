@@ -229,6 +229,9 @@ cudaError_t explicit_sum_finalize(const float* gp, int B, long long DP, int P, c
 // B == 1 second pass: ||G||^2 from the per-tile partials (fixed order), then
 // grad_w = grad_w * min(1, C/||G||) * inv_batch (+ sigma*C*noise on [lo, hi)).
 cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s);
+// deferred clip: scale_out[0] = c * inv_batch and norms_out[0] = ||G||^2 from j's
+// partials, grad_w untouched (j.part == nullptr: scale_out[0] = 1)
+cudaError_t single_sample_factor(const FinJob& j, float* scale_out, cudaStream_t s);
 // spill combine: out = (accumulate ? out : 0) + sum_b fac[b] * G[b] + scale * noise (rank slice)
 cudaError_t spill_combine(float* out, const float* G, int B, long long n, const float* fac, int accumulate,
                           int add_noise, int impl, float scale, uint64_t base, uint64_t base_g,
@@ -287,6 +290,7 @@ struct OptimNoise {
   const long long* step_ptr;
   uint64_t seed_u, layer_u;
   long long offset;
+  const float* grad_scale;  // nullptr or a device scalar: g = grad_scale[0] * grad before the noise (fp32 only)
 };
 cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const void* g, long long n, double eta,
                        double b1, double b2, double eps, const OptimNoise& nz, cudaStream_t s);

@@ -24,6 +24,7 @@ struct NoiseArgs {
   const long long* step_ptr;
   uint64_t seed_u, layer_u;
   long long offset;  // flat index of element 0 in the layer's [0, D*P)
+  const float* gscale;  // deferred clip (fdp_dw_deferred): g = *gscale * grad, rounded, before the noise
 };
 
 template <typename T>
@@ -33,10 +34,14 @@ __device__ __forceinline__ T noise_at(const NoiseArgs& a, uint64_t base, uint64_
   return static_cast<T>(a.scale * noise_draw(a.impl, base_g, base, idx));
 }
 
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }  // never contracted
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_adam(T* __restrict__ theta, T* __restrict__ m, T* __restrict__ v,
                                               const T* __restrict__ g, long long n, T eta, T b1, T b2, T eps,
                                               NoiseArgs na) {
+  const T* gs = reinterpret_cast<const T*>(na.gscale);  // fp32 state only (checked by the C-ABI)
   uint64_t base = na.base, base_g = na.base_g;
   if (na.on && na.step_ptr) {
     base = absorb3(na.seed_u, na.layer_u, static_cast<uint64_t>(*na.step_ptr));
@@ -46,6 +51,7 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ theta, T* __restri
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     T gi = g[i];
+    if (gs) gi = mul_rn(gi, *gs);
     if (na.on) gi += noise_at<T>(na, base, base_g, i);
     const T mi = b1 * m[i] + (one - b1) * gi;
     const T vi = b2 * v[i] + (one - b2) * (gi * gi);
@@ -86,6 +92,7 @@ __global__ void __launch_bounds__(256) k_adam_f32x4(float4* __restrict__ theta, 
   uint64_t base = na.base;
   if (kNoise && na.step_ptr) base = absorb3(na.seed_u, na.layer_u, static_cast<uint64_t>(*na.step_ptr));
   const uint64_t q0 = static_cast<uint64_t>(na.offset) >> 2;
+  const float f = na.gscale ? *na.gscale : 1.0f;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += 2 * stride) {
     const long long j = i + stride;
@@ -97,6 +104,16 @@ __global__ void __launch_bounds__(256) k_adam_f32x4(float4* __restrict__ theta, 
       m1 = __ldcs(m + j);
       v1 = __ldcs(v + j);
       t1 = __ldcs(theta + j);
+    }
+    if (na.gscale) {  // __fmul_rn: the same rounding as the finalize pass (fdp_simt.cu k_single_finalize)
+      g0.x = __fmul_rn(g0.x, f);
+      g0.y = __fmul_rn(g0.y, f);
+      g0.z = __fmul_rn(g0.z, f);
+      g0.w = __fmul_rn(g0.w, f);
+      g1.x = __fmul_rn(g1.x, f);
+      g1.y = __fmul_rn(g1.y, f);
+      g1.z = __fmul_rn(g1.z, f);
+      g1.w = __fmul_rn(g1.w, f);
     }
     if constexpr (kNoise) {
       const float4 z0 = philox_normal4(base, q0 + static_cast<uint64_t>(i));
@@ -128,6 +145,7 @@ __global__ void __launch_bounds__(256) k_adam_f32x4(float4* __restrict__ theta, 
 template <typename T>
 __global__ void __launch_bounds__(256) k_sgd(T* __restrict__ theta, const T* __restrict__ g, long long n, T eta,
                                              NoiseArgs na) {
+  const T* gs = reinterpret_cast<const T*>(na.gscale);  // fp32 state only (checked by the C-ABI)
   uint64_t base = na.base, base_g = na.base_g;
   if (na.on && na.step_ptr) {
     base = absorb3(na.seed_u, na.layer_u, static_cast<uint64_t>(*na.step_ptr));
@@ -136,6 +154,7 @@ __global__ void __launch_bounds__(256) k_sgd(T* __restrict__ theta, const T* __r
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     T gi = g[i];
+    if (gs) gi = mul_rn(gi, *gs);
     if (na.on) gi += noise_at<T>(na, base, base_g, i);
     theta[i] = theta[i] - eta * gi;
   }
@@ -151,7 +170,8 @@ int blocks_for(long long n) {
 
 cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const void* g, long long n, double eta,
                        double b1, double b2, double eps, const OptimNoise& nz, cudaStream_t s) {
-  NoiseArgs na{nz.on, nz.impl, nz.scale, nz.base, nz.base_g, nz.step_ptr, nz.seed_u, nz.layer_u, nz.offset};
+  NoiseArgs na{nz.on, nz.impl, nz.scale, nz.base, nz.base_g, nz.step_ptr, nz.seed_u, nz.layer_u, nz.offset,
+               nz.grad_scale};
   if (n <= 0) return cudaSuccess;
   if (adam) {
     if (f64)

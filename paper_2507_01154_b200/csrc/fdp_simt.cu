@@ -391,6 +391,32 @@ cudaError_t spill_combine(float* out, const float* G, int B, long long n, const 
   return cudaGetLastError();
 }
 
+// Deferred clip (fdp_dw_deferred): the finalize's clip factor without its pass over
+// grad_w. One warp sums the partials in k_single_finalize's fixed order and writes
+// scale_out[0] = float(c) * inv_batch (the same float the pass multiplies by) and
+// ||G||^2; part == nullptr writes scale 1 (the call finalised grad_w in place).
+__global__ void k_single_factor(const float* __restrict__ part, int n_parts, double clip_c, double clip_c2,
+                                float inv_batch, float* norms_out, float* scale_out) {
+  if (!part) {
+    if (threadIdx.x == 0) scale_out[0] = 1.0f;
+    return;
+  }
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n_parts; i += 32) t += static_cast<double>(part[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) {
+    const double cf = (t <= clip_c2) ? 1.0 : clip_c / sqrt(t);  // dpcore.py:41-47
+    scale_out[0] = static_cast<float>(cf) * inv_batch;
+    if (norms_out) norms_out[0] = static_cast<float>(t);
+  }
+}
+
+cudaError_t single_sample_factor(const FinJob& j, float* scale_out, cudaStream_t s) {
+  k_single_factor<<<1, 32, 0, s>>>(j.part, j.n_parts, j.clip_c, j.clip_c2, j.inv_batch, j.norms_out, scale_out);
+  return cudaGetLastError();
+}
+
 cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s) {
   return single_sample_finalize(j.g, j.n, j.part, j.n_parts, j.clip_c, j.clip_c2, j.inv_batch, j.norms_out,
                                 j.add_noise, j.impl, j.scale, j.base, j.base_g, j.step_ptr, j.seed_u, j.layer_u, j.lo,

@@ -269,7 +269,7 @@ def group_max_ctas(device: torch.device, comm_sms: int, world: int) -> int:
 
 class _Bucket:
     __slots__ = ("params", "offsets", "n", "per", "flat", "pflat", "shard", "pending", "launched", "deferred",
-                 "m", "v", "marked")
+                 "m", "v", "marked", "scale", "scale_applied")
 
 
 class GradBuckets:
@@ -296,10 +296,18 @@ class GradBuckets:
     per bucket too (same layout), so an optimizer can step a bucket or a shard of
     it with one kernel and all-gather it in one collective.
 
-    Bucket issue order is the backward's order, identical on every rank."""
+    Bucket issue order is the backward's order, identical on every rank.
+
+    Deferred clip (``isolate``): each listed parameter gets a bucket of its own,
+    so a single-sample DP layer (B = 1 per rank) can hand its gradient over
+    UNCLIPPED with its clip factor as a device scalar (``mark_ready(p, scale=)``,
+    workflows fdp_dw_deferred): the bucket's collective then scales every rank's
+    contribution inside the reduction (NCCL PreMulSum with the device scalar;
+    gloo: an in-place multiply first) and at world 1 the optimizer step applies
+    it -- the elementwise clip pass over the layer's gradient never runs."""
 
     def __init__(self, params, *, bucket_bytes: int = 512 << 20, mode: str = "allreduce", group=None,
-                 rank: int = 0, world: int = 1, flat_params: bool = False, hooks: bool = True):
+                 rank: int = 0, world: int = 1, flat_params: bool = False, hooks: bool = True, isolate=()):
         if mode not in ("allreduce", "reduce_scatter"):
             raise ValueError(f"mode must be allreduce or reduce_scatter, got {mode!r}")
         if world < 1 or not (0 <= rank < world):
@@ -313,8 +321,15 @@ class GradBuckets:
                 raise ValueError(f"GradBuckets keeps fp32 master parameters and gradients, got {p.dtype}")
         self.device = ps[0].device
         self.buckets: list[_Bucket] = []
+        iso = {id(p) for p in isolate}
         cur, size = [], 0
         for p in reversed(ps):
+            if id(p) in iso:  # a bucket of its own (deferred clip), between its neighbours' buckets
+                if cur:
+                    self._close(cur, flat_params)
+                    cur, size = [], 0
+                self._close([p], flat_params)
+                continue
             cur.append(p)
             size += p.numel() * 4
             if size >= bucket_bytes:
@@ -323,6 +338,7 @@ class GradBuckets:
         if cur:
             self._close(cur, flat_params)
         self._external: set = set()  # ids of parameters whose readiness is signalled explicitly
+        self._written: set = set()  # ids of parameters whose .grad region was written since zero_grad
         self._where = {}
         for i, b in enumerate(self.buckets):
             for p in b.params:
@@ -377,6 +393,7 @@ class GradBuckets:
         b.launched = False
         b.marked = set()
         b.m = b.v = None
+        b.scale, b.scale_applied = None, False
         self.buckets.append(b)
 
     def set_deferred(self, weights) -> None:
@@ -400,13 +417,36 @@ class GradBuckets:
             b.pending = len(b.params)
             b.launched = False
             b.marked = set()
+            b.scale, b.scale_applied = None, False
             for p, o in zip(b.params, b.offsets):
                 if p.grad is None or p.grad.data_ptr() != b.flat[o:].data_ptr():
                     p.grad = b.flat[o:o + p.numel()].view_as(p)
         self.issued = []
+        self._written = set()
 
     def bucket_of(self, p) -> int:
         return self._where[id(p)]
+
+    def fresh(self, p) -> bool:
+        """p's .grad is still its zeroed bucket view (nothing written since
+        zero_grad): a kernel may overwrite it instead of accumulating."""
+        i = self._where.get(id(p))
+        if i is None or id(p) in self._written:
+            return False
+        b = self.buckets[i]
+        o = b.offsets[next(k for k, q in enumerate(b.params) if q is p)]
+        return p.grad is not None and p.grad.data_ptr() == b.flat[o:].data_ptr()
+
+    def note_written(self, p) -> None:
+        self._written.add(id(p))
+
+    def can_defer(self, p) -> bool:
+        """p may be handed over unclipped with a scale (mark_ready(p, scale=)): its
+        bucket holds it alone, its gradient is fresh and this is the step's last
+        micro-batch (no later accumulation into it)."""
+        i = self._where.get(id(p))
+        return (i is not None and self.enabled and len(self.buckets[i].params) == 1 and self.fresh(p)
+                and self.device.type == "cuda")
 
     def _hook(self, p):
         # autograd runs post-accumulate hooks even when a Function returned no
@@ -419,13 +459,19 @@ class GradBuckets:
         self._external.add(id(p))
         self.mark_ready(p)
 
-    def mark_ready(self, p) -> None:
+    def mark_ready(self, p, scale: "torch.Tensor | None" = None) -> None:
+        """p's gradient is complete. ``scale`` (a (1,) fp32 device tensor, only for
+        a parameter with can_defer(p)): the gradient is scale[0] * p.grad."""
         if not self.enabled:  # micro-batches before the last: gradients accumulate, no collective
             return
         i = self._where.get(id(p))
         if i is None:
             return
         b = self.buckets[i]
+        if scale is not None:
+            if len(b.params) != 1:
+                raise RuntimeError("a scaled gradient needs a bucket of its own (GradBuckets(isolate=...))")
+            b.scale = scale
         if id(p) in b.marked:  # one readiness signal per parameter and step
             return
         b.marked.add(id(p))
@@ -453,14 +499,22 @@ class GradBuckets:
             self._collective(b)
 
     def _collective(self, b: _Bucket) -> None:
+        nccl = dist.get_backend(self.group) == "nccl"
+        op = dist.ReduceOp.SUM
+        if b.scale is not None:  # deferred clip: each rank's contribution times its own factor
+            if nccl:
+                op = dist._make_nccl_premul_sum(b.scale)
+            else:
+                b.flat.mul_(b.scale.to(b.flat.device))
+            b.scale_applied = True
         if self.mode == "allreduce":
-            dist.all_reduce(b.flat, op=dist.ReduceOp.SUM, group=self.group)
-        elif dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(b.flat, op=op, group=self.group)
+        elif nccl:
             out = torch.empty_like(b.shard)
-            dist.reduce_scatter_tensor(out, b.flat, op=dist.ReduceOp.SUM, group=self.group)
+            dist.reduce_scatter_tensor(out, b.flat, op=op, group=self.group)
             b.shard.copy_(out)
         else:  # gloo: all-reduce, keep this rank's slice (b.shard is a view of it)
-            dist.all_reduce(b.flat, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(b.flat, op=op, group=self.group)
 
     def finish(self) -> None:
         """After backward: issue any bucket not yet issued (parameters without a
@@ -505,10 +559,13 @@ def dp_noise_keys(model) -> dict:
     return keys
 
 
-def _torch_adam_(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel):
-    """Device-agnostic stand-in of fdp_adam_step for CPU tests (no noise)."""
+def _torch_adam_(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
+                 grad_scale=None):
+    """Device-agnostic stand-in of fdp_adam_step(_scaled) for CPU tests (no noise)."""
     if noise_cfg is not None and noise_cfg.sigma > 0:
         raise RuntimeError("the torch Adam stand-in does not draw DP noise")
+    if grad_scale is not None:
+        grad = grad * grad_scale.to(grad.device)
     m.mul_(b1).add_(grad, alpha=1 - b1)
     v.mul_(b2).addcmul_(grad, grad, value=1 - b2)
     theta.sub_(eta * m / (v.sqrt() + eps))
@@ -544,12 +601,13 @@ class BucketedAdam:
             b.v = torch.zeros_like(b.m)
 
     @staticmethod
-    def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel):
+    def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
+                grad_scale=None):
         from .dpcore import OptimizerState, dp_adam_step_
 
         st = OptimizerState(theta=theta, m=m, v=v, eta=eta, beta1=b1, beta2=b2, eps_adam=eps)
         dp_adam_step_(st, grad, noise=noise_cfg, noise_offset=noise_offset, noise_impl=noise_impl or "philox",
-                      layer_numel=layer_numel)
+                      layer_numel=layer_numel, grad_scale=grad_scale)
 
     def _segments(self, b, lo: int, hi: int):
         """(a, z, noise key or None) pieces of [lo, hi) cut at parameter bounds;
@@ -574,9 +632,11 @@ class BucketedAdam:
 
         bk = self.bk
         for b in bk.buckets:
+            # a deferred clip factor no collective applied (world 1): the step multiplies it in
+            kw = {"grad_scale": b.scale} if b.scale is not None and not b.scale_applied else {}
             if bk.mode == "allreduce" and not self.noise_keys:
                 self.adam_fn(b.pflat[:b.n], b.m, b.v, b.flat[:b.n], self.lr, self.beta1, self.beta2, self.eps,
-                             None, 0, None, 0)
+                             None, 0, None, 0, **kw)
                 continue
             # ZeRO-1: this rank's shard; all-reduce with noise keys: the whole bucket on every
             # rank, each element's noise drawn once per rank from the same keys (counter-based,
@@ -588,11 +648,11 @@ class BucketedAdam:
                 th, g = b.pflat[a:z], src[a - lo:z - lo]
                 mm, vv = b.m[a - lo:z - lo], b.v[a - lo:z - lo]
                 if key is None:
-                    self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0)
+                    self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0, **kw)
                 else:
                     cfg, off, glen, impl = key
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps,
-                                 replace(cfg, step=dp_step), off, impl, glen)
+                                 replace(cfg, step=dp_step), off, impl, glen, **kw)
             if bk.world > 1 and bk.mode == "reduce_scatter":
                 mine = b.pflat[bk.rank * b.per:(bk.rank + 1) * b.per]
                 if dist.get_backend(bk.group) == "nccl":
@@ -623,12 +683,20 @@ class DataParallelStep:
 
     The loss must be the sum over samples of per-sample losses, scaled by
     1/global_batch for dp=False (the DP modules take the mean over the logical
-    batch themselves), so the summed gradients are the global-batch ones."""
+    batch themselves), so the summed gradients are the global-batch ones.
+
+    ``defer_clip`` (None = on when every rank holds one sample; DP only with the
+    noise in the optimizer): weight matrices of >= isolate_min_numel elements get
+    buckets of their own (in both arms: same layout)
+    and a single-sample layer hands its gradient over unclipped with its clip
+    factor (GradBuckets), so its elementwise clip pass never runs: the collective
+    (PreMulSum) or, at world 1, the Adam step applies the factor."""
 
     def __init__(self, model, *, dp: bool, mode: str = "allreduce", lr: float = 1e-5, beta1: float = 0.9,
                  beta2: float = 0.999, eps: float = 1e-8, rank: int = 0, world: int = 1, group=None,
                  comm_sms: int = 4, bucket_bytes: int = 512 << 20, global_batch: int = 1, adam_fn=None,
-                 noise_in_optimizer: bool = True):
+                 noise_in_optimizer: bool = True, defer_clip: "bool | None" = None,
+                 isolate_min_numel: int = 1 << 22):
         from .dplinear import DPLinear
 
         self.model, self.dp, self.mode, self.world = model, dp, mode, world
@@ -637,8 +705,13 @@ class DataParallelStep:
         # or, all-reduce only, by the DP kernels on each rank's slice of every layer
         self.noise_in_optimizer = bool(noise_in_optimizer) or mode == "reduce_scatter"
         self.global_batch = global_batch
+        if defer_clip is None:
+            defer_clip = global_batch == world
+        self.defer_clip = bool(defer_clip) and dp and self.noise_in_optimizer
+        # the bucket layout follows the request for both arms (the non-DP baseline gets the same buckets)
+        iso = [p for p in model.parameters() if p.dim() == 2 and p.numel() >= isolate_min_numel] if defer_clip else []
         self.buckets = GradBuckets(model.parameters(), bucket_bytes=bucket_bytes, mode=mode, group=group,
-                                   rank=rank, world=world, flat_params=True)
+                                   rank=rank, world=world, flat_params=True, isolate=iso)
         self.dp_mods = model.dp_modules() if dp else []
         if dp:
             set_data_parallel(self.dp_mods, rank, world)
@@ -651,6 +724,7 @@ class DataParallelStep:
         if world > 1:  # per-layer DP kernels leave NCCL's SMs free too (fdp_capi.cu reserved_sms)
             os.environ["FDP_RESERVE_SMS"] = str(int(comm_sms))
         self.last_flushes = 0
+        self.last_deferred = 0  # layers whose clip was deferred to the collective / optimizer last step
 
     def __call__(self, step: int, loss_fn):
         from .dplinear import GroupedDPBackward
@@ -661,9 +735,10 @@ class DataParallelStep:
             m.set_step(step, last_micro_batch=not self.noise_in_optimizer, logical_batch=self.global_batch)
         loss = loss_fn()
         if self.dp:
-            with GroupedDPBackward(buckets=bk, max_ctas=self.max_ctas) as g:
+            with GroupedDPBackward(buckets=bk, max_ctas=self.max_ctas, defer_clip=self.defer_clip) as g:
                 loss.backward()
             self.last_flushes = g.flushes
+            self.last_deferred = g.deferred_clips
         else:
             loss.backward()
         bk.finish()

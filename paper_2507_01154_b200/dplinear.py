@@ -22,6 +22,7 @@ from __future__ import annotations
 from typing import Optional
 
 import ctypes
+import os
 import weakref
 
 import torch
@@ -128,10 +129,18 @@ class GroupedDPBackward:
     ``defer_finalize``: run the per-layer kernels through a DeferredChain (a B = 1
     layer's clip + noise pass carried by the next layer's GEMM). Off by default:
     measured slower on B200 (Llama-7B block, B = 1: 1174 vs 1074 us; the streamed
-    pass slows the carrying GEMM more than the standalone pass costs)."""
+    pass slows the carrying GEMM more than the standalone pass costs).
+
+    With ``buckets``, a layer whose bucket view is still fresh (nothing written
+    since zero_grad) is written, not accumulated into: a B = 1 layer then takes the
+    single-sample path (its GEMM is the sample's gradient) instead of ghost norms.
+    ``defer_clip``: such a layer, alone in its bucket and without kernel noise,
+    skips even the clip pass -- fdp_dw_deferred leaves the unclipped gradient and
+    hands the factor to the bucket (GradBuckets.mark_ready(scale=)), applied by the
+    collective or the optimizer step."""
 
     def __init__(self, *, noise_impl: Optional[str] = None, max_ctas: int = 0, buckets=None,
-                 defer_finalize: bool = False):
+                 defer_finalize: bool = False, defer_clip: bool = False):
         self.noise_impl = noise_impl
         self.max_ctas = max_ctas
         self.buckets = buckets
@@ -143,6 +152,8 @@ class GroupedDPBackward:
         self._waiting: dict = {}
         self.chain = None  # DeferredChain of the per-layer (solo) kernels; None: built on first use
         self.defer_finalize = defer_finalize
+        self.defer_clip = defer_clip
+        self.deferred_clips = 0  # layers handed over unclipped with a scale in the last backward
 
     def __enter__(self):
         if _ACTIVE_GROUP[0] is not None:
@@ -152,6 +163,7 @@ class GroupedDPBackward:
         self._waiting = {}
         self.flushes = 0
         self.shared_x_calls = 0
+        self.deferred_clips = 0
         return self
 
     def __exit__(self, exc_type, exc, tb):
@@ -196,11 +208,18 @@ class GroupedDPBackward:
             return
         self.flushes += 1
 
+        bk = self.buckets
+
         def out_for(m):  # write straight into an fp32 .grad (bucket view / micro-batch sum)
             g = m.weight.grad
             if g is not None and g.dtype == torch.float32 and g.is_contiguous() and g.shape == m.weight.shape:
                 return g
             return None
+
+        def fresh(m):  # its bucket view holds zeros: overwrite instead of accumulating
+            return bk is not None and out_for(m) is not None and bk.fresh(m.weight)
+
+        scales: dict = {}
 
         def deliver(m, gw, direct):
             if not direct:
@@ -209,8 +228,9 @@ class GroupedDPBackward:
                     m.weight.grad = gw
                 else:
                     m.weight.grad += gw
-            if self.buckets is not None:
-                self.buckets.mark_ready(m.weight)
+            if bk is not None:
+                bk.mark_ready(m.weight, scale=scales.get(id(m)))
+                bk.note_written(m.weight)
 
         buckets: dict = {}
         for item in pending:  # one launch per (noise on/off, mean divisor, partition, noise generator)
@@ -247,9 +267,17 @@ class GroupedDPBackward:
                     continue
                 m, x, dy, cfg, _, _ = run[0]
                 g = out_for(m)
+                new = fresh(m)
+                scale = None
+                if (self.defer_clip and new and not add_noise and x.shape[0] == 1 and not self.defer_finalize
+                        and bk.can_defer(m.weight)):
+                    scale = torch.empty(1, dtype=torch.float32, device=x.device)
+                    scales[id(m)] = scale
+                    self.deferred_clips += 1
                 gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,
-                          rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None,
-                          chain=self._chain() if self.defer_finalize else None).grad_w
+                          rank=rank, world=world, noise_impl=impl, grad_out=g, accumulate=g is not None and not new,
+                          chain=self._chain() if self.defer_finalize else None, grad_scale_out=scale,
+                          path=os.environ.get("FDP_SOLO_PATH", "auto")).grad_w
                 done.append((m, gw, g is not None))
             if done and self.defer_finalize:
                 self._chain().flush()
@@ -258,6 +286,8 @@ class GroupedDPBackward:
             for lo in range(0, len(items), 48):  # fdp_backward_group takes up to 48 layers
                 chunk = items[lo:lo + 48]
                 direct = all(out_for(m) is not None for m, *_ in chunk)
+                # zeroed bucket views (each weight once in the chunk): written, not accumulated into
+                new = direct and all(fresh(m) for m, *_ in chunk) and len({id(m) for m, *_ in chunk}) == len(chunk)
                 try:
                     # a fresh (non-accumulating) group output is written whole by the kernel: no
                     # zero-fill; existing fp32 .grad tensors are accumulated into in place
@@ -266,7 +296,7 @@ class GroupedDPBackward:
                                   for _, x, dy, _, _, _ in chunk])
                     glayers = [(x, dy, cfg) for _, x, dy, cfg, _, _ in chunk]
                     kw = dict(grads=grads_out, noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
-                              mean_batch=mean_batch, max_ctas=self.max_ctas, accumulate=direct)
+                              mean_batch=mean_batch, max_ctas=self.max_ctas, accumulate=direct and not new)
                     try:
                         grp = PreparedGroup(glayers, workspace=self._ws, **kw)
                     except CapacityError:  # cached workspace too small for this layer list: grow it
@@ -281,7 +311,7 @@ class GroupedDPBackward:
                         g = out_for(m) if direct else None
                         grads.append(_run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise,
                                           mean_batch=mean_batch, rank=rank, world=world, noise_impl=impl,
-                                          grad_out=g, accumulate=g is not None).grad_w)
+                                          grad_out=g, accumulate=g is not None and not new).grad_w)
                 for (m, _, _, _, _, _), gw in zip(chunk, grads):
                     deliver(m, gw, direct)
 
@@ -292,6 +322,8 @@ _FITS: dict = {}
 def _fits_group(x_shape, dy_shape) -> bool:
     """Whether one layer's tiles fit the co-resident grid of the fused kernel (the
     multi-layer launch's per-layer condition); cached per shape."""
+    if os.environ.get("FDP_NO_GROUP") == "1":  # debug / tests: every layer through the per-layer kernels
+        return False
     key = (tuple(x_shape), tuple(dy_shape))
     v = _FITS.get(key)
     if v is None:

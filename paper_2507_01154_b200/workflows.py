@@ -125,7 +125,12 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
          accumulate: bool = False, add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
          skip_barrier: bool = False, short_timeout: bool = False, workspace: Optional[torch.Tensor] = None,
          device_step: Optional[torch.Tensor] = None, norm_phase: str = "auto",
-         deterministic: bool = False, chain: Optional[DeferredChain] = None) -> BackwardResult:
+         deterministic: bool = False, chain: Optional[DeferredChain] = None,
+         grad_scale_out: Optional[torch.Tensor] = None) -> BackwardResult:
+    """``grad_scale_out`` (a (1,) fp32 device tensor, FLASHDP only): fdp_dw_deferred --
+    on the single-sample path without noise the result holds the UNCLIPPED gradient
+    and grad_scale_out[0] its clip factor / mean divisor (else 1); the consumer forms
+    the product (include/fdp.h)."""
     dims = _dims(x, dy)
     if kind != WorkflowKind.NON_DP and cfg is None:
         raise UsageError("DP workflows need a DPConfig")
@@ -172,7 +177,14 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         ws = workspace.view(torch.uint8) if workspace.dtype != torch.uint8 else workspace
     else:
         ws = _POOL.get(ws_bytes.value, device, stream)
-    if chain is not None:
+    if grad_scale_out is not None:
+        if kind != WorkflowKind.FLASHDP or chain is not None or host:
+            raise UsageError("grad_scale_out needs kind FLASHDP, device inputs and no chain")
+        _check_out(grad_scale_out, (1,), torch.float32, device, "grad_scale_out")
+        _lib.check(lib.fdp_dw_deferred(ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),
+                                       norms.data_ptr(), grad_scale_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       stream.cuda_stream))
+    elif chain is not None:
         if host:
             raise UsageError("chain= needs device inputs (the pending finalize writes device memory later)")
         rc = lib.fdp_backward_chained(k, ctypes.byref(desc), xd.data_ptr(), yd.data_ptr(), grad.data_ptr(),

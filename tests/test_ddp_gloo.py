@@ -255,3 +255,80 @@ def test_grad_buckets_micro_batches_reduce_once():
             assert issued == issued1
             for a, b in zip(got, ref):
                 assert torch.allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------- deferred clip (scaled bucket)
+
+
+def _scaled_worker(rank, world, port, mode, out):
+    """One isolated weight is handed over UNscaled (grad / s_r) with its rank's
+    factor s_r (GradBuckets.mark_ready(p, scale=)): the collective multiplies every
+    rank's contribution by its own factor (gloo: in place first), at world 1 the
+    Adam step does -- the parameters equal a run with the scaled gradients."""
+    from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets, _torch_adam_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    model = _bucket_model()
+    w = model[2].weight
+    g = torch.Generator().manual_seed(4)
+    x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+    bk = GradBuckets(model.parameters(), bucket_bytes=600, mode=mode, rank=rank, world=world, flat_params=True,
+                     hooks=False, isolate=[w])
+    iso = [b for b in bk.buckets if any(p is w for p in b.params)]
+    assert len(iso) == 1 and len(iso[0].params) == 1
+    opt = BucketedAdam(bk, lr=1e-2, adam_fn=_torch_adam_)
+    per = 8 // world
+    for step in range(2):
+        bk.zero_grad()
+        assert bk.fresh(w)
+        lo, hi = rank * per, (rank + 1) * per
+        (((model(x[lo:hi]) - y[lo:hi]) ** 2).sum(1).sum() / 8).backward()
+        s = torch.tensor([0.5 + 0.25 * rank + 0.125 * step])
+        w.grad.div_(s)  # what the deferred kernel leaves: the gradient before its factor
+        for p in reversed(list(model.parameters())):
+            bk.mark_ready(p, scale=s if p is w else None)
+            bk.note_written(p)
+        assert not bk.fresh(w)
+        bk.finish()
+        opt.step(step)
+    out[(mode, world, rank)] = [p.detach().clone() for p in model.parameters()]
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_grad_buckets_deferred_scale_two_ranks():
+    for mode in ("allreduce", "reduce_scatter"):
+        with mp.Manager() as mgr:
+            out = mgr.dict()
+            _micro_ref = _bucket_model()  # the plain run: scaled gradients never divided
+            g = torch.Generator().manual_seed(4)
+            x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+            from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets, _torch_adam_
+
+            bk = GradBuckets(_micro_ref.parameters(), bucket_bytes=600, flat_params=True, hooks=False)
+            opt = BucketedAdam(bk, lr=1e-2, adam_fn=_torch_adam_)
+            for step in range(2):
+                bk.zero_grad()
+                (((_micro_ref(x) - y) ** 2).sum(1).sum() / 8).backward()
+                bk.finish()
+                opt.step(step)
+            ref = [p.detach().clone() for p in _micro_ref.parameters()]
+            _scaled_worker(0, 1, _free_port(), mode, out)
+            mp.spawn(_scaled_worker, args=(2, _free_port(), mode, out), nprocs=2, join=True)
+            for key in ((mode, 1, 0), (mode, 2, 0), (mode, 2, 1)):
+                for a, b in zip(out[key], ref):
+                    assert torch.allclose(a, b, rtol=1e-5, atol=1e-6), key
+
+
+def test_grad_buckets_scale_needs_own_bucket():
+    from paper_2507_01154_b200.ddp import GradBuckets
+
+    model = _bucket_model()
+    bk = GradBuckets(model.parameters(), bucket_bytes=1 << 20, flat_params=True, hooks=False)
+    assert len(bk.buckets) == 1 and not bk.can_defer(model[2].weight)
+    with pytest.raises(RuntimeError):
+        bk.mark_ready(model[2].weight, scale=torch.ones(1))

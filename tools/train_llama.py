@@ -53,7 +53,7 @@ def run(dp: bool, a, rank: int, world: int, dev: torch.device) -> dict:
     gB = a.batch * world
     step = DataParallelStep(model, dp=dp, mode="reduce_scatter" if a.zero1 else "allreduce", lr=1e-5,
                             rank=rank, world=world, comm_sms=a.comm_sms, bucket_bytes=a.bucket_mb << 20,
-                            global_batch=gB)
+                            global_batch=gB, defer_clip={"auto": None, "on": True, "off": False}[a.defer_clip])
     g = torch.Generator(device=dev).manual_seed(1 + rank)
     idx = torch.randint(0, cfg.vocab, (a.batch, a.seq + 1), device=dev, generator=g)
     x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
@@ -86,7 +86,7 @@ def run(dp: bool, a, rank: int, world: int, dev: torch.device) -> dict:
     out = {"ms_per_step": ms, "tokens_per_s": gB * a.seq / (ms * 1e-3),
            "loss_per_sample": float(loss.detach()) / (a.batch if dp else a.batch / gB),
            "dp_modules": len(step.dp_mods), "params": sum(p.numel() for p in model.parameters()),
-           "buckets": len(step.buckets.buckets), "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+           "buckets": len(step.buckets.buckets), "deferred_clips": step.last_deferred, "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
     return out
 
 
@@ -112,6 +112,8 @@ def main():
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--nondp-linear", default="fp32grad", choices=["fp32grad", "torch"])
     ap.add_argument("--arms", default="nondp,dp")
+    ap.add_argument("--defer-clip", default="auto", choices=["auto", "on", "off"],
+                    help="B = 1 per rank: clip factor applied by the collective / Adam (ddp.DataParallelStep)")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -127,7 +129,8 @@ def main():
         line = {"model": a.model, "layers": a.layers or LlamaConfig.named(a.model).layers, "gpus": world,
                 "batch_per_gpu": a.batch, "global_batch": a.batch * world, "seq": a.seq,
                 "parallelism": ("zero1" if a.zero1 else "allreduce") + f"-dp{world}",
-                "comm_sms": a.comm_sms, "bucket_mb": a.bucket_mb, "nondp_linear": a.nondp_linear}
+                "comm_sms": a.comm_sms, "bucket_mb": a.bucket_mb, "nondp_linear": a.nondp_linear,
+                "defer_clip": a.defer_clip}
         line.update(res)
         if "dp" in res and "nondp" in res:
             line["dp_pct_of_non_dp"] = 100.0 * res["dp"]["tokens_per_s"] / res["nondp"]["tokens_per_s"]
