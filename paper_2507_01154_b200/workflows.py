@@ -366,10 +366,16 @@ class PreparedBackward:
                  path: str = "auto", noise_impl: str = "keyed_f32", accumulate: bool = False,
                  add_noise: bool = True, rank: int = 0, world: int = 1, mean_batch: int = 0,
                  device_step: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
-                 norm_phase: str = "auto", deterministic: bool = False, chain: Optional["DeferredChain"] = None):
+                 norm_phase: str = "auto", deterministic: bool = False, chain: Optional["DeferredChain"] = None,
+                 grad_scale: Optional[torch.Tensor] = None):
         dims = _dims(x, dy)
         if not (x.is_cuda and dy.is_cuda and x.is_contiguous() and dy.is_contiguous() and x.dtype == dy.dtype):
             raise UsageError("PreparedBackward needs contiguous CUDA inputs of one dtype")
+        if grad_scale is not None:  # fdp_dw_deferred (include/fdp.h): the consumer applies grad_scale[0]
+            if kind != WorkflowKind.FLASHDP or chain is not None:
+                raise UsageError("grad_scale needs kind FLASHDP and no chain")
+            _check_out(grad_scale, (1,), torch.float32, x.device, "grad_scale")
+        self.grad_scale = grad_scale
         self.chain = chain
         c = cfg or DPConfig(clip_c=1.0, sigma=0.0)
         self.kind = kind
@@ -416,6 +422,10 @@ class PreparedBackward:
         s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
         if self.chain is not None:  # single-sample finalize deferred into the next chained call
             _lib.check(self._lib.fdp_backward_chained(*self._args, self.chain.handle, s.cuda_stream))
+        elif self.grad_scale is not None:
+            a = self._args
+            _lib.check(self._lib.fdp_dw_deferred(a[1], a[2], a[3], a[4], a[5], self.grad_scale.data_ptr(), a[6], a[7],
+                                                 s.cuda_stream))
         else:
             _lib.check(self._lib.fdp_backward(*self._args, s.cuda_stream))
 

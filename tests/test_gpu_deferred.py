@@ -194,3 +194,39 @@ def test_bucketed_llama_deferred_clip(mode):
             assert min(d2) == 7 * 2 + 1
             for a, b in zip(got2, ref):
                 assert torch.allclose(a, b, rtol=1e-4, atol=2e-6), (r, float((a - b).abs().max()))
+
+
+def _nccl_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2507_01154_b200.ddp import GradBuckets
+
+    res = {}
+    # all-reduce only: NCCL runs a one-rank reduce-scatter as a plain copy (no PreMulSum
+    # pre-op); the multi-rank reduce-scatter path is the gloo emulation's (test_ddp_gloo)
+    for mode in ("allreduce",):
+        w = torch.nn.Parameter(torch.zeros(64, 33, device="cuda"))
+        bk = GradBuckets([w], mode=mode, flat_params=True, hooks=False, isolate=[w])
+        bk.zero_grad()
+        G = torch.randn(64, 33, device="cuda")
+        w.grad.copy_(G)
+        s = torch.tensor([0.3125], device="cuda")
+        bk.mark_ready(w, scale=s)
+        b = bk.buckets[0]
+        bk._collective(b)  # world 1: a real NCCL PreMulSum collective with the device scalar
+        torch.cuda.synchronize()
+        res[mode] = (bool(b.scale_applied), float((w.grad - G * s).abs().max()))
+    out["nccl"] = res
+    dist.destroy_process_group()
+
+
+def test_nccl_premul_sum_collective_applies_scale():
+    """The bucket all-reduce of a deferred-clip bucket on the real NCCL backend
+    (one rank): PreMulSum with the device scalar leaves scale * G in the bucket."""
+    with mp.get_context("spawn").Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
+        for mode, (applied, err) in out["nccl"].items():
+            assert applied and err == 0.0, (mode, err)

@@ -12,6 +12,9 @@ q), back to back on one stream:
   dp_shared_x the unchained calls with q/k/v and gate/up each through ONE
               fdp_backward_shared_x call (they read the same X: one X Gram per tile
               pair in the ghost phase)
+  dp_deferred B = 1: the unchained calls through fdp_dw_deferred (no noise in the
+              call; the clip factor is left for the optimizer step / collective,
+              which adds the noise too -- what ddp.DataParallelStep runs at B = 1)
   nondp       cuBLAS torch.mm(dY^T, X, out_dtype=fp32) per layer
 and each layer alone (dp_us / nondp_us per layer).
 
@@ -61,7 +64,7 @@ def main():
                   ("q", d, d)]
         for B in (int(b) for b in a.batches.split(",")):
             row = {"model": name, "B": B, "T": T, "layers": {}}
-            ins, chained, plain, nd, own = [], [], [], [], []
+            ins, chained, plain, nd, own, deferred = [], [], [], [], [], []
             shared_x = {}
             chain = fdp.DeferredChain()
             ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
@@ -84,6 +87,10 @@ def main():
                                                   grad_w=gw, norms_sq=nrm, workspace=ws))
                 chained.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
                                                     grad_w=gw, norms_sq=nrm, workspace=ws, chain=chain))
+                if B == 1:
+                    deferred.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
+                                                         grad_w=gw, norms_sq=nrm, workspace=ws, add_noise=False,
+                                                         grad_scale=torch.zeros(1, device="cuda")))
                 own.append(fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox",
                                                 grad_w=gw, norms_sq=nrm))  # own workspace (shared-X arm)
                 x2, y2 = x.view(-1, P), dy.view(-1, D)
@@ -116,14 +123,18 @@ def main():
                 for c in sx_calls:
                     c()
 
+            def dp_deferred():
+                for c in deferred:
+                    c()
+
             def nondp():
                 for x2, y2 in nd:
                     torch.mm(y2.t(), x2, out_dtype=torch.float32)
 
             res = {}
             for _ in range(2):  # alternate, keep the best
-                for k, fn in (("dp_chained", dp_chained), ("dp", dp_plain), ("dp_shared_x", dp_shared_x),
-                              ("nondp", nondp)):
+                arms = [("dp_chained", dp_chained), ("dp", dp_plain), ("dp_shared_x", dp_shared_x), ("nondp", nondp)]
+                for k, fn in arms + ([("dp_deferred", dp_deferred)] if deferred else []):
                     t = timed(fn, a.reps)
                     res[k] = min(res.get(k, 1e30), t)
             st = chain.stats()
@@ -134,8 +145,12 @@ def main():
                         "dp_shared_x_us": round(res["dp_shared_x"], 1),
                         "dw_ratio_shared_x": round(res["dp_shared_x"] / res["nondp"], 3),
                         "implied_step_pct_of_nondp": round(100.0 * 3.0 / (2.0 + r), 1), "chain": st})
+            if deferred:
+                rd = res["dp_deferred"] / res["nondp"]
+                row.update({"dp_deferred_us": round(res["dp_deferred"], 1), "dw_ratio_deferred": round(rd, 3),
+                            "implied_step_pct_deferred": round(100.0 * 3.0 / (2.0 + rd), 1)})
             print(json.dumps(row), flush=True)
-            del ins, chained, plain, nd, chain, ws, own, sx_calls, shared_x
+            del ins, chained, plain, nd, chain, ws, own, sx_calls, shared_x, deferred
             torch.cuda.empty_cache()
 
 
