@@ -1514,6 +1514,7 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   gp.trace = (descs[0].flags & FDP_FLAG_TRACE) ? ws_at<unsigned long long>(ws, gpl.total - 2048ull * gpl.grid) : nullptr;
   gp.n_layers = n;
   gp.nosync = env_int("FDP_DEBUG_NOSYNC", 0);
+  gp.dbg_tmem = env_int("FDP_DEBUG_GROUP_TMEM", 0);
   gp.dbg_noise = env_int("FDP_DEBUG_NOISE", 0);
   gp.poll_ns = env_int("FDP_POLL_NS", 0);
   gp.pub_mode = env_int("FDP_PUB_MODE", 1);

@@ -30,13 +30,15 @@
 
 namespace fdp {
 
-template <int BN, int CG>
+// NSTG: store-staging buffers (2 = double-buffered 32-column box pairs; 1 = one
+// buffer, whose 32 KB become a sixth operand stage at BN 256, CG 2: FDP_GROUP_STG1)
+template <int BN, int CG, int NSTG = 2>
 struct GCfg {
   static constexpr int kBCols = BN / CG;
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = kBCols * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStgBytes = 4 * kBM * 128;  // 2 buffers x two 32-column fp32 boxes (one per column half)
+  static constexpr int kStgBytes = NSTG * 2 * kBM * 128;  // NSTG buffers x two 32-column fp32 boxes (column halves)
   static constexpr int kStages = (232448 - 2048 - kStgBytes) / kStageBytes;
   static constexpr int kNBuf = 512 / BN;
   static constexpr int kCPT = BN / 2;
@@ -50,9 +52,9 @@ struct GCfg {
     if (gp.trace && etid == 0 && (slot) < 256) gp.trace[blockIdx.x * 256 + (slot)] = globaltimer_ns(); \
   } while (0)
 
-template <int BN, int CG>
+template <int BN, int CG, int NSTG>
 __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_constant__ GroupParams gp) {
-  using C = GCfg<BN, CG>;
+  using C = GCfg<BN, CG, NSTG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + C::kStages * C::kStageBytes;  // 1024-aligned: two 16 KB swizzled boxes
@@ -263,13 +265,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
     auto pass1_publish = [&](const GLayer& Lx, int bx, int tilex, uint32_t bufx) {
       const uint32_t tbx = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bufx * BN + col0;
       float part = 0.0f;
+      if (gp.dbg_tmem != 1) {
 #pragma unroll
-      for (int c = 0; c < C::kCPT / 16; ++c) {
-        float v[16];
-        tmem_ld16(tbx + c * 16, v);
-        tmem_wait_ld();
+        for (int c = 0; c < C::kCPT / 16; ++c) {
+          float v[16];
+          tmem_ld16(tbx + c * 16, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+          for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -362,13 +366,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
         }
         named_bar_sync(1, 32 * kEpiWarps);
         const float f = *bcast;
+        if (gp.dbg_tmem != 2) {
 #pragma unroll
-        for (int c = 0; c < C::kCPT / 16; ++c) {
-          float v[16];
-          tmem_ld16(tb + c * 16, v);
-          tmem_wait_ld();
+          for (int c = 0; c < C::kCPT / 16; ++c) {
+            float v[16];
+            tmem_ld16(tb + c * 16, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+            for (int i = 0; i < 16; ++i) acc[c * 16 + i] = fmaf(f, v[i], acc[c * 16 + i]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -402,8 +408,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
       if (l < 16) GTRACE(8 * l + 3);
 #pragma unroll
       for (int c = 0; c < C::kCPT / 32; ++c) {
-        uint8_t* sbuf = stg + (c & 1) * (2 * kBM * 128);
-        if (etid == 0) bulk_wait_read_le1();  // the boxes issued two rounds ago have left this buffer
+        uint8_t* sbuf = stg + (NSTG == 2 ? (c & 1) : 0) * (2 * kBM * 128);
+        if (etid == 0) {  // the boxes issued NSTG rounds ago have left this buffer
+          if constexpr (NSTG == 2) bulk_wait_read_le1();
+          else bulk_wait_read_all();
+        }
         named_bar_sync(1, 32 * kEpiWarps);
         uint8_t* box = sbuf + half * (kBM * 128) + row * 128;
 #pragma unroll
@@ -454,14 +463,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) dpdw_group_kernel(const __grid_
   }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int NSTG = 2>
 static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream_t stream) {
-  using C = GCfg<BN, CG>;
+  using C = GCfg<BN, CG, NSTG>;
   static bool done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(dpdw_group_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dpdw_group_kernel<BN, CG, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) done[dev] = true;
@@ -487,7 +496,7 @@ static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG, NSTG>, gp);
   // The in-kernel norm all-reduce spin-waits on other CTAs: it needs the
   // co-residency guarantee of the cooperative launch, especially while a
   // collective runs concurrently on other SMs. A rejected cooperative launch is
@@ -498,14 +507,18 @@ static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream
   if (e != cudaSuccess && CG == 2 && std::getenv("FDP_ALLOW_NONCOOP")) {
     (void)cudaGetLastError();
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG>, gp);
+    e = cudaLaunchKernelEx(&cfg, dpdw_group_kernel<BN, CG, NSTG>, gp);
   }
   return e;
 }
 
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream) {
   if (cg == 2) {
-    if (bn == 256) return launch_group_impl<256, 2>(gp, grid, stream);
+    if (bn == 256) {
+      const char* v = std::getenv("FDP_GROUP_STG1");  // read per call (A/B tooling)
+      const bool stg1 = v && std::atoi(v) != 0;
+      return stg1 ? launch_group_impl<256, 2, 1>(gp, grid, stream) : launch_group_impl<256, 2>(gp, grid, stream);
+    }
     return launch_group_impl<128, 2>(gp, grid, stream);
   }
   if (bn == 256) return launch_group_impl<256, 1>(gp, grid, stream);

@@ -159,6 +159,7 @@ struct GroupParams {
   int dbg_noise;  // debug (FDP_DEBUG_NOISE): 1 = no draws (zero pre-fill), 2 = draws scaled by 0
   int pub_mode, poll_mode, poll_ns;  // experiments (FDP_PUB_MODE, FDP_POLL_MODE, FDP_POLL_NS)
   int nosync;  // debug (FDP_DEBUG_NOSYNC): clip factors from whatever partials are present, no wait
+  int dbg_tmem;  // timing experiments only (FDP_DEBUG_GROUP_TMEM): 1 skip the norm pass's TMEM loads, 2 the clip pass's
   // noise / row pre-fill run-ahead bound: the noise warps start layer l once the
   // epilogue has started layer l - pf_ahead (FDP_PF_AHEAD; < 0 = unbounded)
   int pf_ahead;
