@@ -14,7 +14,8 @@ from pathlib import Path
 from .errors import CapacityError, ShapeError, UsageError
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_fdp.so"
+# FDP_LIB_PATH: an alternative build of the same sources (A/B of compile-time variants only)
+LIB_PATH = Path(os.environ["FDP_LIB_PATH"]) if os.environ.get("FDP_LIB_PATH") else _HERE / "_fdp.so"
 
 FDP_OK, FDP_ERR_SHAPE, FDP_ERR_USAGE, FDP_ERR_CAPACITY, FDP_ERR_CUDA = range(5)
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
