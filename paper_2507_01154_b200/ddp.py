@@ -345,6 +345,12 @@ class GradBuckets:
                 self._where[id(p)] = i
         cuda = self.device.type == "cuda"
         self.comm = torch.cuda.Stream(self.device) if cuda and world > 1 else None
+        # deferred-clip buckets at N > 1 scale inside the collective (NCCL PreMulSum with a
+        # device scalar); a one-time probe at construction (every rank builds its buckets)
+        # checks that both collectives of the mode apply it, else each bucket is scaled in
+        # place before a plain collective
+        self.premul = bool(iso) and world > 1 and dist.is_initialized() and dist.get_backend(group) == "nccl" \
+            and self._probe_premul()
         self._handles = []
         if hooks:
             import weakref
@@ -366,6 +372,25 @@ class GradBuckets:
         self.issued: list[int] = []  # bucket issue order of the last backward (tests / traces)
         self.enabled = True  # False while accumulating micro-batches (no collectives)
         self.trace = [] if os.environ.get("FDP_DDP_TRACE") == "1" else None  # (bucket, param, pending) per ready
+
+    def _probe_premul(self) -> bool:
+        w, dev = self.world, self.device
+        want = float(sum(r + 2 for r in range(w)))
+        s = torch.tensor([float(self.rank + 2)], device=dev)
+        try:
+            t = torch.ones(4 * w, device=dev)
+            dist.all_reduce(t, op=dist._make_nccl_premul_sum(s), group=self.group)
+            ok = bool(torch.all(t == want))
+            if self.mode == "reduce_scatter":
+                out = torch.empty(4, device=dev)
+                dist.reduce_scatter_tensor(out, torch.ones(4 * w, device=dev), op=dist._make_nccl_premul_sum(s),
+                                           group=self.group)
+                ok = ok and bool(torch.all(out == want))
+        except (RuntimeError, AttributeError, TypeError):
+            ok = False
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)  # one decision for every rank
+        return bool(flag.item())
 
     def _close(self, params, flat_params):
         b = _Bucket()
@@ -502,9 +527,9 @@ class GradBuckets:
         nccl = dist.get_backend(self.group) == "nccl"
         op = dist.ReduceOp.SUM
         if b.scale is not None:  # deferred clip: each rank's contribution times its own factor
-            if nccl:
+            if nccl and self.premul:
                 op = dist._make_nccl_premul_sum(b.scale)
-            else:
+            else:  # gloo, or an NCCL whose PreMulSum failed the probe: scale in place first
                 b.flat.mul_(b.scale.to(b.flat.device))
             b.scale_applied = True
         if self.mode == "allreduce":

@@ -215,7 +215,9 @@ def _nccl_worker(rank, world, port, out):
         s = torch.tensor([0.3125], device="cuda")
         bk.mark_ready(w, scale=s)
         b = bk.buckets[0]
-        bk._collective(b)  # world 1: a real NCCL PreMulSum collective with the device scalar
+        assert not bk.premul  # the probe only runs at world > 1
+        bk.premul = True  # world 1: force a real NCCL PreMulSum collective with the device scalar
+        bk._collective(b)
         torch.cuda.synchronize()
         res[mode] = (bool(b.scale_applied), float((w.grad - G * s).abs().max()))
     out["nccl"] = res
