@@ -15,7 +15,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 from paper_2507_01154_b200.ddp import DataParallelStep  # noqa: E402
 from paper_2507_01154_b200.llama import Llama, LlamaConfig  # noqa: E402
 
-GROUPS = [("fdp_dp_dW", ("dpdw_", "ghost_norm", "k_single_finalize", "k_reduce_norms")),
+GROUPS = [("fdp_dp_dW", ("dpdw_", "ghost_norm", "k_single_finalize", "k_reduce_norms", "k_single_factor")),
           ("fdp_optimizer", ("k_adam", "k_sgd")),
           ("fdp_param_groups", ("k_vec_", "k_emb_")),
           ("gemm (cuBLAS)", ("nvjet", "gemm", "cutlass", "sm90_", "sm100_")),
