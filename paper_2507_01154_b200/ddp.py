@@ -541,6 +541,16 @@ class GradBuckets:
         else:  # gloo: all-reduce, keep this rank's slice (b.shard is a view of it)
             dist.all_reduce(b.flat, op=op, group=self.group)
 
+    def materialize_scales(self) -> None:
+        """Apply every pending deferred-clip factor to its bucket in place (for a
+        caller that reads .grad itself -- logging, clipping diagnostics -- instead of
+        handing the buckets to BucketedAdam). After finish(); world 1 only has
+        pending factors (at N > 1 the collective applied them)."""
+        for b in self.buckets:
+            if b.scale is not None and not b.scale_applied:
+                b.flat.mul_(b.scale)
+                b.scale_applied = True
+
     def finish(self) -> None:
         """After backward: issue any bucket not yet issued (parameters without a
         gradient this step), in bucket order, then order the current stream after

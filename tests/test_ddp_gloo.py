@@ -332,3 +332,27 @@ def test_grad_buckets_scale_needs_own_bucket():
     assert len(bk.buckets) == 1 and not bk.can_defer(model[2].weight)
     with pytest.raises(RuntimeError):
         bk.mark_ready(model[2].weight, scale=torch.ones(1))
+
+
+def test_grad_buckets_materialize_scales_and_isolation_layout():
+    from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets, _torch_adam_
+
+    model = _bucket_model()
+    w = model[2].weight
+    bk = GradBuckets(model.parameters(), bucket_bytes=1 << 20, flat_params=True, hooks=False, isolate=[w])
+    # the isolated weight sits alone between the buckets of its neighbours (reverse registration order)
+    owners = [[q for q in b.params] for b in bk.buckets]
+    assert [len(o) for o in owners] == [3, 1, 2] and owners[1][0] is w
+    opt = BucketedAdam(bk, lr=1e-2, adam_fn=_torch_adam_)
+    bk.zero_grad()
+    w.grad.copy_(torch.ones_like(w))
+    bk.mark_ready(w, scale=torch.tensor([0.25]))
+    bk.materialize_scales()
+    assert torch.all(w.grad == 0.25) and bk.buckets[1].scale_applied
+    before = w.detach().clone()
+    opt.step(0)  # the optimizer does not apply the factor a second time
+    ref = before.clone()
+    m, v = torch.zeros_like(ref), torch.zeros_like(ref)
+    _torch_adam_(ref.view(-1), m.view(-1), v.view(-1), torch.full_like(ref, 0.25).view(-1), 1e-2, 0.9, 0.999, 1e-8,
+                 None, 0, None, 0)
+    assert torch.allclose(w.detach(), ref)
