@@ -216,8 +216,11 @@ class GroupedDPBackward:
                 return g
             return None
 
+        claimed: set = set()  # weights already written by an earlier call of this flush
+
         def fresh(m):  # its bucket view holds zeros: overwrite instead of accumulating
-            return bk is not None and out_for(m) is not None and bk.fresh(m.weight)
+            return (bk is not None and id(m.weight) not in claimed and out_for(m) is not None
+                    and bk.fresh(m.weight))
 
         scales: dict = {}
 
@@ -264,10 +267,12 @@ class GroupedDPBackward:
                                         noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
                                         mean_batch=mean_batch)
                     done.extend((m, gw, out_for(m) is not None) for (m, *_), gw in zip(run, gws))
+                    claimed.update(id(m.weight) for m, *_ in run)
                     continue
                 m, x, dy, cfg, _, _ = run[0]
                 g = out_for(m)
                 new = fresh(m)
+                claimed.add(id(m.weight))
                 scale = None
                 if (self.defer_clip and new and not add_noise and x.shape[0] == 1 and not self.defer_finalize
                         and bk.can_defer(m.weight)):
@@ -288,6 +293,7 @@ class GroupedDPBackward:
                 direct = all(out_for(m) is not None for m, *_ in chunk)
                 # zeroed bucket views (each weight once in the chunk): written, not accumulated into
                 new = direct and all(fresh(m) for m, *_ in chunk) and len({id(m) for m, *_ in chunk}) == len(chunk)
+                claimed.update(id(m.weight) for m, *_ in chunk)
                 try:
                     # a fresh (non-accumulating) group output is written whole by the kernel: no
                     # zero-fill; existing fp32 .grad tensors are accumulated into in place
