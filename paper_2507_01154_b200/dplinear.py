@@ -263,7 +263,9 @@ class GroupedDPBackward:
             for run in runs:
                 if len(run) > 1:
                     self.shared_x_calls += 1
-                    gws = _run_shared_x(run[0][1], [(dy, cfg, out_for(m)) for m, _, dy, cfg, _, _ in run],
+                    # fresh bucket views are written, not accumulated into (no read of the zeros)
+                    specs = [(dy, cfg, out_for(m), not fresh(m)) for m, _, dy, cfg, _, _ in run]
+                    gws = _run_shared_x(run[0][1], specs,
                                         noise_impl=impl, add_noise=add_noise, rank=rank, world=world,
                                         mean_batch=mean_batch)
                     done.extend((m, gw, out_for(m) is not None) for (m, *_), gw in zip(run, gws))

@@ -229,8 +229,8 @@ def _run_shared_x(x: torch.Tensor, layers: list, *, noise_impl: str = "keyed_f32
                   rank: int = 0, world: int = 1, mean_batch: int = 0) -> list:
     """FLASHDP backward of 1..3 layers that read the same device input X through ONE
     fdp_backward_shared_x call (include/fdp.h: the ghost phase computes X X^T once for
-    all of them). `layers`: (dy, cfg, grad_out or None) per layer; returns the grads
-    (grad_out, accumulated into, when given)."""
+    all of them). `layers`: (dy, cfg, grad_out or None[, accumulate]) per layer; returns
+    the grads (grad_out, accumulated into when given unless accumulate is False)."""
     n = len(layers)
     if not 1 <= n <= 3:
         raise UsageError(f"_run_shared_x takes 1..3 layers, got {n}")
@@ -238,12 +238,14 @@ def _run_shared_x(x: torch.Tensor, layers: list, *, noise_impl: str = "keyed_f32
     device = x.device
     descs = (_lib.FdpDesc * n)()
     grads, norms, sizes = [], [], []
-    for k, (dy, cfg, g) in enumerate(layers):
+    for k, entry in enumerate(layers):
+        dy, cfg, g = entry[:3]
+        acc = bool(entry[3]) if len(entry) > 3 else g is not None
         dims = _dims(x, dy)
         descs[k] = _lib.make_desc(B=dims.B, T=dims.T, P=dims.P, D=dims.D, in_dtype=_input_dtype_code(x),
                                   reduction=cfg.reduction, clip_c=cfg.clip_c, sigma=cfg.sigma, seed=cfg.seed,
                                   layer_id=cfg.layer_id, step=cfg.step, rank=rank, world=world,
-                                  mean_batch=mean_batch, accumulate=g is not None, add_noise=add_noise,
+                                  mean_batch=mean_batch, accumulate=acc and g is not None, add_noise=add_noise,
                                   noise_impl=noise_impl)
         nb = ctypes.c_size_t()
         _lib.check(lib.fdp_workspace_bytes(ctypes.byref(descs[k]), _lib.KIND["flashdp"], ctypes.byref(nb)))
@@ -256,7 +258,7 @@ def _run_shared_x(x: torch.Tensor, layers: list, *, noise_impl: str = "keyed_f32
     # one workspace per layer (the ghost phase fills every layer's partials before any reweight)
     wss = [_POOL.get(sizes[k], device, stream, slot=("shared_x", k)) for k in range(n)]
     ptrs = ctypes.c_void_p * n
-    rc = lib.fdp_backward_shared_x(n, descs, x.data_ptr(), ptrs(*[dy.data_ptr() for dy, _, _ in layers]),
+    rc = lib.fdp_backward_shared_x(n, descs, x.data_ptr(), ptrs(*[e[0].data_ptr() for e in layers]),
                                    ptrs(*[g.data_ptr() for g in grads]), ptrs(*[t.data_ptr() for t in norms]),
                                    ptrs(*[w.data_ptr() for w in wss]),
                                    (ctypes.c_size_t * n)(*[w.numel() for w in wss]), stream.cuda_stream)
