@@ -1022,9 +1022,14 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
   // TWO_PHASE: norm phase (ghost Gram norms or recompute), factors, one reweighted pass
   {
     fdp::TcParams p = tc_params(d, pl, c, grad_w, norms, ws, fdp::MODE_NORMS);
+    bool pdl = false;
     if (pl.norm_phase == FDP_NORMS_GHOST && pre_parts > 0) {
+      // shared X: the partials come from the Gram launch (first layer) -- or wait on the
+      // previous layer's reweight, which the PDL reduce does by itself (it waits for the
+      // grid before it to complete)
+      pdl = use_stream && env_int("FDP_PDL", 1) != 0;
       if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, pre_parts, d->clip_c, p.clip_c2, c.inv_batch, norms,
-                                            ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+                                            ws_at<float>(ws, pl.off_factor), s, pdl)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     } else if (pl.norm_phase == FDP_NORMS_GHOST) {
       CUtensorMap gx, gy;
@@ -1053,8 +1058,11 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
         const int grid = g.n_items < slots ? g.n_items : slots;
         if ((e = fdp::launch_ghost(gx, gy, g, grid, s)) != cudaSuccess) return cuda_fail(e, "ghost-norm launch");
       }
+      // programmatic dependent launches (FDP_PDL, default on): the reduce and the reweight
+      // are queued while the ghost kernel drains; only the reweight's epilogue waits
+      pdl = use_stream && env_int("FDP_PDL", 1) != 0;
       if ((e = fdp::reduce_norms_to_factors(p.ws_part, p.B, gs.parts, d->clip_c, p.clip_c2, c.inv_batch, norms,
-                                            ws_at<float>(ws, pl.off_factor), s)) != cudaSuccess)
+                                            ws_at<float>(ws, pl.off_factor), s, pdl)) != cudaSuccess)
         return cuda_fail(e, "factor reduce");
     } else {
       if ((e = fdp::launch_tc(pl.bn, pl.cg, tm_dy, tm_x, em, p, pl.grid, false, s)) != cudaSuccess)
@@ -1066,6 +1074,7 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
     if (use_stream) {  // stream-K over (tile, sample) units: no partial last wave
       fdp::StreamParams q = stream_params(d, pl, c, grad_w, ws, true);
       q.fin = carry;
+      q.pdl = pdl ? 1 : 0;
       if ((e = fdp::launch_stream(pl.bn, pl.cg, tm_dy, tm_x, em.gw, q, stream_grid(d, pl, di), s)) != cudaSuccess)
         return cuda_fail(e, "stream-K reweight launch");
       stream_trace_report(q, "reweight", stream_grid(d, pl, di), s);

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   unsigned* err = p.err;
+  if (threadIdx.x == 0) pdl_launch_dependents();  // the factor reduce / reweight may queue up behind us
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&full[s], 1);
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int cid = blockIdx.x / 2, n_clusters = gridDim.x / 2;
   // layers sharing X (n_dy > 1, split == 1): one Gx per item, then one Gy per layer
   const int n_dy = p.n_dy > 1 ? p.n_dy : 1;
+  if (threadIdx.x == 0) pdl_launch_dependents();  // the factor reduce / reweight may queue up behind us
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&full[s], 1);

@@ -122,6 +122,7 @@ struct StreamParams {
   int swizzle;  // tile raster: 0/1 row-major, G > 1 grouped by G row blocks (FDP_STREAM_SWIZZLE)
   int dbg;      // timing experiments only (FDP_DEBUG_STREAM): 1 skip the TMEM readout, 2 skip the MMAs
   unsigned long long* trace;  // FDP_STREAM_TRACE: per-CTA wait-time totals [gridDim.x][8] (ns), or null
+  int pdl;  // launched as a programmatic dependent of the factor reduce (epilogue waits on it)
 };
 // Work tiles of the stream kernel (MC pair tiles stacked along D) and its per-CTA tile slots.
 inline int stream_wtiles(int n_wtiles, int n_pt, int mc) {
@@ -216,8 +217,10 @@ struct SimtParams {
   int with_clip;      // 0: non-DP sum
 };
 cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s);
+// pdl: launched as a programmatic dependent of the norm-phase kernel (starts while it drains)
 cudaError_t reduce_norms_to_factors(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
-                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s);
+                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s,
+                                    bool pdl = false);
 cudaError_t simt_weighted_sum(const SimtParams& p, cudaStream_t s);
 
 // explicit (Opacus-style) stages over a materialised G (B,D,P)

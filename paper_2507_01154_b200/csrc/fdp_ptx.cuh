@@ -325,6 +325,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Programmatic dependent launch: let the next kernel on the stream (launched with the
+// programmatic-serialization attribute) start its prologue now / wait for the previous
+// grid's completion and memory before reading what it produced (no-ops otherwise).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // generic-proxy writes -> subsequent async-proxy (TMA) accesses, and vice versa
 __device__ __forceinline__ void fence_proxy_async_global() {

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "fdp_internal.h"
+#include "fdp_ptx.cuh"
 #include "fdp_rng.cuh"
 #include <cuda_bf16.h>
 
@@ -74,6 +75,8 @@ __global__ void __launch_bounds__(256) k_partial_norms(const SimtParams p) {
 // One warp per sample: fixed-order double sum of the partials -> norm^2, clip factor.
 __global__ void k_reduce_norms(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
                                float inv_batch, float* norms_out, float* factors) {
+  pdl_launch_dependents();  // the reweight may start its prologue / mainloop now
+  pdl_wait();               // the norm partials are complete (no-op without PDL)
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -429,11 +432,18 @@ cudaError_t simt_partial_norms(const SimtParams& p, cudaStream_t s) {
 }
 
 cudaError_t reduce_norms_to_factors(const float* part, int B, int n_tiles, double clip_c, double clip_c2,
-                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s) {
+                                    float inv_batch, float* norms_out, float* factors, cudaStream_t s, bool pdl) {
   const int warps_per_block = 4;
-  k_reduce_norms<<<(B + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, s>>>(
-      part, B, n_tiles, clip_c, clip_c2, inv_batch, norms_out, factors);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((B + warps_per_block - 1) / warps_per_block);
+  cfg.blockDim = dim3(32 * warps_per_block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_reduce_norms, part, B, n_tiles, clip_c, clip_c2, inv_batch, norms_out, factors);
 }
 
 cudaError_t simt_weighted_sum(const SimtParams& p, cudaStream_t s) {

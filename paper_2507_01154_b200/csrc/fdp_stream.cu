@@ -456,6 +456,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ======================= epilogue =======================
+    // PDL launch: the clip factors come from the grid before us (the factor reduce);
+    // producer and MMA warps (inputs only) run ahead while it finishes
+    if (p.pdl) pdl_wait();
     const int ew = warp - kEpiWarp0;
     const int q = warp & 3, half = ew >> 2, etid = ew * 32 + lane;
     const int row = q * 32 + lane, col0 = half * C::kCPT;
@@ -661,14 +664,19 @@ static cudaError_t launch_stream_impl(const CUtensorMap& tm_dy, const CUtensorMa
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int na = 0;
   if (CG * MC > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG * MC;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    na = 1;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CG * MC;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (p.pdl) {  // programmatic dependent of the factor reduce: CTAs start as SMs free up
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
