@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256, kMode == 0 ? 1 : kMinB)
                       double clip_c2, float inv_batch, float* norms_out, int add_noise, int impl, float scale,
                       uint64_t base, uint64_t base_g, const long long* step_ptr, uint64_t seed_u, uint64_t layer_u,
                       long long lo, long long hi) {
+  pdl_wait();  // PDL launch behind the single-sample GEMM: G and its partials are complete
   float4* g4 = reinterpret_cast<float4*>(g);
   const long long n4 = n >> 2;  // n = D * P, P % 8 == 0
   constexpr int kU = kMode == 0 ? 4 : kUV;  // float4 per thread per iteration: loads in flight
@@ -294,6 +295,12 @@ __global__ void __launch_bounds__(256, kMode == 0 ? 1 : kMinB)
   }
 }
 
+// FDP_PDL=0 turns the programmatic dependent launches off (A/B)
+bool pdl_enabled() {
+  const char* v = std::getenv("FDP_PDL");
+  return !v || std::atoi(v) != 0;
+}
+
 int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -310,11 +317,21 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
   // Philox over the whole tensor (the common case) or no noise: the lean variants
   const int mode = !add_noise || hi <= lo ? 2 : (impl == 2 && lo <= 0 && hi >= n) ? 1 : 0;
   const int threads = 256;
+  // plain launch: as a programmatic dependent of the GEMM (its blocks resident early, waiting)
+  // it measured 1-2 % slower on the up / down projections, neutral on square ones
+  // (profiles/r2_pdl_ab.jsonl); the kernel's griddepcontrol.wait is then a no-op
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
   if (mode == 0) {
-    k_single_finalize<0><<<grid_for(n / 16, threads), threads, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2,
-                                                                         inv_batch, norms_out, add_noise, impl,
-                                                                         noise_scale, base, base_g, step_ptr, seed_u,
-                                                                         layer_u, lo, hi);
+    cfg.gridDim = dim3(grid_for(n / 16, threads));
+    return cudaLaunchKernelEx(&cfg, k_single_finalize<0>, grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch,
+                              norms_out, add_noise, impl, noise_scale, base, base_g, step_ptr, seed_u, layer_u, lo, hi);
   } else {
     long long blocks = (n / 8 + threads - 1) / threads;
     const long long cap = 148LL * 6 * 4;  // 6 resident blocks per SM, a few rounds each
@@ -323,11 +340,10 @@ cudaError_t single_sample_finalize(float* grad_w, long long n, const float* part
     // measured (tools/ab_layer.py): 4 float4 per thread at 4 blocks/SM, or 8 blocks/SM, are slower;
     // the pass sits at HBM speed without noise and the Philox draws add ~20 %
     auto k = mode == 1 ? k_single_finalize<1> : k_single_finalize<2>;
-    k<<<static_cast<int>(blocks), threads, 0, s>>>(grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch, norms_out,
-                                                  add_noise, impl, noise_scale, base, base_g, step_ptr, seed_u,
-                                                  layer_u, lo, hi);
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+    return cudaLaunchKernelEx(&cfg, k, grad_w, n, part, n_parts, clip_c, clip_c2, inv_batch, norms_out, add_noise,
+                              impl, noise_scale, base, base_g, step_ptr, seed_u, layer_u, lo, hi);
   }
-  return cudaGetLastError();
 }
 
 // spill combine: out = (accumulate ? out : 0) + sum_b fac[b] * G[b] (+ noise), b in order
@@ -400,6 +416,7 @@ cudaError_t spill_combine(float* out, const float* G, int B, long long n, const 
 // ||G||^2; part == nullptr writes scale 1 (the call finalised grad_w in place).
 __global__ void k_single_factor(const float* __restrict__ part, int n_parts, double clip_c, double clip_c2,
                                 float inv_batch, float* norms_out, float* scale_out) {
+  pdl_wait();  // PDL launch behind the single-sample GEMM
   if (!part) {
     if (threadIdx.x == 0) scale_out[0] = 1.0f;
     return;
@@ -416,8 +433,17 @@ __global__ void k_single_factor(const float* __restrict__ part, int n_parts, dou
 }
 
 cudaError_t single_sample_factor(const FinJob& j, float* scale_out, cudaStream_t s) {
-  k_single_factor<<<1, 32, 0, s>>>(j.part, j.n_parts, j.clip_c, j.clip_c2, j.inv_batch, j.norms_out, scale_out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_single_factor, static_cast<const float*>(j.part), j.n_parts, j.clip_c, j.clip_c2,
+                            j.inv_batch, j.norms_out, scale_out);
 }
 
 cudaError_t single_sample_finalize(const FinJob& j, cudaStream_t s) {

@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                        const __grid_constant__ CUtensorMap tm_gw, const StreamParams p) {
   using C = SCfg<BN, CG>;
   constexpr int CL = CG * MC;  // CTAs per cluster
+  // a PDL-launched successor (the single-sample finalize / clip factor) may queue up now;
+  // it waits for this grid's completion before it reads anything
+  if (threadIdx.x == 0) pdl_launch_dependents();
   static_assert(MC == 1 || (CG == 2 && C::kBCols / 64 == MC), "multicast: one X box per pair");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
