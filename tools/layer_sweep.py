@@ -28,8 +28,19 @@ def timed(fn, n=5):
     return e0.elapsed_time(e1) / n * 1e-3
 
 
+def peak_tflops():
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured bf16 burst (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 1617.0, "fallback"
+
+
 def main():
     quick = "--quick" in sys.argv
+    peak, peak_src = peak_tflops()
+    print(json.dumps({"peak_tflops": peak, "peak_source": peak_src}), flush=True)
     points = []
     for d in (1024, 2048, 4096, 8192):
         for B, T in ((1, 4096), (8, 1024), (32, 512), (64, 128), (4, 2048)):
@@ -51,10 +62,19 @@ def main():
         s = timed(c)
         row["dp_ms"] = s * 1e3
         row["dp_tflops"] = F / s / 1e12
+        row["dp_frac_of_peak"] = row["dp_tflops"] / peak
+        if B == 1:  # the training step's form: clip factor left to the optimizer / collective
+            dfr = fdp.PreparedBackward(fdp.WorkflowKind.FLASHDP, x, dy, cfg, noise_impl="philox", add_noise=False,
+                                       grad_scale=torch.zeros(1, device="cuda"))
+            s = timed(dfr)
+            row["dp_deferred_tflops"] = F / s / 1e12
+            row["dp_deferred_frac_of_peak"] = row["dp_deferred_tflops"] / peak
+            del dfr
         x2, y2 = x.view(-1, P), dy.view(-1, D)
         s = timed(lambda: torch.mm(y2.t(), x2, out_dtype=torch.float32))
         row["nondp_cublas_tflops"] = F / s / 1e12
         row["dp_over_nondp"] = row["dp_tflops"] / row["nondp_cublas_tflops"]
+        row["nondp_cublas_frac_of_peak"] = row["nondp_cublas_tflops"] / peak
         if B * D * P * 4 * 2 < 24e9:  # explicit materialises G and G' (fp32)
             e = fdp.PreparedBackward(fdp.WorkflowKind.EXPLICIT_DP, x, dy, cfg, noise_impl="philox")
             s = timed(e, 3)
