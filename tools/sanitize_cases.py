@@ -72,5 +72,15 @@ for acc in (False, True):
                        grad_out=gout, accumulate=acc)
 st = fdp.OptimizerState.fresh(torch.zeros(1000, device="cuda"), eta=0.1)
 fdp.dp_adam_step_(st, torch.ones(1000, device="cuda"))
+# session 2: deferred clip (single-sample GEMM + PDL factor kernel; fallback scale 1), scaled Adam / SGD,
+# PDL ghost -> factor reduce -> reweight (the default two-phase launches above already use it)
+sc = torch.zeros(1, device="cuda")
+fdp.workflows._run(fdp.WorkflowKind.FLASHDP, *inputs(1, 256, 512, 384), cfg, None, None, path="two_phase",
+                   noise_impl="philox", add_noise=False, grad_scale_out=sc)
+fdp.workflows._run(fdp.WorkflowKind.FLASHDP, *inputs(2, 256, 512, 384), cfg, None, None, path="two_phase",
+                   noise_impl="philox", add_noise=False, grad_scale_out=sc)
+st = fdp.OptimizerState.fresh(torch.zeros(1003, device="cuda"), eta=0.1)
+fdp.dp_adam_step_(st, torch.ones(1003, device="cuda"), grad_scale=sc, noise=cfg, layer_numel=1003)
+fdp.dp_sgd_step_(torch.zeros(1003, device="cuda"), torch.ones(1003, device="cuda"), 0.1, grad_scale=sc)
 torch.cuda.synchronize()
 print("sanitize cases done")
