@@ -50,7 +50,7 @@ def main():
     for B, T, P, D in shapes:
         x = torch.randn(B, T, P, device="cuda", generator=g).to(torch.bfloat16)
         dy = (torch.randn(B, T, D, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
-        cfg = fdp.DPConfig(1.0, 1.0, "mean", seed=1, layer_id=2)
+        cfg = fdp.DPConfig(1.0, float(os.environ.get("PH_SIGMA", "1.0")), "mean", seed=1, layer_id=2)
         row = {"shape": [B, T, P, D]}
         for name, kind, path in (("two_phase", fdp.WorkflowKind.FLASHDP, "two_phase"),
                                  ("fused", fdp.WorkflowKind.FLASHDP, "fused"),
