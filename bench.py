@@ -249,8 +249,10 @@ def main():
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
     if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":  # NCCL held to comm_sms CTAs: it runs beside the capped group launches
+            from paper_2507_01154_b200.ddp import init_distributed
+
+            init_distributed("nccl", comm_sms=a.comm_sms, device=dev)
         else:
             dist.init_process_group(backend)
 
