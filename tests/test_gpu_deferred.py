@@ -232,3 +232,51 @@ def test_nccl_premul_sum_collective_applies_scale():
         mp.start_processes(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
         for mode, (applied, err) in out["nccl"].items():
             assert applied and err == 0.0, (mode, err)
+
+
+def test_micro_batches_never_defer_and_match_full_batch(monkeypatch):
+    """Two micro-batches of one sample each through GradBuckets + GroupedDPBackward
+    (defer_clip on, isolated buckets): the first micro-batch writes its fresh
+    bucket view (single-sample path, clip pass in place -- no collective after it,
+    so nothing may be deferred), the second accumulates; the sum equals one
+    backward over both samples (ghost norms), and no factor is left pending."""
+    monkeypatch.setenv("FDP_NO_GROUP", "1")
+    monkeypatch.setenv("FDP_SOLO_PATH", "two_phase")
+    from paper_2507_01154_b200.ddp import GradBuckets
+    from paper_2507_01154_b200.dplinear import DPLinear, GroupedDPBackward
+
+    torch.manual_seed(0)
+    lin = DPLinear(256, 384, bias=False, clip_c=0.05, sigma=0.0, noise_impl="philox", layer_id=3).cuda()
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 128, 256, generator=g).cuda()
+    w_ref = torch.randn(128, 384, generator=g).cuda()
+
+    def loss_of(xs):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            y = lin(xs)
+        return (y.float() * w_ref).sum()
+
+    bk = GradBuckets([lin.weight], flat_params=False, isolate=[lin.weight])
+    bk.set_deferred([lin.weight])
+    outs = []
+    for split in (False, True):
+        bk.zero_grad()
+        if split:
+            for mb in range(2):
+                bk.enabled = mb == 1
+                lin.set_step(0, last_micro_batch=mb == 1, logical_batch=2)
+                with GroupedDPBackward(buckets=bk, defer_clip=True) as grp:
+                    loss_of(x[mb:mb + 1]).backward()
+                assert grp.deferred_clips == 0
+        else:
+            bk.enabled = True
+            lin.set_step(0, logical_batch=2)
+            with GroupedDPBackward(buckets=bk, defer_clip=True) as grp:
+                loss_of(x).backward()
+            assert grp.deferred_clips == 0  # B = 2: ghost norms, nothing to defer
+        bk.finish()
+        assert all(b.scale is None for b in bk.buckets)
+        torch.cuda.synchronize()
+        outs.append(lin.weight.grad.detach().clone())
+    full, split = outs
+    assert float((split - full).abs().max()) <= 1e-3 * float(full.abs().max())
