@@ -634,6 +634,10 @@ class BucketedAdam:
             n = b.per if zero1 else b.n
             b.m = torch.zeros(n, dtype=torch.float32, device=b.flat.device)
             b.v = torch.zeros_like(b.m)
+        # ZeRO-1 on CUDA at N > 1: each bucket's parameter all-gather runs on the buckets'
+        # communication stream as soon as its shard is stepped; `gathered[i]` is the event a
+        # reader of bucket i's parameters waits on (DataParallelStep: forward pre-hooks)
+        self.gathered: dict = {}
 
     @staticmethod
     def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
@@ -666,7 +670,12 @@ class BucketedAdam:
         from dataclasses import replace
 
         bk = self.bk
-        for b in bk.buckets:
+        zero1_gather = bk.world > 1 and bk.mode == "reduce_scatter"
+        # ZeRO-1: step the buckets in forward order (the last buckets hold the first layers), so
+        # the all-gathers the next forward needs first are issued first
+        order = range(len(bk.buckets) - 1, -1, -1) if zero1_gather else range(len(bk.buckets))
+        for i in order:
+            b = bk.buckets[i]
             # a deferred clip factor no collective applied (world 1): the step multiplies it in
             kw = {"grad_scale": b.scale} if b.scale is not None and not b.scale_applied else {}
             if bk.mode == "allreduce" and not self.noise_keys:
@@ -688,13 +697,38 @@ class BucketedAdam:
                     cfg, off, glen, impl = key
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps,
                                  replace(cfg, step=dp_step), off, impl, glen, **kw)
-            if bk.world > 1 and bk.mode == "reduce_scatter":
-                mine = b.pflat[bk.rank * b.per:(bk.rank + 1) * b.per]
-                if dist.get_backend(bk.group) == "nccl":
-                    dist.all_gather_into_tensor(b.pflat, mine.clone(), group=bk.group)
-                else:
-                    pieces = list(b.pflat.chunk(bk.world))
-                    dist.all_gather(pieces, mine.clone(), group=bk.group)
+            if zero1_gather:
+                self._gather(i, b)
+
+    def _gather(self, i: int, b) -> None:
+        bk = self.bk
+        mine = b.pflat[bk.rank * b.per:(bk.rank + 1) * b.per]
+
+        def run():
+            if dist.get_backend(bk.group) == "nccl":
+                dist.all_gather_into_tensor(b.pflat, mine.clone(), group=bk.group)
+            else:
+                pieces = list(b.pflat.chunk(bk.world))
+                dist.all_gather(pieces, mine.clone(), group=bk.group)
+
+        if bk.comm is None:  # CPU: synchronous
+            run()
+            return
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(b.pflat.device))  # this shard's Adam step is enqueued
+        bk.comm.wait_event(ev)
+        with torch.cuda.stream(bk.comm):
+            run()
+            done = torch.cuda.Event()
+            done.record(bk.comm)
+        self.gathered[i] = done
+
+    def wait_gathered(self, indices=None) -> None:
+        """Order the current stream after the parameter all-gathers of the given buckets
+        (all pending ones when None)."""
+        keys = list(self.gathered) if indices is None else [i for i in indices if i in self.gathered]
+        for i in keys:
+            torch.cuda.current_stream(self.bk.device).wait_event(self.gathered.pop(i))
 
 
 class DataParallelStep:
@@ -756,10 +790,33 @@ class DataParallelStep:
                                 adam_fn=adam_fn)
         dev = next(model.parameters()).device
         self.max_ctas = group_max_ctas(dev, comm_sms, world)
+        # ZeRO-1 at N > 1: the next forward overlaps the parameter all-gathers -- a module
+        # waits only for the buckets holding its own parameters (parameters are first read
+        # inside their own module's forward; whatever is left is waited for after the forward)
+        if mode == "reduce_scatter" and world > 1 and dev.type == "cuda":
+            import weakref
+
+            wopt = weakref.ref(self.opt)
+            for mod in model.modules():
+                idx = sorted({self.buckets.bucket_of(p) for p in mod.parameters(recurse=False)
+                              if id(p) in self.buckets._where})
+                if idx:
+                    def _pre(m, args, idx=tuple(idx), wopt=wopt):
+                        o = wopt()
+                        if o is not None and o.gathered:
+                            o.wait_gathered(idx)
+                    mod.register_forward_pre_hook(_pre)
         if world > 1:  # per-layer DP kernels leave NCCL's SMs free too (fdp_capi.cu reserved_sms)
             os.environ["FDP_RESERVE_SMS"] = str(int(comm_sms))
         self.last_flushes = 0
         self.last_deferred = 0  # layers whose clip was deferred to the collective / optimizer last step
+
+    def finish(self) -> None:
+        """Order the current stream after the last step's parameter all-gathers (ZeRO-1
+        at N > 1 leaves them running under the next forward); call before reading the
+        parameters outside a step."""
+        if self.opt.gathered:
+            self.opt.wait_gathered()
 
     def __call__(self, step: int, loss_fn):
         from .dplinear import GroupedDPBackward
@@ -769,6 +826,8 @@ class DataParallelStep:
         for m in self.dp_mods:  # kernel noise only when the optimizer does not add it
             m.set_step(step, last_micro_batch=not self.noise_in_optimizer, logical_batch=self.global_batch)
         loss = loss_fn()
+        if self.opt.gathered:  # parameter all-gathers no forward hook waited for
+            self.opt.wait_gathered()
         if self.dp:
             with GroupedDPBackward(buckets=bk, max_ctas=self.max_ctas, defer_clip=self.defer_clip) as g:
                 loss.backward()

@@ -266,6 +266,7 @@ def _llama_step_worker(rank, world, port, mode, dp, out, opt_noise=True):
             bk = step.buckets
             grads = [(b.flat if mode == "allreduce" else b.shard).detach().cpu().clone() for b in bk.buckets]
             pers = [b.per for b in bk.buckets]
+    step.finish()
     torch.cuda.synchronize()
     out[(mode, dp, world, rank, opt_noise)] = ([p.detach().cpu().clone() for p in model.parameters()],
                                     list(step.buckets.issued), len(step.buckets.buckets), step.last_flushes,
