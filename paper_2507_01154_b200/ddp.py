@@ -269,7 +269,7 @@ def group_max_ctas(device: torch.device, comm_sms: int, world: int) -> int:
 
 class _Bucket:
     __slots__ = ("params", "offsets", "n", "per", "flat", "pflat", "shard", "pending", "launched", "deferred",
-                 "m", "v", "marked", "scale", "scale_applied")
+                 "m", "v", "marked", "scale", "scale_applied", "ready")
 
 
 class GradBuckets:
@@ -419,6 +419,7 @@ class GradBuckets:
         b.marked = set()
         b.m = b.v = None
         b.scale, b.scale_applied = None, False
+        b.ready = None  # event on the communication stream after this bucket's collective
         self.buckets.append(b)
 
     def set_deferred(self, weights) -> None:
@@ -443,6 +444,7 @@ class GradBuckets:
             b.launched = False
             b.marked = set()
             b.scale, b.scale_applied = None, False
+            b.ready = None
             for p, o in zip(b.params, b.offsets):
                 if p.grad is None or p.grad.data_ptr() != b.flat[o:].data_ptr():
                     p.grad = b.flat[o:o + p.numel()].view_as(p)
@@ -520,6 +522,8 @@ class GradBuckets:
             self.comm.wait_event(ev)
             with torch.cuda.stream(self.comm):
                 self._collective(b)
+                b.ready = torch.cuda.Event()
+                b.ready.record(self.comm)
         else:
             self._collective(b)
 
@@ -551,17 +555,23 @@ class GradBuckets:
                 b.flat.mul_(b.scale)
                 b.scale_applied = True
 
-    def finish(self) -> None:
+    def finish(self, wait: bool = True) -> None:
         """After backward: issue any bucket not yet issued (parameters without a
         gradient this step), in bucket order, then order the current stream after
-        the collectives."""
+        the collectives (wait=False: the caller waits per bucket, wait_bucket)."""
         if not self.enabled:
             return
         for i, b in enumerate(self.buckets):
             if not b.launched:
                 self._launch(i)
-        if self.comm is not None:
+        if self.comm is not None and wait:
             torch.cuda.current_stream(self.device).wait_stream(self.comm)
+
+    def wait_bucket(self, i: int) -> None:
+        """Order the current stream after bucket i's collective (if it had one)."""
+        b = self.buckets[i]
+        if b.ready is not None:
+            torch.cuda.current_stream(self.device).wait_event(b.ready)
 
 
 def dp_noise_keys(model) -> dict:
@@ -676,6 +686,7 @@ class BucketedAdam:
         order = range(len(bk.buckets) - 1, -1, -1) if zero1_gather else range(len(bk.buckets))
         for i in order:
             b = bk.buckets[i]
+            bk.wait_bucket(i)  # this bucket's reduction is complete (later ones may still run)
             # a deferred clip factor no collective applied (world 1): the step multiplies it in
             kw = {"grad_scale": b.scale} if b.scale is not None and not b.scale_applied else {}
             if bk.mode == "allreduce" and not self.noise_keys:
@@ -835,6 +846,6 @@ class DataParallelStep:
             self.last_deferred = g.deferred_clips
         else:
             loss.backward()
-        bk.finish()
+        bk.finish(wait=False)  # the Adam step waits bucket by bucket, under the remaining collectives
         self.opt.step(dp_step=step)
         return loss
