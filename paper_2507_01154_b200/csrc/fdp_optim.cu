@@ -84,8 +84,15 @@ __device__ __forceinline__ void adam_quad(float4& t, float4& mm, float4& vv, con
 // kNoise: add the shard's Philox noise first, one quad draw per float4 (the noise
 // index offset is a multiple of 4, so quad i4 of this segment is Philox block
 // offset / 4 + i4 -- the same draws as the scalar kernel's per-element calls)
+// The noisy variant is held to 3 resident blocks per SM (<= 85 registers; unbounded it
+// took 78 and the occupancy that went with them): 134 M parameters 685-777 -> 603 us,
+// the Philox draws then cost nothing over the plain step (6.23 TB/s, tools/hbm_timing.py,
+// profiles/r2_adam_occupancy_ab.jsonl)
+#ifndef FDP_ADAM_NOISE_MINB
+#define FDP_ADAM_NOISE_MINB 3
+#endif
 template <bool kNoise>
-__global__ void __launch_bounds__(256) k_adam_f32x4(float4* __restrict__ theta, float4* __restrict__ m,
+__global__ void __launch_bounds__(256, kNoise ? FDP_ADAM_NOISE_MINB : 1) k_adam_f32x4(float4* __restrict__ theta, float4* __restrict__ m,
                                                     float4* __restrict__ v, const float4* __restrict__ g,
                                                     long long n4, float eta, float b1, float b2, float eps,
                                                     NoiseArgs na) {
