@@ -125,7 +125,7 @@ def ledger(kind: str, B: int, T: int, P: int, D: int, width: int, plan=None, dp:
 
 def device_ledger(kind: str, path: str, norm_phase: str, launches: int, B: int, T: int, P: int, D: int,
                   in_width: int, out_width: int, *, n_tiles: int = 1, groups: int = 1, accumulate: bool = False,
-                  add_noise: bool = True) -> TrafficReport:
+                  add_noise: bool = True, deferred: bool = False) -> TrafficReport:
     """Ledger of the path the device actually executed (the report
     describes the path taken), in BYTES of the real element types: X / dY of
     `in_width` bytes, grad_w and norms of `out_width` bytes.
@@ -138,7 +138,9 @@ def device_ledger(kind: str, path: str, norm_phase: str, launches: int, B: int, 
                             (inputs twice), Gram flops T^2 (P+D) per sample redundant
                  recompute: inputs twice, the per-sample contraction computed twice
                  single:    B == 1, the GEMM writes G, one pass reads it and writes
-                            c * G + noise (grad_w written twice, read once)
+                            c * G + noise (grad_w written twice, read once);
+                            deferred (fdp_dw_deferred): no pass, G written once and
+                            the factor left to the consumer
       simt       partial-norm pass + weighted pass: inputs twice, contraction twice
       explicit   G and G' materialised (2 B D P out_width bytes), 5 launches
       non_dp     inputs once, grad_w once
@@ -166,6 +168,10 @@ def device_ledger(kind: str, path: str, norm_phase: str, launches: int, B: int, 
                              bytes_stored=gw + norm_slots + extra + B * out_width,
                              flops=grad_flops + clip_flops + emit, barriers=B, kernel_launches=launches,
                              peak_scratch_bytes=norm_slots)
+    if kind == "flashdp" and path == "two_phase" and norm_phase == "single" and deferred:
+        return TrafficReport(bytes_loaded=inputs + n_tiles * 4, bytes_stored=gw + n_tiles * 4 + B * out_width + 4,
+                             flops=grad_flops + 2 * D * P, barriers=launches - 1, kernel_launches=launches,
+                             peak_scratch_bytes=n_tiles * 4)
     if kind == "flashdp" and path == "two_phase" and norm_phase == "single":
         return TrafficReport(bytes_loaded=inputs + gw + acc_read, bytes_stored=2 * gw + B * out_width,
                              flops=grad_flops + 2 * D * P + emit, barriers=launches - 1, kernel_launches=launches,

@@ -214,7 +214,8 @@ def _run(kind: WorkflowKind, x, dy, cfg: Optional[DPConfig], spec: Optional[MemS
         wplan = plan_blocks(dims, spec or B200_SPEC)
     width = (spec or B200_SPEC).dtype_width_bytes
     ref_report = ledger(kind.value, dims.B, dims.T, dims.P, dims.D, width, plan=wplan)
-    report = _executed_ledger(kind, desc, dims, xd.element_size(), out_dtype, accumulate, add_noise and c.sigma > 0)
+    report = _executed_ledger(kind, desc, dims, xd.element_size(), out_dtype, accumulate, add_noise and c.sigma > 0,
+                              deferred=grad_scale_out is not None)
 
     if host_torch:
         return BackwardResult(grad.cpu(), report, norms.cpu() if norms is not None else torch.zeros(0), ref_report)
@@ -270,7 +271,7 @@ _PLAN_CACHE: dict = {}
 
 
 def _executed_ledger(kind: WorkflowKind, desc, dims: LayerDims, in_width: int, out_dtype, accumulate: bool,
-                     add_noise: bool) -> TrafficReport:
+                     add_noise: bool, deferred: bool = False) -> TrafficReport:
     """device_ledger of the plan the C library resolved for this descriptor."""
     key = (kind.value, dims.B, dims.T, dims.P, dims.D, desc.in_dtype, desc.path, desc.norm_phase, desc.flags,
            torch.cuda.current_device())
@@ -285,7 +286,8 @@ def _executed_ledger(kind: WorkflowKind, desc, dims: LayerDims, in_width: int, o
     out_w = 8 if out_dtype == torch.float64 else 4
     n_tiles = max(1, info.n_d * info.n_p)
     return device_ledger(kind.value, path, phase, info.launches, dims.B, dims.T, dims.P, dims.D, in_width, out_w,
-                         n_tiles=n_tiles, groups=info.groups, accumulate=accumulate, add_noise=add_noise)
+                         n_tiles=n_tiles, groups=info.groups, accumulate=accumulate, add_noise=add_noise,
+                         deferred=deferred and path == "two_phase" and phase == "single" and not add_noise)
 
 
 def _check_out(t: torch.Tensor, shape: tuple, dtype: torch.dtype, device: torch.device, name: str) -> None:

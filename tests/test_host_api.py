@@ -224,3 +224,18 @@ def test_parameter_group_entry_points_validate_without_gpu():
     small = ctypes.c_size_t(nb.value - 1)
     assert lib.fdp_embedding_dw(ctypes.byref(emb), ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16),
                                 None, ctypes.c_void_p(16), small, None) == _lib.FDP_ERR_CAPACITY
+
+
+def test_device_ledger_deferred_single_path_skips_the_pass():
+    """The executed-path ledger of a deferred single-sample call (fdp_dw_deferred):
+    grad_w written once, never read back, no noise draws -- the pass's D*P read and
+    second write are gone."""
+    from paper_2507_01154_b200.memmodel import device_ledger
+
+    args = ("flashdp", "two_phase", "single", 2, 1, 2048, 4096, 4096, 2, 4)
+    full = device_ledger(*args, n_tiles=128, add_noise=False)
+    dfr = device_ledger(*args, n_tiles=128, add_noise=False, deferred=True)
+    gw = 4096 * 4096 * 4
+    assert full.bytes_stored - dfr.bytes_stored >= gw - 1024
+    assert full.bytes_loaded - dfr.bytes_loaded >= gw - 1024
+    assert dfr.kernel_launches == 2 and dfr.per_sample_grad_bytes_stored == 0
