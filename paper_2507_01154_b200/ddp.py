@@ -648,15 +648,17 @@ class BucketedAdam:
         # communication stream as soon as its shard is stepped; `gathered[i]` is the event a
         # reader of bucket i's parameters waits on (DataParallelStep: forward pre-hooks)
         self.gathered: dict = {}
+        # a CUDA int64 scalar: the noise keys' step is read from it (captured CUDA graphs)
+        self.device_step = None
 
     @staticmethod
     def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
-                grad_scale=None):
+                grad_scale=None, device_step=None):
         from .dpcore import OptimizerState, dp_adam_step_
 
         st = OptimizerState(theta=theta, m=m, v=v, eta=eta, beta1=b1, beta2=b2, eps_adam=eps)
         dp_adam_step_(st, grad, noise=noise_cfg, noise_offset=noise_offset, noise_impl=noise_impl or "philox",
-                      layer_numel=layer_numel, grad_scale=grad_scale)
+                      layer_numel=layer_numel, grad_scale=grad_scale, device_step=device_step)
 
     def _segments(self, b, lo: int, hi: int):
         """(a, z, noise key or None) pieces of [lo, hi) cut at parameter bounds;
@@ -706,8 +708,9 @@ class BucketedAdam:
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0, **kw)
                 else:
                     cfg, off, glen, impl = key
+                    nkw = dict(kw, device_step=self.device_step) if self.device_step is not None else kw
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps,
-                                 replace(cfg, step=dp_step), off, impl, glen, **kw)
+                                 replace(cfg, step=dp_step), off, impl, glen, **nkw)
             if zero1_gather:
                 self._gather(i, b)
 
@@ -849,3 +852,55 @@ class DataParallelStep:
         bk.finish(wait=False)  # the Adam step waits bucket by bucket, under the remaining collectives
         self.opt.step(dp_step=step)
         return loss
+
+
+class GraphedStep:
+    """A DataParallelStep captured in ONE CUDA graph (one GPU): forward, the backward
+    with its DP kernels and bucket hooks, and the bucketed Adam step replay as a
+    single graph launch, so a small-batch step (hundreds of kernel launches, Python
+    autograd and ctypes calls) is no longer bound by the host.
+
+    ``loss_fn`` must read its batch from static tensors (copy each batch into them
+    before the call). The optimizer's DP noise is keyed on a device step counter
+    (BucketedAdam.device_step), so every replay draws the noise of its own step --
+    which is why the DP kernels must not draw any (noise_in_optimizer, the default).
+    ``warmup`` eager steps run first on a side stream (steps first_step ..
+    first_step + warmup - 1; PyTorch's whole-network capture recipe), then step
+    first_step + warmup is captured; each call replays the next step.
+
+        g = GraphedStep(step, lambda: model.loss(x_static, y_static, reduction="sample_sum"))
+        for i in range(g.next_step, n_steps):
+            x_static.copy_(...); y_static.copy_(...)
+            loss = g()"""
+
+    def __init__(self, dstep: DataParallelStep, loss_fn, *, warmup: int = 3, first_step: int = 0):
+        from .errors import UsageError
+
+        if dstep.world != 1:
+            raise UsageError("GraphedStep captures a one-GPU step (collectives stay eager)")
+        if dstep.dp and not dstep.noise_in_optimizer:
+            raise UsageError("GraphedStep needs the DP noise in the optimizer (kernel noise keys are host values)")
+        if warmup < 1:
+            raise UsageError("GraphedStep needs at least one warm-up step")
+        dev = dstep.buckets.device
+        self.dstep = dstep
+        self.device_step = torch.zeros(1, dtype=torch.int64, device=dev)
+        dstep.opt.device_step = self.device_step
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for i in range(warmup):
+                self.device_step.fill_(first_step + i)
+                dstep(first_step + i, loss_fn)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.next_step = first_step + warmup
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):  # recorded, not run: the first replay is this step
+            self.loss = dstep(self.next_step, loss_fn)
+
+    def __call__(self, step: "int | None" = None):
+        i = self.next_step if step is None else int(step)
+        self.device_step.fill_(i)
+        self.graph.replay()
+        self.next_step = i + 1
+        return self.loss

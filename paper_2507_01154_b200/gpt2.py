@@ -142,6 +142,6 @@ class GPT2(torch.nn.Module):
         return self.lm_head(h)[..., :self.cfg.vocab]
 
     def loss(self, idx, targets):
-        with torch.autocast("cuda", dtype=torch.bfloat16):
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):  # CUDA-graph capturable
             logits = self(idx)
         return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))

@@ -154,7 +154,7 @@ class Llama(torch.nn.Module):
         samples of each sample's mean token loss -- the per-sample loss whose
         gradient is the sample's own, independent of how the batch is split over
         ranks (the DP modules then take the mean over the logical batch)."""
-        with torch.autocast("cuda", dtype=torch.bfloat16):
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):  # CUDA-graph capturable
             logits = self(idx)
         if reduction == "mean":
             return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.view(-1))

@@ -1,0 +1,63 @@
+"""GraphedStep (ddp.py): a whole DataParallelStep -- forward, backward with the DP
+kernels and bucket hooks, bucketed DP-Adam -- captured in one CUDA graph. Replays
+must reproduce the eager steps exactly (the optimizer's noise keyed on a device step
+counter: every replay draws the noise of its own step)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(graphed: bool, dp: bool, mode: str, B: int, n_steps: int = 6, warmup: int = 3):
+    from paper_2507_01154_b200.ddp import DataParallelStep, GraphedStep
+    from paper_2507_01154_b200.llama import Llama, LlamaConfig
+
+    cfg = LlamaConfig(vocab=512, d=256, heads=4, layers=2, mlp=512, seq=128)
+    torch.manual_seed(0)
+    with torch.device("cuda"):
+        model = Llama(cfg, dp=dp, clip_c=0.5, sigma=1.0, noise_impl="philox", nondp_linear="fp32grad")
+    g = torch.Generator().manual_seed(5)
+    idx = torch.randint(0, cfg.vocab, (B, cfg.seq + 1), generator=g).cuda()
+    x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
+    step = DataParallelStep(model, dp=dp, mode=mode, lr=1e-3, global_batch=B, bucket_bytes=1 << 20)
+    scale = 1.0 if dp else 1.0 / B
+
+    def loss_fn():
+        return model.loss(x, y, reduction="sample_sum") * scale
+
+    losses = []
+    if graphed:
+        gs = GraphedStep(step, loss_fn, warmup=warmup)
+        for _ in range(gs.next_step, n_steps):
+            losses.append(float(gs()))
+    else:
+        for i in range(n_steps):
+            lo = step(i, loss_fn)
+            if i >= warmup:
+                losses.append(float(lo.detach()))
+    torch.cuda.synchronize()
+    return [p.detach().clone() for p in model.parameters()], losses
+
+
+@pytest.mark.parametrize("dp,mode,B", [(True, "allreduce", 1), (True, "reduce_scatter", 2), (False, "allreduce", 2)])
+def test_graphed_step_replays_equal_eager_steps(dp, mode, B):
+    eager, le = _run(False, dp, mode, B)
+    graphed, lg = _run(True, dp, mode, B)
+    assert len(le) == len(lg) == 3
+    for a, b in zip(le, lg):
+        assert abs(a - b) <= 1e-5 * max(1.0, abs(a))
+    for a, b in zip(eager, graphed):
+        assert torch.allclose(a, b, rtol=1e-5, atol=1e-7), float((a - b).abs().max())
+
+
+def test_graphed_step_rejects_kernel_noise():
+    from paper_2507_01154_b200.ddp import DataParallelStep, GraphedStep
+    from paper_2507_01154_b200.errors import UsageError
+    from paper_2507_01154_b200.llama import Llama, LlamaConfig
+
+    with torch.device("cuda"):
+        model = Llama(LlamaConfig(vocab=64, d=64, heads=2, layers=1, mlp=128, seq=16), dp=True)
+    step = DataParallelStep(model, dp=True, noise_in_optimizer=False)
+    with pytest.raises(UsageError):
+        GraphedStep(step, lambda: None)
