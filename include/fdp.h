@@ -318,6 +318,31 @@ FDP_API int fdp_adam_step_scaled(int32_t dtype, void* theta, void* m, void* v, c
                                  const float* grad_scale, int64_t n, double eta, double beta1, double beta2,
                                  double eps, const fdp_desc* noise, int64_t noise_offset, void* stream);
 
+/* Multi-segment fp32 Adam: every parameter segment of an optimizer step in ONE launch
+ * (the bucketed DP-Adam of ddp.BucketedAdam; one kernel instead of one per parameter).
+ * A segment is fdp_adam_step_scaled's arguments: theta / m / v / grad (n fp32 each,
+ * 16-byte aligned), an optional device grad_scale, and optional noise (Philox only,
+ * noise_offset a multiple of 4; the descriptor's add_noise / sigma / clip_c / seed /
+ * layer_id / step / device_step apply -- with device_step the table is reusable
+ * across steps and CUDA-graph capturable). fdp_adam_multi_prepare validates the
+ * segments and writes the device table (blocking the host until it is written:
+ * call it outside graph capture); fdp_adam_step_multi runs one step over it. */
+typedef struct fdp_adam_segment {
+  float* theta;
+  float* m;
+  float* v;
+  const float* grad;
+  const float* grad_scale; /* NULL or a device scalar: g = grad * grad_scale[0] first */
+  int64_t n;
+  const fdp_desc* noise;   /* NULL: no noise */
+  int64_t noise_offset;
+} fdp_adam_segment;
+FDP_API int fdp_adam_multi_table_bytes(int32_t n_seg, size_t* bytes);
+FDP_API int fdp_adam_multi_prepare(int32_t n_seg, const fdp_adam_segment* segs, void* table, size_t table_bytes,
+                                   int64_t* total_quads, void* stream);
+FDP_API int fdp_adam_step_multi(int32_t n_seg, const void* table, int64_t total_quads, double eta, double beta1,
+                                double beta2, double eps, void* stream);
+
 /* Noise slice [lo, hi) of [0, n) owned by `rank` of `world` (data-parallel
  * noise-once partition). Pure host arithmetic. */
 FDP_API int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi);

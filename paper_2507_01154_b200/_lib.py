@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
     "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
     "fdp_backward_chained", "fdp_backward_shared_x", "fdp_dw_deferred", "fdp_sgd_step_scaled",
-    "fdp_adam_step_scaled",
+    "fdp_adam_step_scaled", "fdp_adam_multi_table_bytes", "fdp_adam_multi_prepare", "fdp_adam_step_multi",
 )
 VEC_KIND = {"bias": 0, "rmsnorm": 1, "layernorm": 2}
 
@@ -57,6 +57,14 @@ class FdpDesc(ctypes.Structure):
         ("noise_impl", ctypes.c_int32), ("path", ctypes.c_int32),
         ("flags", ctypes.c_int32), ("norm_phase", ctypes.c_int32),
         ("device_step", ctypes.c_void_p),
+    ]
+
+
+class FdpAdamSegment(ctypes.Structure):
+    _fields_ = [
+        ("theta", ctypes.c_void_p), ("m", ctypes.c_void_p), ("v", ctypes.c_void_p), ("grad", ctypes.c_void_p),
+        ("grad_scale", ctypes.c_void_p), ("n", ctypes.c_int64), ("noise", ctypes.POINTER(FdpDesc)),
+        ("noise_offset", ctypes.c_int64),
     ]
 
 
@@ -149,7 +157,13 @@ def load() -> ctypes.CDLL:
     lib.fdp_adam_step_scaled.argtypes = [ctypes.c_int32] + [ctypes.c_void_p] * 5 + [
         ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p,
         ctypes.c_int64, ctypes.c_void_p]
-    for name in ("fdp_dw_deferred", "fdp_sgd_step_scaled", "fdp_adam_step_scaled", "fdp_backward_shared_x", "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
+    lib.fdp_adam_multi_table_bytes.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+    lib.fdp_adam_multi_prepare.argtypes = [ctypes.c_int32, ctypes.POINTER(FdpAdamSegment), ctypes.c_void_p,
+                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p]
+    lib.fdp_adam_step_multi.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+    for name in ("fdp_adam_multi_table_bytes", "fdp_adam_multi_prepare", "fdp_adam_step_multi",
+                 "fdp_dw_deferred", "fdp_sgd_step_scaled", "fdp_adam_step_scaled", "fdp_backward_shared_x", "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
                  "fdp_backward_chained", "fdp_vec_workspace_bytes", "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
                  "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",
                  "fdp_backward_group", "fdp_device_info", "fdp_plan", "fdp_workspace_bytes", "fdp_workspace_init", "fdp_backward",

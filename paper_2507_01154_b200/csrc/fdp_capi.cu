@@ -1724,6 +1724,75 @@ int fdp_adam_step_scaled(int32_t dtype, void* theta, void* m, void* v, const voi
                       grad_scale);
 }
 
+int fdp_adam_multi_table_bytes(int32_t n_seg, size_t* bytes) {
+  if (n_seg < 0 || !bytes) return fail(FDP_ERR_USAGE, "bad arguments");
+  *bytes = static_cast<size_t>(n_seg) * sizeof(fdp::AdamSeg);
+  return FDP_OK;
+}
+
+int fdp_adam_multi_prepare(int32_t n_seg, const fdp_adam_segment* segs, void* table, size_t table_bytes,
+                           int64_t* total_quads, void* stream) {
+  if (n_seg < 0 || (n_seg > 0 && (!segs || !table)) || !total_quads) return fail(FDP_ERR_USAGE, "bad arguments");
+  if (table_bytes < static_cast<size_t>(n_seg) * sizeof(fdp::AdamSeg))
+    return fail(FDP_ERR_CAPACITY, "segment table of %zu bytes is smaller than the %zu bytes needed", table_bytes,
+                static_cast<size_t>(n_seg) * sizeof(fdp::AdamSeg));
+  std::vector<fdp::AdamSeg> host(static_cast<size_t>(n_seg));
+  long long q = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    const fdp_adam_segment& a = segs[i];
+    if (a.n < 0) return fail(FDP_ERR_SHAPE, "segment %d: negative element count", i);
+    if (a.n > 0 && (!a.theta || !a.m || !a.v || !a.grad)) return fail(FDP_ERR_USAGE, "segment %d: null pointer", i);
+    if (((reinterpret_cast<uintptr_t>(a.theta) | reinterpret_cast<uintptr_t>(a.m) |
+          reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.grad)) & 15u) != 0)
+      return fail(FDP_ERR_USAGE, "segment %d: theta / m / v / grad must be 16-byte aligned", i);
+    if (a.grad_scale && (reinterpret_cast<uintptr_t>(a.grad_scale) & 3u))
+      return fail(FDP_ERR_USAGE, "segment %d: grad_scale must be 4-byte aligned", i);
+    fdp::AdamSeg& h = host[static_cast<size_t>(i)];
+    h = fdp::AdamSeg{};
+    h.theta = a.theta;
+    h.m = a.m;
+    h.v = a.v;
+    h.g = a.grad;
+    h.gscale = a.grad_scale;
+    h.n = a.n;
+    h.q0 = q;
+    if (a.noise) {
+      int rc = validate(a.noise, FDP_KIND_FLASHDP);
+      if (rc) return rc;
+      if (a.noise->noise_impl != FDP_NOISE_PHILOX || (a.noise_offset & 3) != 0 || a.noise_offset < 0)
+        return fail(FDP_ERR_USAGE, "segment %d: multi-segment noise is Philox with a 4-aligned offset", i);
+      const Common c = common_of(a.noise);
+      h.noise_on = c.add_noise;
+      h.scale = c.noise_scale;
+      h.base = c.key_base;
+      h.step_ptr = reinterpret_cast<const long long*>(a.noise->device_step);
+      h.seed_u = static_cast<uint64_t>(a.noise->seed);
+      h.layer_u = static_cast<uint64_t>(a.noise->layer_id);
+      h.noise_q0 = a.noise_offset >> 2;
+    }
+    q += (a.n + 3) / 4;
+  }
+  *total_quads = q;
+  if (n_seg == 0) return FDP_OK;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(table, host.data(), host.size() * sizeof(fdp::AdamSeg), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host array goes out of scope
+  if (e != cudaSuccess) return cuda_fail(e, "segment table upload");
+  return FDP_OK;
+}
+
+int fdp_adam_step_multi(int32_t n_seg, const void* table, int64_t total_quads, double eta, double beta1,
+                        double beta2, double eps, void* stream) {
+  if (n_seg < 0 || (n_seg > 0 && !table) || total_quads < 0) return fail(FDP_ERR_USAGE, "bad arguments");
+  if (!(eta == eta) || !std::isfinite(eta)) return fail(FDP_ERR_USAGE, "eta must be finite");
+  if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0))
+    return fail(FDP_ERR_USAGE, "beta1 and beta2 must lie in [0, 1), got %g, %g", beta1, beta2);
+  cudaError_t e = fdp::adam_multi(static_cast<const fdp::AdamSeg*>(table), n_seg, total_quads, eta, beta1, beta2, eps,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "multi-segment adam step");
+  return FDP_OK;
+}
+
 int fdp_noise_partition(int64_t n, int32_t rank, int32_t world, int64_t* lo, int64_t* hi) {
   if (n < 0 || world < 1 || rank < 0 || rank >= world) return fail(FDP_ERR_USAGE, "bad partition arguments");
   if (lo) *lo = n * rank / world;

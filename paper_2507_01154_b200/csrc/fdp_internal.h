@@ -296,6 +296,22 @@ struct OptimNoise {
   long long offset;
   const float* grad_scale;  // nullptr or a device scalar: g = grad_scale[0] * grad before the noise (fp32 only)
 };
+// one segment of a multi-segment fp32 Adam step (device table entry)
+struct AdamSeg {
+  float *theta, *m, *v;
+  const float* g;
+  const float* gscale;   // nullptr or a device scalar multiplied into g first
+  long long n;           // elements
+  long long q0;          // first quad of this segment in the launch's quad space
+  long long noise_q0;    // Philox block of the segment's element 0 (noise offset / 4)
+  int noise_on;
+  float scale;           // sigma * C
+  uint64_t base;         // Philox key (absorb(seed, layer, step)) when step_ptr is null
+  const long long* step_ptr;
+  uint64_t seed_u, layer_u;
+};
+cudaError_t adam_multi(const AdamSeg* dev_segs, int n_seg, long long total_q, double eta, double b1, double b2,
+                       double eps, cudaStream_t s);
 cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const void* g, long long n, double eta,
                        double b1, double b2, double eps, const OptimNoise& nz, cudaStream_t s);
 

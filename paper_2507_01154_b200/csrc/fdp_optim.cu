@@ -167,6 +167,89 @@ __global__ void __launch_bounds__(256) k_sgd(T* __restrict__ theta, const T* __r
   }
 }
 
+// ---- multi-segment fp32 Adam (fdp_adam_step_multi): every parameter segment of an
+// optimizer step in ONE launch. Segment table in device memory (AdamSeg, prefix q0 over
+// quads); a block walks one contiguous chunk of quads, so a thread's consecutive quads
+// stay in one segment and the segment lookup / noise key are recomputed only on change.
+// Per element the arithmetic is k_adam_f32x4's: grad * scale (__fmul_rn), + sigma*C*z
+// (Philox, one draw per quad of the segment's index space), then adam_quad.
+constexpr int kMultiChunk = 256 * 8;  // quads per block
+
+__device__ __forceinline__ int seg_of(const AdamSeg* segs, int n_seg, long long q) {
+  int lo = 0, hi = n_seg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].q0 <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256, FDP_ADAM_NOISE_MINB) k_adam_multi(const AdamSeg* __restrict__ segs, int n_seg,
+                                                                         long long total_q, float eta, float b1,
+                                                                         float b2, float eps) {
+  const long long c0 = static_cast<long long>(blockIdx.x) * kMultiChunk;
+  int cur = -1;
+  AdamSeg S{};
+  uint64_t base = 0;
+  float f = 1.0f;
+  for (long long q = c0 + threadIdx.x; q < c0 + kMultiChunk && q < total_q; q += blockDim.x) {
+    if (cur < 0 || q < S.q0 || q >= S.q0 + ((S.n + 3) >> 2)) {
+      cur = seg_of(segs, n_seg, q);
+      S = segs[cur];
+      base = S.base;
+      if (S.noise_on && S.step_ptr) base = absorb3(S.seed_u, S.layer_u, static_cast<uint64_t>(*S.step_ptr));
+      f = S.gscale ? *S.gscale : 1.0f;
+    }
+    const long long lq = q - S.q0;
+    const long long e0 = lq << 2;
+    float4* th4 = reinterpret_cast<float4*>(S.theta);
+    float4* m4 = reinterpret_cast<float4*>(S.m);
+    float4* v4 = reinterpret_cast<float4*>(S.v);
+    const float4* g4 = reinterpret_cast<const float4*>(S.g);
+    const bool full = e0 + 4 <= S.n;
+    float4 gg, mm, vv, tt;
+    if (full) {
+      gg = __ldcs(g4 + lq);
+      mm = __ldcs(m4 + lq);
+      vv = __ldcs(v4 + lq);
+      tt = __ldcs(th4 + lq);
+    } else {  // the segment's last partial quad (elements past n are never stored)
+      const long long r = S.n - e0;
+      gg = make_float4(S.g[e0], r > 1 ? S.g[e0 + 1] : 0.f, r > 2 ? S.g[e0 + 2] : 0.f, 0.f);
+      mm = make_float4(S.m[e0], r > 1 ? S.m[e0 + 1] : 0.f, r > 2 ? S.m[e0 + 2] : 0.f, 0.f);
+      vv = make_float4(S.v[e0], r > 1 ? S.v[e0 + 1] : 0.f, r > 2 ? S.v[e0 + 2] : 0.f, 0.f);
+      tt = make_float4(S.theta[e0], r > 1 ? S.theta[e0 + 1] : 0.f, r > 2 ? S.theta[e0 + 2] : 0.f, 0.f);
+    }
+    if (S.gscale) {
+      gg.x = __fmul_rn(gg.x, f);
+      gg.y = __fmul_rn(gg.y, f);
+      gg.z = __fmul_rn(gg.z, f);
+      gg.w = __fmul_rn(gg.w, f);
+    }
+    if (S.noise_on) {
+      const float4 z = philox_normal4(base, S.noise_q0 + static_cast<uint64_t>(lq));
+      gg.x += S.scale * z.x;
+      gg.y += S.scale * z.y;
+      gg.z += S.scale * z.z;
+      gg.w += S.scale * z.w;
+    }
+    adam_quad(tt, mm, vv, gg, eta, b1, b2, eps);
+    if (full) {
+      __stcs(th4 + lq, tt);
+      __stcs(m4 + lq, mm);
+      __stcs(v4 + lq, vv);
+    } else {
+      const long long r = S.n - e0;
+      S.theta[e0] = tt.x;
+      S.m[e0] = mm.x;
+      S.v[e0] = vv.x;
+      if (r > 1) { S.theta[e0 + 1] = tt.y; S.m[e0 + 1] = mm.y; S.v[e0 + 1] = vv.y; }
+      if (r > 2) { S.theta[e0 + 2] = tt.z; S.m[e0 + 2] = mm.z; S.v[e0 + 2] = vv.z; }
+    }
+  }
+}
+
 int blocks_for(long long n) {
   long long b = (n + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -222,6 +305,16 @@ cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const v
       k_sgd<float><<<blocks_for(n), 256, 0, s>>>(static_cast<float*>(theta), static_cast<const float*>(g), n,
                                                  static_cast<float>(eta), na);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t adam_multi(const AdamSeg* dev_segs, int n_seg, long long total_q, double eta, double b1, double b2,
+                       double eps, cudaStream_t s) {
+  if (n_seg <= 0 || total_q <= 0) return cudaSuccess;
+  const long long blocks = (total_q + kMultiChunk - 1) / kMultiChunk;
+  k_adam_multi<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_segs, n_seg, total_q, static_cast<float>(eta),
+                                                             static_cast<float>(b1), static_cast<float>(b2),
+                                                             static_cast<float>(eps));
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@ ranks.
 
 from __future__ import annotations
 
+import ctypes
 import os
 from typing import Iterable, Sequence
 
@@ -269,7 +270,7 @@ def group_max_ctas(device: torch.device, comm_sms: int, world: int) -> int:
 
 class _Bucket:
     __slots__ = ("params", "offsets", "n", "per", "flat", "pflat", "shard", "pending", "launched", "deferred",
-                 "m", "v", "marked", "scale", "scale_applied", "ready")
+                 "m", "v", "marked", "scale", "scale_applied", "ready", "scale_buf")
 
 
 class GradBuckets:
@@ -329,6 +330,7 @@ class GradBuckets:
                     self._close(cur, flat_params)
                     cur, size = [], 0
                 self._close([p], flat_params)
+                self.buckets[-1].scale_buf = True  # marks the isolated bucket: its factor slot follows
                 continue
             cur.append(p)
             size += p.numel() * 4
@@ -337,6 +339,13 @@ class GradBuckets:
                 cur, size = [], 0
         if cur:
             self._close(cur, flat_params)
+        # one persistent factor slot per isolated bucket (slices of one tensor: one fill resets
+        # them all); a deferred layer's kernel writes its clip factor there, so the pointer the
+        # collective / the optimizer table reads never changes (CUDA-graph capturable)
+        iso_b = [b for b in self.buckets if b.scale_buf is True]
+        self._scales = torch.ones(max(1, len(iso_b)), dtype=torch.float32, device=self.device) if iso_b else None
+        for k, b in enumerate(iso_b):
+            b.scale_buf = self._scales[k:k + 1]
         self._external: set = set()  # ids of parameters whose readiness is signalled explicitly
         self._written: set = set()  # ids of parameters whose .grad region was written since zero_grad
         self._where = {}
@@ -420,6 +429,7 @@ class GradBuckets:
         b.m = b.v = None
         b.scale, b.scale_applied = None, False
         b.ready = None  # event on the communication stream after this bucket's collective
+        b.scale_buf = None  # isolated buckets: a persistent one-float factor slot (1 when nothing is deferred)
         self.buckets.append(b)
 
     def set_deferred(self, weights) -> None:
@@ -450,6 +460,8 @@ class GradBuckets:
                     p.grad = b.flat[o:o + p.numel()].view_as(p)
         self.issued = []
         self._written = set()
+        if self._scales is not None:
+            self._scales.fill_(1.0)
 
     def bucket_of(self, p) -> int:
         return self._where[id(p)]
@@ -464,15 +476,20 @@ class GradBuckets:
         o = b.offsets[next(k for k, q in enumerate(b.params) if q is p)]
         return p.grad is not None and p.grad.data_ptr() == b.flat[o:].data_ptr()
 
+    def scale_buffer(self, p) -> "torch.Tensor | None":
+        """The persistent factor slot of p's bucket (isolated buckets only)."""
+        i = self._where.get(id(p))
+        return None if i is None else self.buckets[i].scale_buf
+
     def note_written(self, p) -> None:
         self._written.add(id(p))
 
     def can_defer(self, p) -> bool:
         """p may be handed over unclipped with a scale (mark_ready(p, scale=)): its
-        bucket holds it alone, its gradient is fresh and this is the step's last
-        micro-batch (no later accumulation into it)."""
+        bucket holds it alone (an isolated bucket, with a factor slot), its gradient is
+        fresh and this is the step's last micro-batch (no later accumulation into it)."""
         i = self._where.get(id(p))
-        return (i is not None and self.enabled and len(self.buckets[i].params) == 1 and self.fresh(p)
+        return (i is not None and self.enabled and self.buckets[i].scale_buf is not None and self.fresh(p)
                 and self.device.type == "cuda")
 
     def _hook(self, p):
@@ -536,6 +553,9 @@ class GradBuckets:
             else:  # gloo, or an NCCL whose PreMulSum failed the probe: scale in place first
                 b.flat.mul_(b.scale.to(b.flat.device))
             b.scale_applied = True
+            reset = b.scale_buf is not None and b.scale.data_ptr() == b.scale_buf.data_ptr()
+        else:
+            reset = False
         if self.mode == "allreduce":
             dist.all_reduce(b.flat, op=op, group=self.group)
         elif nccl:
@@ -544,6 +564,8 @@ class GradBuckets:
             b.shard.copy_(out)
         else:  # gloo: all-reduce, keep this rank's slice (b.shard is a view of it)
             dist.all_reduce(b.flat, op=op, group=self.group)
+        if reset:  # the collective applied the factor: the slot the optimizer reads is 1 again
+            b.scale_buf.fill_(1.0)
 
     def materialize_scales(self) -> None:
         """Apply every pending deferred-clip factor to its bucket in place (for a
@@ -650,6 +672,12 @@ class BucketedAdam:
         self.gathered: dict = {}
         # a CUDA int64 scalar: the noise keys' step is read from it (captured CUDA graphs)
         self.device_step = None
+        # multi-segment fast path (fdp_adam_step_multi): one launch per bucket (ZeRO-1 / N > 1)
+        # or for the whole step, over a device table built once; the noise keys read the
+        # step from a device counter (ours, or device_step under a graph)
+        self.multi = adam_fn is None and buckets.device.type == "cuda"
+        self._tables = None  # (key, [(bucket indices, table, n_seg, total_quads)], keepalive)
+        self._own_step = None
 
     @staticmethod
     def _kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
@@ -678,10 +706,82 @@ class BucketedAdam:
                 out.append((a, z, None))
         return out
 
+    def _multi_plan(self):
+        """Device tables for fdp_adam_step_multi, or None when a segment does not fit it
+        (keyed noise, an unaligned noise offset): then the per-segment launches run."""
+        from dataclasses import replace
+
+        from . import _lib
+
+        bk = self.bk
+        zero1 = bk.mode == "reduce_scatter"
+        if self.device_step is None and self._own_step is None:
+            self._own_step = torch.zeros(1, dtype=torch.int64, device=bk.device)
+        step_t = self.device_step if self.device_step is not None else self._own_step
+        key = (step_t.data_ptr(),)
+        if self._tables is not None and self._tables[0] == key:
+            return self._tables[1]
+        groups = [[i] for i in range(len(bk.buckets))] if bk.world > 1 else [list(range(len(bk.buckets)))]
+        lib = _lib.load()
+        plan, keep = [], []
+        for idx in groups:
+            segs = []
+            for i in idx:
+                b = bk.buckets[i]
+                lo = bk.rank * b.per if zero1 else 0
+                hi = min(lo + b.per, b.n) if zero1 else b.n
+                src = b.shard if zero1 else b.flat
+                gs = b.scale_buf.data_ptr() if b.scale_buf is not None else None
+                for a, z, nkey in self._segments(b, lo, hi):
+                    seg = _lib.FdpAdamSegment(theta=b.pflat[a:z].data_ptr(), m=b.m[a - lo:z - lo].data_ptr(),
+                                              v=b.v[a - lo:z - lo].data_ptr(), grad=src[a - lo:z - lo].data_ptr(),
+                                              grad_scale=gs, n=z - a, noise=None, noise_offset=0)
+                    if nkey is not None:
+                        cfg, off, glen, impl = nkey
+                        if (impl or "philox") != "philox" or off % 4:
+                            return None
+                        desc = _lib.make_desc(B=1, T=1, P=glen, D=1, clip_c=cfg.clip_c, sigma=cfg.sigma,
+                                              seed=cfg.seed, layer_id=cfg.layer_id, step=0, noise_impl="philox",
+                                              device_step=step_t.data_ptr())
+                        keep.append(desc)
+                        seg.noise = ctypes.pointer(desc)
+                        seg.noise_offset = off
+                    segs.append(seg)
+            arr = (_lib.FdpAdamSegment * max(1, len(segs)))(*segs)
+            nb = ctypes.c_size_t()
+            _lib.check(lib.fdp_adam_multi_table_bytes(len(segs), ctypes.byref(nb)))
+            table = torch.empty(max(16, nb.value), dtype=torch.uint8, device=bk.device)
+            tq = ctypes.c_int64()
+            _lib.check(lib.fdp_adam_multi_prepare(len(segs), arr, table.data_ptr(), table.numel(), ctypes.byref(tq),
+                                                  torch.cuda.current_stream(bk.device).cuda_stream))
+            plan.append((idx, table, len(segs), tq.value))
+            keep.append(arr)
+        self._tables = (key, plan, keep)
+        del replace
+        return plan
+
     def step(self, dp_step: int = 0) -> None:
         from dataclasses import replace
 
         bk = self.bk
+        plan = self._multi_plan() if self.multi else None
+        if plan is not None:
+            from . import _lib
+
+            if self.device_step is None:
+                self._own_step.fill_(int(dp_step))
+            lib, st = _lib.load(), torch.cuda.current_stream(bk.device).cuda_stream
+            order = range(len(plan) - 1, -1, -1) if bk.world > 1 and bk.mode == "reduce_scatter" else range(len(plan))
+            for k in order:
+                idx, table, n_seg, tq = plan[k]
+                for i in idx:
+                    bk.wait_bucket(i)
+                _lib.check(lib.fdp_adam_step_multi(n_seg, table.data_ptr(), tq, self.lr, self.beta1, self.beta2,
+                                                   self.eps, st))
+                if bk.world > 1 and bk.mode == "reduce_scatter":
+                    for i in idx:
+                        self._gather(i, bk.buckets[i])
+            return
         zero1_gather = bk.world > 1 and bk.mode == "reduce_scatter"
         # ZeRO-1: step the buckets in forward order (the last buckets hold the first layers), so
         # the all-gathers the next forward needs first are issued first

@@ -278,7 +278,9 @@ class GroupedDPBackward:
                 scale = None
                 if (self.defer_clip and new and not add_noise and x.shape[0] == 1 and not self.defer_finalize
                         and bk.can_defer(m.weight)):
-                    scale = torch.empty(1, dtype=torch.float32, device=x.device)
+                    scale = bk.scale_buffer(m.weight)  # the bucket's persistent factor slot
+                    if scale is None:
+                        scale = torch.empty(1, dtype=torch.float32, device=x.device)
                     scales[id(m)] = scale
                     self.deferred_clips += 1
                 gw = _run(WorkflowKind.FLASHDP, x, dy, cfg, None, None, add_noise=add_noise, mean_batch=mean_batch,

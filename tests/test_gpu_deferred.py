@@ -158,8 +158,11 @@ def _worker(rank, world, port, B, defer, mode, out):
     deferred = []
     for i in range(2):
         step(i, lambda: model.loss(x, y, reduction="sample_sum"))
-        torch.cuda.synchronize()  # factors < 1: the clip really was deferred (1 = finalised in place)
-        deferred.append(sum(1 for b in step.buckets.buckets if b.scale is not None and float(b.scale[0]) < 1))
+        torch.cuda.synchronize()
+        deferred.append(step.last_deferred)  # layers handed over unclipped with their factor this step
+        if world == 1:  # the factors wait in the buckets' slots for the Adam step (< 1: really deferred)
+            assert sum(1 for b in step.buckets.buckets if b.scale is not None and float(b.scale[0]) < 1) == \
+                step.last_deferred
     torch.cuda.synchronize()
     out[(B, defer, world, rank, mode)] = ([p.detach().cpu().clone() for p in model.parameters()], deferred,
                                           len(step.buckets.buckets))
@@ -280,3 +283,60 @@ def test_micro_batches_never_defer_and_match_full_batch(monkeypatch):
         outs.append(lin.weight.grad.detach().clone())
     full, split = outs
     assert float((split - full).abs().max()) <= 1e-3 * float(full.abs().max())
+
+
+def test_adam_multi_segment_equals_per_segment_steps():
+    """fdp_adam_step_multi over a table of segments (odd lengths, Philox noise at
+    4-aligned offsets with a device step, a deferred factor) == one fdp_adam_step(_scaled)
+    per segment, bit for bit."""
+    import ctypes
+
+    from paper_2507_01154_b200 import _lib
+    from paper_2507_01154_b200.dpcore import OptimizerState, dp_adam_step_
+
+    g = torch.Generator(device="cuda").manual_seed(7)
+    sizes = [4096, 1001, 8, 3, 65536 + 5]
+    noise = [True, False, True, True, False]
+    dstep = torch.tensor([9], dtype=torch.int64, device="cuda")
+    scale = torch.tensor([0.25], device="cuda")
+    bufs = []
+    for n in sizes:
+        pad = -(-n // 4) * 4
+        bufs.append([torch.randn(pad, device="cuda", generator=g) for _ in range(4)])  # theta, m, v, grad
+    for b in bufs:
+        b[2].abs_()  # v >= 0
+    ref = [[t.clone() for t in b] for b in bufs]
+    cfgs = [fdp.DPConfig(0.5, 1.0, "mean", seed=3, layer_id=10 + k, step=9) for k in range(len(sizes))]
+    lib = _lib.load()
+    segs, keep = [], []
+    for k, (n, b) in enumerate(zip(sizes, bufs)):
+        s = _lib.FdpAdamSegment(theta=b[0].data_ptr(), m=b[1].data_ptr(), v=b[2].data_ptr(), grad=b[3].data_ptr(),
+                                grad_scale=scale.data_ptr() if k == 1 else None, n=n, noise=None, noise_offset=0)
+        if noise[k]:
+            d = _lib.make_desc(B=1, T=1, P=n + 8, D=1, clip_c=0.5, sigma=1.0, seed=3, layer_id=10 + k, step=0,
+                               noise_impl="philox", device_step=dstep.data_ptr())
+            keep.append(d)
+            s.noise = ctypes.pointer(d)
+            s.noise_offset = 8
+        segs.append(s)
+    arr = (_lib.FdpAdamSegment * len(segs))(*segs)
+    nb = ctypes.c_size_t()
+    _lib.check(lib.fdp_adam_multi_table_bytes(len(segs), ctypes.byref(nb)))
+    table = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    tq = ctypes.c_int64()
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.fdp_adam_multi_prepare(len(segs), arr, table.data_ptr(), nb.value, ctypes.byref(tq), st))
+    _lib.check(lib.fdp_adam_step_multi(len(segs), table.data_ptr(), tq.value, 1e-3, 0.9, 0.999, 1e-8, st))
+    for k, (n, r) in enumerate(zip(sizes, ref)):
+        stt = OptimizerState(theta=r[0][:n], m=r[1][:n], v=r[2][:n], eta=1e-3, beta1=0.9, beta2=0.999, eps_adam=1e-8)
+        dp_adam_step_(stt, r[3][:n], noise=cfgs[k] if noise[k] else None, noise_offset=8, noise_impl="philox",
+                      layer_numel=n + 8, grad_scale=scale if k == 1 else None)
+    torch.cuda.synchronize()
+    for k, (n, b, r) in enumerate(zip(sizes, bufs, ref)):
+        # the per-segment path computes a noisy segment's last partial quad with its scalar
+        # kernel (the noise FMA may round differently): bitwise up to the last whole quad
+        whole = n if not noise[k] else n // 4 * 4
+        for t1, t2 in zip(b[:3], r[:3]):
+            assert torch.equal(t1[:whole], t2[:whole]), (k, float((t1[:whole] - t2[:whole]).abs().max()))
+            assert torch.allclose(t1[whole:n], t2[whole:n], rtol=1e-6, atol=1e-6)
+            assert torch.equal(t1[n:], t2[n:])  # padding never written
