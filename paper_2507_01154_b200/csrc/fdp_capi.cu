@@ -224,12 +224,15 @@ struct GhostShape {
   bool pair;
   int nT, n_pairs, parts;  // parts: norm partials per sample
   int split, split_x;      // K slices of the larger operand per tile pair
+  int n_full;              // > 0: mixed schedule (whole items for the full waves, the last wave split)
+  long long units;         // work units of the launch
 };
 GhostShape ghost_shape(const fdp_desc* d, int sms) {
   const long long nT2 = (d->T + 255) / 256, np2 = nT2 * (nT2 + 1) / 2;
   const long long nT1 = (d->T + 127) / 128, np1 = nT1 * (nT1 + 1) / 2;
-  const long long clusters = sms / 2 > 0 ? sms / 2 : 1;
-  const long long ctas = sms > 0 ? sms : 1;
+  const int eff = std::max(2, sms - reserved_sms());  // the SMs the ghost launch gets
+  const long long clusters = eff / 2 > 0 ? eff / 2 : 1;
+  const long long ctas = eff > 0 ? eff : 1;
   const long long nkx = (d->P + 63) / 64, nky = (d->D + 63) / 64;
   const long long big = std::max(nkx, nky), small = std::min(nkx, nky);
   const int forced = env_int("FDP_GHOST_PAIR", -1);
@@ -239,19 +242,38 @@ GhostShape ghost_shape(const fdp_desc* d, int sms) {
   // 1 SM). Slicing the larger operand's K range S ways multiplies the items by S
   // and recomputes the smaller Gram per slice (tools/ghost_split_sweep.py: LM head
   // 768 -> 50304 at B=8 974 -> 924 us per layer, Llama 4096 -> 32000 at B=1 665 -> 610).
+  // Mixed schedule: when the items leave a partial last wave, the full waves run whole
+  // items and only the last wave's items are split (FDP_GHOST_MIXED=0 turns it off).
+  const bool mixed_ok = forced_split == 0 && env_int("FDP_GHOST_MIXED", 1) != 0;
   double best = 1e300;
   GhostShape g{};
   for (int pair = 1; pair >= 0; --pair) {
     if (forced >= 0 && forced != pair) continue;
     const long long items = d->B * (pair ? np2 : np1), slots = pair ? clusters : ctas;
+    const double f = pair ? 1.1 : 1.0;
     for (long long S = 1; S <= 16 && S <= big; ++S) {
       if (forced_split > 0 && S != forced_split) continue;
       const long long waves = (items * S + slots - 1) / slots;
-      const double t = static_cast<double>(waves) * static_cast<double>(small + (big + S - 1) / S) * (pair ? 1.1 : 1.0);
+      const double t = static_cast<double>(waves) * static_cast<double>(small + (big + S - 1) / S) * f;
       if (t < best * 0.98) {
         best = t;
         g.pair = pair != 0;
         g.split = static_cast<int>(S);
+        g.n_full = 0;
+      }
+    }
+    const long long fw = items / slots, tail = items - fw * slots;
+    if (mixed_ok && fw >= 1 && tail > 0) {
+      const long long S = std::min<long long>({16, big, slots / tail});
+      if (S >= 2) {
+        const double t = (static_cast<double>(fw) * static_cast<double>(small + big) +
+                          static_cast<double>(small + (big + S - 1) / S)) * f;
+        if (t < best * 0.98) {
+          best = t;
+          g.pair = pair != 0;
+          g.split = static_cast<int>(S);
+          g.n_full = static_cast<int>(fw * slots);
+        }
       }
     }
   }
@@ -263,6 +285,8 @@ GhostShape ghost_shape(const fdp_desc* d, int sms) {
   g.nT = static_cast<int>(g.pair ? nT2 : nT1);
   g.n_pairs = static_cast<int>(g.pair ? np2 : np1);
   g.parts = (g.pair ? 2 : 1) * g.n_pairs * g.split;
+  const long long items = d->B * static_cast<long long>(g.n_pairs);
+  g.units = g.n_full > 0 ? g.n_full + (items - g.n_full) * g.split : items * g.split;
   return g;
 }
 
@@ -1045,7 +1069,8 @@ int run(int32_t kind, const fdp_desc* d, const void* x, const void* dy, float* g
       g.n_pairs = gs.n_pairs;
       g.split = gs.split;
       g.split_x = gs.split_x;
-      g.n_items = g.n_pairs * g.B * g.split;
+      g.n_full = gs.n_full;
+      g.n_items = static_cast<int>(gs.units);
       g.part = p.ws_part;
       g.err = p.ws_ctrl + 1;
       g.budget_ns = p.budget_ns;

@@ -39,9 +39,14 @@ __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) { return make_sdesc_sw
 // Gram, so a slice of the larger operand's K range paired with the full Gram of
 // the smaller one gives a partial that sums to the sample's norm^2 (the smaller
 // Gram is recomputed per slice: cheap when P and D differ a lot, e.g. an LM head).
+// Mixed schedule (p.n_full > 0): work units 0 .. n_full - 1 are whole items (every
+// full wave of the launch), the remaining items are split `split` ways so the last
+// wave is filled instead of running a few whole items on mostly idle SMs; a whole
+// item writes slot 0 of its `split` partial slots and zeroes the others.
 struct GItem {
   int b, i, j, pair, s;
   int kx0, nx, ky0, ny;  // k-block ranges of the X and dY operands
+  bool whole;            // mixed schedule: an unsplit item (zeroes its other partial slots)
 };
 
 __device__ __forceinline__ void decode_item(int wi, int n_pairs, int nT, int& b, int& i, int& j) {
@@ -58,14 +63,23 @@ __device__ __forceinline__ void decode_item(int wi, int n_pairs, int nT, int& b,
 
 __device__ __forceinline__ GItem decode_split(int wi, const GhostParams& p, int nkx, int nky) {
   GItem it;
-  it.s = wi % p.split;
-  const int wp = wi / p.split;
+  int wp;
+  it.whole = p.n_full > 0 && wi < p.n_full;
+  if (it.whole) {
+    it.s = 0;
+    wp = wi;
+  } else {
+    const int j = wi - p.n_full;  // n_full = 0: the uniform schedule
+    it.s = j % p.split;
+    wp = p.n_full + j / p.split;
+  }
   decode_item(wp, p.n_pairs, p.nT, it.b, it.i, it.j);
   it.pair = wp % p.n_pairs;
   it.kx0 = 0;
   it.nx = nkx;
   it.ky0 = 0;
   it.ny = nky;
+  if (it.whole) return it;
   if (p.split_x) {
     it.kx0 = it.s * nkx / p.split;
     it.nx = (it.s + 1) * nkx / p.split - it.kx0;
@@ -201,7 +215,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float s = 0.0f;
 #pragma unroll
         for (int w = 0; w < kEpiWarps; ++w) s += red[w];
-        p.part[(static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s] = (i == j ? 1.0f : 2.0f) * s;
+        float* slot = p.part + (static_cast<long long>(b) * p.n_pairs + it.pair) * p.split;
+        slot[it.s] = (i == j ? 1.0f : 2.0f) * s;
+        if (it.whole)
+          for (int k = 1; k < p.split; ++k) slot[k] = 0.0f;
       }
       named_bar_sync(1, 32 * kEpiWarps);
     }
@@ -387,8 +404,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int w = 0; w < kEpiWarps; ++w) s += red[w];
           float* out = l == 0 ? p.part : (l == 1 ? p.part1 : p.part2);
-          out[((static_cast<long long>(b) * p.n_pairs + it.pair) * p.split + it.s) * 2 + rank] =
-              (i == j ? 1.0f : 2.0f) * s;
+          float* slot = out + (static_cast<long long>(b) * p.n_pairs + it.pair) * p.split * 2;
+          slot[it.s * 2 + rank] = (i == j ? 1.0f : 2.0f) * s;
+          if (it.whole)
+            for (int k = 1; k < p.split; ++k) slot[k * 2 + rank] = 0.0f;
         }
         named_bar_sync(1, 32 * kEpiWarps);
       }

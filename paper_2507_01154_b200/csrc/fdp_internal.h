@@ -176,6 +176,7 @@ struct GhostParams {
   int n_items;   // B * n_pairs * split
   int split;     // K slices of the larger operand per tile pair (1 = none)
   int split_x;   // 1: slice X's K (P >= D), 0: slice dY's K
+  int n_full;    // > 0: mixed schedule -- work units [0, n_full) are whole items, the rest split `split` ways
   float* part;   // [B][n_pairs][split] weighted partials (x2 for the CTA-pair kernel)
   unsigned* err;
   unsigned long long budget_ns;

@@ -240,3 +240,16 @@ def test_spill_noise_partition_and_accumulate(noise_impl, rank, world):
                          world=world, grad_out=ref, accumulate=True)
     torch.cuda.synchronize()
     assert float((got - ref).abs().max() / ref.abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("mixed", ["1", "0"])
+@pytest.mark.parametrize("B,T,P,D,pair", [(8, 1024, 1024, 1024, "1"), (3, 2048, 4096, 4096, "1"),
+                                          (8, 512, 2048, 1024, "0")])
+def test_ghost_mixed_schedule(B, T, P, D, pair, mixed, monkeypatch):
+    """Ghost norms with the mixed schedule (whole items for the full waves, the last
+    wave's items K-split, their unused partial slots zeroed) vs the uniform one: both
+    equal the oracle. Shapes whose items leave a partial last wave (80 pair items on
+    74 clusters; B = 3 at T = 2048: 108; single-CTA items over 148)."""
+    monkeypatch.setenv("FDP_GHOST_MIXED", mixed)
+    monkeypatch.setenv("FDP_GHOST_PAIR", pair)
+    _run_case(B, T, P, D, seed=70 + B, path="two_phase", norm_phase="ghost")
