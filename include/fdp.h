@@ -329,7 +329,7 @@ FDP_API int fdp_adam_step_scaled(int32_t dtype, void* theta, void* m, void* v, c
  * call it outside graph capture); fdp_adam_step_multi runs one step over it. */
 typedef struct fdp_adam_segment {
   float* theta;
-  float* m;
+  float* m;                /* Adam moments (NULL for an SGD-only table) */
   float* v;
   const float* grad;
   const float* grad_scale; /* NULL or a device scalar: g = grad * grad_scale[0] first */
@@ -342,6 +342,9 @@ FDP_API int fdp_adam_multi_prepare(int32_t n_seg, const fdp_adam_segment* segs, 
                                    int64_t* total_quads, void* stream);
 FDP_API int fdp_adam_step_multi(int32_t n_seg, const void* table, int64_t total_quads, double eta, double beta1,
                                 double beta2, double eps, void* stream);
+/* The DP-SGD step theta -= eta * g (g after grad_scale and noise, as fdp_sgd_step_scaled)
+ * over the same kind of table; its segments may leave m / v NULL (dpcore.py:131-136). */
+FDP_API int fdp_sgd_step_multi(int32_t n_seg, const void* table, int64_t total_quads, double eta, void* stream);
 
 /* Noise slice [lo, hi) of [0, n) owned by `rank` of `world` (data-parallel
  * noise-once partition). Pure host arithmetic. */

@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
     "fdp_backward_chained", "fdp_backward_shared_x", "fdp_dw_deferred", "fdp_sgd_step_scaled",
     "fdp_adam_step_scaled", "fdp_adam_multi_table_bytes", "fdp_adam_multi_prepare", "fdp_adam_step_multi",
+    "fdp_sgd_step_multi",
 )
 VEC_KIND = {"bias": 0, "rmsnorm": 1, "layernorm": 2}
 
@@ -162,7 +163,9 @@ def load() -> ctypes.CDLL:
                                            ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p]
     lib.fdp_adam_step_multi.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
-    for name in ("fdp_adam_multi_table_bytes", "fdp_adam_multi_prepare", "fdp_adam_step_multi",
+    lib.fdp_sgd_step_multi.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                       ctypes.c_void_p]
+    for name in ("fdp_sgd_step_multi", "fdp_adam_multi_table_bytes", "fdp_adam_multi_prepare", "fdp_adam_step_multi",
                  "fdp_dw_deferred", "fdp_sgd_step_scaled", "fdp_adam_step_scaled", "fdp_backward_shared_x", "fdp_chain_create", "fdp_chain_destroy", "fdp_chain_flush", "fdp_chain_stats", "fdp_dw_chained",
                  "fdp_backward_chained", "fdp_vec_workspace_bytes", "fdp_vec_dw", "fdp_embedding_workspace_bytes", "fdp_embedding_dw",
                  "fdp_bias_workspace_bytes", "fdp_bias_dw", "fdp_sgd_step", "fdp_adam_step", "fdp_group_workspace_bytes_ex", "fdp_backward_group_ex", "fdp_group_workspace_bytes",

@@ -1766,7 +1766,8 @@ int fdp_adam_multi_prepare(int32_t n_seg, const fdp_adam_segment* segs, void* ta
   for (int i = 0; i < n_seg; ++i) {
     const fdp_adam_segment& a = segs[i];
     if (a.n < 0) return fail(FDP_ERR_SHAPE, "segment %d: negative element count", i);
-    if (a.n > 0 && (!a.theta || !a.m || !a.v || !a.grad)) return fail(FDP_ERR_USAGE, "segment %d: null pointer", i);
+    if (a.n > 0 && (!a.theta || !a.grad)) return fail(FDP_ERR_USAGE, "segment %d: null pointer", i);
+    if (a.n > 0 && (!a.m != !a.v)) return fail(FDP_ERR_USAGE, "segment %d: m and v both set or both NULL", i);
     if (((reinterpret_cast<uintptr_t>(a.theta) | reinterpret_cast<uintptr_t>(a.m) |
           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.grad)) & 15u) != 0)
       return fail(FDP_ERR_USAGE, "segment %d: theta / m / v / grad must be 16-byte aligned", i);
@@ -1815,6 +1816,15 @@ int fdp_adam_step_multi(int32_t n_seg, const void* table, int64_t total_quads, d
   cudaError_t e = fdp::adam_multi(static_cast<const fdp::AdamSeg*>(table), n_seg, total_quads, eta, beta1, beta2, eps,
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "multi-segment adam step");
+  return FDP_OK;
+}
+
+int fdp_sgd_step_multi(int32_t n_seg, const void* table, int64_t total_quads, double eta, void* stream) {
+  if (n_seg < 0 || (n_seg > 0 && !table) || total_quads < 0) return fail(FDP_ERR_USAGE, "bad arguments");
+  if (!(eta == eta) || !std::isfinite(eta)) return fail(FDP_ERR_USAGE, "eta must be finite");
+  cudaError_t e = fdp::adam_multi(static_cast<const fdp::AdamSeg*>(table), n_seg, total_quads, eta, 0.0, 0.0, 0.0,
+                                  static_cast<cudaStream_t>(stream), false);
+  if (e != cudaSuccess) return cuda_fail(e, "multi-segment sgd step");
   return FDP_OK;
 }
 

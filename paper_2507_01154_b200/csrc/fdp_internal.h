@@ -312,7 +312,7 @@ struct AdamSeg {
   uint64_t seed_u, layer_u;
 };
 cudaError_t adam_multi(const AdamSeg* dev_segs, int n_seg, long long total_q, double eta, double b1, double b2,
-                       double eps, cudaStream_t s);
+                       double eps, cudaStream_t s, bool adam = true);
 cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const void* g, long long n, double eta,
                        double b1, double b2, double eps, const OptimNoise& nz, cudaStream_t s);
 

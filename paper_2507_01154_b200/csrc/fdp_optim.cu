@@ -185,6 +185,8 @@ __device__ __forceinline__ int seg_of(const AdamSeg* segs, int n_seg, long long 
   return lo;
 }
 
+// kAdam false: the plain DP-SGD step theta -= eta * g (k_sgd's arithmetic; m / v unused)
+template <bool kAdam>
 __global__ void __launch_bounds__(256, FDP_ADAM_NOISE_MINB) k_adam_multi(const AdamSeg* __restrict__ segs, int n_seg,
                                                                          long long total_q, float eta, float b1,
                                                                          float b2, float eps) {
@@ -208,17 +210,21 @@ __global__ void __launch_bounds__(256, FDP_ADAM_NOISE_MINB) k_adam_multi(const A
     float4* v4 = reinterpret_cast<float4*>(S.v);
     const float4* g4 = reinterpret_cast<const float4*>(S.g);
     const bool full = e0 + 4 <= S.n;
-    float4 gg, mm, vv, tt;
+    float4 gg, mm = make_float4(0.f, 0.f, 0.f, 0.f), vv = mm, tt;
     if (full) {
       gg = __ldcs(g4 + lq);
-      mm = __ldcs(m4 + lq);
-      vv = __ldcs(v4 + lq);
+      if constexpr (kAdam) {
+        mm = __ldcs(m4 + lq);
+        vv = __ldcs(v4 + lq);
+      }
       tt = __ldcs(th4 + lq);
     } else {  // the segment's last partial quad (elements past n are never stored)
       const long long r = S.n - e0;
       gg = make_float4(S.g[e0], r > 1 ? S.g[e0 + 1] : 0.f, r > 2 ? S.g[e0 + 2] : 0.f, 0.f);
-      mm = make_float4(S.m[e0], r > 1 ? S.m[e0 + 1] : 0.f, r > 2 ? S.m[e0 + 2] : 0.f, 0.f);
-      vv = make_float4(S.v[e0], r > 1 ? S.v[e0 + 1] : 0.f, r > 2 ? S.v[e0 + 2] : 0.f, 0.f);
+      if constexpr (kAdam) {
+        mm = make_float4(S.m[e0], r > 1 ? S.m[e0 + 1] : 0.f, r > 2 ? S.m[e0 + 2] : 0.f, 0.f);
+        vv = make_float4(S.v[e0], r > 1 ? S.v[e0 + 1] : 0.f, r > 2 ? S.v[e0 + 2] : 0.f, 0.f);
+      }
       tt = make_float4(S.theta[e0], r > 1 ? S.theta[e0 + 1] : 0.f, r > 2 ? S.theta[e0 + 2] : 0.f, 0.f);
     }
     if (S.gscale) {
@@ -234,18 +240,31 @@ __global__ void __launch_bounds__(256, FDP_ADAM_NOISE_MINB) k_adam_multi(const A
       gg.z += S.scale * z.z;
       gg.w += S.scale * z.w;
     }
-    adam_quad(tt, mm, vv, gg, eta, b1, b2, eps);
+    if constexpr (kAdam) {
+      adam_quad(tt, mm, vv, gg, eta, b1, b2, eps);
+    } else {
+      tt.x = tt.x - eta * gg.x;
+      tt.y = tt.y - eta * gg.y;
+      tt.z = tt.z - eta * gg.z;
+      tt.w = tt.w - eta * gg.w;
+    }
     if (full) {
       __stcs(th4 + lq, tt);
-      __stcs(m4 + lq, mm);
-      __stcs(v4 + lq, vv);
+      if constexpr (kAdam) {
+        __stcs(m4 + lq, mm);
+        __stcs(v4 + lq, vv);
+      }
     } else {
       const long long r = S.n - e0;
       S.theta[e0] = tt.x;
-      S.m[e0] = mm.x;
-      S.v[e0] = vv.x;
-      if (r > 1) { S.theta[e0 + 1] = tt.y; S.m[e0 + 1] = mm.y; S.v[e0 + 1] = vv.y; }
-      if (r > 2) { S.theta[e0 + 2] = tt.z; S.m[e0 + 2] = mm.z; S.v[e0 + 2] = vv.z; }
+      if (r > 1) S.theta[e0 + 1] = tt.y;
+      if (r > 2) S.theta[e0 + 2] = tt.z;
+      if constexpr (kAdam) {
+        S.m[e0] = mm.x;
+        S.v[e0] = vv.x;
+        if (r > 1) { S.m[e0 + 1] = mm.y; S.v[e0 + 1] = vv.y; }
+        if (r > 2) { S.m[e0 + 2] = mm.z; S.v[e0 + 2] = vv.z; }
+      }
     }
   }
 }
@@ -309,12 +328,13 @@ cudaError_t optim_step(int adam, int f64, void* theta, void* m, void* v, const v
 }
 
 cudaError_t adam_multi(const AdamSeg* dev_segs, int n_seg, long long total_q, double eta, double b1, double b2,
-                       double eps, cudaStream_t s) {
+                       double eps, cudaStream_t s, bool adam) {
   if (n_seg <= 0 || total_q <= 0) return cudaSuccess;
   const long long blocks = (total_q + kMultiChunk - 1) / kMultiChunk;
-  k_adam_multi<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_segs, n_seg, total_q, static_cast<float>(eta),
-                                                             static_cast<float>(b1), static_cast<float>(b2),
-                                                             static_cast<float>(eps));
+  auto k = adam ? k_adam_multi<true> : k_adam_multi<false>;
+  k<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_segs, n_seg, total_q, static_cast<float>(eta),
+                                                  static_cast<float>(b1), static_cast<float>(b2),
+                                                  static_cast<float>(eps));
   return cudaGetLastError();
 }
 

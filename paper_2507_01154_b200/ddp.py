@@ -626,6 +626,16 @@ def dp_noise_keys(model) -> dict:
     return keys
 
 
+def _torch_sgd_(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
+                grad_scale=None):
+    """Device-agnostic stand-in of fdp_sgd_step(_scaled) for CPU tests (no noise)."""
+    if noise_cfg is not None and noise_cfg.sigma > 0:
+        raise RuntimeError("the torch SGD stand-in does not draw DP noise")
+    if grad_scale is not None:
+        grad = grad * grad_scale.to(grad.device)
+    theta.sub_(eta * grad)
+
+
 def _torch_adam_(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
                  grad_scale=None):
     """Device-agnostic stand-in of fdp_adam_step(_scaled) for CPU tests (no noise)."""
@@ -654,18 +664,24 @@ class BucketedAdam:
     noise_impl, layer_numel)` replaces the CUDA kernel in CPU tests."""
 
     def __init__(self, buckets: GradBuckets, *, lr: float, beta1: float = 0.9, beta2: float = 0.999,
-                 eps: float = 1e-8, noise_keys: "dict | None" = None, adam_fn=None):
+                 eps: float = 1e-8, noise_keys: "dict | None" = None, adam_fn=None, kind: str = "adam"):
         if any(b.pflat is None for b in buckets.buckets):
             raise ValueError("BucketedAdam needs GradBuckets(flat_params=True)")
+        if kind not in ("adam", "sgd"):
+            raise ValueError(f"kind must be adam or sgd, got {kind!r}")
+        self.kind = kind
         self.bk = buckets
         self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
         self.noise_keys = noise_keys or {}
-        self.adam_fn = adam_fn or self._kernel
+        self.adam_fn = adam_fn or (self._kernel if kind == "adam" else self._sgd_kernel)
         zero1 = buckets.mode == "reduce_scatter"
         for b in buckets.buckets:
             n = b.per if zero1 else b.n
-            b.m = torch.zeros(n, dtype=torch.float32, device=b.flat.device)
-            b.v = torch.zeros_like(b.m)
+            if kind == "adam":
+                b.m = torch.zeros(n, dtype=torch.float32, device=b.flat.device)
+                b.v = torch.zeros_like(b.m)
+            else:  # plain DP-SGD (dpcore.py:131-136): no moments
+                b.m = b.v = None
         # ZeRO-1 on CUDA at N > 1: each bucket's parameter all-gather runs on the buckets'
         # communication stream as soon as its shard is stepped; `gathered[i]` is the event a
         # reader of bucket i's parameters waits on (DataParallelStep: forward pre-hooks)
@@ -687,6 +703,14 @@ class BucketedAdam:
         st = OptimizerState(theta=theta, m=m, v=v, eta=eta, beta1=b1, beta2=b2, eps_adam=eps)
         dp_adam_step_(st, grad, noise=noise_cfg, noise_offset=noise_offset, noise_impl=noise_impl or "philox",
                       layer_numel=layer_numel, grad_scale=grad_scale, device_step=device_step)
+
+    @staticmethod
+    def _sgd_kernel(theta, m, v, grad, eta, b1, b2, eps, noise_cfg, noise_offset, noise_impl, layer_numel,
+                    grad_scale=None, device_step=None):
+        from .dpcore import dp_sgd_step_
+
+        dp_sgd_step_(theta, grad, eta, noise=noise_cfg, noise_offset=noise_offset, noise_impl=noise_impl or "philox",
+                     layer_numel=layer_numel, grad_scale=grad_scale, device_step=device_step)
 
     def _segments(self, b, lo: int, hi: int):
         """(a, z, noise key or None) pieces of [lo, hi) cut at parameter bounds;
@@ -733,9 +757,12 @@ class BucketedAdam:
                 src = b.shard if zero1 else b.flat
                 gs = b.scale_buf.data_ptr() if b.scale_buf is not None else None
                 for a, z, nkey in self._segments(b, lo, hi):
-                    seg = _lib.FdpAdamSegment(theta=b.pflat[a:z].data_ptr(), m=b.m[a - lo:z - lo].data_ptr(),
-                                              v=b.v[a - lo:z - lo].data_ptr(), grad=src[a - lo:z - lo].data_ptr(),
-                                              grad_scale=gs, n=z - a, noise=None, noise_offset=0)
+                    adam = self.kind == "adam"
+                    seg = _lib.FdpAdamSegment(theta=b.pflat[a:z].data_ptr(),
+                                              m=b.m[a - lo:z - lo].data_ptr() if adam else None,
+                                              v=b.v[a - lo:z - lo].data_ptr() if adam else None,
+                                              grad=src[a - lo:z - lo].data_ptr(), grad_scale=gs, n=z - a, noise=None,
+                                              noise_offset=0)
                     if nkey is not None:
                         cfg, off, glen, impl = nkey
                         if (impl or "philox") != "philox" or off % 4:
@@ -776,8 +803,11 @@ class BucketedAdam:
                 idx, table, n_seg, tq = plan[k]
                 for i in idx:
                     bk.wait_bucket(i)
-                _lib.check(lib.fdp_adam_step_multi(n_seg, table.data_ptr(), tq, self.lr, self.beta1, self.beta2,
-                                                   self.eps, st))
+                if self.kind == "adam":
+                    _lib.check(lib.fdp_adam_step_multi(n_seg, table.data_ptr(), tq, self.lr, self.beta1, self.beta2,
+                                                       self.eps, st))
+                else:
+                    _lib.check(lib.fdp_sgd_step_multi(n_seg, table.data_ptr(), tq, self.lr, st))
                 if bk.world > 1 and bk.mode == "reduce_scatter":
                     for i in idx:
                         self._gather(i, bk.buckets[i])
@@ -803,7 +833,8 @@ class BucketedAdam:
             src = b.shard if bk.mode == "reduce_scatter" else b.flat
             for a, z, key in self._segments(b, lo, hi):
                 th, g = b.pflat[a:z], src[a - lo:z - lo]
-                mm, vv = b.m[a - lo:z - lo], b.v[a - lo:z - lo]
+                mm = b.m[a - lo:z - lo] if b.m is not None else None
+                vv = b.v[a - lo:z - lo] if b.v is not None else None
                 if key is None:
                     self.adam_fn(th, mm, vv, g, self.lr, self.beta1, self.beta2, self.eps, None, 0, None, 0, **kw)
                 else:
@@ -873,13 +904,16 @@ class DataParallelStep:
     buckets of their own (in both arms: same layout)
     and a single-sample layer hands its gradient over unclipped with its clip
     factor (GradBuckets), so its elementwise clip pass never runs: the collective
-    (PreMulSum) or, at world 1, the Adam step applies the factor."""
+    (PreMulSum) or, at world 1, the Adam step applies the factor.
+
+    ``optimizer``: "adam" (the reference's DP-Adam, default) or "sgd" (plain DP-SGD,
+    theta -= lr * g, dpcore.py:131-136: BASELINE config 2's optimizer)"""
 
     def __init__(self, model, *, dp: bool, mode: str = "allreduce", lr: float = 1e-5, beta1: float = 0.9,
                  beta2: float = 0.999, eps: float = 1e-8, rank: int = 0, world: int = 1, group=None,
                  comm_sms: int = 4, bucket_bytes: int = 512 << 20, global_batch: int = 1, adam_fn=None,
                  noise_in_optimizer: bool = True, defer_clip: "bool | None" = None,
-                 isolate_min_numel: int = 1 << 22):
+                 isolate_min_numel: int = 1 << 22, optimizer: str = "adam"):
         from .dplinear import DPLinear
 
         self.model, self.dp, self.mode, self.world = model, dp, mode, world
@@ -901,7 +935,7 @@ class DataParallelStep:
             self.buckets.set_deferred([m.weight for m in self.dp_mods if isinstance(m, DPLinear)])
         keys = dp_noise_keys(model) if dp and self.noise_in_optimizer else None
         self.opt = BucketedAdam(self.buckets, lr=lr, beta1=beta1, beta2=beta2, eps=eps, noise_keys=keys,
-                                adam_fn=adam_fn)
+                                adam_fn=adam_fn, kind=optimizer)
         dev = next(model.parameters()).device
         self.max_ctas = group_max_ctas(dev, comm_sms, world)
         # ZeRO-1 at N > 1: the next forward overlaps the parameter all-gathers -- a module

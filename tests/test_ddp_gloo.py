@@ -356,3 +356,48 @@ def test_grad_buckets_materialize_scales_and_isolation_layout():
     _torch_adam_(ref.view(-1), m.view(-1), v.view(-1), torch.full_like(ref, 0.25).view(-1), 1e-2, 0.9, 0.999, 1e-8,
                  None, 0, None, 0)
     assert torch.allclose(w.detach(), ref)
+
+
+def _sgd_worker(rank, world, port, mode, out):
+    from paper_2507_01154_b200.ddp import DataParallelStep, _torch_sgd_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    model = _bucket_model()
+    g = torch.Generator().manual_seed(3)
+    x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+    lo, hi = 8 * rank // world, 8 * (rank + 1) // world
+    step = DataParallelStep(model, dp=False, mode=mode, lr=1e-2, rank=rank, world=world, global_batch=8,
+                            adam_fn=_torch_sgd_, bucket_bytes=600, optimizer="sgd")
+    assert all(b.m is None for b in step.buckets.buckets)
+    for i in range(3):
+        step(i, lambda: ((model(x[lo:hi]) - y[lo:hi]) ** 2).sum(1).sum() / 8)
+    out[(mode, world, rank)] = [p.detach().clone() for p in model.parameters()]
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_bucketed_sgd_step_two_ranks_equals_plain_sgd():
+    """DataParallelStep(optimizer="sgd"): plain SGD on the bucket layout, world 2 over
+    gloo in both bucket modes == three plain SGD steps on the global batch."""
+    model = _bucket_model()
+    g = torch.Generator().manual_seed(3)
+    x, y = torch.randn(8, 16, generator=g), torch.randn(8, 8, generator=g)
+    for _ in range(3):
+        model.zero_grad()
+        (((model(x) - y) ** 2).sum(1).sum() / 8).backward()
+        with torch.no_grad():
+            for p in model.parameters():
+                p -= 1e-2 * p.grad
+    ref = [p.detach().clone() for p in model.parameters()]
+    for mode in ("allreduce", "reduce_scatter"):
+        with mp.Manager() as mgr:
+            out = mgr.dict()
+            _sgd_worker(0, 1, _free_port(), mode, out)
+            mp.spawn(_sgd_worker, args=(2, _free_port(), mode, out), nprocs=2, join=True)
+            for key in ((mode, 1, 0), (mode, 2, 0), (mode, 2, 1)):
+                for a, b in zip(out[key], ref):
+                    assert torch.allclose(a, b, rtol=1e-5, atol=1e-6), key

@@ -9,7 +9,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _run(graphed: bool, dp: bool, mode: str, B: int, n_steps: int = 6, warmup: int = 3, d: int = 256):
+def _run(graphed: bool, dp: bool, mode: str, B: int, n_steps: int = 6, warmup: int = 3, d: int = 256,
+         optimizer: str = "adam", multi: bool = True):
     from paper_2507_01154_b200.ddp import DataParallelStep, GraphedStep
     from paper_2507_01154_b200.llama import Llama, LlamaConfig
 
@@ -20,7 +21,9 @@ def _run(graphed: bool, dp: bool, mode: str, B: int, n_steps: int = 6, warmup: i
     g = torch.Generator().manual_seed(5)
     idx = torch.randint(0, cfg.vocab, (B, cfg.seq + 1), generator=g).cuda()
     x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
-    step = DataParallelStep(model, dp=dp, mode=mode, lr=1e-3, global_batch=B, bucket_bytes=1 << 20)
+    step = DataParallelStep(model, dp=dp, mode=mode, lr=1e-3, global_batch=B, bucket_bytes=1 << 20,
+                            optimizer=optimizer)
+    step.opt.multi = multi
     scale = 1.0 if dp else 1.0 / B
 
     def loss_fn():
@@ -76,3 +79,19 @@ def test_graphed_step_with_deferred_clips():
         assert abs(a - b) <= 5e-4 * max(1.0, abs(a))
     for a, b in zip(eager, graphed):
         assert torch.allclose(a, b, rtol=1e-4, atol=2e-5), float((a - b).abs().max())
+
+
+@pytest.mark.parametrize("optimizer", ["adam", "sgd"])
+def test_one_launch_optimizer_equals_per_segment_launches(optimizer):
+    """The bucketed DP optimizer as ONE multi-segment launch (fdp_adam_step_multi /
+    fdp_sgd_step_multi over a device table, noise keyed on a device step counter) gives
+    the parameters of one launch per parameter segment (fdp_adam_step / fdp_sgd_step
+    with host step keys); and a captured SGD step replays the eager ones."""
+    multi, _ = _run(False, True, "allreduce", 2, n_steps=3, warmup=1, optimizer=optimizer)
+    per_seg, _ = _run(False, True, "allreduce", 2, n_steps=3, warmup=1, optimizer=optimizer, multi=False)
+    for a, b in zip(multi, per_seg):
+        assert torch.allclose(a, b, rtol=1e-6, atol=1e-7), float((a - b).abs().max())
+    if optimizer == "sgd":
+        graphed, _ = _run(True, True, "allreduce", 2, n_steps=3, warmup=1, optimizer="sgd")
+        for a, b in zip(graphed, multi):
+            assert torch.allclose(a, b, rtol=1e-5, atol=1e-7), float((a - b).abs().max())

@@ -18,11 +18,11 @@ from paper_2507_01154_b200.ddp import DataParallelStep, GraphedStep  # noqa: E40
 from paper_2507_01154_b200.gpt2 import GPT2, GPT2Config  # noqa: E402
 
 
-def run(dp: bool, graphed: bool, B: int, steps: int) -> dict:
+def run(dp: bool, graphed: bool, B: int, steps: int, optimizer: str = "adam") -> dict:
     torch.manual_seed(0)
     cfg = GPT2Config(seq=1024)
     model = GPT2(cfg, dp="full" if dp else False, clip_c=1.0, sigma=1.0, tied=False, nondp_linear="fp32grad").cuda()
-    step = DataParallelStep(model, dp=dp, lr=1e-4, global_batch=B)
+    step = DataParallelStep(model, dp=dp, lr=1e-4, global_batch=B, optimizer=optimizer)
     g = torch.Generator(device="cuda").manual_seed(1)
     idx = torch.randint(0, cfg.vocab, (B, cfg.seq + 1), device="cuda", generator=g)
     x, y = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
@@ -64,14 +64,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", default="1,2,4,8")
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"],
+                    help="sgd: plain DP-SGD (BASELINE config 2's optimizer)")
     a = ap.parse_args()
     for B in (int(b) for b in a.batches.split(",")):
         row = {"model": "gpt2-small, every parameter DP (untied LM head, vocab padded to 50304) vs FP32GradLinear "
-                        "non-DP, DataParallelStep + bucketed Adam", "batch": B, "seq": 1024}
+                        "non-DP, DataParallelStep + bucketed " + a.optimizer, "batch": B, "seq": 1024}
         for graphed in (False, True):
             tag = "graphed" if graphed else "eager"
-            nd = run(False, graphed, B, a.steps)
-            dp = run(True, graphed, B, a.steps)
+            nd = run(False, graphed, B, a.steps, a.optimizer)
+            dp = run(True, graphed, B, a.steps, a.optimizer)
             row[tag] = {"dp": dp, "non_dp": nd, "dp_pct_of_non_dp": round(100.0 * dp["tokens_per_s"] /
                                                                           nd["tokens_per_s"], 1)}
         print(json.dumps(row), flush=True)
