@@ -553,14 +553,15 @@ def main():
                                 "dp_modules": dp_f["dp_modules"],
                                 "dp_scope": "every parameter: 48 linear weights + biases, 25 LayerNorms, token and "
                                             "position embeddings, untied LM head (vocab padded to 50304)"}
-            # the same step captured in ONE CUDA graph (ddp.GraphedStep), every parameter DP vs
-            # non-DP, at the paper's smallest batch (host-bound eager) and at the bench's B
+            # BASELINE config 2 as stated (DP-SGD): the step through DataParallelStep(optimizer="sgd")
+            # captured in ONE CUDA graph (ddp.GraphedStep), every parameter DP vs non-DP, at the
+            # paper's smallest batch (host-bound eager) and at the bench's B
             import train_graphed as tgr
 
-            graphed = {}
+            graphed = {"optimizer": "DP-SGD (one fdp_sgd_step_multi launch; noise keyed on a device step)"}
             for gb in sorted({1, B}):
-                nd_g = tgr.run(False, True, gb, 20)
-                dp_g = tgr.run(True, True, gb, 20)
+                nd_g = tgr.run(False, True, gb, 20, "sgd")
+                dp_g = tgr.run(True, True, gb, 20, "sgd")
                 graphed[f"B{gb}"] = {"dp_tokens_per_s": dp_g["tokens_per_s"], "non_dp_tokens_per_s":
                                      nd_g["tokens_per_s"], "dp_pct_of_non_dp":
                                      100.0 * dp_g["tokens_per_s"] / nd_g["tokens_per_s"]}
