@@ -82,5 +82,20 @@ fdp.workflows._run(fdp.WorkflowKind.FLASHDP, *inputs(2, 256, 512, 384), cfg, Non
 st = fdp.OptimizerState.fresh(torch.zeros(1003, device="cuda"), eta=0.1)
 fdp.dp_adam_step_(st, torch.ones(1003, device="cuda"), grad_scale=sc, noise=cfg, layer_numel=1003)
 fdp.dp_sgd_step_(torch.zeros(1003, device="cuda"), torch.ones(1003, device="cuda"), 0.1, grad_scale=sc)
+# session 2 (cont.): mixed ghost schedule (whole items + K-split last wave), multi-segment Adam / SGD
+os.environ["FDP_GHOST_PAIR"] = "1"
+fdp.backward_flashdp(*inputs(8, 256, 256, 256), cfg, path="two_phase", norm_phase="ghost")  # 8 items, few clusters
+os.environ.pop("FDP_GHOST_PAIR")
+from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets  # noqa: E402
+
+for kind in ("adam", "sgd"):
+    ps = [torch.nn.Parameter(torch.randn(n, device="cuda")) for n in (1001, 3, 4096)]
+    bk = GradBuckets(ps, flat_params=True, hooks=False, isolate=[ps[2]])
+    bk.zero_grad()
+    for p_ in ps:
+        p_.grad.copy_(torch.randn_like(p_))
+    keys = {id(ps[0]): (cfg, 0, 1001, "philox"), id(ps[2]): (cfg, 0, 4096, "philox")}
+    opt = BucketedAdam(bk, lr=1e-3, noise_keys=keys, kind=kind)
+    opt.step(3)
 torch.cuda.synchronize()
 print("sanitize cases done")
