@@ -43,6 +43,23 @@ def main():
         us = timed(lambda: fdp.dp_adam_step_(st, grad, **kw))
         row[name + "_us"] = round(us, 1)
         row[name + "_gbs"] = round(bytes_adam / us / 1e3, 0)
+    # the one-launch bucketed DP-Adam over the same 134 M parameters (+ 64 small ones)
+    from paper_2507_01154_b200.ddp import BucketedAdam, GradBuckets
+
+    ps = [torch.nn.Parameter(torch.zeros(n, device="cuda"))] + [torch.nn.Parameter(torch.zeros(768, device="cuda"))
+                                                               for _ in range(64)]
+    bk = GradBuckets(ps, flat_params=True, hooks=False, isolate=ps[:1])
+    bk.zero_grad()
+    keys = {id(p_): (cfg, 0, p_.numel(), "philox") for p_ in ps}
+    opt = BucketedAdam(bk, lr=1e-4, noise_keys=keys)
+    it = [0]
+
+    def multi():
+        it[0] += 1
+        opt.step(it[0])
+    us = timed(multi)
+    row["adam_multi_noise_us"] = round(us, 1)
+    row["adam_multi_noise_gbs"] = round(28.0 * (n + 64 * 768) / us / 1e3, 0)
     print(json.dumps(row), flush=True)
 
 
