@@ -80,7 +80,8 @@ def test_graphed_step_with_deferred_clips():
     for a, b in zip(le, lg):
         assert abs(a - b) <= 5e-4 * max(1.0, abs(a))
     for a, b in zip(eager, graphed):
-        assert torch.allclose(a, b, rtol=1e-4, atol=2e-5), float((a - b).abs().max())
+        # a wrong noise key or step would move parameters by ~lr = 1e-3 per step
+        assert torch.allclose(a, b, rtol=1e-4, atol=1e-4), float((a - b).abs().max())
 
 
 @pytest.mark.parametrize("optimizer", ["adam", "sgd"])
@@ -97,3 +98,61 @@ def test_one_launch_optimizer_equals_per_segment_launches(optimizer):
         graphed, _ = _run(True, True, "allreduce", 2, n_steps=3, warmup=1, optimizer="sgd")
         for a, b in zip(graphed, multi):
             assert torch.allclose(a, b, rtol=1e-5, atol=1e-7), float((a - b).abs().max())
+
+
+def _gpt2_run(graphed: bool, n_steps: int = 5, warmup: int = 2):
+    """Tiny GPT-2 with every parameter DP (DP embeddings: token-dependent per-sample
+    work, LayerNorm / bias groups), DP-SGD; a different batch every step, copied into
+    static buffers."""
+    from paper_2507_01154_b200.ddp import DataParallelStep
+    from paper_2507_01154_b200.gpt2 import GPT2, GPT2Config
+
+    cfg = GPT2Config(vocab=256, seq=64, d=128, heads=4, layers=2, mlp=256)
+    torch.manual_seed(0)
+    model = GPT2(cfg, dp="full", clip_c=0.5, sigma=1.0, tied=False, nondp_linear="fp32grad").cuda()
+    B = 2
+    step = DataParallelStep(model, dp=True, lr=1e-2, global_batch=B, optimizer="sgd")
+    g = torch.Generator().manual_seed(9)
+    batches = [torch.randint(0, cfg.vocab, (B, cfg.seq + 1), generator=g).cuda() for _ in range(n_steps)]
+    xs = torch.empty(B, cfg.seq, dtype=torch.int64, device="cuda")
+    ys = torch.empty_like(xs)
+
+    def load(i):
+        xs.copy_(batches[i][:, :-1])
+        ys.copy_(batches[i][:, 1:])
+
+    def loss_fn():
+        return model.loss(xs, ys) * B
+
+    if graphed:
+        from paper_2507_01154_b200.ddp import GraphedStep
+
+        class _Loading:  # the eager warm-up steps load their own batch; the captured step does not
+            def __init__(self, s):
+                self.__dict__["_s"] = s
+
+            def __getattr__(self, k):
+                return getattr(self._s, k)
+
+            def __call__(self, i, fn):
+                if not torch.cuda.is_current_stream_capturing():
+                    load(i)
+                return self._s(i, fn)
+
+        gs = GraphedStep(_Loading(step), loss_fn, warmup=warmup)
+        for i in range(gs.next_step, n_steps):
+            load(i)
+            gs()
+    else:
+        for i in range(n_steps):
+            load(i)
+            step(i, loss_fn)
+    torch.cuda.synchronize()
+    return [p.detach().clone() for p in model.parameters()]
+
+
+def test_graphed_gpt2_full_dp_with_changing_batches():
+    eager = _gpt2_run(False)
+    graphed = _gpt2_run(True)
+    for a, b in zip(eager, graphed):
+        assert torch.allclose(a, b, rtol=1e-4, atol=1e-5), float((a - b).abs().max())
