@@ -19,8 +19,11 @@
 // run of equal tokens (never materialising G_b); a streaming pass writes every
 // row's noise, and the add pass walks all samples' sorted runs per vocabulary row
 // in fixed order onto the touched rows -- deterministic, no atomics.
+#include <cstdlib>
+
 #include "../../include/fdp.h"
 #include "fdp_internal.h"
+#include "fdp_ptx.cuh"
 #include "fdp_rng.cuh"
 #include <cuda_bf16.h>
 
@@ -53,6 +56,7 @@ __device__ __forceinline__ float ld(const T* p, long long i) {
 template <typename T, int kKind, int VW>
 __global__ void __launch_bounds__(kVCols) k_vec_rows(const T* __restrict__ dy, const T* __restrict__ xh, int T_, int D,
                                                      int n_tc, float* __restrict__ gpart) {
+  if (threadIdx.x == 0) pdl_launch_dependents();  // the reduce may queue up behind this pass
   const int b = blockIdx.z, tc = blockIdx.y;
   const int d = (blockIdx.x * kVCols + threadIdx.x) * VW;
   if (d >= D) return;
@@ -117,6 +121,8 @@ __global__ void __launch_bounds__(kVCols) k_vec_rows(const T* __restrict__ dy, c
 // pass 2: g[b][l] = sum_tc gpart[b][tc][l] (fixed order), part[b][chunk] = sum over the block of g^2
 __global__ void __launch_bounds__(kVCols) k_vec_reduce(const float* __restrict__ gpart, int n_tc, int L,
                                                        float* __restrict__ g, float* __restrict__ part, int n_chunks) {
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // PDL launch: the row partials are complete
   const int b = blockIdx.y, chunk = blockIdx.x;
   const int l = chunk * kVCols + threadIdx.x;
   float s = 0.0f;
@@ -144,6 +150,7 @@ __global__ void __launch_bounds__(256) k_vec_finalize(const float* __restrict__ 
                                                       float inv_batch, float* out, float* norms_out, int accumulate,
                                                       NoiseKey nk) {
   extern __shared__ float fac[];  // [B] clip factor x mean scale
+  pdl_wait();  // PDL launch: g and the norm partials are complete
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[static_cast<long long>(b) * n_chunks + c]);
@@ -439,13 +446,30 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
 #undef FDP_VEC_ROWS
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_vec_reduce<<<dim3(n_chunks, B), kVCols, 0, s>>>(gpart, n_tc, static_cast<int>(L), g, part, n_chunks);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // the reduce and the finalize are programmatic dependents of the pass before them: their
+  // launch latency hides under it (three small kernels per group; FDP_PDL=0 turns it off)
+  const char* pv = std::getenv("FDP_PDL");
+  const bool pdl = !pv || std::atoi(pv) != 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t c2{};
+  c2.gridDim = dim3(n_chunks, B);
+  c2.blockDim = dim3(kVCols);
+  c2.stream = s;
+  c2.attrs = attr;
+  c2.numAttrs = pdl ? 1 : 0;
+  if ((e = cudaLaunchKernelEx(&c2, k_vec_reduce, static_cast<const float*>(gpart), n_tc, static_cast<int>(L), g, part,
+                              n_chunks)) != cudaSuccess)
+    return e;
   const long long blocks = (L + 255) / 256 < 148 ? (L + 255) / 256 : 148;
   // factor table rounded up to whole 16-byte words: the unrolled sample loop may read fac[] in vectors
-  k_vec_finalize<<<static_cast<int>(blocks), 256, static_cast<size_t>((B + 3) / 4) * 16, s>>>(
-      g, part, B, L, n_chunks, clip_c, clip_c * clip_c, inv_batch, out, norms_out, accumulate, nk);
-  return cudaGetLastError();
+  cudaLaunchConfig_t c3 = c2;
+  c3.gridDim = dim3(static_cast<unsigned>(blocks));
+  c3.blockDim = dim3(256);
+  c3.dynamicSmemBytes = static_cast<size_t>((B + 3) / 4) * 16;
+  return cudaLaunchKernelEx(&c3, k_vec_finalize, static_cast<const float*>(g), static_cast<const float*>(part), B, L,
+                            n_chunks, clip_c, clip_c * clip_c, inv_batch, out, norms_out, accumulate, nk);
 }
 
 size_t emb_dp_work_bytes(int B, int T_, int D) {
