@@ -7,10 +7,12 @@
 // per-sample gradients, pinned to oracle/dp_oracle.py's restatements.
 //
 // Vector groups (length L = D, or 2 D for LayerNorm's [gamma, beta]): per-sample
-// g_b = sum_t dY (bias, beta), sum_t dY * xhat (gamma). Three deterministic passes:
-// row-chunk partial sums (parallel over samples x T chunks x columns), a fixed-
-// order sum of the chunks with per-block norm^2 partials, and the clip / sum /
-// noise pass. All HBM-bound on reading dY (and xhat) once.
+// g_b = sum_t dY (bias, beta), sum_t dY * xhat (gamma). Aligned rows: one CTA per
+// (sample, 32-byte column slice) sums all T rows (k_vec_cols) with the slice's norm^2
+// partial, then the clip / sum / noise pass (k_vec_finalize, PDL dependent). Unaligned
+// rows: three deterministic passes -- row-chunk partial sums, a fixed-order sum of the
+// chunks with per-block norm^2 partials, the same finalize. All HBM-bound on reading dY
+// (and xhat) once.
 //
 // Embedding (V x d table, tokens (B, T)): the per-sample gradient is a scatter of
 // dY rows onto the rows of the sample's tokens, so ||G_b||^2 is the token-
@@ -19,6 +21,7 @@
 // run of equal tokens (never materialising G_b); a streaming pass writes every
 // row's noise, and the add pass walks all samples' sorted runs per vocabulary row
 // in fixed order onto the touched rows -- deterministic, no atomics.
+#include <algorithm>
 #include <cstdlib>
 
 #include "../../include/fdp.h"
@@ -151,12 +154,18 @@ __global__ void __launch_bounds__(256) k_vec_finalize(const float* __restrict__ 
                                                       NoiseKey nk) {
   extern __shared__ float fac[];  // [B] clip factor x mean scale
   pdl_wait();  // PDL launch: g and the norm partials are complete
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+  // one warp per sample: lane-strided fp64 partial sums, then a fixed butterfly
+  for (int b = threadIdx.x >> 5; b < B; b += blockDim.x >> 5) {
     double s = 0.0;
-    for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[static_cast<long long>(b) * n_chunks + c]);
-    const double cf = (s <= clip_c2) ? 1.0 : clip_c / sqrt(s);  // dpcore.py:41-47
-    fac[b] = static_cast<float>(cf) * inv_batch;
-    if (blockIdx.x == 0 && norms_out) norms_out[b] = static_cast<float>(s);
+    for (int c = threadIdx.x & 31; c < n_chunks; c += 32)
+      s += static_cast<double>(part[static_cast<long long>(b) * n_chunks + c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) {
+      const double cf = (s <= clip_c2) ? 1.0 : clip_c / sqrt(s);  // dpcore.py:41-47
+      fac[b] = static_cast<float>(cf) * inv_batch;
+      if (blockIdx.x == 0 && norms_out) norms_out[b] = static_cast<float>(s);
+    }
   }
   __syncthreads();
   nk_resolve(nk);
@@ -167,6 +176,106 @@ __global__ void __launch_bounds__(256) k_vec_finalize(const float* __restrict__ 
     if (nk.add_noise && l >= nk.lo && l < nk.hi) v += nk.scale * nk_draw(nk, static_cast<uint64_t>(l));
     if (accumulate) v += out[l];
     out[l] = v;
+  }
+}
+
+// ---- two-launch vector group: every CTA owns a column slice (kTPR x 16 bytes) of one
+// sample over ALL T rows, so the per-sample sum needs no cross-CTA pass. 256 threads =
+// 256/kTPR row lanes x kTPR 16-byte loads per row; each row lane sums its rows
+// (t = lane, lane + 256/kTPR, ...), a fixed butterfly over the row lanes of a warp and a
+// fixed-order sum over the 8 warps give g[b][slice] and the slice's norm^2 partial
+// part[b][cb]; k_vec_finalize (PDL dependent) then clips, sums and adds noise. One HBM
+// read of dY (and xhat), two launches instead of three and no row-chunk partials.
+template <typename T, int kKind, int kTPR>
+__global__ void __launch_bounds__(256) k_vec_cols(const T* __restrict__ dy, const T* __restrict__ xh, int T_, int D,
+                                                  int n_cb, float* __restrict__ g, float* __restrict__ part) {
+  constexpr int VW = 16 / sizeof(T);  // columns per thread
+  constexpr int CW = kTPR * VW;       // columns per CTA (kTPR x 16 bytes)
+  constexpr int kLanes = 256 / kTPR;  // row lanes
+  constexpr int kH = kKind == FDP_VEC_LAYERNORM ? 2 : 1;
+  __shared__ float red[8][kH][CW];
+  __shared__ float wsq[kH * CW];
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  const int half = threadIdx.x % kTPR, row = threadIdx.x / kTPR, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cb = blockIdx.x, b = blockIdx.y;
+  const int d = cb * CW + half * VW;
+  const long long L = static_cast<long long>(kH) * D;
+  float s[VW], sx[VW];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) s[j] = sx[j] = 0.0f;
+  if (d < D) {
+    const T* py = dy + static_cast<long long>(b) * T_ * D + d;
+    const T* px = xh + static_cast<long long>(b) * T_ * D + d;
+#pragma unroll 8
+    for (int t = row; t < T_; t += kLanes) {
+      const long long i = static_cast<long long>(t) * D;
+      float y[VW], x[VW];
+      if constexpr (sizeof(T) == 4) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(py + i));
+        y[0] = a.x; y[1] = a.y; y[2] = a.z; y[3] = a.w;
+        if constexpr (kKind != FDP_VEC_BIAS) {
+          const float4 c = __ldcs(reinterpret_cast<const float4*>(px + i));
+          x[0] = c.x; x[1] = c.y; x[2] = c.z; x[3] = c.w;
+        }
+      } else {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4*>(py + i));
+        const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(pa[j]);
+          y[2 * j] = f.x;
+          y[2 * j + 1] = f.y;
+        }
+        if constexpr (kKind != FDP_VEC_BIAS) {
+          const uint4 c = __ldcs(reinterpret_cast<const uint4*>(px + i));
+          const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(pc[j]);
+            x[2 * j] = f.x;
+            x[2 * j + 1] = f.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < VW; ++j) {
+        if constexpr (kKind != FDP_VEC_RMSNORM) s[j] += y[j];
+        if constexpr (kKind != FDP_VEC_BIAS) sx[j] = fmaf(y[j], x[j], sx[j]);
+      }
+    }
+  }
+  // sum the row lanes of the warp (lanes equal mod kTPR), fixed butterfly
+#pragma unroll
+  for (int o = kTPR; o < 32; o <<= 1) {
+#pragma unroll
+    for (int j = 0; j < VW; ++j) {
+      s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+      sx[j] += __shfl_xor_sync(0xffffffffu, sx[j], o);
+    }
+  }
+  if (lane < kTPR) {
+#pragma unroll
+    for (int j = 0; j < VW; ++j) {  // half 0 = the xhat term (gamma / RMSNorm weight) or the bias sum
+      red[warp][0][half * VW + j] = kKind == FDP_VEC_BIAS ? s[j] : sx[j];
+      if constexpr (kH == 2) red[warp][1][half * VW + j] = s[j];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kH * CW) {
+    const int h = threadIdx.x / CW, c = threadIdx.x % CW;
+    float v = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][h][c];
+    const bool in = cb * CW + c < D;
+    if (in) g[static_cast<long long>(b) * L + static_cast<long long>(h) * D + cb * CW + c] = v;
+    wsq[threadIdx.x] = in ? v * v : 0.0f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+#pragma unroll
+    for (int c = 0; c < kH * CW; ++c) t += wsq[c];
+    part[static_cast<long long>(b) * n_cb + cb] = t;
   }
 }
 
@@ -409,6 +518,8 @@ int pow2_at_least(int n) {
 }  // namespace
 
 size_t vec_dp_work_bytes(int kind, int B, int T_, int D) {
+  // three-pass layout [gpart | g | part(L/256)]; the column-slice schedule's [g | part(<= D/8)]
+  // fits inside it (gpart alone holds at least B L floats)
   const long long L = kind == FDP_VEC_LAYERNORM ? 2LL * D : D;
   const long long n_chunks = (L + kVCols - 1) / kVCols;
   return sizeof(float) * static_cast<size_t>(B * n_tchunks(T_) * L + B * L + B * n_chunks);
@@ -418,15 +529,63 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
                    double clip_c, float inv_batch, float* out, float* norms_out, int accumulate, const NoiseKey& nk,
                    cudaStream_t s) {
   const long long L = kind == FDP_VEC_LAYERNORM ? 2LL * D : D;
-  const int n_tc = static_cast<int>(n_tchunks(T_));
-  const int n_chunks = static_cast<int>((L + kVCols - 1) / kVCols);
-  float* gpart = work;                                           // [B][n_tc][L]
-  float* g = gpart + static_cast<long long>(B) * n_tc * L;       // [B][L]
-  float* part = g + static_cast<long long>(B) * L;               // [B][n_chunks]
   // 16-byte loads when every row start stays aligned (D a multiple of the vector width)
   const bool aligned = (reinterpret_cast<uintptr_t>(dy) % 16 == 0) && (reinterpret_cast<uintptr_t>(xhat) % 16 == 0);
   const int vw = !aligned ? 1 : in_f32 ? ((D % 4 == 0) ? 4 : 1) : ((D % 8 == 0) ? 8 : 1);
-  const dim3 g1((D / vw + kVCols - 1) / kVCols, n_tc, B);
+  // column-slice schedule whenever the rows take 16-byte loads (FDP_VEC_COLS=0: three passes)
+  const char* cv = std::getenv("FDP_VEC_COLS");
+  const bool cols = vw > 1 && !(cv && std::atoi(cv) == 0);
+  float *g, *part;
+  int n_chunks;
+  cudaError_t e;
+  if (cols) {
+    // widest slice (longer contiguous row segments) that still gives two CTAs per SM
+    int tpr = 8;
+    while (tpr > 2 && static_cast<long long>((D + tpr * vw - 1) / (tpr * vw)) * B < 2 * 148) tpr >>= 1;
+    const int cw = tpr * vw;
+    n_chunks = (D + cw - 1) / cw;
+    g = work;                                   // [B][L]
+    part = g + static_cast<long long>(B) * L;   // [B][n_chunks]
+    const dim3 grid(n_chunks, B);
+#define FDP_VEC_C(TY, K, P) \
+  k_vec_cols<TY, K, P><<<grid, 256, 0, s>>>(static_cast<const TY*>(dy), static_cast<const TY*>(xhat), T_, D, n_chunks, g, part)
+#define FDP_VEC_CP(TY, K)                       \
+  do {                                          \
+    if (tpr == 8) FDP_VEC_C(TY, K, 8);          \
+    else if (tpr == 4) FDP_VEC_C(TY, K, 4);     \
+    else FDP_VEC_C(TY, K, 2);                   \
+  } while (0)
+#define FDP_VEC_CK(TY)                                               \
+  do {                                                               \
+    if (kind == FDP_VEC_BIAS) FDP_VEC_CP(TY, FDP_VEC_BIAS);           \
+    else if (kind == FDP_VEC_RMSNORM) FDP_VEC_CP(TY, FDP_VEC_RMSNORM); \
+    else FDP_VEC_CP(TY, FDP_VEC_LAYERNORM);                           \
+  } while (0)
+    if (in_f32) FDP_VEC_CK(float);
+    else FDP_VEC_CK(__nv_bfloat16);
+#undef FDP_VEC_CK
+#undef FDP_VEC_CP
+#undef FDP_VEC_C
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // the reduce and the finalize are programmatic dependents of the pass before them: their
+  // launch latency hides under it (FDP_PDL=0 turns it off)
+  const char* pv = std::getenv("FDP_PDL");
+  const bool pdl = !pv || std::atoi(pv) != 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t c2{};
+  c2.stream = s;
+  c2.attrs = attr;
+  c2.numAttrs = pdl ? 1 : 0;
+  if (!cols) {
+    const int n_tc = static_cast<int>(n_tchunks(T_));
+    n_chunks = static_cast<int>((L + kVCols - 1) / kVCols);
+    float* gpart = work;                                    // [B][n_tc][L]
+    g = gpart + static_cast<long long>(B) * n_tc * L;       // [B][L]
+    part = g + static_cast<long long>(B) * L;               // [B][n_chunks]
+    const dim3 g1((D / vw + kVCols - 1) / kVCols, n_tc, B);
 #define FDP_VEC_ROWS(TY, K, V) \
   k_vec_rows<TY, K, V><<<g1, kVCols, 0, s>>>(static_cast<const TY*>(dy), static_cast<const TY*>(xhat), T_, D, n_tc, gpart)
 #define FDP_VEC_KINDS(TY, V)                                        \
@@ -435,33 +594,22 @@ cudaError_t vec_dp(int kind, const void* dy, const void* xhat, int in_f32, int B
     else if (kind == FDP_VEC_RMSNORM) FDP_VEC_ROWS(TY, FDP_VEC_RMSNORM, V); \
     else FDP_VEC_ROWS(TY, FDP_VEC_LAYERNORM, V);                    \
   } while (0)
-  if (in_f32) {
-    if (vw == 4) FDP_VEC_KINDS(float, 4);
-    else FDP_VEC_KINDS(float, 1);
-  } else {
-    if (vw == 8) FDP_VEC_KINDS(__nv_bfloat16, 8);
-    else FDP_VEC_KINDS(__nv_bfloat16, 1);
-  }
+    if (in_f32) {
+      if (vw == 4) FDP_VEC_KINDS(float, 4);
+      else FDP_VEC_KINDS(float, 1);
+    } else {
+      if (vw == 8) FDP_VEC_KINDS(__nv_bfloat16, 8);
+      else FDP_VEC_KINDS(__nv_bfloat16, 1);
+    }
 #undef FDP_VEC_KINDS
 #undef FDP_VEC_ROWS
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // the reduce and the finalize are programmatic dependents of the pass before them: their
-  // launch latency hides under it (three small kernels per group; FDP_PDL=0 turns it off)
-  const char* pv = std::getenv("FDP_PDL");
-  const bool pdl = !pv || std::atoi(pv) != 0;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t c2{};
-  c2.gridDim = dim3(n_chunks, B);
-  c2.blockDim = dim3(kVCols);
-  c2.stream = s;
-  c2.attrs = attr;
-  c2.numAttrs = pdl ? 1 : 0;
-  if ((e = cudaLaunchKernelEx(&c2, k_vec_reduce, static_cast<const float*>(gpart), n_tc, static_cast<int>(L), g, part,
-                              n_chunks)) != cudaSuccess)
-    return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    c2.gridDim = dim3(n_chunks, B);
+    c2.blockDim = dim3(kVCols);
+    if ((e = cudaLaunchKernelEx(&c2, k_vec_reduce, static_cast<const float*>(gpart), n_tc, static_cast<int>(L), g, part,
+                                n_chunks)) != cudaSuccess)
+      return e;
+  }
   const long long blocks = (L + 255) / 256 < 148 ? (L + 255) / 256 : 148;
   // factor table rounded up to whole 16-byte words: the unrolled sample loop may read fac[] in vectors
   cudaLaunchConfig_t c3 = c2;

@@ -39,7 +39,12 @@ def ocfg(c: fdp.DPConfig) -> O.Cfg:
 @pytest.mark.parametrize("kind", ["bias", "rmsnorm", "layernorm"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("B,T,D", [(5, 70, 777), (1, 1, 64), (3, 200, 256), (16, 9, 1030), (2, 65, 8), (4, 33, 1028)])
-def test_vector_groups_against_oracle(kind, dtype, B, T, D):
+@pytest.mark.parametrize("sched", ["auto", "three_pass"])
+def test_vector_groups_against_oracle(kind, dtype, B, T, D, sched, monkeypatch):
+    """auto: aligned rows take the column-slice kernel (k_vec_cols + finalize), unaligned
+    ones (D not a multiple of the vector width) the three passes."""
+    if sched == "three_pass":
+        monkeypatch.setenv("FDP_VEC_COLS", "0")
     g = torch.Generator().manual_seed(B * 1000 + T + D)
     dy = (torch.randn(B, T, D, generator=g) * 0.1).to(dtype).cuda()
     xh = torch.randn(B, T, D, generator=g).to(dtype).cuda()
@@ -84,6 +89,40 @@ def test_vector_group_unaligned_view():
     out = fdp.vector_dp_grad("rmsnorm", dy, xh, cfg)
     want, _ = O.dp_vector_backward(host(dy), host(xh), "rmsnorm", ocfg(cfg))
     assert rel(host(out), want) < TOL
+
+
+@pytest.mark.parametrize("kind", ["bias", "layernorm", "rmsnorm"])
+@pytest.mark.parametrize("B,T,D", [(1, 1024, 768), (1, 1024, 3072), (2, 4096, 4096), (8, 1000, 1536), (1, 7, 40)])
+def test_vector_group_column_slices_match_three_pass(kind, B, T, D, monkeypatch):
+    """The column-slice schedule (one CTA per 32-byte column slice over all T rows) against
+    the three-pass one at model shapes: same values to fp32 reordering, bitwise
+    repeatable, and unchanged under CUDA-graph replay."""
+    g = torch.Generator().manual_seed(B + T + D)
+    dy = (torch.randn(B, T, D, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    xh = torch.randn(B, T, D, generator=g).to(torch.bfloat16).cuda()
+    cfg = fdp.DPConfig(0.3, 0.9, "mean", seed=4, layer_id=2, step=5)
+    xa = None if kind == "bias" else xh
+    fused = fdp.vector_dp_grad(kind, dy, xa, cfg, noise_impl="keyed_f64")
+    again = fdp.vector_dp_grad(kind, dy, xa, cfg, noise_impl="keyed_f64")
+    assert torch.equal(fused, again)
+    monkeypatch.setenv("FDP_VEC_COLS", "0")
+    three = fdp.vector_dp_grad(kind, dy, xa, cfg, noise_impl="keyed_f64")
+    monkeypatch.delenv("FDP_VEC_COLS")
+    assert rel(host(fused), host(three)) < 1e-5
+    out = torch.zeros_like(fused)
+    fdp.vector_dp_grad(kind, dy, xa, cfg, noise_impl="keyed_f64", out=out)  # warm the workspace cache
+    gr = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(gr, stream=s):
+            fdp.vector_dp_grad(kind, dy, xa, cfg, noise_impl="keyed_f64", out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        out.zero_()
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, fused)
 
 
 def test_bias_dw_is_the_bias_vector_group():
