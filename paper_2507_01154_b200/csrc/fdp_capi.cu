@@ -1181,6 +1181,11 @@ int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, int
   const int cands[4][2] = {{256, 2}, {128, 2}, {256, 1}, {128, 1}};
   const int forced_bn = env_int("FDP_FORCE_BN", 0), forced_cg = env_int("FDP_FORCE_CG", 0);
   const bool no_pack = env_int("FDP_NO_PACK", 0) != 0;
+  // cost of splitting a tile's samples over g > 1 clusters (the groups' reduce-add combine),
+  // and of a cluster holding ONE sample of a B > 1 layer: nothing to run while its norm
+  // barrier resolves (with two or more, the next sample's MMAs overlap the wait)
+  const double g_pen = 1e-9 * env_int("FDP_GROUP_GPEN_NS", 3000);
+  const double x_pen = 1e-9 * env_int("FDP_GROUP_XPEN_NS", 5000);
   double best = 1e300;
   for (auto& cd : cands) {
     const int bn = cd[0], cg = cd[1];
@@ -1215,7 +1220,8 @@ int plan_group_uncached(int32_t n, const fdp_desc* descs, const DevInfo& di, int
       for (int g = 1; g <= gmax; ++g) {
         if (no_pack && (g & (g - 1))) continue;
         const int nc = nwt * g;
-        const double t = static_cast<double>((d->B + g - 1) / g) * unit + (g > 1 ? 3e-6 : 0.0);
+        const long long per = (d->B + g - 1) / g;
+        const double t = static_cast<double>(per) * unit + (g > 1 ? g_pen : 0.0) + (per == 1 && d->B > 1 ? x_pen : 0.0);
         for (int off = 0; off < (no_pack ? 1 : K); ++off) {
           double m = 0.0, sum = 0.0;
           for (int i = 0; i < nc; ++i) {

@@ -45,15 +45,20 @@ def main():
             for _ in range(5):
                 gs()
             torch.cuda.synchronize()
-        tot, cnt = {}, {}
+        tot, cnt, per = {}, {}, {}
         for ev in prof.events():
             if ev.device_type != torch.autograd.DeviceType.CUDA:
                 continue
             g = grp(ev.name)
+            if g in ("dp_dW", "dp_vec", "gemm"):
+                k = (g, ev.name[:70])
+                per[k] = per.get(k, 0.0) + ev.time_range.elapsed_us() / 5
             tot[g] = tot.get(g, 0.0) + ev.time_range.elapsed_us() / 5
             cnt[g] = cnt.get(g, 0) + 1 / 5
         print(json.dumps({"dp": dp, "B": B, "us_per_step": {k: round(v, 1) for k, v in sorted(tot.items(), key=lambda kv: -kv[1])},
-                          "launches_per_step": {k: round(v) for k, v in cnt.items()}}), flush=True)
+                          "launches_per_step": {k: round(v) for k, v in cnt.items()},
+                          "top_kernels_us": [[g, n, round(v, 1)] for (g, n), v in
+                                             sorted(per.items(), key=lambda kv: -kv[1])[:12]]}), flush=True)
         del model, step, gs
         torch.cuda.empty_cache()
 
