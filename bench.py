@@ -608,7 +608,12 @@ def main():
             "config": bench_config(a, world, global_B, T, bool(graph is not None)),
             "tflops_per_gpu": flops_per_step_rank / (ms_per_step * 1e-3) / 1e12,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": (a.steps if group is not None else len(calls) * a.steps),
+            # + the pre-drawn noise pass the group launch runs before itself at B <= 2
+            # (fdp_capi.cu, FDP_GROUP_PRENOISE_MAXB) when a layer has one sample group:
+            # every layer at B = 1, most of the 48 at B = 2 (the planner's packing)
+            "gpu_launches": ((a.steps * (2 if (a.sigma > 0 and B <= int(os.environ.get("FDP_GROUP_PRENOISE_MAXB", "2")))
+                                         else 1))
+                             if group is not None else len(calls) * a.steps),
             "plans": {k: {"path": fdp._lib.PATH_NAMES[v.path], "tile": [v.tile_d, v.tile_p], "groups": v.groups,
                           "grid": v.grid} for k, v in plans.items()},
         }

@@ -1561,6 +1561,34 @@ int fdp_backward_group_ex(int32_t n, const fdp_desc* descs, const void* const* x
   gp.poll_mode = env_int("FDP_POLL_MODE", 0);
   gp.pf_ahead = env_int("FDP_PF_AHEAD", 0);
   gp.pair_dsmem = env_int("FDP_PAIR_DSMEM", 0);
+  // small batches: a noised, non-accumulating layer whose tiles hold all its samples
+  // (one sample group: reduce-add straight onto the rows, no pre-fill copy) gets its
+  // noise drawn by the whole GPU first (fdp_group.cu k_group_noise); the group launch
+  // then reduce-adds onto it. FDP_GROUP_PRENOISE_MAXB (default 2; 0 = off) bounds B:
+  // from B = 3 the MMAs hide the noise warps' draws and the pass only adds a DRAM
+  // round trip of grad_w (48 GPT-2 layers: B = 3 0.81 -> 0.99 ms).
+  {
+    const int maxb = env_int("FDP_GROUP_PRENOISE_MAXB", 2);
+    bool pre[fdp::kMaxGroupLayers], any = false;
+    for (int l = 0; l < n; ++l) {
+      const fdp::GLayer& L = gp.L[l];
+      pre[l] = maxb > 0 && L.add_noise && !L.accumulate && L.groups == 1 && L.B <= maxb;
+      any |= pre[l];
+    }
+    if (any) {
+      static thread_local fdp::GroupParams gn;  // the pass's view: only the pre-drawn layers noised
+      gn = gp;
+      for (int l = 0; l < n; ++l)
+        if (!pre[l]) gn.L[l].add_noise = 0;
+      cudaError_t e = fdp::launch_group_noise(gn, static_cast<cudaStream_t>(stream));
+      if (e != cudaSuccess) return cuda_fail(e, "group noise launch");
+      for (int l = 0; l < n; ++l)
+        if (pre[l]) {
+          gp.L[l].add_noise = 0;
+          gp.L[l].accumulate = 1;
+        }
+    }
+  }
   cudaError_t e = fdp::launch_group(gpl.bn, gpl.cg, gp, gpl.grid, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "group launch");
   return FDP_OK;

@@ -512,6 +512,57 @@ static cudaError_t launch_group_impl(const GroupParams& gp, int grid, cudaStream
   return e;
 }
 
+// ---- pre-drawn noise (small batches). At B <= 4 the two noise warps' draws bound
+// the group launch (48 GPT-2 layers, B = 1: 0.652 ms with noise, 0.370 with a zero
+// pre-fill). This grid-wide pass writes every noised layer's sigma C N(d P + p) into
+// grad_w with all SMs' warps first; the group launch then reduce-adds onto it
+// (accumulate, no draws). Bit for bit the pre-fill path: round(sigma C N) + acc in
+// one fp32 add either way. Quads of 4 flat indices (P % 8 == 0); outside [lo, hi)
+// (rank partition) the rows are written as zeros.
+__global__ void __launch_bounds__(256) k_group_noise(const GroupParams gp) {
+  __shared__ long long start[kMaxGroupLayers + 1];
+  __shared__ uint64_t kb_s[kMaxGroupLayers], kbg_s[kMaxGroupLayers];
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int l = 0; l < gp.n_layers; ++l) {
+      const GLayer& L = gp.L[l];
+      start[l] = s;
+      if (L.add_noise) s += static_cast<long long>(L.D) * L.P / 4;
+      uint64_t kb = L.key_base;
+      if (L.step_ptr) kb = absorb3(L.seed_u, L.layer_u, static_cast<uint64_t>(*L.step_ptr));
+      kb_s[l] = kb;
+      kbg_s[l] = L.step_ptr ? kb + kGamma : L.key_base_g;
+    }
+    start[gp.n_layers] = s;
+  }
+  __syncthreads();
+  const long long total = start[gp.n_layers];
+  int l = 0;
+  for (long long q = blockIdx.x * 256LL + threadIdx.x; q < total; q += static_cast<long long>(gridDim.x) * 256) {
+    while (q >= start[l + 1]) ++l;  // q only grows: the layer index only moves forward
+    const GLayer& L = gp.L[l];
+    const long long f = (q - start[l]) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gp.dbg_noise != 1 && f + 3 >= L.noise_lo && f < L.noise_hi) {
+      const float4 n = noise_draw4(L.noise_impl, kbg_s[l], kb_s[l], static_cast<uint64_t>(f >> 2));
+      const float sc = gp.dbg_noise == 2 ? 0.0f : L.noise_scale;
+      if (f + 0 >= L.noise_lo && f + 0 < L.noise_hi) v.x = __fmul_rn(sc, n.x);
+      if (f + 1 >= L.noise_lo && f + 1 < L.noise_hi) v.y = __fmul_rn(sc, n.y);
+      if (f + 2 >= L.noise_lo && f + 2 < L.noise_hi) v.z = __fmul_rn(sc, n.z);
+      if (f + 3 >= L.noise_lo && f + 3 < L.noise_hi) v.w = __fmul_rn(sc, n.w);
+    }
+    __stcg(reinterpret_cast<float4*>(L.grad_w + f), v);
+  }
+}
+
+cudaError_t launch_group_noise(const GroupParams& gp, cudaStream_t stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_group_noise<<<sms * 8, 256, 0, stream>>>(gp);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream) {
   if (cg == 2) {
     if (bn == 256) {

@@ -167,6 +167,7 @@ struct GroupParams {
   int pair_dsmem;  // CTA-pair norm partials combined in DSMEM before publishing (FDP_PAIR_DSMEM; default off)
 };
 cudaError_t launch_group(int bn, int cg, const GroupParams& gp, int grid, cudaStream_t stream);
+cudaError_t launch_group_noise(const GroupParams& gp, cudaStream_t stream);  // pre-drawn noise (fdp_group.cu)
 
 // ---- ghost norms (TWO_PHASE first phase): ||G_b||^2 = <X_b X_b^T, dY_b dY_b^T>
 struct GhostParams {
