@@ -20,7 +20,10 @@ __device__ __forceinline__ void prefill_rows_impl(float* __restrict__ grad_w, in
                                                   bool accumulate, bool draw, uint64_t kbg, uint64_t kb, float scale,
                                                   long long lo, long long hi, int ntid) {
   constexpr int kQ = BN / 4;  // float4 per tile row
-  constexpr int kIlp = 4;
+#ifndef FDP_PREFILL_ILP
+#define FDP_PREFILL_ILP 4
+#endif
+  constexpr int kIlp = FDP_PREFILL_ILP;
   const int q_all = (d_hi - d_lo) * kQ;
   for (int base = ntid; base < q_all; base += 64 * kIlp) {
     long long flat[kIlp];
