@@ -916,12 +916,14 @@ def test_stream_multicast_keyed_noise_and_accumulate(epi, monkeypatch):
     assert rel(host(r.per_sample_norms_sq), wn) < BF16_TOL
 
 
-def test_group_launch_graph_capture_with_device_step():
+@pytest.mark.parametrize("B", [4, 2, 1])
+def test_group_launch_graph_capture_with_device_step(B):
     """PreparedGroup inside a CUDA graph: replays run the persistent multi-layer
     launch (not an empty graph), and the device step counter keys fresh noise per
-    replay exactly as direct calls with that step would."""
+    replay exactly as direct calls with that step would. B <= 2 also captures the
+    pre-drawn noise pass (which reads the step counter itself)."""
     shapes = [(256, 768), (768, 256), (512, 512)]
-    B, T = 4, 128
+    T = 128
     layers = []
     for i, (P, D) in enumerate(shapes):
         x, dy = randn(B, T, P, D, seed=300 + i, scale_dy=1e-2)
